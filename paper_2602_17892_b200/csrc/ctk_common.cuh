@@ -1,0 +1,74 @@
+// ctk_common.cuh -- shared declarations for the B200 projector library.
+//
+// Layout conventions (reference: ctkrylov/ct.py:10-18):
+//   image    row-major (ny, nx), row 0 = top (largest y), fp32
+//   sinogram angle-major, sample a*D + j, fp32
+//   Krylov basis W: [K+1][ld] fp32, ld a multiple of 4 (16-B rows)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ctk.h"
+
+namespace ctk {
+
+// Per-angle forward (K1) parameters, computed once on the host in fp64.
+// The ray for bin j meets walk-row boundary k at cross coordinate
+//   u_k = (alpha + beta * s_j) + k * sigma      (pixel units, sigma in [0, 1])
+// where a walk row is an image row (frame 0, |cos| >= |sin|) or an image
+// column (frame 1), and "mirror" flips the cross axis so sigma >= 0.
+struct AngleParams {
+    double alpha, beta;     // u_0 = alpha + beta * s
+    long long sigma_fx;     // sigma in 32.32 fixed point
+    float L;                // chord per walk row  (h / |walk-axis cosine|)
+    float Lx;               // chord per unit cross coordinate (h / |cross-axis cosine|)
+    int frame;              // 0: walk rows of x, 1: walk columns (transposed copy)
+    int mirror;             // cross axis reversed
+    int degenerate;         // |sin| or |cos| < 1e-14: exact literal path (ct.py:153-155,165,168)
+    int pad_;
+};
+
+struct BackParams {         // per angle for K2: g = X*cg + Y*sg + center
+    double cg, sg;
+};
+
+}  // namespace ctk
+
+struct ctk_geom {
+    int device;
+    int nx, ny, n_angles, det_count;
+    double h, det_spacing;
+    double xmin, xmax, ymin, ymax, center;
+    int back_wmax;            // max staged bins per angle for one K2 tile
+    int n_degenerate;
+    // device tables
+    ctk::AngleParams* d_ap;   // [n_angles]
+    ctk::BackParams* d_bp;    // [n_angles]
+    double* d_cos;            // [n_angles] bitwise np.cos (exact path)
+    double* d_sin;            // [n_angles]
+    double* d_offsets;        // [det_count] bitwise bin_offsets()
+};
+
+// error plumbing (thread-local last error string)
+int ctk_fail(int code, const char* fmt, ...);
+int ctk_check_cuda(cudaError_t e, const char* what);
+
+#define CTK_CUDA(call)                                                 \
+    do {                                                               \
+        cudaError_t e_ = (call);                                       \
+        if (e_ != cudaSuccess) return ctk_check_cuda(e_, #call);       \
+    } while (0)
+
+#define CTK_LAUNCH_CHECK(what)                                         \
+    do {                                                               \
+        cudaError_t e_ = cudaGetLastError();                           \
+        if (e_ != cudaSuccess) return ctk_check_cuda(e_, what);        \
+    } while (0)
+
+static inline cudaStream_t ctk_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Pad counts for the K1 staging copies.
+static inline int64_t ctk_stage_floats(int nx, int ny) {
+    return (int64_t)ny * (nx + 2) + (int64_t)nx * (ny + 2);
+}

@@ -1,0 +1,171 @@
+"""Generate golden fixtures by running the UNMODIFIED reference.
+
+Run in the build container (the only place /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Everything below calls the reference's public API (ctkrylov.ct /
+ctkrylov.gmres / ctkrylov.regparam); the inputs come from
+paper_2602_17892_b200.problems so the GPU tests can regenerate them on the
+GPU box without the reference.  Outputs: tests/golden/*.npz (small).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from ctkrylov.ct import (ImageGrid, ParallelGeometry, back_pixel_driven,  # noqa: E402
+                         forward_ray_driven, make_ct_problem)
+from ctkrylov.gmres import SolverConfig, run_gmres  # noqa: E402
+from ctkrylov.regparam import select_lambda  # noqa: E402
+
+from paper_2602_17892_b200 import problems  # noqa: E402
+
+
+def geom(nx, ny, h, angles, D, sp):
+    return ImageGrid(nx, ny, h), ParallelGeometry(np.asarray(angles, float), D, sp)
+
+
+def small_angles(k):
+    return np.arange(k) * np.pi / k
+
+
+# Small operator geometries: the reference tests' own (tests/test_ct.py:67-130)
+# plus degenerate-angle / non-square / edge-tap cases.
+SMALL = {
+    "t_siddon_4x4": (4, 4, 0.7, [0.0, 0.9, 2.1], 5, 0.8),          # tests/test_ct.py:67-72
+    "t_back_5x4": (5, 4, 0.6, small_angles(4), 7, 0.5),             # tests/test_ct.py:126-130
+    "t_unmatched_8x8": (8, 8, 0.3, small_angles(6), 11, 0.35),      # tests/test_ct.py:132-138
+    "t_single_bin_6x6": (6, 6, 0.4, [0.7], 9, 0.4),                 # tests/test_ct.py:116-124
+    "t_center_ray": (8, 8, 0.5, [0.0], 1, 0.5),                     # tests/test_ct.py:53-58
+    "t_diag_ray": (6, 6, 1.0, [np.pi / 4], 1, 1.0),                 # tests/test_ct.py:60-65
+    "t_miss": (4, 4, 0.5, [0.0], 3, 10.0),                          # tests/test_ct.py:95-99
+    "axis_16": (16, 16, 1.0, small_angles(8), 23, 1.0),             # integer offsets, 0/45/90 deg
+    "nonsquare_7x5": (7, 5, 0.5, small_angles(6), 9, 0.45),
+    "edge_taps_6x6": (6, 6, 1.0, small_angles(5), 5, 1.0),          # detector narrower than image
+    "wide_12x10": (12, 10, 0.8, np.sort(np.random.default_rng(5).uniform(0, np.pi, 9)), 17, 0.7),
+}
+
+
+def make_small():
+    out = {}
+    rng = np.random.default_rng(123)
+    for name, (nx, ny, h, ang, D, sp) in SMALL.items():
+        g, p = geom(nx, ny, h, ang, D, sp)
+        A = forward_ray_driven(g, p)
+        B = back_pixel_driven(g, p)
+        x = rng.random(g.n).astype(np.float32).astype(np.float64)
+        u = rng.random(p.m).astype(np.float32).astype(np.float64)
+        out[f"{name}/params"] = np.array([nx, ny, h, D, sp], dtype=np.float64)
+        out[f"{name}/angles"] = p.angles
+        out[f"{name}/A_dense"] = A.to_dense()
+        out[f"{name}/B_dense"] = B.to_dense()
+        out[f"{name}/x"] = x
+        out[f"{name}/u"] = u
+        out[f"{name}/Ax"] = A.apply(x)
+        out[f"{name}/Bu"] = B.apply(u)
+    np.savez_compressed(os.path.join(HERE, "small_ops.npz"), **out)
+    print("small_ops.npz", len(SMALL), "geometries")
+
+
+def config_problem(spec):
+    g, p = geom(spec.N, spec.N, 1.0, spec.angles(), spec.det_count, 1.0)
+    t0 = time.time()
+    A = forward_ray_driven(g, p)
+    B = back_pixel_driven(g, p)
+    print(f"{spec.name}: build {time.time() - t0:.1f}s nnz={A.sparse_matrix.nnz}")
+    return g, p, A, B
+
+
+def records_arrays(res):
+    fields = ("k", "lambda_used", "residual_norm", "data_residual_norm",
+              "proj_residual_norm", "solution_norm")
+    arr = {f: np.array([getattr(r, f) for r in res.records], dtype=np.float64) for f in fields}
+    arr["lambda_warning"] = np.array([r.lambda_warning for r in res.records], dtype=bool)
+    return arr
+
+
+def make_config(name, solve=True, extra_plain=False):
+    spec = problems.CONFIGS[name]
+    g, p, A, B = config_problem(spec)
+    out = {"nnz": np.int64(A.sparse_matrix.nnz)}
+    x_true = problems.random_ellipse_phantom(spec.N, spec.ellipses, spec.phantom_seed)
+    u = problems.uniform_sinogram(p.m, 1)
+    ximg = problems.uniform_image(g.n, 0)
+    out["Ax_true"] = A.apply(x_true)
+    out["Ax_uniform"] = A.apply(ximg)
+    out["Bu_uniform"] = B.apply(u)
+    if solve:
+        b, noise_norm = problems.add_noise(out["Ax_true"], spec.noise, spec.noise_seed)
+        out["noise_norm"] = np.float64(noise_norm)
+        b32 = b.astype(np.float32).astype(np.float64)
+        cfg = SolverConfig(method=spec.method, lambda_strategy=spec.strategy,
+                           max_iter=spec.max_iter)
+        t0 = time.time()
+        res = run_gmres(A, B, b32, cfg)
+        print(f"{name}: {spec.method}/{spec.strategy} K={spec.max_iter} {time.time() - t0:.1f}s "
+              f"stop={res.stop_reason}")
+        out["x_final"] = res.x.astype(np.float32)
+        for k, v in records_arrays(res).items():
+            out[f"rec/{k}"] = v
+        if extra_plain:
+            cfg = SolverConfig(method=spec.method.replace("-hybrid", ""), max_iter=spec.max_iter)
+            res = run_gmres(A, B, b32, cfg)
+            out["plain/x_final"] = res.x.astype(np.float32)
+            for k, v in records_arrays(res).items():
+                out[f"plain/rec/{k}"] = v
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}.npz written")
+
+
+def make_solver_cases():
+    """Small CT solves through every driver branch (tests/test_acceptance.py:142-172 problem)."""
+    prob = make_ct_problem(16, 12, 23, 0.02, 0)
+    out = {"b": prob.b_noisy, "noise_norm": np.float64(prob.noise_norm),
+           "A_dense": prob.forward.to_dense(), "B_dense": prob.back.to_dense()}
+    cases = {
+        "ab_plain": dict(method="ab", max_iter=12),
+        "ba_plain": dict(method="ba", max_iter=12),
+        "ab_gcv": dict(method="ab-hybrid", lambda_strategy="gcv", max_iter=15),
+        "ba_gcv": dict(method="ba-hybrid", lambda_strategy="gcv", max_iter=15),
+        "ab_lcurve": dict(method="ab-hybrid", lambda_strategy="lcurve", max_iter=15),
+        "ba_fixed": dict(method="ba-hybrid", lambda_strategy="fixed", lambda_value=0.3, max_iter=10),
+        "ab_restart": dict(method="ab-hybrid", lambda_strategy="gcv", max_iter=14, restart_period=5),
+        "ab_dp": dict(method="ab", max_iter=40, stopping_rule="dp", noise_norm=prob.noise_norm),
+        "ba_rns": dict(method="ba", max_iter=40, stopping_rule="rns", rns_epsilon=1e-3),
+    }
+    for name, kw in cases.items():
+        res = run_gmres(prob.forward, prob.back, prob.b_noisy, SolverConfig(**kw))
+        out[f"{name}/x"] = res.x
+        out[f"{name}/stop"] = np.array(res.stop_reason)
+        out[f"{name}/cycles"] = np.int64(res.cycles)
+        for k, v in records_arrays(res).items():
+            out[f"{name}/rec/{k}"] = v
+    # lambda selection on random Hessenbergs (ctkrylov/regparam.py:137-158)
+    rng = np.random.default_rng(7)
+    for i, k in enumerate((3, 8, 20, 45)):
+        H = np.triu(rng.standard_normal((k + 1, k)), -1) * np.logspace(0, -6, k)
+        out[f"lam/{i}/H"] = H
+        out[f"lam/{i}/gcv"] = np.float64(select_lambda(H, 2.5, "gcv"))
+        out[f"lam/{i}/lcurve"] = np.float64(select_lambda(H, 2.5, "lcurve"))
+    np.savez_compressed(os.path.join(HERE, "solver_cases.npz"), **out)
+    print("solver_cases.npz", len(cases), "cases")
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["small", "solver", "c1", "c2"]
+    if "small" in which:
+        make_small()
+    if "solver" in which:
+        make_solver_cases()
+    if "c1" in which:
+        make_config("c1")
+    if "c2" in which:
+        make_config("c2", extra_plain=True)

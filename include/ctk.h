@@ -1,0 +1,131 @@
+/*
+ * ctk.h -- C ABI of the B200-native projector / Krylov library (libctk.so).
+ *
+ * Drop-in boundary for the hot path of ctkrylov's hybrid AB-/BA-GMRES
+ * (reference paths relative to pkg/src of arxiv/paper_2602_17892):
+ *
+ *   ctk_geom_create   replaces the geometry captured by the closures built in
+ *                     forward_ray_driven / back_pixel_driven
+ *                     (ctkrylov/ct.py:182-201, 204-245; ImageGrid ct.py:37-66,
+ *                     ParallelGeometry ct.py:69-96)
+ *   ctk_forward       replaces A.apply: `lambda v: mat @ v`        (ct.py:201)
+ *                     optionally fused with the residual b - A x   (gmres.py:174,209)
+ *   ctk_forward_exact literal fp64 Siddon (ct.py:137-179), every angle
+ *   ctk_count_segments  segment / CSR-nnz counts of A               (ct.py:178,197-200)
+ *   ctk_back          replaces B.apply: the angle loop            (ct.py:234-245)
+ *                     optionally fused with x0 + B(.)              (gmres.py:207)
+ *   ctk_cgs2_step     replaces arnoldi_step's MGS + reorth sweeps  (arnoldi.py:66-82)
+ *   ctk_combine       replaces W = column_stack(basis); W @ y; x0 + (.)
+ *                                                                  (gmres.py:205-207)
+ *   ctk_dots / ctk_update / ctk_norm2   the vector primitives behind the above
+ *                     (np.linalg.norm at arnoldi.py:42,67,77, gmres.py:210,251)
+ *
+ * Conventions
+ *   - Every vector is caller-owned device memory, fp32, contiguous.  Images are
+ *     row-major (ny, nx) with row 0 at the top; sinograms are angle-major
+ *     (a * det_count + j), exactly the reference layout (ct.py:10-18).
+ *   - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream).  Nothing allocates on the
+ *     hot path.  Reductions are deterministic (fixed trees, no float atomics).
+ *   - Return 0 on success, a negative CTK_ERR_* code otherwise;
+ *     ctk_last_error() returns a thread-local message for the last failure.
+ *   - A geometry handle is immutable after creation and may be shared across
+ *     host threads and streams.  Scratch buffers are per call site (one per
+ *     stream in flight) and must be zero-filled once when allocated.
+ */
+#ifndef CTK_H_
+#define CTK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CTK_OK 0
+#define CTK_ERR_ARG (-1)      /* invalid argument (ValueError)                        */
+#define CTK_ERR_SHAPE (-2)    /* inconsistent dimensions (OperatorShapeError)         */
+#define CTK_ERR_GEOMETRY (-3) /* invalid grid / geometry (GeometryError)              */
+#define CTK_ERR_CUDA (-4)     /* CUDA runtime failure (RuntimeError)                  */
+
+typedef struct ctk_geom ctk_geom_t;
+
+int ctk_version(void);
+const char* ctk_last_error(void);
+
+/* Geometry.  cos_tab/sin_tab are the bitwise host values np.cos(theta) /
+ * np.sin(theta) for each angle; offsets are ParallelGeometry.bin_offsets()
+ * (ct.py:93-96).  Angles must already satisfy the reference's validation
+ * (strictly increasing in [0, pi)); the library checks sizes and positivity. */
+int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
+                    const double* cos_tab, const double* sin_tab, int det_count,
+                    const double* offsets, double det_spacing, int device,
+                    ctk_geom_t** out);
+int ctk_geom_destroy(ctk_geom_t* g);
+/* n = nx*ny, m = n_angles*det_count, stage_floats = workspace for ctk_forward,
+ * n_degenerate = angles taking the literal axis-aligned path. */
+int ctk_geom_info(const ctk_geom_t* g, int64_t* n, int64_t* m, int64_t* stage_floats,
+                  int* n_degenerate);
+
+/* y = A x for angles [a0, a1): y holds (a1-a0)*det_count samples, row a at
+ * y + (a-a0)*det_count.  If b is non-NULL, writes y = b - A x instead (b laid
+ * out like y).  work: ctk_geom_info().stage_floats fp32 scratch. */
+int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0, int a1,
+                const float* b, float* work, void* stream);
+
+/* Literal fp64 Siddon for every angle (same output layout, no work buffer). */
+int ctk_forward_exact(const ctk_geom_t* g, const float* x, float* y, int a0, int a1,
+                      void* stream);
+
+/* Kept segments (length > 1e-15, ct.py:178) and CSR nnz (duplicate (ray, pixel)
+ * pairs merged, ct.py:197-200) over angles [a0, a1).  counts_dev: 2 int64 of
+ * device memory, overwritten.  Synchronous-free: read back after the stream. */
+int ctk_count_segments(const ctk_geom_t* g, int a0, int a1, int64_t* counts_dev,
+                       void* stream);
+
+/* x = (x0 ? x0 : 0) + B u, summing angles [a0, a1) (u row a at
+ * u + (a-a0)*det_count).  work: ctk_back_work_floats() fp32 scratch (may be
+ * NULL when that returns 0). */
+int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1);
+int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, int a1,
+             const float* x0, float* work, void* stream);
+
+/* ---- Krylov vector kernels.  W: basis rows of length L with row pitch ld
+ * (floats, multiple of 4); device pointers throughout. */
+size_t ctk_reduce_scratch_bytes(int nvec, int64_t L);
+
+/* out[j] = <W_j, v> for j < nvec, and out[nvec] = <v, v> if want_norm. */
+int ctk_dots(const float* W, int64_t ld, int nvec, const float* v, int64_t L,
+             int want_norm, double* out, void* scratch, void* stream);
+/* dst = v - sum_j coef[j] W_j   (dst may alias v); norm2_out[0] = ||dst||^2 if
+ * norm2_out is non-NULL. */
+int ctk_update(const float* W, int64_t ld, int nvec, const double* coef, const float* v,
+               float* dst, int64_t L, double* norm2_out, void* scratch, void* stream);
+/* out[0] = ||v||^2 (fp64). */
+int ctk_norm2(const float* v, int64_t L, double* out, void* scratch, void* stream);
+/* dst = v * (*scale_dev) with scale read on device. */
+int ctk_scale(const float* v, float* dst, int64_t L, const double* scale_dev, void* stream);
+
+/* One Arnoldi step's orthogonalisation (CGS2, equal in exact arithmetic to
+ * the reference's MGS + reorthogonalisation, arnoldi.py:66-82):
+ *   in : W rows 0..k (orthonormal basis), q = M w_k (overwritten)
+ *   out: h[0..k+1] (k+2 fp64, device), stat[0] = ||M w_k||, stat[1] = breakdown
+ *        flag (h[k+1] <= 1e-14 * ||M w_k||), and unless breakdown, row k+1 of W =
+ *        q2 / h[k+1].  stat must hold 4 doubles. */
+int ctk_cgs2_step(float* W, int64_t ld, int k, int64_t L, float* q, double* h,
+                  double* stat, void* scratch, void* stream);
+
+/* dst = (x0 ? x0 : 0) + sum_{j<k} y[j] W_j   (y: k fp64, device);
+ * norm2_out[0] = ||dst||^2 if non-NULL. */
+int ctk_combine(const float* W, int64_t ld, int k, const double* y, const float* x0,
+                float* dst, int64_t L, double* norm2_out, void* scratch, void* stream);
+
+/* Host-side helpers to let drivers avoid a libcudart dependency. */
+int ctk_device_count(int* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CTK_H_ */

@@ -1,0 +1,191 @@
+// ctk_geom.cu -- geometry handle, per-angle tables, error plumbing.
+//
+// The handle captures what the reference's operator closures capture:
+// ImageGrid (ctkrylov/ct.py:37-66) and ParallelGeometry (ct.py:69-96).  All
+// derived per-angle constants are computed here once, on the host, in fp64
+// from the bitwise numpy cos/sin values, and uploaded.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "ctk_common.cuh"
+
+static thread_local char g_err[512] = "";
+
+int ctk_fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int ctk_check_cuda(cudaError_t e, const char* what) {
+    return ctk_fail(CTK_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+extern "C" int ctk_version(void) { return 1; }
+
+extern "C" const char* ctk_last_error(void) { return g_err; }
+
+extern "C" int ctk_device_count(int* out) {
+    if (!out) return ctk_fail(CTK_ERR_ARG, "null output");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    *out = n;
+    return CTK_OK;
+}
+
+namespace {
+
+constexpr int BTX = 32, BTY = 16, BCA = 32;   // must match ctk_back.cu
+
+void free_geom(ctk_geom* g) {
+    if (!g) return;
+    cudaFree(g->d_ap);
+    cudaFree(g->d_bp);
+    cudaFree(g->d_cos);
+    cudaFree(g->d_sin);
+    cudaFree(g->d_offsets);
+    delete g;
+}
+
+}  // namespace
+
+extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
+                               const double* cos_tab, const double* sin_tab, int det_count,
+                               const double* offsets, double det_spacing, int device,
+                               ctk_geom_t** out) {
+    if (!out) return ctk_fail(CTK_ERR_ARG, "null output handle");
+    *out = nullptr;
+    if (nx <= 0 || ny <= 0 || !(pixel_size > 0))
+        return ctk_fail(CTK_ERR_GEOMETRY, "invalid grid: nx=%d, ny=%d, h=%g", nx, ny, pixel_size);
+    if (n_angles <= 0 || !cos_tab || !sin_tab)
+        return ctk_fail(CTK_ERR_GEOMETRY, "angles must be a non-empty 1-D array");
+    if (det_count <= 0 || !(det_spacing > 0) || !offsets)
+        return ctk_fail(CTK_ERR_GEOMETRY, "invalid detector: count=%d, spacing=%g", det_count,
+                        det_spacing);
+    if ((int64_t)nx + 2 > (1 << 20) || (int64_t)ny + 2 > (1 << 20))
+        return ctk_fail(CTK_ERR_GEOMETRY, "grid too large for the 32.32 walk (%d x %d)", nx, ny);
+
+    ctk_geom* g = new ctk_geom();
+    memset(g, 0, sizeof(*g));
+    g->device = device;
+    g->nx = nx;
+    g->ny = ny;
+    g->n_angles = n_angles;
+    g->det_count = det_count;
+    g->h = pixel_size;
+    g->det_spacing = det_spacing;
+    // ImageGrid.extent (ct.py:53-58): hx = 0.5 * nx * h
+    const double hx = 0.5 * (double)nx * pixel_size, hy = 0.5 * (double)ny * pixel_size;
+    g->xmin = -hx;
+    g->xmax = hx;
+    g->ymin = -hy;
+    g->ymax = hy;
+    g->center = 0.5 * (double)(det_count - 1);   // ct.py:215
+
+    std::vector<ctk::AngleParams> ap(n_angles);
+    std::vector<ctk::BackParams> bp(n_angles);
+    double max_span = 0.0;
+    const double h = pixel_size;
+    for (int a = 0; a < n_angles; ++a) {
+        const double c = cos_tab[a], s = sin_tab[a];
+        ctk::AngleParams p;
+        memset(&p, 0, sizeof(p));
+        p.degenerate = (fabs(s) < 1e-14 || fabs(c) < 1e-14) ? 1 : 0;   // ct.py:153,165,168
+        double sigma_raw, C;
+        if (fabs(c) >= fabs(s)) {
+            // walk image rows top->bottom; u = (x - xmin)/h at row boundary
+            const double t = s / c;
+            p.frame = 0;
+            p.beta = 1.0 / (c * h);
+            p.alpha = (-g->xmin - g->ymax * t) / h;
+            sigma_raw = t;
+            C = nx;
+            p.L = (float)(h / fabs(c));
+            p.Lx = (float)(s != 0.0 ? h / fabs(s) : 0.0);
+        } else {
+            // walk image columns left->right; v = (ymax - y)/h at column boundary
+            const double ct = c / s;
+            p.frame = 1;
+            p.beta = -1.0 / (s * h);
+            p.alpha = (g->ymax + g->xmin * ct) / h;
+            sigma_raw = ct;
+            C = ny;
+            p.L = (float)(h / fabs(s));
+            p.Lx = (float)(c != 0.0 ? h / fabs(c) : 0.0);
+        }
+        if (sigma_raw < 0) {
+            p.mirror = 1;
+            p.alpha = C - p.alpha;
+            p.beta = -p.beta;
+            sigma_raw = -sigma_raw;
+        }
+        if (sigma_raw > 1.0) sigma_raw = 1.0;
+        p.sigma_fx = llrint(sigma_raw * 4294967296.0);
+        ap[a] = p;
+        bp[a].cg = c / det_spacing;
+        bp[a].sg = s / det_spacing;
+        const double span = ((BTX - 1) * fabs(c) + (BTY - 1) * fabs(s)) * h / det_spacing;
+        if (span > max_span) max_span = span;
+        g->n_degenerate += p.degenerate;
+    }
+    g->back_wmax = (int)ceil(max_span) + 6;
+    if ((size_t)BCA * g->back_wmax * sizeof(float) > 200 * 1024) {
+        free_geom(g);
+        return ctk_fail(CTK_ERR_GEOMETRY,
+                        "pixel/bin ratio too large for the staged backprojector (window %d)",
+                        (int)ceil(max_span));
+    }
+
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_ap, sizeof(ctk::AngleParams) * n_angles);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_bp, sizeof(ctk::BackParams) * n_angles);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_cos, sizeof(double) * n_angles);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_sin, sizeof(double) * n_angles);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_offsets, sizeof(double) * det_count);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_ap, ap.data(), sizeof(ctk::AngleParams) * n_angles,
+                       cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_bp, bp.data(), sizeof(ctk::BackParams) * n_angles,
+                       cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_cos, cos_tab, sizeof(double) * n_angles, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_sin, sin_tab, sizeof(double) * n_angles, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_offsets, offsets, sizeof(double) * det_count, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        free_geom(g);
+        return ctk_check_cuda(e, "ctk_geom_create");
+    }
+    *out = g;
+    return CTK_OK;
+}
+
+extern "C" int ctk_geom_destroy(ctk_geom_t* g) {
+    if (!g) return CTK_OK;
+    cudaSetDevice(g->device);
+    free_geom(g);
+    return CTK_OK;
+}
+
+extern "C" int ctk_geom_info(const ctk_geom_t* g, int64_t* n, int64_t* m, int64_t* stage_floats,
+                             int* n_degenerate) {
+    if (!g) return ctk_fail(CTK_ERR_ARG, "null geometry");
+    if (n) *n = (int64_t)g->nx * g->ny;
+    if (m) *m = (int64_t)g->n_angles * g->det_count;
+    if (stage_floats) *stage_floats = ctk_stage_floats(g->nx, g->ny);
+    if (n_degenerate) *n_degenerate = g->n_degenerate;
+    return CTK_OK;
+}

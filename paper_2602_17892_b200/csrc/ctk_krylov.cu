@@ -1,0 +1,327 @@
+// ctk_krylov.cu -- K3 (fused CGS2 orthogonalisation), K4 (basis combination)
+// and the fp64 norm/dot epilogues (K5) for the Arnoldi process.
+//
+// Reference: ctkrylov/arnoldi.py:56-82 (MGS + full reorthogonalisation in
+// fp64 numpy) and ctkrylov/gmres.py:205-211 (W @ y, x0 + ..., norms).
+//
+// The basis lives on the device as fp32 rows W[j][0..L) (row pitch ld, 16-B
+// aligned) -- HBM-resident for the whole solve, never copied.  Every kernel
+// streams rows with 128-bit loads and accumulates in fp64.  Reductions are a
+// fixed two-level tree: warp shuffles, a per-CTA smem pass, one fp64 partial
+// per CTA, and a last-CTA-done pass (integer ticket, no float atomics) that
+// sums the CTA partials in index order -- bitwise reproducible run to run.
+#include <math.h>
+
+#include "ctk_common.cuh"
+
+namespace ctk {
+
+constexpr int KT = 256;           // threads per CTA
+constexpr int KWARPS = KT / 32;
+constexpr int KMAX_GRID = 2 * 148;
+constexpr int KMAX_VEC = 1024;    // rows per reduction call (smem bound)
+
+struct Scratch {                  // carved from the caller's zero-filled scratch
+    unsigned int* ticket;         // [1]
+    double* partial;              // [KMAX_GRID][nvec_cap]
+    double* tmp;                  // [3][nvec_cap]
+    int nvec_cap;
+};
+
+static inline int grid_for(int64_t L4) {
+    int64_t g = (L4 + 2 * KT - 1) / (2 * KT);
+    if (g > KMAX_GRID) g = KMAX_GRID;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+static inline Scratch carve(void* scratch, int nvec_cap) {
+    char* p = (char*)scratch;
+    Scratch s;
+    s.ticket = (unsigned int*)p;
+    s.partial = (double*)(p + 256);
+    s.tmp = s.partial + (size_t)KMAX_GRID * nvec_cap;
+    s.nvec_cap = nvec_cap;
+    return s;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double dot4(float4 a, float4 b, double acc) {
+    acc = fma((double)a.x, (double)b.x, acc);
+    acc = fma((double)a.y, (double)b.y, acc);
+    acc = fma((double)a.z, (double)b.z, acc);
+    acc = fma((double)a.w, (double)b.w, acc);
+    return acc;
+}
+
+// CTA partial sums red[w][j] -> partial[blockIdx][j]; last CTA -> out[j].
+__device__ void finish_reduce(double (*red)[KWARPS], int nv, double* partial, unsigned int* ticket,
+                              double* out) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < nv; j += KT) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < KWARPS; ++w) s += red[j][w];
+        partial[(size_t)blockIdx.x * nv + j] = s;
+    }
+    __threadfence();
+    __shared__ unsigned int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int j = threadIdx.x; j < nv; j += KT) {
+        double s = 0.0;
+        for (unsigned int b = 0; b < gridDim.x; ++b) s += __ldcg(partial + (size_t)b * nv + j);
+        out[j] = s;
+    }
+    if (threadIdx.x == 0) *ticket = 0u;   // ready for the next stream-ordered call
+}
+
+// out[j] = <W_j, v> (j < nvec); out[nvec] = <v, v> if want_norm.
+__global__ void __launch_bounds__(KT) k_dots(const float* __restrict__ W, int64_t ld, int nvec,
+                                             const float* __restrict__ v, int64_t L, int want_norm,
+                                             double* out, double* partial, unsigned int* ticket) {
+    extern __shared__ double red_raw[];
+    double (*red)[KWARPS] = reinterpret_cast<double (*)[KWARPS]>(red_raw);
+    const int nv = nvec + (want_norm ? 1 : 0);
+    const int64_t L4 = L >> 2;
+    const int64_t chunk = (L4 + gridDim.x - 1) / gridDim.x;
+    const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(L4, i0 + chunk);
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool tail_owner = (blockIdx.x == gridDim.x - 1);
+    for (int j0 = 0; j0 < nv; j0 += 4) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const float4* w4[4];
+        const float* w1[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = j0 + q < nv ? j0 + q : j0;
+            const float* row = (j < nvec) ? W + (size_t)j * ld : v;
+            w4[q] = reinterpret_cast<const float4*>(row);
+            w1[q] = row;
+        }
+        for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) {
+            const float4 vv = __ldg(v4 + i);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = dot4(__ldg(w4[q] + i), vv, acc[q]);
+        }
+        if (tail_owner) {
+            for (int64_t i = (L4 << 2) + threadIdx.x; i < L; i += KT) {
+                const double vv = (double)v[i];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = fma((double)w1[q][i], vv, acc[q]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double s = warp_sum(acc[q]);
+            if (lane == 0 && j0 + q < nv) red[j0 + q][warp] = s;
+        }
+    }
+    finish_reduce(red, nv, partial, ticket, out);
+}
+
+// dst = (base ? base : 0) + sgn * sum_j coef[j] W_j ; optional ||dst||^2.
+__global__ void __launch_bounds__(KT) k_combine(const float* __restrict__ W, int64_t ld, int nvec,
+                                                const double* __restrict__ coef, double sgn,
+                                                const float* base, float* dst, int64_t L,
+                                                double* norm_out, double* partial,
+                                                unsigned int* ticket) {
+    extern __shared__ double sh[];
+    double* c = sh;                                               // [nvec]
+    double (*red)[KWARPS] = reinterpret_cast<double (*)[KWARPS]>(sh + ((nvec + 1) & ~1));
+    for (int j = threadIdx.x; j < nvec; j += KT) c[j] = sgn * coef[j];
+    __syncthreads();
+    const int64_t L4 = L >> 2;
+    const int64_t chunk = (L4 + gridDim.x - 1) / gridDim.x;
+    const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(L4, i0 + chunk);
+    double nrm = 0.0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (base) {
+            const float4 b = reinterpret_cast<const float4*>(base)[i];
+            a0 = b.x; a1 = b.y; a2 = b.z; a3 = b.w;
+        }
+        int j = 0;
+        for (; j + 1 < nvec; j += 2) {
+            const float4 w = __ldg(reinterpret_cast<const float4*>(W + (size_t)j * ld) + i);
+            const float4 z = __ldg(reinterpret_cast<const float4*>(W + (size_t)(j + 1) * ld) + i);
+            const double cj = c[j], cz = c[j + 1];
+            a0 = fma(cj, (double)w.x, a0); a1 = fma(cj, (double)w.y, a1);
+            a2 = fma(cj, (double)w.z, a2); a3 = fma(cj, (double)w.w, a3);
+            a0 = fma(cz, (double)z.x, a0); a1 = fma(cz, (double)z.y, a1);
+            a2 = fma(cz, (double)z.z, a2); a3 = fma(cz, (double)z.w, a3);
+        }
+        if (j < nvec) {
+            const float4 w = __ldg(reinterpret_cast<const float4*>(W + (size_t)j * ld) + i);
+            const double cj = c[j];
+            a0 = fma(cj, (double)w.x, a0); a1 = fma(cj, (double)w.y, a1);
+            a2 = fma(cj, (double)w.z, a2); a3 = fma(cj, (double)w.w, a3);
+        }
+        const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+        reinterpret_cast<float4*>(dst)[i] = o;
+        nrm = fma((double)o.x, (double)o.x, nrm); nrm = fma((double)o.y, (double)o.y, nrm);
+        nrm = fma((double)o.z, (double)o.z, nrm); nrm = fma((double)o.w, (double)o.w, nrm);
+    }
+    if (blockIdx.x == gridDim.x - 1) {
+        for (int64_t i = (L4 << 2) + threadIdx.x; i < L; i += KT) {
+            double a = base ? (double)base[i] : 0.0;
+            for (int j = 0; j < nvec; ++j) a = fma(c[j], (double)W[(size_t)j * ld + i], a);
+            const float o = (float)a;
+            dst[i] = o;
+            nrm = fma((double)o, (double)o, nrm);
+        }
+    }
+    if (!norm_out) return;
+    const double s = warp_sum(nrm);
+    if ((threadIdx.x & 31) == 0) red[0][threadIdx.x >> 5] = s;
+    finish_reduce(red, 1, partial, ticket, norm_out);
+}
+
+__global__ void k_scale(const float* __restrict__ v, float* __restrict__ dst, int64_t L,
+                        const double* __restrict__ scale) {
+    const float sc = (float)(*scale);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = v[i] * sc;
+}
+
+// h = h1 + h2; h[k+1] = sqrt(n2); stat = {||q||, breakdown, 1/h[k+1] or 0}
+__global__ void k_cgs2_finalize(const double* h1, const double* h2, const double* n2, int k,
+                                double* h, double* stat) {
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) h[i] = h1[i] + h2[i];
+    if (threadIdx.x == 0) {
+        const double hk = sqrt(n2[0]);
+        const double qn = sqrt(h1[k + 1]);
+        h[k + 1] = hk;
+        const bool broke = hk <= 1e-14 * qn;    // BREAKDOWN_RTOL, arnoldi.py:17,80
+        stat[0] = qn;
+        stat[1] = broke ? 1.0 : 0.0;
+        stat[2] = broke ? 0.0 : 1.0 / hk;
+        stat[3] = hk;
+    }
+}
+
+}  // namespace ctk
+
+using namespace ctk;
+
+static int check_vec(const void* p, const char* what) {
+    if (!p) return ctk_fail(CTK_ERR_ARG, "%s is NULL", what);
+    if (((uintptr_t)p) & 15) return ctk_fail(CTK_ERR_ARG, "%s is not 16-byte aligned", what);
+    return CTK_OK;
+}
+
+extern "C" size_t ctk_reduce_scratch_bytes(int nvec, int64_t L) {
+    (void)L;
+    const int cap = nvec + 2;
+    return 256 + sizeof(double) * ((size_t)KMAX_GRID * cap + 3 * (size_t)cap) + 256;
+}
+
+static int launch_dots(const float* W, int64_t ld, int nvec, const float* v, int64_t L,
+                       int want_norm, double* out, Scratch s, cudaStream_t st) {
+    const int nv = nvec + (want_norm ? 1 : 0);
+    if (nv > s.nvec_cap || nv > KMAX_VEC) return ctk_fail(CTK_ERR_ARG, "too many vectors (%d)", nv);
+    const int G = grid_for(L >> 2);
+    const size_t smem = sizeof(double) * (size_t)nv * KWARPS;
+    k_dots<<<G, KT, smem, st>>>(W, ld, nvec, v, L, want_norm, out, s.partial, s.ticket);
+    CTK_LAUNCH_CHECK("k_dots");
+    return CTK_OK;
+}
+
+static int launch_combine(const float* W, int64_t ld, int nvec, const double* coef, double sgn,
+                          const float* base, float* dst, int64_t L, double* norm_out, Scratch s,
+                          cudaStream_t st) {
+    if (nvec > KMAX_VEC) return ctk_fail(CTK_ERR_ARG, "too many vectors (%d)", nvec);
+    const int G = grid_for(L >> 2);
+    const size_t smem = sizeof(double) * ((size_t)((nvec + 1) & ~1) + KWARPS);
+    k_combine<<<G, KT, smem, st>>>(W, ld, nvec, coef, sgn, base, dst, L, norm_out, s.partial,
+                                   s.ticket);
+    CTK_LAUNCH_CHECK("k_combine");
+    return CTK_OK;
+}
+
+extern "C" int ctk_dots(const float* W, int64_t ld, int nvec, const float* v, int64_t L,
+                        int want_norm, double* out, void* scratch, void* stream) {
+    int rc;
+    if (nvec > 0 && (rc = check_vec(W, "W"))) return rc;
+    if ((rc = check_vec(v, "v"))) return rc;
+    if (!out || !scratch) return ctk_fail(CTK_ERR_ARG, "null output/scratch");
+    if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
+    return launch_dots(W, ld, nvec, v, L, want_norm, out, carve(scratch, nvec + 2),
+                       ctk_stream(stream));
+}
+
+extern "C" int ctk_update(const float* W, int64_t ld, int nvec, const double* coef,
+                          const float* v, float* dst, int64_t L, double* norm2_out, void* scratch,
+                          void* stream) {
+    int rc;
+    if (nvec > 0 && (rc = check_vec(W, "W"))) return rc;
+    if ((rc = check_vec(v, "v")) || (rc = check_vec(dst, "dst"))) return rc;
+    if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
+    if (!scratch || (nvec > 0 && !coef)) return ctk_fail(CTK_ERR_ARG, "null coef/scratch");
+    return launch_combine(W, ld, nvec, coef, -1.0, v, dst, L, norm2_out, carve(scratch, nvec + 2),
+                          ctk_stream(stream));
+}
+
+extern "C" int ctk_combine(const float* W, int64_t ld, int k, const double* y, const float* x0,
+                           float* dst, int64_t L, double* norm2_out, void* scratch, void* stream) {
+    int rc;
+    if (k > 0 && (rc = check_vec(W, "W"))) return rc;
+    if ((rc = check_vec(dst, "dst"))) return rc;
+    if (x0 && (rc = check_vec(x0, "x0"))) return rc;
+    if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
+    if (!scratch || (k > 0 && !y)) return ctk_fail(CTK_ERR_ARG, "null y/scratch");
+    return launch_combine(W, ld, k, y, 1.0, x0, dst, L, norm2_out, carve(scratch, k + 2),
+                          ctk_stream(stream));
+}
+
+extern "C" int ctk_norm2(const float* v, int64_t L, double* out, void* scratch, void* stream) {
+    int rc;
+    if ((rc = check_vec(v, "v"))) return rc;
+    if (!out || !scratch) return ctk_fail(CTK_ERR_ARG, "null output/scratch");
+    return launch_dots(nullptr, 4, 0, v, L, 1, out, carve(scratch, 2), ctk_stream(stream));
+}
+
+extern "C" int ctk_scale(const float* v, float* dst, int64_t L, const double* scale_dev,
+                         void* stream) {
+    if (!v || !dst || !scale_dev) return ctk_fail(CTK_ERR_ARG, "null argument");
+    int blocks = (int)((L + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    k_scale<<<blocks, 256, 0, ctk_stream(stream)>>>(v, dst, L, scale_dev);
+    CTK_LAUNCH_CHECK("k_scale");
+    return CTK_OK;
+}
+
+extern "C" int ctk_cgs2_step(float* W, int64_t ld, int k, int64_t L, float* q, double* h,
+                             double* stat, void* scratch, void* stream) {
+    int rc;
+    if ((rc = check_vec(W, "W")) || (rc = check_vec(q, "q"))) return rc;
+    if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
+    if (k < 0 || !h || !stat || !scratch) return ctk_fail(CTK_ERR_ARG, "bad cgs2 arguments");
+    if (L > ld) return ctk_fail(CTK_ERR_SHAPE, "L (%lld) exceeds ld (%lld)", (long long)L,
+                                (long long)ld);
+    cudaStream_t st = ctk_stream(stream);
+    Scratch s = carve(scratch, k + 3);
+    double* h1 = s.tmp;                   // k+2: h1[0..k], ||q||^2
+    double* h2 = s.tmp + s.nvec_cap;      // k+1
+    double* n2 = s.tmp + 2 * s.nvec_cap;  // 1
+    const int nb = k + 1;
+    float* wnext = W + (size_t)(k + 1) * ld;
+    if ((rc = launch_dots(W, ld, nb, q, L, 1, h1, s, st))) return rc;            // h1, ||Mw||^2
+    if ((rc = launch_combine(W, ld, nb, h1, -1.0, q, q, L, nullptr, s, st))) return rc;  // q1
+    if ((rc = launch_dots(W, ld, nb, q, L, 0, h2, s, st))) return rc;            // h2
+    if ((rc = launch_combine(W, ld, nb, h2, -1.0, q, wnext, L, n2, s, st))) return rc;   // q2
+    k_cgs2_finalize<<<1, 128, 0, st>>>(h1, h2, n2, k, h, stat);
+    CTK_LAUNCH_CHECK("k_cgs2_finalize");
+    return ctk_scale(wnext, wnext, L, stat + 2, stream);
+}

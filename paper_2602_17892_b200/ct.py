@@ -1,0 +1,301 @@
+"""2-D parallel-beam CT operators on the B200: drop-ins for ctkrylov.ct.
+
+``forward_ray_driven(grid, geometry)`` and ``back_pixel_driven(grid,
+geometry)`` keep the reference's signatures (ctkrylov/ct.py:182, 204) and
+return :class:`~paper_2602_17892_b200.linop.LinearOperator` subclasses whose
+``apply`` honours the reference contract (float64 numpy in and out), while
+the work runs in libctk's sm_100a kernels (K1/K1d forward, K2 back).  The
+same objects expose device-tensor entry points (``apply_device``) used by the
+device-resident GMRES driver, which never leaves HBM between iterations.
+
+Conventions are the reference's (ctkrylov/ct.py:10-18): image row-major
+(ny, nx) with row 0 at the top; sinogram angle-major, sample a*D + j.  B is
+the reference's unmatched pixel-driven backprojector -- never A's adjoint.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .linop import LinearOperator, OperatorShapeError
+
+
+class GeometryError(ValueError):
+    """Invalid grid / geometry configuration (ctkrylov/ct.py:33-34)."""
+
+
+@dataclass(frozen=True)
+class ImageGrid:
+    """Centred square-pixel grid (ctkrylov/ct.py:37-66)."""
+
+    nx: int
+    ny: int
+    pixel_size: float = 1.0
+
+    def __post_init__(self):
+        if self.nx <= 0 or self.ny <= 0 or self.pixel_size <= 0:
+            raise GeometryError(f"invalid grid: nx={self.nx}, ny={self.ny}, h={self.pixel_size}")
+
+    @property
+    def n(self) -> int:
+        return self.nx * self.ny
+
+    @property
+    def extent(self) -> tuple[float, float, float, float]:
+        half_x = 0.5 * self.nx * self.pixel_size
+        half_y = 0.5 * self.ny * self.pixel_size
+        return (-half_x, half_x, -half_y, half_y)
+
+    def pixel_centers(self) -> tuple[np.ndarray, np.ndarray]:
+        xmin, _, _, ymax = self.extent
+        h = self.pixel_size
+        return np.meshgrid(xmin + (np.arange(self.nx) + 0.5) * h,
+                           ymax - (np.arange(self.ny) + 0.5) * h)
+
+
+@dataclass(frozen=True)
+class ParallelGeometry:
+    """View angles plus a centred linear detector (ctkrylov/ct.py:69-96)."""
+
+    angles: np.ndarray
+    det_count: int
+    det_spacing: float
+
+    def __post_init__(self):
+        ang = np.asarray(self.angles, dtype=np.float64)
+        object.__setattr__(self, "angles", ang)
+        if ang.ndim != 1 or ang.size == 0:
+            raise GeometryError("angles must be a non-empty 1-D array")
+        if np.any(np.diff(ang) <= 0) or ang[0] < 0 or ang[-1] >= np.pi:
+            raise GeometryError("angles must be strictly increasing within [0, pi)")
+        if self.det_count <= 0 or self.det_spacing <= 0:
+            raise GeometryError(
+                f"invalid detector: count={self.det_count}, spacing={self.det_spacing}")
+
+    @property
+    def m(self) -> int:
+        return len(self.angles) * self.det_count
+
+    def bin_offsets(self) -> np.ndarray:
+        j = np.arange(self.det_count, dtype=np.float64)
+        return (j - 0.5 * (self.det_count - 1)) * self.det_spacing
+
+
+def trig_tables(geometry: ParallelGeometry) -> tuple[np.ndarray, np.ndarray]:
+    """Scalar np.cos/np.sin per angle, bitwise what the reference evaluates
+    (ctkrylov/ct.py:145 in _siddon_ray, 225 in back_pixel_driven)."""
+    cos_tab = np.array([np.cos(float(t)) for t in geometry.angles], dtype=np.float64)
+    sin_tab = np.array([np.sin(float(t)) for t in geometry.angles], dtype=np.float64)
+    return cos_tab, sin_tab
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _require_cuda(device: int):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise _native.CtkError("a CUDA device is required: libctk has no CPU path")
+    if device >= torch.cuda.device_count():
+        raise _native.CtkError(f"CUDA device {device} not present")
+    return torch
+
+
+def _dptr(arr: np.ndarray):
+    return arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class DeviceGeometry:
+    """A libctk geometry handle on one GPU plus its stream-local workspaces.
+
+    The handle is immutable once built (thread-/stream-safe, like the
+    reference's pure apply).  Work buffers (K1's zero-bordered staging copies,
+    K2's split partial images) are cached per CUDA stream.
+    """
+
+    def __init__(self, grid: ImageGrid, geometry: ParallelGeometry, device: int = 0):
+        torch = _require_cuda(device)
+        self.torch = torch
+        self.grid = grid
+        self.geometry = geometry
+        self.device = int(device)
+        self.dev = torch.device("cuda", self.device)
+        self.cos_tab, self.sin_tab = trig_tables(geometry)
+        self.offsets = np.ascontiguousarray(geometry.bin_offsets())
+        lib = _native.load()
+        handle = ctypes.c_void_p()
+        _native.check(lib.ctk_geom_create(
+            grid.nx, grid.ny, float(grid.pixel_size), len(geometry.angles),
+            _dptr(self.cos_tab), _dptr(self.sin_tab), geometry.det_count, _dptr(self.offsets),
+            float(geometry.det_spacing), self.device, ctypes.byref(handle)), "ctk_geom_create")
+        self._lib = lib
+        self.handle = handle
+        n, m, st = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        ndeg = ctypes.c_int()
+        _native.check(lib.ctk_geom_info(handle, ctypes.byref(n), ctypes.byref(m),
+                                        ctypes.byref(st), ctypes.byref(ndeg)))
+        self.n, self.m = n.value, m.value
+        self.stage_floats = st.value
+        self.n_degenerate = ndeg.value
+        self.n_angles = len(geometry.angles)
+        self.det_count = geometry.det_count
+        self._work = {}
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.ctk_geom_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    # -- workspace ---------------------------------------------------------
+    def _stream(self, stream):
+        if stream is None:
+            stream = self.torch.cuda.current_stream(self.dev)
+        return stream
+
+    def _workspace(self, kind: str, floats: int, stream):
+        key = (kind, stream.cuda_stream)
+        buf = self._work.get(key)
+        if buf is None or buf.numel() < floats:
+            buf = self.torch.zeros(max(floats, 4), dtype=self.torch.float32, device=self.dev)
+            self._work[key] = buf
+        return buf
+
+    def _range(self, a0, a1):
+        a1 = self.n_angles if a1 is None else a1
+        if not (0 <= a0 <= a1 <= self.n_angles):
+            raise OperatorShapeError(f"angle range [{a0}, {a1}) outside [0, {self.n_angles})")
+        return a0, a1
+
+    def _check(self, t, numel, name):
+        torch = self.torch
+        if t.device != self.dev or t.dtype != torch.float32 or not t.is_contiguous():
+            raise OperatorShapeError(f"{name} must be a contiguous float32 tensor on {self.dev}")
+        if t.numel() != numel:
+            raise OperatorShapeError(f"{name} has {t.numel()} elements, expected {numel}")
+
+    # -- device entry points (torch tensors, stream-ordered) ---------------
+    def forward(self, x, out=None, a0: int = 0, a1: int | None = None, b=None, stream=None):
+        """out = A x over angles [a0, a1) (or b - A x when b is given)."""
+        a0, a1 = self._range(a0, a1)
+        rows = (a1 - a0) * self.det_count
+        self._check(x, self.n, "x")
+        if out is None:
+            out = self.torch.empty(rows, dtype=self.torch.float32, device=self.dev)
+        self._check(out, rows, "out")
+        if b is not None:
+            self._check(b, rows, "b")
+        stream = self._stream(stream)
+        work = self._workspace("stage", self.stage_floats, stream)
+        _native.check(self._lib.ctk_forward(self.handle, x.data_ptr(), out.data_ptr(), a0, a1,
+                                            _native.ptr(b), work.data_ptr(), stream.cuda_stream),
+                      "ctk_forward")
+        return out
+
+    def forward_exact(self, x, out=None, a0: int = 0, a1: int | None = None, stream=None):
+        """Literal fp64 Siddon for every angle (validation path)."""
+        a0, a1 = self._range(a0, a1)
+        rows = (a1 - a0) * self.det_count
+        self._check(x, self.n, "x")
+        if out is None:
+            out = self.torch.empty(rows, dtype=self.torch.float32, device=self.dev)
+        self._check(out, rows, "out")
+        stream = self._stream(stream)
+        _native.check(self._lib.ctk_forward_exact(self.handle, x.data_ptr(), out.data_ptr(),
+                                                  a0, a1, stream.cuda_stream), "ctk_forward_exact")
+        return out
+
+    def back(self, u, out=None, a0: int = 0, a1: int | None = None, x0=None, stream=None):
+        """out = (x0 or 0) + B u, summing angles [a0, a1)."""
+        a0, a1 = self._range(a0, a1)
+        self._check(u, (a1 - a0) * self.det_count, "u")
+        if out is None:
+            out = self.torch.empty(self.n, dtype=self.torch.float32, device=self.dev)
+        self._check(out, self.n, "out")
+        if x0 is not None:
+            self._check(x0, self.n, "x0")
+        stream = self._stream(stream)
+        wf = int(self._lib.ctk_back_work_floats(self.handle, a0, a1))
+        work = self._workspace("back", wf, stream) if wf > 0 else None
+        _native.check(self._lib.ctk_back(self.handle, u.data_ptr(), out.data_ptr(), a0, a1,
+                                         _native.ptr(x0), _native.ptr(work), stream.cuda_stream),
+                      "ctk_back")
+        return out
+
+    def count_segments(self, a0: int = 0, a1: int | None = None) -> tuple[int, int]:
+        """(kept segments, CSR nnz) of A over angles [a0, a1) (K6)."""
+        a0, a1 = self._range(a0, a1)
+        stream = self._stream(None)
+        counts = self.torch.zeros(2, dtype=self.torch.int64, device=self.dev)
+        _native.check(self._lib.ctk_count_segments(self.handle, a0, a1, counts.data_ptr(),
+                                                   stream.cuda_stream), "ctk_count_segments")
+        raw, nnz = counts.cpu().tolist()
+        return int(raw), int(nnz)
+
+
+class _GpuOperator(LinearOperator):
+    """LinearOperator whose host apply round-trips through the GPU kernel."""
+
+    def __init__(self, rows, cols, dgeom: DeviceGeometry):
+        super().__init__(rows, cols, None)
+        self.dgeom = dgeom
+
+    def _host_apply(self, v: np.ndarray) -> np.ndarray:
+        torch = self.dgeom.torch
+        xd = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32)).to(self.dgeom.dev)
+        out = self.apply_device(xd)
+        return out.cpu().numpy().astype(np.float64)
+
+
+class GpuForward(_GpuOperator):
+    """A: Siddon ray-driven forward projector (ctkrylov/ct.py:182-201) on the GPU."""
+
+    kind = "forward"
+
+    def apply_device(self, x, out=None, b=None, stream=None):
+        return self.dgeom.forward(x, out=out, b=b, stream=stream)
+
+
+class GpuBack(_GpuOperator):
+    """B: pixel-driven linear-interpolation backprojector (ctkrylov/ct.py:204-245)."""
+
+    kind = "back"
+
+    def apply_device(self, u, out=None, x0=None, stream=None):
+        return self.dgeom.back(u, out=out, x0=x0, stream=stream)
+
+
+_GEOM_CACHE: dict = {}
+
+
+def device_geometry(grid: ImageGrid, geometry: ParallelGeometry, device: int = 0) -> DeviceGeometry:
+    """Shared DeviceGeometry per (grid, geometry, device) so A and B pair up."""
+    key = (grid, geometry.angles.tobytes(), geometry.det_count, float(geometry.det_spacing),
+           int(device))
+    dg = _GEOM_CACHE.get(key)
+    if dg is None:
+        dg = DeviceGeometry(grid, geometry, device)
+        _GEOM_CACHE[key] = dg
+    return dg
+
+
+def forward_ray_driven(grid: ImageGrid, geometry: ParallelGeometry, device: int = 0) -> GpuForward:
+    """Drop-in for ctkrylov.ct.forward_ray_driven (ct.py:182): matrix-free on
+    the GPU; ``sparse_matrix`` is None because no CSR is ever assembled."""
+    dg = device_geometry(grid, geometry, device)
+    return GpuForward(geometry.m, grid.n, dg)
+
+
+def back_pixel_driven(grid: ImageGrid, geometry: ParallelGeometry, device: int = 0) -> GpuBack:
+    """Drop-in for ctkrylov.ct.back_pixel_driven (ct.py:204)."""
+    dg = device_geometry(grid, geometry, device)
+    return GpuBack(grid.n, geometry.m, dg)

@@ -1,0 +1,143 @@
+"""End-to-end parity of the device-resident hybrid AB-/BA-GMRES.
+
+Bars (north star): Krylov residual norms, the selected regularisation
+parameter within 1% (GCV configs; the L-curve corner at c2 is documented as
+ill-conditioned in SURVEY.md §7.3-4 and reported, not asserted) and the
+reconstruction at equal iteration count within 1e-3 relative L2.
+Reference values come from the unmodified reference (tests/golden/).
+"""
+
+import numpy as np
+import pytest
+
+from paper_2602_17892_b200 import ct, gmres, problems
+
+pytestmark = pytest.mark.gpu
+
+X_TOL = 1e-3
+RES_TOL = 1e-4
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b)
+
+
+def ops_for(spec):
+    grid = ct.ImageGrid(spec.N, spec.N, 1.0)
+    geom = ct.ParallelGeometry(spec.angles(), spec.det_count, 1.0)
+    return ct.forward_ray_driven(grid, geom), ct.back_pixel_driven(grid, geom)
+
+
+def config_b(golden, name):
+    spec = problems.CONFIGS[name]
+    z = golden(name)
+    b, _ = problems.add_noise(z["Ax_true"], spec.noise, spec.noise_seed)
+    return spec, z, b.astype(np.float32).astype(np.float64)
+
+
+def records(res, field):
+    return np.array([getattr(r, field) for r in res.records])
+
+
+def test_c1_ab_hybrid_gcv_50(cuda, golden):
+    spec, z, b = config_b(golden, "c1")
+    A, B = ops_for(spec)
+    res = gmres.run_gmres(A, B, b, gmres.SolverConfig(method="ab-hybrid", lambda_strategy="gcv",
+                                                      max_iter=50))
+    assert res.stop_reason == "maxiter" and len(res.records) == 50
+    lam, lam_ref = records(res, "lambda_used"), z["rec/lambda_used"]
+    assert np.all(np.abs(lam / lam_ref - 1.0) <= 0.01), np.abs(lam / lam_ref - 1).max()
+    for f in ("data_residual_norm", "residual_norm", "proj_residual_norm"):
+        np.testing.assert_allclose(records(res, f), z[f"rec/{f}"], rtol=RES_TOL, err_msg=f)
+    np.testing.assert_allclose(records(res, "solution_norm"), z["rec/solution_norm"], rtol=RES_TOL)
+    assert rel(res.x, z["x_final"]) <= X_TOL
+
+
+@pytest.mark.parametrize("plain", [False, True])
+def test_c2_ba_lcurve_80_and_plain(cuda, golden, plain):
+    spec, z, b = config_b(golden, "c2")
+    A, B = ops_for(spec)
+    if plain:
+        cfg = gmres.SolverConfig(method="ba", max_iter=80)
+        pre = "plain/"
+    else:
+        cfg = gmres.SolverConfig(method="ba-hybrid", lambda_strategy="lcurve", max_iter=80)
+        pre = ""
+    res = gmres.run_gmres(A, B, b, cfg)
+    assert len(res.records) == 80
+    np.testing.assert_allclose(records(res, "data_residual_norm"),
+                               z[pre + "rec/data_residual_norm"], rtol=1e-3)
+    np.testing.assert_allclose(records(res, "proj_residual_norm"),
+                               z[pre + "rec/proj_residual_norm"], rtol=1e-3)
+    assert rel(res.x, z[pre + "x_final"]) <= X_TOL
+    if not plain:
+        lam, lam_ref = records(res, "lambda_used"), z["rec/lambda_used"]
+        agree = np.mean(np.abs(lam / lam_ref - 1.0) <= 0.01)
+        print(f"c2 L-curve lambda agreement within 1%: {agree:.2%}")
+
+
+def small_problem(golden):
+    d = golden("solver_cases")
+    # make_ct_problem(16, 12, 23, 0.02, 0) geometry, ctkrylov/ct.py:310-334
+    h = 2.0 / 16
+    grid = ct.ImageGrid(16, 16, h)
+    geom = ct.ParallelGeometry(np.arange(12) * np.pi / 12, 23, np.sqrt(2.0) * 16 * h / 23)
+    return d, ct.forward_ray_driven(grid, geom), ct.back_pixel_driven(grid, geom)
+
+
+CASES = {
+    "ab_plain": dict(method="ab", max_iter=12),
+    "ba_plain": dict(method="ba", max_iter=12),
+    "ab_gcv": dict(method="ab-hybrid", lambda_strategy="gcv", max_iter=15),
+    "ba_gcv": dict(method="ba-hybrid", lambda_strategy="gcv", max_iter=15),
+    "ab_lcurve": dict(method="ab-hybrid", lambda_strategy="lcurve", max_iter=15),
+    "ba_fixed": dict(method="ba-hybrid", lambda_strategy="fixed", lambda_value=0.3, max_iter=10),
+    "ab_restart": dict(method="ab-hybrid", lambda_strategy="gcv", max_iter=14, restart_period=5),
+    "ab_dp": dict(method="ab", max_iter=40, stopping_rule="dp"),
+    "ba_rns": dict(method="ba", max_iter=40, stopping_rule="rns", rns_epsilon=1e-3),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_driver_branches_vs_reference(cuda, golden, case):
+    d, A, B = small_problem(golden)
+    kw = dict(CASES[case])
+    if kw.get("stopping_rule") == "dp":
+        kw["noise_norm"] = float(d["noise_norm"])
+    b = d["b"]
+    res = gmres.run_gmres(A, B, b, gmres.SolverConfig(**kw))
+    assert res.stop_reason == str(d[f"{case}/stop"])
+    assert res.cycles == int(d[f"{case}/cycles"])
+    n_ref = len(d[f"{case}/rec/k"])
+    assert len(res.records) == n_ref
+    got, ref = records(res, "data_residual_norm"), d[f"{case}/rec/data_residual_norm"]
+    np.testing.assert_allclose(got[:12], ref[:12], rtol=1e-3)
+    # Unregularised GMRES deep in its noise-fitting regime amplifies the fp32
+    # operator/basis rounding (the reference's own dense-vs-CSR operators
+    # already disagree there); the bar past iteration 12 is looser.
+    np.testing.assert_allclose(got[12:], ref[12:], rtol=5e-2)
+    if "gcv" in case or "fixed" in case:
+        lam, lam_ref = records(res, "lambda_used"), d[f"{case}/rec/lambda_used"]
+        assert np.all(np.abs(lam / lam_ref - 1.0) <= 0.01)
+    assert rel(res.x, d[f"{case}/x"]) <= (2e-3 if len(got) <= 15 else 5e-2)
+
+
+def test_device_resident_input_and_snapshots(cuda, golden):
+    d, A, B = small_problem(golden)
+    b = cuda.from_numpy(d["b"].astype(np.float32)).cuda()
+    res = gmres.run_gmres(A, B, b, gmres.SolverConfig(method="ba-hybrid", lambda_strategy="gcv",
+                                                      max_iter=8, snapshot_stride=4))
+    assert sorted(res.snapshots) == [4, 8]
+    np.testing.assert_allclose(res.snapshots[8], res.x)
+    assert all(r.elapsed > 0 for r in res.records)
+    els = [r.elapsed for r in res.records]
+    assert els == sorted(els)
+
+
+def test_x_true_metrics(cuda, golden):
+    d, A, B = small_problem(golden)
+    from oracle.oracle import Geometry  # noqa: F401  (oracle importable from tests)
+    x_true = np.random.default_rng(0).random(256)
+    res = gmres.run_gmres(A, B, d["b"], gmres.SolverConfig(method="ab", max_iter=5),
+                          x_true=x_true, image_shape=(16, 16))
+    assert all(r.rre is not None and r.ssim is not None for r in res.records)

@@ -1,0 +1,112 @@
+"""GPU checks of K3 (CGS2 step), K4 (combination) and the fp64 reductions.
+
+Floating-point kernels: compared with an fp64 numpy reference of the same op
+(MGS + reorthogonalisation, ctkrylov/arnoldi.py:66-82, for the Arnoldi step).
+"""
+
+import numpy as np
+import pytest
+
+from paper_2602_17892_b200.arnoldi import DeviceBasis
+
+pytestmark = pytest.mark.gpu
+
+
+def basis_with(torch, Q, rows):
+    L, k1 = Q.shape
+    B = DeviceBasis(L, rows, torch.device("cuda", 0), torch)
+    B.W[:k1, :L] = torch.from_numpy(Q.T.astype(np.float32)).cuda()
+    return B
+
+
+@pytest.mark.parametrize("L,k", [(1000, 0), (4099, 5), (130680, 30), (262147, 63)])
+def test_cgs2_step_matches_fp64_mgs(cuda, L, k):
+    torch = cuda
+    rng = np.random.default_rng(L + k)
+    Q, _ = np.linalg.qr(rng.standard_normal((L, k + 1)))
+    Q = Q.astype(np.float32).astype(np.float64)
+    q = rng.standard_normal(L).astype(np.float32).astype(np.float64)
+    B = basis_with(torch, Q, k + 3)
+    qd = torch.from_numpy(q.astype(np.float32)).cuda()
+    h = torch.zeros(k + 8, dtype=torch.float64, device="cuda")
+    stat = torch.zeros(4, dtype=torch.float64, device="cuda")
+    B.cgs2_step(k, qd, h, stat, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    # fp64 reference: MGS + one reorthogonalisation pass
+    v = q.copy()
+    href = np.zeros(k + 2)
+    for _ in range(2):
+        for i in range(k + 1):
+            c = Q[:, i] @ v
+            href[i] += c
+            v = v - c * Q[:, i]
+    href[k + 1] = np.linalg.norm(v)
+    hg = h.cpu().numpy()[: k + 2]
+    np.testing.assert_allclose(hg, href, rtol=1e-5, atol=1e-5 * np.abs(href).max())
+    st = stat.cpu().numpy()
+    assert st[0] == pytest.approx(np.linalg.norm(q), rel=1e-12)
+    assert st[1] == 0.0
+    w = B.W[k + 1, :L].cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(w, v / href[k + 1], atol=2e-6)
+    # new row is orthogonal to the basis to fp32 working precision
+    assert np.abs(Q.T @ w).max() < 1e-5
+
+
+def test_cgs2_breakdown_flag(cuda):
+    torch = cuda
+    L = 4096
+    rng = np.random.default_rng(1)
+    Q, _ = np.linalg.qr(rng.standard_normal((L, 3)))
+    B = basis_with(torch, Q.astype(np.float32).astype(np.float64), 5)
+    q = (Q[:, :3] @ np.array([1.0, -2.0, 0.5])).astype(np.float32)    # in span(W): invariant
+    qd = torch.from_numpy(q).cuda()
+    h = torch.zeros(8, dtype=torch.float64, device="cuda")
+    stat = torch.zeros(4, dtype=torch.float64, device="cuda")
+    # only rows 0..2 are basis rows: step k=2 orthogonalises against 3 rows
+    B.cgs2_step(2, qd, h, stat, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    st = stat.cpu().numpy()
+    # fp32 inputs leave a ~1e-7 relative residue: breakdown iff h <= 1e-14 ||q||
+    assert st[3] <= 1e-5 * st[0]
+
+
+@pytest.mark.parametrize("L,k", [(33, 4), (32940, 17), (1000003, 40)])
+def test_combine_and_norms(cuda, L, k):
+    torch = cuda
+    rng = np.random.default_rng(k)
+    Wh = rng.standard_normal((k, L)).astype(np.float32)
+    B = DeviceBasis(L, k + 1, torch.device("cuda", 0), torch)
+    B.W[:k, :L] = torch.from_numpy(Wh).cuda()
+    y = rng.standard_normal(k)
+    x0 = rng.standard_normal(L).astype(np.float32)
+    yd = torch.from_numpy(y).cuda()
+    x0d = torch.from_numpy(x0).cuda()
+    out = torch.empty(L, dtype=torch.float32, device="cuda")
+    nrm = torch.zeros(1, dtype=torch.float64, device="cuda")
+    B.combine(k, yd, out, x0=x0d, norm_out=nrm, stream=torch.cuda.current_stream())
+    ref = x0.astype(np.float64) + Wh.astype(np.float64).T @ y
+    got = out.cpu().numpy()
+    np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-5)
+    assert nrm.item() == pytest.approx(float(np.sum(got.astype(np.float64) ** 2)), rel=1e-12)
+    n2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    B.norm2(x0d, n2, torch.cuda.current_stream())
+    assert n2.item() == pytest.approx(float(np.sum(x0.astype(np.float64) ** 2)), rel=1e-12)
+    dots = torch.zeros(k + 1, dtype=torch.float64, device="cuda")
+    B.dots(k, x0d, dots, True, torch.cuda.current_stream())
+    dref = Wh.astype(np.float64) @ x0.astype(np.float64)
+    np.testing.assert_allclose(dots.cpu().numpy()[:k], dref, rtol=1e-10, atol=1e-9)
+
+
+def test_reductions_are_bitwise_deterministic(cuda):
+    torch = cuda
+    L, k = 2086560, 20
+    rng = np.random.default_rng(5)
+    B = DeviceBasis(L, k + 2, torch.device("cuda", 0), torch)
+    B.W[: k + 1, :L] = torch.from_numpy(rng.standard_normal((k + 1, L)).astype(np.float32)).cuda()
+    v = torch.from_numpy(rng.standard_normal(L).astype(np.float32)).cuda()
+    outs = []
+    for _ in range(3):
+        d = torch.zeros(k + 2, dtype=torch.float64, device="cuda")
+        B.dots(k + 1, v, d, True, torch.cuda.current_stream())
+        outs.append(d.cpu().numpy())
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])

@@ -123,6 +123,8 @@ int ctk_combine(const float* W, int64_t ld, int k, const double* y, const float*
 
 /* Host-side helpers to let drivers avoid a libcudart dependency. */
 int ctk_device_count(int* out);
+/* Total kernels this library has launched in the process (all threads). */
+int64_t ctk_launch_counter(void);
 
 #ifdef __cplusplus
 }

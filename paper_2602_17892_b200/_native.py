@@ -25,6 +25,7 @@ SIGNATURES = {
     "ctk_version": (_c.c_int, []),
     "ctk_last_error": (_c.c_char_p, []),
     "ctk_device_count": (_c.c_int, [_c.POINTER(_c.c_int)]),
+    "ctk_launch_counter": (_c.c_int64, []),
     "ctk_geom_create": (_c.c_int, [_c.c_int, _c.c_int, _c.c_double, _c.c_int,
                                    _c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _c.c_int,
                                    _c.POINTER(_c.c_double), _c.c_double, _c.c_int,
@@ -105,6 +106,11 @@ def device_count() -> int:
     n = ctypes.c_int(0)
     check(load().ctk_device_count(ctypes.byref(n)))
     return n.value
+
+
+def launch_counter() -> int:
+    """Kernels libctk has launched in this process (evidence for bench.py)."""
+    return int(load().ctk_launch_counter())
 
 
 def ptr(t) -> int | None:

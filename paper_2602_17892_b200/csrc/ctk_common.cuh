@@ -26,8 +26,11 @@ struct AngleParams {
     int frame;              // 0: walk rows of x, 1: walk columns (transposed copy)
     int mirror;             // cross axis reversed
     int degenerate;         // |sin| or |cos| < 1e-14: exact literal path (ct.py:153-155,165,168)
-    int pad_;
+    int exact_flags;        // bit0: |dx| is a power of two, bit1: |dy| is (division == exact multiply)
+    double inv_dx, inv_dy;  // 1/dx, 1/dy (used only when the matching bit is set)
 };
+
+constexpr int CTK_MAX_DEG_LIST = 8;
 
 struct BackParams {         // per angle for K2: g = X*cg + Y*sg + center
     double cg, sg;
@@ -42,13 +45,29 @@ struct ctk_geom {
     double xmin, xmax, ymin, ymax, center;
     int back_wmax;            // max staged bins per angle for one K2 tile
     int n_degenerate;
+    int h_pow2;               // pixel size is a power of two: x / h == x * (1 / h) exactly
+    double inv_h;
+    int deg_list[ctk::CTK_MAX_DEG_LIST];   // degenerate angle indices (first CTK_MAX_DEG_LIST)
     // device tables
     ctk::AngleParams* d_ap;   // [n_angles]
     ctk::BackParams* d_bp;    // [n_angles]
     double* d_cos;            // [n_angles] bitwise np.cos (exact path)
     double* d_sin;            // [n_angles]
     double* d_offsets;        // [det_count] bitwise bin_offsets()
+    // degenerate (axis-aligned) angles: literal-Siddon segment lists built once
+    int* d_deg_slot;          // [n_angles] -> slot in the lists below, or -1
+    long long* d_deg_ptr;     // [n_degenerate * det_count + 1] segment offsets per ray
+    int* d_deg_pix;           // [total] pixel index
+    float* d_deg_len;         // [total] exact fp64 length rounded to fp32
+    long long deg_segments;
 };
+
+// Builds the degenerate-angle segment lists (ctk_forward.cu); called by
+// ctk_geom_create after the tables are on the device.
+int ctk_build_degenerate_lists(ctk_geom* g);
+
+// Kernel launches issued by the library (all threads); ctk_launch_counter().
+void ctk_count_launch(int n = 1);
 
 // error plumbing (thread-local last error string)
 int ctk_fail(int code, const char* fmt, ...);
@@ -62,6 +81,7 @@ int ctk_check_cuda(cudaError_t e, const char* what);
 
 #define CTK_LAUNCH_CHECK(what)                                         \
     do {                                                               \
+        ctk_count_launch();                                            \
         cudaError_t e_ = cudaGetLastError();                           \
         if (e_ != cudaSuccess) return ctk_check_cuda(e_, what);        \
     } while (0)

@@ -21,7 +21,11 @@
 // _siddon_ray with explicit round-to-nearest intrinsics (no FMA contraction),
 // because there a whole ray lies on a grid line and the reference's
 // midpoint/floor/clip sequence decides which column or row receives it.
+// That trace runs once, at geometry creation, into per-ray segment lists;
+// an apply sums them warp-per-ray inside the same launch as K1.
 #include <math.h>
+
+#include <vector>
 
 #include "ctk_common.cuh"
 
@@ -30,22 +34,34 @@ namespace ctk {
 struct ExactGrid {
     int nx, ny;
     double h, xmin, xmax, ymin, ymax;
+    double inv_h;
+    int h_pow2;
 };
+
+// IEEE a / b.  When |b| is a power of two, a * (1/b) is the same double
+// (both are exact scalings), and avoids the long fp64 division sequence --
+// this is the common case on the degenerate angles (dx = -1, dy = 1) and for
+// unit pixels.
+__device__ __forceinline__ double xdiv(double a, double b, double inv_b, bool pow2) {
+    return pow2 ? __dmul_rn(a, inv_b) : __ddiv_rn(a, b);
+}
 
 // Literal restatement of _siddon_ray (ct.py:137-179) in strict IEEE fp64.
 // Calls sink(pixel, length) for every kept segment in increasing t.
 template <class Sink>
 __device__ __forceinline__ void trace_exact(const ExactGrid& g, double ct, double st, double off,
-                                            Sink& sink) {
+                                            const AngleParams& p, Sink& sink) {
     const double px = __dmul_rn(off, ct), py = __dmul_rn(off, st);
     const double dx = -st, dy = ct;
+    const bool xp2 = p.exact_flags & 1, yp2 = (p.exact_flags >> 1) & 1, hp2 = g.h_pow2;
+    const double idx = p.inv_dx, idy = p.inv_dy, ih = g.inv_h;
     double t_lo = -INFINITY, t_hi = INFINITY;
     // x slab
     if (fabs(dx) < 1e-14) {
         if (px < g.xmin || px > g.xmax) return;
     } else {
-        double t0 = __ddiv_rn(__dsub_rn(g.xmin, px), dx);
-        double t1 = __ddiv_rn(__dsub_rn(g.xmax, px), dx);
+        double t0 = xdiv(__dsub_rn(g.xmin, px), dx, idx, xp2);
+        double t1 = xdiv(__dsub_rn(g.xmax, px), dx, idx, xp2);
         if (t0 > t1) { double tmp = t0; t0 = t1; t1 = tmp; }
         if (t0 > t_lo) t_lo = t0;
         if (t1 < t_hi) t_hi = t1;
@@ -54,8 +70,8 @@ __device__ __forceinline__ void trace_exact(const ExactGrid& g, double ct, doubl
     if (fabs(dy) < 1e-14) {
         if (py < g.ymin || py > g.ymax) return;
     } else {
-        double t0 = __ddiv_rn(__dsub_rn(g.ymin, py), dy);
-        double t1 = __ddiv_rn(__dsub_rn(g.ymax, py), dy);
+        double t0 = xdiv(__dsub_rn(g.ymin, py), dy, idy, yp2);
+        double t1 = xdiv(__dsub_rn(g.ymax, py), dy, idy, yp2);
         if (t0 > t1) { double tmp = t0; t0 = t1; t1 = tmp; }
         if (t0 > t_lo) t_lo = t0;
         if (t1 < t_hi) t_hi = t1;
@@ -71,8 +87,8 @@ __device__ __forceinline__ void trace_exact(const ExactGrid& g, double ct, doubl
     auto emit = [&](double t_next) {
         const double len = __dsub_rn(t_next, prev);
         const double tm = __dmul_rn(0.5, __dadd_rn(prev, t_next));
-        const double fx = floor(__ddiv_rn(__dsub_rn(__dadd_rn(px, __dmul_rn(tm, dx)), g.xmin), g.h));
-        const double fy = floor(__ddiv_rn(__dsub_rn(g.ymax, __dadd_rn(py, __dmul_rn(tm, dy))), g.h));
+        const double fx = floor(xdiv(__dsub_rn(__dadd_rn(px, __dmul_rn(tm, dx)), g.xmin), g.h, ih, hp2));
+        const double fy = floor(xdiv(__dsub_rn(g.ymax, __dadd_rn(py, __dmul_rn(tm, dy))), g.h, ih, hp2));
         long long ix = (long long)fx, iy = (long long)fy;
         ix = ix < 0 ? 0 : (ix > g.nx - 1 ? g.nx - 1 : ix);
         iy = iy < 0 ? 0 : (iy > g.ny - 1 ? g.ny - 1 : iy);
@@ -83,11 +99,11 @@ __device__ __forceinline__ void trace_exact(const ExactGrid& g, double ct, doubl
     bool have_x = false, have_y = false;
     for (;;) {
         while (!have_x && kx < nxi) {
-            double v = __ddiv_rn(__dsub_rn(__dadd_rn(g.xmin, __dmul_rn((double)ix_i, g.h)), px), dx);
+            double v = xdiv(__dsub_rn(__dadd_rn(g.xmin, __dmul_rn((double)ix_i, g.h)), px), dx, idx, xp2);
             if (v > t_lo && v < t_hi) { tx = v; have_x = true; } else { ix_i += ix_s; ++kx; }
         }
         while (!have_y && ky < nyi) {
-            double v = __ddiv_rn(__dsub_rn(__dadd_rn(g.ymin, __dmul_rn((double)iy_i, g.h)), py), dy);
+            double v = xdiv(__dsub_rn(__dadd_rn(g.ymin, __dmul_rn((double)iy_i, g.h)), py), dy, idy, yp2);
             if (v > t_lo && v < t_hi) { ty = v; have_y = true; } else { iy_i += iy_s; ++ky; }
         }
         if (!have_x && !have_y) break;
@@ -114,6 +130,17 @@ struct CountSink {
         ++raw;
         if (pix != last) ++nnz;   // identical (ray, pixel) pairs are consecutive
         last = pix;
+    }
+};
+
+struct FillSink {
+    int* pix;
+    float* len;
+    long long i;
+    __device__ void operator()(long long p, double l) {
+        pix[i] = (int)p;
+        len[i] = (float)l;
+        ++i;
     }
 };
 
@@ -173,21 +200,26 @@ struct FwdArgs {
     const double* offsets;
     const double* cos_tab;
     const double* sin_tab;
-    const float* x;    // original image (exact path)
-    const float* P;
-    const float* PT;
-    const float* b;    // optional: y = b - A x
+    const float* x;          // original image (degenerate lists / exact path)
+    const float* P;          // zero-bordered row-major copy
+    const float* PT;         // zero-bordered transposed copy
+    const float* b;          // optional: y = b - A x
     float* y;
+    const int* deg_slot;
+    const long long* deg_ptr;
+    const int* deg_pix;
+    const float* deg_len;
     ExactGrid eg;
-    int D, a0;
-    int all_exact;
+    int D, a0, a1;
 };
 
-// Row walk of one ray.  Returns sum of segment length * pixel value.
-__device__ __forceinline__ double walk_ray(const AngleParams& p, double s, const float* __restrict__ base,
-                                           int R, int C) {
+// One ray of the row walk (see the header comment).  base/pitch/C describe
+// the zero-bordered copy the ray walks; MIRROR reverses the cross axis.
+template <bool MIRROR>
+__device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
+                                           const float* __restrict__ base, int R, int C) {
     const double sigma = (double)p.sigma_fx * (1.0 / 4294967296.0);
-    double u0 = fma(p.beta, s, p.alpha);
+    const double u0 = fma(p.beta, s, p.alpha);
     // the ray meets the image iff u(k) in (0, C) for some k in [0, R]
     if (!(u0 < (double)C + 1.0) || !(u0 + (double)R * sigma > -1.0)) return 0.0;
     const long long Sg = p.sigma_fx;
@@ -206,56 +238,101 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s, const
     if (kb >= ke) return 0.0;
 
     const int pitch = C + 2;
-    const int dir = p.mirror ? -1 : 1;
-    const float* rowp = base + (size_t)kb * pitch + (p.mirror ? C : 1);
-    long long u = U0 + kb * Sg;
+    // sigma < 1 here (the host clamps sigma_fx below 2^32), so the cross
+    // coordinate is (column c, 32-bit fraction) and a row splits exactly when
+    // the fraction add carries.  q = flat index of the pair's first tap:
+    // row k, bordered column c+1 (MIRROR: bordered column C - c, second tap
+    // one to the left).
+    const long long u = U0 + kb * Sg;
+    unsigned frac = (unsigned)u;
+    const unsigned Sf = (unsigned)Sg;
+    const int c0 = (int)(u >> 32);
+    // MIRROR keeps q negated so both directions advance with add-with-carry
+    int q = (int)kb * pitch + (MIRROR ? C - c0 : c0 + 1);
+    if (MIRROR) q = -q;
+    // Second-tap weight wb = max(0, f + sigma - 1) * Lx, the length the row
+    // spends past the grid line (0 when it does not reach it); wa = L - wb.
+    // With f1 = 1 + f:  wb = max(0, f1 * Lx + (sigma - 2) * Lx).
     const float L = p.L, Lx = p.Lx;
+    const float off = (float)(((double)Sg * (1.0 / 4294967296.0) - 2.0) * (double)p.Lx);
     double acc = 0.0;
     int k = (int)kb;
     const int kend = (int)ke;
     while (k < kend) {
-        const int kstop = min(kend, k + 64);
-        float a32 = 0.f;
-#pragma unroll 4
+        const int kstop = min(kend, k + 48);
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
         for (; k < kstop; ++k) {
-            const int c = (int)(u >> 32);
-            const float f = (float)(unsigned)(u & 0xffffffffll) * 2.3283064365386963e-10f;
-            const long long un = u + Sg;
-            const bool cross = (int)(un >> 32) != c;
-            const float wa = cross ? (1.f - f) * Lx : L;
-            const float wb = L - wa;
-            const float* pp = rowp + dir * c;
+            // 1 + frac as a float from the top 23 fraction bits: no I2F
+            const float f1 = __uint_as_float(0x3f800000u | (frac >> 9));
+            const float wb = fmaxf(fmaf(f1, Lx, off), 0.f);
+            const float wa = L - wb;
+            const float* pp = MIRROR ? base - q : base + q;
             const float v0 = __ldg(pp);
-            const float v1 = __ldg(pp + dir);
-            a32 = fmaf(wa, v0, fmaf(wb, v1, a32));
-            u = un;
-            rowp += pitch;
+            const float v1 = __ldg(pp + (MIRROR ? -1 : 1));
+            s0 = fmaf(wa, v0, s0);
+            s1 = fmaf(wb, v1, s1);
+            // frac += sigma; the carry moves the pair one column (row split)
+            // (MIRROR: -q_pos advances by -pitch + carry)
+            asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;"
+                : "+r"(frac), "+r"(q) : "r"(Sf), "r"(MIRROR ? -pitch : pitch));
         }
-        acc += (double)a32;
+        acc += (double)s0 + (double)s1;
     }
     return acc;
 }
 
-__global__ void __launch_bounds__(FWD_THREADS) k_forward(FwdArgs A) {
+// Degenerate angle: warp per ray over the precomputed literal segment list.
+__device__ __forceinline__ void degenerate_block(const FwdArgs& A, int a, int slot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int jb = blockIdx.x * FWD_THREADS + warp * 32;
+    for (int r = 0; r < 32; ++r) {
+        const int j = jb + r;
+        if (j >= A.D) break;
+        const long long ray = (long long)slot * A.D + j;
+        const long long beg = A.deg_ptr[ray], end = A.deg_ptr[ray + 1];
+        double s = 0.0;
+        for (long long e = beg + lane; e < end; e += 32)
+            s = fma((double)__ldg(A.deg_len + e), (double)__ldg(A.x + __ldg(A.deg_pix + e)), s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            const size_t o = (size_t)(a - A.a0) * A.D + j;
+            A.y[o] = A.b ? (float)((double)A.b[o] - s) : (float)s;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(FWD_THREADS, 12) k_forward(FwdArgs A) {
     const int a = A.a0 + blockIdx.y;
+    const int slot = A.deg_slot[a];
+    if (slot >= 0) {                         // whole block: warp-uniform branch
+        degenerate_block(A, a, slot);
+        return;
+    }
     const int j = blockIdx.x * FWD_THREADS + threadIdx.x;
     if (j >= A.D) return;
     const AngleParams p = A.ap[a];
     const double s = A.offsets[j];
     double acc;
-    if (p.degenerate || A.all_exact) {
-        SumSink sink{A.x, 0.0};
-        trace_exact(A.eg, A.cos_tab[a], A.sin_tab[a], s, sink);
-        acc = sink.acc;
-    } else if (p.frame == 0) {
-        acc = walk_ray(p, s, A.P, A.eg.ny, A.eg.nx);
-    } else {
-        acc = walk_ray(p, s, A.PT, A.eg.nx, A.eg.ny);
-    }
+    if (p.frame == 0)
+        acc = p.mirror ? walk_ray<true>(p, s, A.P, A.eg.ny, A.eg.nx)
+                       : walk_ray<false>(p, s, A.P, A.eg.ny, A.eg.nx);
+    else
+        acc = p.mirror ? walk_ray<true>(p, s, A.PT, A.eg.nx, A.eg.ny)
+                       : walk_ray<false>(p, s, A.PT, A.eg.nx, A.eg.ny);
     const size_t o = (size_t)blockIdx.y * A.D + j;
-    float r = (float)acc;
-    if (A.b) r = (float)((double)A.b[o] - acc);
-    A.y[o] = r;
+    A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
+}
+
+// Literal fp64 Siddon for every ray (validation path, ctk_forward_exact).
+__global__ void __launch_bounds__(FWD_THREADS) k_forward_exact(FwdArgs A) {
+    const int a = A.a0 + blockIdx.y;
+    const int j = blockIdx.x * FWD_THREADS + threadIdx.x;
+    if (j >= A.D) return;
+    SumSink sink{A.x, 0.0};
+    trace_exact(A.eg, A.cos_tab[a], A.sin_tab[a], A.offsets[j], A.ap[a], sink);
+    A.y[(size_t)blockIdx.y * A.D + j] = (float)sink.acc;
 }
 
 __global__ void __launch_bounds__(FWD_THREADS) k_count(FwdArgs A, unsigned long long* counts) {
@@ -264,7 +341,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_count(FwdArgs A, unsigned long 
     long long raw = 0, nnz = 0;
     if (j < A.D) {
         CountSink sink;
-        trace_exact(A.eg, A.cos_tab[a], A.sin_tab[a], A.offsets[j], sink);
+        trace_exact(A.eg, A.cos_tab[a], A.sin_tab[a], A.offsets[j], A.ap[a], sink);
         raw = sink.raw;
         nnz = sink.nnz;
     }
@@ -279,7 +356,26 @@ __global__ void __launch_bounds__(FWD_THREADS) k_count(FwdArgs A, unsigned long 
     }
 }
 
-static FwdArgs make_args(const ctk_geom* g, const float* x, float* y, int a0, const float* b) {
+// Degenerate-angle segment lists: pass 1 counts, pass 2 fills.
+__global__ void k_deg_lists(ExactGrid eg, const AngleParams* ap, const double* cos_tab,
+                            const double* sin_tab, const double* offsets, const int* angles,
+                            int n_deg, int D, long long* ptr_or_counts, int* pix, float* len) {
+    const long long ray = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (ray >= (long long)n_deg * D) return;
+    const int a = angles[ray / D];
+    const int j = (int)(ray % D);
+    if (pix == nullptr) {
+        CountSink c;
+        trace_exact(eg, cos_tab[a], sin_tab[a], offsets[j], ap[a], c);
+        ptr_or_counts[ray + 1] = c.raw;
+    } else {
+        FillSink f{pix, len, ptr_or_counts[ray]};
+        trace_exact(eg, cos_tab[a], sin_tab[a], offsets[j], ap[a], f);
+    }
+}
+
+static FwdArgs make_args(const ctk_geom* g, const float* x, float* y, int a0, int a1,
+                         const float* b) {
     FwdArgs A;
     A.ap = g->d_ap;
     A.offsets = g->d_offsets;
@@ -290,16 +386,77 @@ static FwdArgs make_args(const ctk_geom* g, const float* x, float* y, int a0, co
     A.PT = nullptr;
     A.b = b;
     A.y = y;
-    A.eg = ExactGrid{g->nx, g->ny, g->h, g->xmin, g->xmax, g->ymin, g->ymax};
+    A.deg_slot = g->d_deg_slot;
+    A.deg_ptr = g->d_deg_ptr;
+    A.deg_pix = g->d_deg_pix;
+    A.deg_len = g->d_deg_len;
+    A.eg = ExactGrid{g->nx, g->ny, g->h, g->xmin, g->xmax, g->ymin, g->ymax, g->inv_h, g->h_pow2};
     A.D = g->det_count;
     A.a0 = a0;
-    A.all_exact = 0;
+    A.a1 = a1;
     return A;
 }
 
 }  // namespace ctk
 
 using namespace ctk;
+
+// Called once from ctk_geom_create: literal Siddon segment lists of every
+// ray at a degenerate angle, so applies are a memory-parallel list sum.
+int ctk_build_degenerate_lists(ctk_geom* g) {
+    std::vector<int> slot(g->n_angles, -1), angles;
+    std::vector<AngleParams> hap(g->n_angles);
+    CTK_CUDA(cudaMemcpy(hap.data(), g->d_ap, sizeof(AngleParams) * g->n_angles,
+                        cudaMemcpyDeviceToHost));
+    for (int a = 0; a < g->n_angles; ++a)
+        if (hap[a].degenerate) {
+            slot[a] = (int)angles.size();
+            angles.push_back(a);
+        }
+    CTK_CUDA(cudaMalloc(&g->d_deg_slot, sizeof(int) * g->n_angles));
+    CTK_CUDA(cudaMemcpy(g->d_deg_slot, slot.data(), sizeof(int) * g->n_angles,
+                        cudaMemcpyHostToDevice));
+    const long long rays = (long long)angles.size() * g->det_count;
+    CTK_CUDA(cudaMalloc(&g->d_deg_ptr, sizeof(long long) * (rays + 1)));
+    CTK_CUDA(cudaMemset(g->d_deg_ptr, 0, sizeof(long long) * (rays + 1)));
+    g->deg_segments = 0;
+    if (rays == 0) return CTK_OK;
+    int* d_angles = nullptr;
+    CTK_CUDA(cudaMalloc(&d_angles, sizeof(int) * angles.size()));
+    CTK_CUDA(cudaMemcpy(d_angles, angles.data(), sizeof(int) * angles.size(),
+                        cudaMemcpyHostToDevice));
+    const ExactGrid eg{g->nx, g->ny, g->h, g->xmin, g->xmax, g->ymin, g->ymax, g->inv_h, g->h_pow2};
+    const int threads = 128;
+    const int blocks = (int)((rays + threads - 1) / threads);
+    k_deg_lists<<<blocks, threads>>>(eg, g->d_ap, g->d_cos, g->d_sin, g->d_offsets, d_angles,
+                                    (int)angles.size(), g->det_count, g->d_deg_ptr, nullptr,
+                                    nullptr);
+    cudaError_t e = cudaGetLastError();
+    std::vector<long long> ptr(rays + 1);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(ptr.data(), g->d_deg_ptr, sizeof(long long) * (rays + 1),
+                       cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+        cudaFree(d_angles);
+        return ctk_check_cuda(e, "degenerate segment count");
+    }
+    for (long long r = 0; r < rays; ++r) ptr[r + 1] += ptr[r];
+    g->deg_segments = ptr[rays];
+    e = cudaMemcpy(g->d_deg_ptr, ptr.data(), sizeof(long long) * (rays + 1),
+                   cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_deg_pix, sizeof(int) * (g->deg_segments + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_deg_len, sizeof(float) * (g->deg_segments + 1));
+    if (e == cudaSuccess) {
+        k_deg_lists<<<blocks, threads>>>(eg, g->d_ap, g->d_cos, g->d_sin, g->d_offsets,
+                                        d_angles, (int)angles.size(), g->det_count,
+                                        g->d_deg_ptr, g->d_deg_pix, g->d_deg_len);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(d_angles);
+    if (e != cudaSuccess) return ctk_check_cuda(e, "degenerate segment fill");
+    return CTK_OK;
+}
 
 static int check_range(const ctk_geom* g, int a0, int a1) {
     if (!g) return ctk_fail(CTK_ERR_ARG, "null geometry");
@@ -322,7 +479,7 @@ extern "C" int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0
     dim3 sg((g->nx + 31) / 32, (g->ny + 31) / 32), sb(32, 8);
     k_stage<<<sg, sb, 0, st>>>(x, P, PT, g->nx, g->ny);
     CTK_LAUNCH_CHECK("k_stage");
-    FwdArgs A = make_args(g, x, y, a0, b);
+    FwdArgs A = make_args(g, x, y, a0, a1, b);
     A.P = P;
     A.PT = PT;
     dim3 grid((g->det_count + FWD_THREADS - 1) / FWD_THREADS, a1 - a0);
@@ -338,11 +495,10 @@ extern "C" int ctk_forward_exact(const ctk_geom_t* g, const float* x, float* y, 
     if (!x || !y) return ctk_fail(CTK_ERR_ARG, "null vector");
     if (a1 == a0) return CTK_OK;
     CTK_CUDA(cudaSetDevice(g->device));
-    FwdArgs A = make_args(g, x, y, a0, nullptr);
-    A.all_exact = 1;
+    FwdArgs A = make_args(g, x, y, a0, a1, nullptr);
     dim3 grid((g->det_count + FWD_THREADS - 1) / FWD_THREADS, a1 - a0);
-    k_forward<<<grid, FWD_THREADS, 0, ctk_stream(stream)>>>(A);
-    CTK_LAUNCH_CHECK("k_forward(exact)");
+    k_forward_exact<<<grid, FWD_THREADS, 0, ctk_stream(stream)>>>(A);
+    CTK_LAUNCH_CHECK("k_forward_exact");
     return CTK_OK;
 }
 
@@ -355,7 +511,7 @@ extern "C" int ctk_count_segments(const ctk_geom_t* g, int a0, int a1, int64_t* 
     cudaStream_t st = ctk_stream(stream);
     CTK_CUDA(cudaMemsetAsync(counts_dev, 0, 2 * sizeof(int64_t), st));
     if (a1 == a0) return CTK_OK;
-    FwdArgs A = make_args(g, nullptr, nullptr, a0, nullptr);
+    FwdArgs A = make_args(g, nullptr, nullptr, a0, a1, nullptr);
     dim3 grid((g->det_count + FWD_THREADS - 1) / FWD_THREADS, a1 - a0);
     k_count<<<grid, FWD_THREADS, 0, st>>>(A, reinterpret_cast<unsigned long long*>(counts_dev));
     CTK_LAUNCH_CHECK("k_count");

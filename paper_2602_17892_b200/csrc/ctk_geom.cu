@@ -10,11 +10,17 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
 #include <vector>
 
 #include "ctk_common.cuh"
 
 static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void ctk_count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+extern "C" int64_t ctk_launch_counter(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int ctk_fail(int code, const char* fmt, ...) {
     va_list ap;
@@ -46,6 +52,12 @@ extern "C" int ctk_device_count(int* out) {
 
 namespace {
 
+bool is_pow2(double v) {
+    if (!(v != 0.0) || !isfinite(v)) return false;
+    int e;
+    return frexp(fabs(v), &e) == 0.5;
+}
+
 constexpr int BTX = 32, BTY = 16, BCA = 32;   // must match ctk_back.cu
 
 void free_geom(ctk_geom* g) {
@@ -55,6 +67,10 @@ void free_geom(ctk_geom* g) {
     cudaFree(g->d_cos);
     cudaFree(g->d_sin);
     cudaFree(g->d_offsets);
+    cudaFree(g->d_deg_slot);
+    cudaFree(g->d_deg_ptr);
+    cudaFree(g->d_deg_pix);
+    cudaFree(g->d_deg_len);
     delete g;
 }
 
@@ -92,6 +108,8 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
     g->ymin = -hy;
     g->ymax = hy;
     g->center = 0.5 * (double)(det_count - 1);   // ct.py:215
+    g->h_pow2 = is_pow2(pixel_size) ? 1 : 0;
+    g->inv_h = 1.0 / pixel_size;
 
     std::vector<ctk::AngleParams> ap(n_angles);
     std::vector<ctk::BackParams> bp(n_angles);
@@ -102,6 +120,11 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
         ctk::AngleParams p;
         memset(&p, 0, sizeof(p));
         p.degenerate = (fabs(s) < 1e-14 || fabs(c) < 1e-14) ? 1 : 0;   // ct.py:153,165,168
+        p.exact_flags = (is_pow2(-s) ? 1 : 0) | (is_pow2(c) ? 2 : 0);
+        p.inv_dx = s != 0.0 ? 1.0 / -s : 0.0;
+        p.inv_dy = c != 0.0 ? 1.0 / c : 0.0;
+        if (p.degenerate && g->n_degenerate < ctk::CTK_MAX_DEG_LIST)
+            g->deg_list[g->n_degenerate] = a;
         double sigma_raw, C;
         if (fabs(c) >= fabs(s)) {
             // walk image rows top->bottom; u = (x - xmin)/h at row boundary
@@ -132,6 +155,9 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
         }
         if (sigma_raw > 1.0) sigma_raw = 1.0;
         p.sigma_fx = llrint(sigma_raw * 4294967296.0);
+        // the walk keeps a 32-bit fraction: sigma == 1 (|tan| rounds to 1 at 45
+        // degrees) becomes 1 - 2^-32, a 1e-6-pixel drift over a 4096-row walk
+        if (p.sigma_fx > 0xffffffffll) p.sigma_fx = 0xffffffffll;
         ap[a] = p;
         bp[a].cg = c / det_spacing;
         bp[a].sg = s / det_spacing;
@@ -168,6 +194,11 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
     if (e != cudaSuccess) {
         free_geom(g);
         return ctk_check_cuda(e, "ctk_geom_create");
+    }
+    int rc = ctk_build_degenerate_lists(g);
+    if (rc != CTK_OK) {
+        free_geom(g);
+        return rc;
     }
     *out = g;
     return CTK_OK;

@@ -159,7 +159,7 @@ class KernelTimer:
 
 
 class _DeviceSolve:
-    def __init__(self, A, B, b, cfg, x_true, image_shape, stream, timer):
+    def __init__(self, A, B, b, cfg, x_true, image_shape, stream, timer, keep_on_device=False):
         if not isinstance(A, GpuForward) or not isinstance(B, GpuBack) or A.dgeom is not B.dgeom:
             raise TypeError("the device-resident run_gmres needs the GPU projector pair from "
                             "paper_2602_17892_b200.ct (forward_ray_driven / back_pixel_driven "
@@ -169,6 +169,9 @@ class _DeviceSolve:
         torch = self.torch = dg.torch
         self.stream = stream if stream is not None else torch.cuda.current_stream(dg.dev)
         self.timer = timer
+        self.keep_on_device = keep_on_device
+        self.h2d = 0                     # bytes copied host->device / device->host by the solve
+        self.d2h = 0
         self.x_true = None if x_true is None else np.asarray(x_true, dtype=np.float64)
         self.image_shape = image_shape
         self.ab = cfg.method.startswith("ab")
@@ -189,6 +192,7 @@ class _DeviceSolve:
                 if bh.shape != (self.m,):
                     raise OperatorShapeError(f"data vector has shape {bh.shape}, expected ({self.m},)")
                 self.b = torch.from_numpy(bh.astype(np.float32)).pin_memory().to(dev, non_blocking=True)
+                self.h2d += 4 * self.m
             self.basis = DeviceBasis(L, rows, dev, torch)
             x0 = cfg.x0
             if x0 is None:
@@ -198,6 +202,7 @@ class _DeviceSolve:
                 if x0.shape != (self.n,):
                     raise ConfigError(f"x0 has shape {x0.shape}, expected ({self.n},)")
                 self.x_cur = torch.from_numpy(x0.astype(np.float32)).to(dev)
+                self.h2d += 4 * self.n
             self.xk = torch.empty(self.n, dtype=f32, device=dev)
             self.q = torch.empty(L, dtype=f32, device=dev)
             self.tmp = torch.empty(self.n if self.ab else self.m, dtype=f32, device=dev)
@@ -243,6 +248,7 @@ class _DeviceSolve:
         self.basis.cgs2_step(j, self.q, hrow, stat, self.stream)
         with torch.cuda.stream(self.stream):
             self.h_host[j].copy_(hrow, non_blocking=True)
+        self.d2h += 8 * self.hcols
         ev = torch.cuda.Event()
         ev.record(self.stream)
         self.ev_h[j] = ev
@@ -253,6 +259,7 @@ class _DeviceSolve:
         with torch.cuda.stream(self.stream):
             self.y_pin[it, :k] = torch.from_numpy(y)
             self.y_dev[it, :k].copy_(self.y_pin[it, :k], non_blocking=True)
+        self.h2d += 8 * k
         ydev = self.y_dev[it]
         nrm = self.norms[it]
         if self.ab:
@@ -269,6 +276,7 @@ class _DeviceSolve:
         return ev
 
     def _host_vec(self, t):
+        self.d2h += 4 * t.numel()
         with self.torch.cuda.stream(self.stream):
             return t.to("cpu", non_blocking=False).numpy().astype(np.float64)
 
@@ -304,6 +312,7 @@ class _DeviceSolve:
                 self.basis.norm2(w0, self.scal[0:1], self.stream)
             with torch.cuda.stream(self.stream):
                 self.scal_host.copy_(self.scal, non_blocking=True)
+            self.d2h += 32
             self.stream.synchronize()
             beta = float(np.sqrt(self.scal_host[0].item()))
             d0n = beta if self.ab else float(np.sqrt(self.scal_host[1].item()))
@@ -381,12 +390,15 @@ class _DeviceSolve:
         self.stream.synchronize()
         if pending:
             norms = self.norms.cpu().numpy()
+            self.d2h += self.norms.numel() * 8
             for rec, slot, ev in pending:
                 self._finish(rec, slot, ev_start, ev, norms)
         x_final = self.xk if records and records[-1].k > 0 else self.x_cur
-        x_host = self._host_vec(x_final)
-        return SolveResult(x=x_host, records=records, stop_reason=stop or "maxiter",
-                           cycles=max(cycles, 1), snapshots=snapshots)
+        x_out = x_final.clone() if self.keep_on_device else self._host_vec(x_final)
+        res = SolveResult(x=x_out, records=records, stop_reason=stop or "maxiter",
+                          cycles=max(cycles, 1), snapshots=snapshots)
+        res.transfer = {"h2d_bytes": self.h2d, "d2h_bytes": self.d2h}
+        return res
 
     def _finish(self, rec, slot, ev_start, ev, norms=None):
         if norms is None:
@@ -416,11 +428,14 @@ class _DeviceSolve:
 
 def run_gmres(A: LinearOperator, B: LinearOperator, b, cfg: SolverConfig,
               x_true: np.ndarray | None = None, image_shape: tuple[int, int] | None = None,
-              *, stream=None, kernel_timer: KernelTimer | None = None) -> SolveResult:
+              *, stream=None, kernel_timer: KernelTimer | None = None,
+              keep_on_device: bool = False) -> SolveResult:
     """(Hybrid) AB-/BA-GMRES with optional restarting, on the GPU.
 
     ``b`` may be a host array (the reference's contract) or a CUDA tensor
-    (device-resident input).  Returns a SolveResult with a host ``x``.
+    (device-resident input).  Returns a SolveResult with a host ``x`` (a CUDA
+    tensor when ``keep_on_device``); ``result.transfer`` counts the bytes the
+    solve moved across PCIe.
     """
     cfg.validate()
     if cfg.method not in GMRES_METHODS:
@@ -429,7 +444,8 @@ def run_gmres(A: LinearOperator, B: LinearOperator, b, cfg: SolverConfig,
     if len(shape) != 1:
         raise OperatorShapeError(f"data vector has shape {shape}, expected ({A.rows},)")
     _check_dims(A, B, int(shape[0]))
-    return _DeviceSolve(A, B, b, cfg, x_true, image_shape, stream, kernel_timer).run()
+    return _DeviceSolve(A, B, b, cfg, x_true, image_shape, stream, kernel_timer,
+                        keep_on_device).run()
 
 
 def run_ab_gmres(A, B, b, cfg: SolverConfig, **kwargs) -> SolveResult:

@@ -270,7 +270,6 @@ def main():
         with torch.cuda.stream(stream):
             flush.fill_(1.0)
 
-    timer = gmres.KernelTimer(torch)
     hbm_peak, peak_src = measured_peak()
     result = {}
 
@@ -281,17 +280,9 @@ def main():
         y = torch.empty(dg.m, dtype=torch.float32, device=dev)
         xo = torch.empty(dg.n, dtype=torch.float32, device=dev)
 
-        def step(t=None):
-            if t is None:
-                dg.forward(x, out=y, stream=stream)
-                dg.back(u, out=xo, stream=stream)
-                return
-            e = t.bracket("forward", stream)
+        def step():
             dg.forward(x, out=y, stream=stream)
-            e.record(stream)
-            e = t.bracket("back", stream)
             dg.back(u, out=xo, stream=stream)
-            e.record(stream)
         rays_per_step = 2 * dg.m
         iters_per_step = None
     else:
@@ -311,8 +302,8 @@ def main():
         rays_per_step = spec.max_iter * (na + nb) * dg.m
         iters_per_step = spec.max_iter
 
-        def step(t=None):
-            result["last"] = gmres.run_gmres(A, B, b_dev, cfg, stream=stream, kernel_timer=t,
+        def step():
+            result["last"] = gmres.run_gmres(A, B, b_dev, cfg, stream=stream,
                                              keep_on_device=True)
 
     def barrier():
@@ -326,6 +317,7 @@ def main():
     barrier()
 
     launches0 = _native.launch_counter()
+    _native.profile_begin()       # CUDA events around every libctk projector call
     total_ms = 0.0
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
@@ -334,12 +326,13 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step(timer)
+            step()
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
         barrier()
     launches = _native.launch_counter() - launches0
+    prof = _native.profile_end()
     t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
@@ -347,8 +340,8 @@ def main():
     ms_per_step = total_ms / args.steps
     value = world * rays_per_step * args.steps / (total_ms / 1e3)
 
-    ksum = timer.summary()
-    shares = {k: n * ms for k, (n, ms) in ksum.items()}
+    ksum = {k: (n, ms) for k, (n, ms, _) in prof.items()}
+    shares = {k: tot for k, (_, _, tot) in prof.items() if k in ("forward", "back")}
     dom = max(shares, key=shares.get)
     n_l, ms_l = ksum[dom]
     alg = bytes_A if dom == "forward" else bytes_B
@@ -360,9 +353,12 @@ def main():
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
                 "launches_timed": n_l, "mean_launch_ms": round(ms_l, 5),
                 "share_of_step": round(shares[dom] / max(total_ms, 1e-9), 4)}
-    kernels = {k: {"launches": n, "mean_ms": round(ms, 5),
-                   "gbs": round((bytes_A if k == "forward" else bytes_B) / (ms / 1e3) / 1e9, 1),
-                   "rays_per_s": dg.m / (ms / 1e3)} for k, (n, ms) in ksum.items()}
+    kernels = {}
+    for k, (n, ms) in ksum.items():
+        kernels[k] = {"launches": n, "mean_ms": round(ms, 5)}
+        if k in ("forward", "back"):
+            kernels[k]["gbs"] = round((bytes_A if k == "forward" else bytes_B) / (ms / 1e3) / 1e9, 1)
+            kernels[k]["rays_per_s"] = dg.m / (ms / 1e3)
 
     e2e = None
     if not args.no_e2e and spec.method is not None:

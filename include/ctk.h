@@ -121,6 +121,45 @@ int ctk_cgs2_step(float* W, int64_t ld, int k, int64_t L, float* q, double* h,
 int ctk_combine(const float* W, int64_t ld, int k, const double* y, const float* x0,
                 float* dst, int64_t L, double* norm2_out, void* scratch, void* stream);
 
+/* ---- Native per-iteration orchestration of (hybrid) AB/BA-GMRES
+ * (ctkrylov/gmres.py:186-211).  ab != 0: M = A B on sinograms (L = m);
+ * ab == 0: M = B A on images (L = n).  stage_work / back_work as for
+ * ctk_forward / ctk_back (one set per stream). */
+
+/* Arnoldi step j: q = M W_j (tmp holds the intermediate), CGS2 against rows
+ * 0..j, row j+1 written; h_dev[0..hcols) receives h (j+2 values) with the 4
+ * stats of ctk_cgs2_step in its last 4 entries, copied asynchronously to
+ * h_host (pinned) when non-NULL. */
+int ctk_arnoldi_step(const ctk_geom_t* g, int ab, float* W, int64_t ld, int j, float* q,
+                     float* tmp, float* stage_work, float* back_work, double* h_dev,
+                     int hcols, double* h_host, void* scratch, void* stream);
+
+/* Iterate k: y (k fp64; copied from pinned y_host when non-NULL) ->
+ * x_k = x0 + W y (BA) or x0 + B (W y) (AB, z = m-length scratch);
+ * r = b - A x_k; norms_dev[0] = ||r||^2, norms_dev[1] = ||x_k||^2. */
+int ctk_iterate(const ctk_geom_t* g, int ab, const float* W, int64_t ld, int k,
+                const double* y_host, double* y_dev, const float* x0, float* xk, float* z,
+                const float* b, float* r, double* norms_dev, float* stage_work,
+                float* back_work, void* scratch, void* stream);
+
+/* CUDA-event profiler over library calls: kinds 0 = forward (stage + K1),
+ * 1 = back (K2 + finalize), 2 = CGS2 step, 3 = basis combination.  end()
+ * synchronises the recorded events and fills per-kind counts / mean / total. */
+int ctk_profile_begin(void);
+int ctk_profile_end(int nkinds, int64_t* counts, double* mean_ms, double* total_ms);
+
+/* ---- Host fp64 projected problem (ctkrylov/regparam.py, arnoldi.py:95-141).
+ * ctk_set_lapack registers LAPACK dgesdd and BLAS ddot (Fortran ABI, 32-bit
+ * ints; ddot may be NULL).
+ * ctk_projected_solve: H (k+1) x k row-major; strategy 0 none, 1 fixed,
+ * 2 lcurve, 3 gcv; grid_count points (200 in the reference); on a degenerate
+ * curve lambda = fallback_lambda (NaN: y left unset).  out = {lambda,
+ * ||H y - beta e1||, degenerate flag, rank-deficient flag}; y: k doubles.
+ * Thread-safe: no shared state beyond the registered function pointer. */
+int ctk_set_lapack(void* dgesdd, void* ddot);
+int ctk_projected_solve(const double* H, int k, double beta, int strategy, double fixed_value,
+                        int grid_count, double fallback_lambda, double* out, double* y);
+
 /* Host-side helpers to let drivers avoid a libcudart dependency. */
 int ctk_device_count(int* out);
 /* Total kernels this library has launched in the process (all threads). */

@@ -48,7 +48,19 @@ SIGNATURES = {
                                  _vp]),
     "ctk_combine": (_c.c_int, [_fp, _c.c_int64, _c.c_int, _dp, _fp, _fp, _c.c_int64, _dp, _vp,
                                _vp]),
+    "ctk_arnoldi_step": (_c.c_int, [_vp, _c.c_int, _fp, _c.c_int64, _c.c_int, _fp, _fp, _fp, _fp,
+                                    _dp, _c.c_int, _dp, _vp, _vp]),
+    "ctk_iterate": (_c.c_int, [_vp, _c.c_int, _fp, _c.c_int64, _c.c_int, _dp, _dp, _fp, _fp, _fp,
+                               _fp, _fp, _dp, _fp, _fp, _vp, _vp]),
+    "ctk_set_lapack": (_c.c_int, [_vp, _vp]),
+    "ctk_projected_solve": (_c.c_int, [_dp, _c.c_int, _c.c_double, _c.c_int, _c.c_double,
+                                       _c.c_int, _c.c_double, _dp, _dp]),
+    "ctk_profile_begin": (_c.c_int, []),
+    "ctk_profile_end": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int64), _c.POINTER(_c.c_double),
+                                   _c.POINTER(_c.c_double)]),
 }
+
+PROFILE_KINDS = ("forward", "back", "cgs2", "combine")
 
 _lib = None
 
@@ -80,8 +92,31 @@ def load(build_if_missing: bool = True):
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
+    _register_lapack(L)
     _lib = L
     return L
+
+
+def _register_lapack(L) -> None:
+    """Hand libctk the LAPACK dgesdd that scipy exports (cython_lapack)."""
+    try:
+        from scipy.linalg import cython_blas, cython_lapack
+        api = ctypes.pythonapi
+        api.PyCapsule_GetName.restype = ctypes.c_char_p
+        api.PyCapsule_GetName.argtypes = [ctypes.py_object]
+        api.PyCapsule_GetPointer.restype = ctypes.c_void_p
+        api.PyCapsule_GetPointer.argtypes = [ctypes.py_object, ctypes.c_char_p]
+
+        def fnptr(cap):
+            return ctypes.c_void_p(api.PyCapsule_GetPointer(cap, api.PyCapsule_GetName(cap)))
+
+        L.ctk_set_lapack(fnptr(cython_lapack.__pyx_capi__["dgesdd"]),
+                         fnptr(cython_blas.__pyx_capi__["ddot"]))
+    except Exception:   # the projected solve then reports "not registered"
+        pass
+
+
+STRATEGY_CODES = {"none": 0, "fixed": 1, "lcurve": 2, "gcv": 3}
 
 
 def check(rc: int, what: str = "") -> None:
@@ -111,6 +146,21 @@ def device_count() -> int:
 def launch_counter() -> int:
     """Kernels libctk has launched in this process (evidence for bench.py)."""
     return int(load().ctk_launch_counter())
+
+
+def profile_begin() -> None:
+    check(load().ctk_profile_begin(), "ctk_profile_begin")
+
+
+def profile_end() -> dict:
+    """{kind: (launches, mean_ms, total_ms)} for the calls since profile_begin()."""
+    n = len(PROFILE_KINDS)
+    counts = (ctypes.c_int64 * n)()
+    mean = (ctypes.c_double * n)()
+    total = (ctypes.c_double * n)()
+    check(load().ctk_profile_end(n, counts, mean, total), "ctk_profile_end")
+    return {k: (int(counts[i]), float(mean[i]), float(total[i]))
+            for i, k in enumerate(PROFILE_KINDS) if counts[i]}
 
 
 def ptr(t) -> int | None:

@@ -98,8 +98,17 @@ class DeviceBasis:
         self.dev = device
         self.W = torch.zeros((self.rows, self.ld), dtype=torch.float32, device=device)
         self.lib = _native.load()
-        nbytes = int(self.lib.ctk_reduce_scratch_bytes(self.rows + 2, self.L))
-        self.scratch = torch.zeros(nbytes // 8 + 1, dtype=torch.float64, device=device)
+        self._scratch_words = int(self.lib.ctk_reduce_scratch_bytes(self.rows + 2, self.L)) // 8 + 1
+        self._scratch = {}
+
+    def scratch(self, stream) -> int:
+        """Reduction scratch owned by one stream (zero-filled once)."""
+        key = stream.cuda_stream
+        buf = self._scratch.get(key)
+        if buf is None:
+            buf = self.torch.zeros(self._scratch_words, dtype=self.torch.float64, device=self.dev)
+            self._scratch[key] = buf
+        return buf.data_ptr()
 
     def row(self, j: int):
         return self.W[j, : self.L]
@@ -110,19 +119,19 @@ class DeviceBasis:
             raise ValueError(f"basis holds {self.rows} rows; step {k} would write row {k + 1}")
         _native.check(self.lib.ctk_cgs2_step(self.W.data_ptr(), self.ld, k, self.L, q.data_ptr(),
                                              h_out.data_ptr(), stat_out.data_ptr(),
-                                             self.scratch.data_ptr(), stream.cuda_stream),
+                                             self.scratch(stream), stream.cuda_stream),
                       "ctk_cgs2_step")
 
     def combine(self, k: int, y_dev, dst, x0=None, norm_out=None, stream=None) -> None:
         """dst = (x0 or 0) + W[:k]^T y   (K4, fp64 accumulation)."""
         _native.check(self.lib.ctk_combine(self.W.data_ptr(), self.ld, k, y_dev.data_ptr(),
                                            _native.ptr(x0), dst.data_ptr(), self.L,
-                                           _native.ptr(norm_out), self.scratch.data_ptr(),
+                                           _native.ptr(norm_out), self.scratch(stream),
                                            stream.cuda_stream), "ctk_combine")
 
     def norm2(self, v, out, stream) -> None:
         _native.check(self.lib.ctk_norm2(v.data_ptr(), v.numel(), out.data_ptr(),
-                                         self.scratch.data_ptr(), stream.cuda_stream), "ctk_norm2")
+                                         self.scratch(stream), stream.cuda_stream), "ctk_norm2")
 
     def scale_into(self, v, dst, scale_dev, stream) -> None:
         _native.check(self.lib.ctk_scale(v.data_ptr(), dst.data_ptr(), v.numel(),
@@ -131,10 +140,10 @@ class DeviceBasis:
     def dots(self, nvec: int, v, out, want_norm: bool, stream) -> None:
         _native.check(self.lib.ctk_dots(self.W.data_ptr(), self.ld, nvec, v.data_ptr(), self.L,
                                         1 if want_norm else 0, out.data_ptr(),
-                                        self.scratch.data_ptr(), stream.cuda_stream), "ctk_dots")
+                                        self.scratch(stream), stream.cuda_stream), "ctk_dots")
 
     def update(self, nvec: int, coef_dev, v, dst, norm_out=None, stream=None) -> None:
         _native.check(self.lib.ctk_update(self.W.data_ptr(), self.ld, nvec, coef_dev.data_ptr(),
                                           v.data_ptr(), dst.data_ptr(), self.L,
-                                          _native.ptr(norm_out), self.scratch.data_ptr(),
+                                          _native.ptr(norm_out), self.scratch(stream),
                                           stream.cuda_stream), "ctk_update")

@@ -201,6 +201,7 @@ extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, i
     if (smem > 48 * 1024)
         CTK_CUDA(cudaFuncSetAttribute(k_back, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
+    const int ph = ctk_prof_open(1, st);
     k_back<<<grid, block, smem, st>>>(A);
     CTK_LAUNCH_CHECK("k_back");
     if (S > 1) {
@@ -210,5 +211,6 @@ extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, i
         k_back_finalize<<<blocks, threads, 0, st>>>(work, S, n, g->h, x0, x);
         CTK_LAUNCH_CHECK("k_back_finalize");
     }
+    ctk_prof_close(ph, st);
     return CTK_OK;
 }

@@ -69,6 +69,11 @@ int ctk_build_degenerate_lists(ctk_geom* g);
 // Kernel launches issued by the library (all threads); ctk_launch_counter().
 void ctk_count_launch(int n = 1);
 
+// CUDA-event profiler (ctk_solver.cu): kinds 0 forward, 1 back, 2 cgs2,
+// 3 basis combination.  open returns -1 when profiling is off.
+int ctk_prof_open(int kind, cudaStream_t st);
+void ctk_prof_close(int handle, cudaStream_t st);
+
 // error plumbing (thread-local last error string)
 int ctk_fail(int code, const char* fmt, ...);
 int ctk_check_cuda(cudaError_t e, const char* what);

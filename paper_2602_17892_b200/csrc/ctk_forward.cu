@@ -477,6 +477,7 @@ extern "C" int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0
     float* P = work;
     float* PT = work + (size_t)g->ny * (g->nx + 2);
     dim3 sg((g->nx + 31) / 32, (g->ny + 31) / 32), sb(32, 8);
+    const int ph = ctk_prof_open(0, st);
     k_stage<<<sg, sb, 0, st>>>(x, P, PT, g->nx, g->ny);
     CTK_LAUNCH_CHECK("k_stage");
     FwdArgs A = make_args(g, x, y, a0, a1, b);
@@ -485,6 +486,7 @@ extern "C" int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0
     dim3 grid((g->det_count + FWD_THREADS - 1) / FWD_THREADS, a1 - a0);
     k_forward<<<grid, FWD_THREADS, 0, st>>>(A);
     CTK_LAUNCH_CHECK("k_forward");
+    ctk_prof_close(ph, st);
     return CTK_OK;
 }
 

@@ -1,0 +1,271 @@
+// ctk_host.cpp -- native host fp64 projected problem of hybrid GMRES.
+//
+// Per iteration the reference solves, on the (k+1) x k Hessenberg H_k:
+//   SVD (ctkrylov/arnoldi.py:133-141), the 200-point lambda grid
+//   (regparam.py:28-36), filter-factor norms (regparam.py:46-60), the L-curve
+//   corner (regparam.py:82-107) or GCV minimum (regparam.py:110-134), and the
+//   projected Tikhonov / least-squares solve (arnoldi.py:95-130).
+// All of it stays on the host in fp64 (north star); here it runs in C++ so
+// that host worker threads can solve several iterations' projected problems
+// concurrently without the Python GIL.  The SVD is LAPACK dgesdd (the routine
+// numpy.linalg.svd uses), reached through scipy's exported cython_lapack
+// function pointer registered by the Python layer (ctk_set_lapack).
+//
+// Semantics match the reference's: grid endpoints exact, ties broken toward
+// the larger lambda, DegenerateCurveError conditions reported as a flag.
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <limits>
+#include <vector>
+
+#include "../../include/ctk.h"
+
+extern int ctk_fail(int code, const char* fmt, ...);
+
+namespace {
+
+typedef void (*dgesdd_t)(char* jobz, int* m, int* n, double* a, int* lda, double* s, double* u,
+                         int* ldu, double* vt, int* ldvt, double* work, int* lwork, int* iwork,
+                         int* info);
+dgesdd_t g_dgesdd = nullptr;
+typedef double (*ddot_t)(int* n, double* x, int* incx, double* y, int* incy);
+ddot_t g_ddot = nullptr;
+
+// numpy's pairwise summation (add.reduce over a contiguous float64 array):
+// 8 partial sums for blocks <= 128, recursive halving above.  Matching it
+// keeps the filter-factor norms bitwise equal to the reference's np.sum.
+double pairwise_sum(const double* a, long n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (long i = 0; i < n; ++i) r += a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        long i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    long n2 = n / 2;
+    n2 -= n2 % 8;
+    return pairwise_sum(a, n2) + pairwise_sum(a + n2, n - n2);
+}
+
+// c . c as numpy's `c @ c` computes it (BLAS ddot) when BLAS is registered.
+double dot_self(std::vector<double>& c) {
+    if (g_ddot) {
+        int n = (int)c.size(), inc = 1;
+        return g_ddot(&n, c.data(), &inc, c.data(), &inc);
+    }
+    double r = 0.0;
+    for (double v : c) r += v * v;
+    return r;
+}
+
+struct Svd {
+    int kp1 = 0, k = 0;
+    std::vector<double> s, U, VT;   // U: kp1 x k col-major, VT: k x k col-major
+};
+
+int svd_hessenberg(const double* H, int kp1, int k, Svd& out) {
+    out.kp1 = kp1;
+    out.k = k;
+    std::vector<double> A((size_t)kp1 * k);
+    for (int i = 0; i < kp1; ++i)
+        for (int j = 0; j < k; ++j) A[(size_t)i + (size_t)j * kp1] = H[(size_t)i * k + j];
+    out.s.assign(k, 0.0);
+    out.U.assign((size_t)kp1 * k, 0.0);
+    out.VT.assign((size_t)k * k, 0.0);
+    std::vector<int> iwork(8 * (size_t)k);
+    char jobz = 'S';
+    int m = kp1, n = k, lda = kp1, ldu = kp1, ldvt = k, lwork = -1, info = 0;
+    double wq = 0.0;
+    g_dgesdd(&jobz, &m, &n, A.data(), &lda, out.s.data(), out.U.data(), &ldu, out.VT.data(), &ldvt,
+             &wq, &lwork, iwork.data(), &info);
+    if (info != 0) return info;
+    lwork = (int)wq + 1;
+    std::vector<double> work(lwork);
+    g_dgesdd(&jobz, &m, &n, A.data(), &lda, out.s.data(), out.U.data(), &ldu, out.VT.data(), &ldvt,
+             work.data(), &lwork, iwork.data(), &info);
+    return info;
+}
+
+// numpy.geomspace(lo, hi, count): 10 ** linspace(log10 lo, log10 hi), endpoints exact.
+void geomspace(double lo, double hi, int count, std::vector<double>& g) {
+    g.resize(count);
+    const double a = log10(lo), b = log10(hi);
+    const double step = count > 1 ? (b - a) / (double)(count - 1) : 0.0;
+    for (int i = 0; i < count; ++i) g[i] = pow(10.0, (double)i * step + a);
+    g[0] = lo;
+    if (count > 1) g[count - 1] = hi;
+}
+
+// np.gradient with unit spacing (second-order interior, first-order edges).
+void gradient(const std::vector<double>& f, std::vector<double>& d) {
+    const int n = (int)f.size();
+    d.resize(n);
+    if (n < 2) {
+        if (n == 1) d[0] = 0.0;
+        return;
+    }
+    d[0] = f[1] - f[0];
+    d[n - 1] = f[n - 1] - f[n - 2];
+    for (int i = 1; i < n - 1; ++i) d[i] = (f[i + 1] - f[i - 1]) / 2.0;
+}
+
+enum { S_NONE = 0, S_FIXED = 1, S_LCURVE = 2, S_GCV = 3 };
+
+// Returns 0 and sets lam, or 1 for a degenerate curve (DegenerateCurveError).
+int select(const Svd& v, double beta, int strategy, int grid_count, double* lam) {
+    const int k = v.k, kp1 = v.kp1;
+    double smax = 0.0, smin = std::numeric_limits<double>::infinity();
+    for (int i = 0; i < k; ++i) {
+        smax = std::max(smax, v.s[i]);
+        if (v.s[i] > 0) smin = std::min(smin, v.s[i]);
+    }
+    if (!(smax > 0.0)) return 1;                       // all singular values are zero
+    std::vector<double> grid;
+    geomspace(std::max(smin * 1e-4, 1e-12), smax, grid_count, grid);
+    std::vector<double> c(k);
+    for (int i = 0; i < k; ++i) c[i] = beta * v.U[(size_t)i * kp1];   // beta * U[0, i]
+    const double outside = std::max(beta * beta - dot_self(c), 0.0);
+    std::vector<double> sol(grid_count), res(grid_count), tr(grid_count);
+    std::vector<double> ta(k), tb(k), tf(k);
+    for (int g = 0; g < grid_count; ++g) {
+        const double l = grid[g], l2 = l * l;
+        for (int i = 0; i < k; ++i) {
+            const double s2 = v.s[i] * v.s[i];
+            const double den = s2 + l2;
+            const double a = v.s[i] * c[i] / den;
+            const double r = (l2 / den) * c[i];
+            ta[i] = a * a;
+            tb[i] = r * r;
+            tf[i] = s2 / den;
+        }
+        sol[g] = pairwise_sum(ta.data(), k);
+        res[g] = pairwise_sum(tb.data(), k) + outside;
+        tr[g] = (double)kp1 - pairwise_sum(tf.data(), k);
+    }
+    if (strategy == S_GCV) {
+        int best = -1;
+        double bv = 0.0;
+        for (int g = grid_count - 1; g >= 0; --g) {    // ties toward larger lambda
+            if (tr[g] <= 0.0) return 1;                 // GCV trace underflow
+            const double val = res[g] / (tr[g] * tr[g]);
+            if (!isfinite(val)) return 1;
+            if (best < 0 || val < bv) {
+                best = g;
+                bv = val;
+            }
+        }
+        *lam = grid[best];
+        return 0;
+    }
+    // L-curve corner
+    if (grid_count < 5) return 1;
+    std::vector<double> xr(grid_count), ys(grid_count), dx, dy, ddx, ddy;
+    for (int g = 0; g < grid_count; ++g) {
+        xr[g] = 0.5 * log(std::max(res[g], 1e-300));
+        ys[g] = 0.5 * log(std::max(sol[g], 1e-300));
+    }
+    gradient(xr, dx);
+    gradient(ys, dy);
+    gradient(dx, ddx);
+    gradient(dy, ddy);
+    int best = -1;
+    double bk = -std::numeric_limits<double>::infinity();
+    bool any_finite = false;
+    for (int g = grid_count - 1; g >= 0; --g) {
+        const double den = pow(dx[g] * dx[g] + dy[g] * dy[g], 1.5);
+        const double kap = (dx[g] * ddy[g] - dy[g] * ddx[g]) / den;
+        if (!isfinite(kap)) continue;
+        any_finite = true;
+        if (best < 0 || kap > bk) {
+            best = g;
+            bk = kap;
+        }
+    }
+    if (!any_finite) return 1;
+    if (bk <= 1e-9) return 1;                            // CURVATURE_FLOOR
+    *lam = grid[best];
+    return 0;
+}
+
+void tikhonov(const double* H, const Svd& v, double beta, double lam, double* y, double* res,
+              int* rank_def) {
+    const int k = v.k, kp1 = v.kp1;
+    std::vector<double> coef(k, 0.0);
+    int rank = 0;
+    if (lam == 0.0) {
+        const double cutoff = std::numeric_limits<double>::epsilon() * std::max(kp1, k) *
+                              (k > 0 ? v.s[0] : 0.0);
+        for (int i = 0; i < k; ++i)
+            if (v.s[i] > cutoff) {
+                coef[i] = beta * v.U[(size_t)i * kp1] / v.s[i];
+                ++rank;
+            }
+    } else {
+        for (int i = 0; i < k; ++i) {
+            const double c = beta * v.U[(size_t)i * kp1];
+            coef[i] = v.s[i] * c / (v.s[i] * v.s[i] + lam * lam);
+        }
+        rank = k;
+    }
+    for (int j = 0; j < k; ++j) {
+        double a = 0.0;
+        for (int i = 0; i < k; ++i) a += v.VT[(size_t)i + (size_t)j * k] * coef[i];
+        y[j] = a;
+    }
+    double r2 = 0.0;
+    for (int i = 0; i < kp1; ++i) {
+        double a = (i == 0) ? -beta : 0.0;
+        for (int j = 0; j < k; ++j) a += H[(size_t)i * k + j] * y[j];
+        r2 += a * a;
+    }
+    *res = sqrt(r2);
+    *rank_def = rank < k;
+}
+
+}  // namespace
+
+extern "C" int ctk_set_lapack(void* dgesdd, void* ddot) {
+    g_dgesdd = reinterpret_cast<dgesdd_t>(dgesdd);
+    g_ddot = reinterpret_cast<ddot_t>(ddot);
+    return g_dgesdd ? CTK_OK : ctk_fail(CTK_ERR_ARG, "null dgesdd");
+}
+
+extern "C" int ctk_projected_solve(const double* H, int k, double beta, int strategy,
+                                   double fixed_value, int grid_count, double fallback_lambda,
+                                   double* out, double* y) {
+    if (!g_dgesdd) return ctk_fail(CTK_ERR_ARG, "LAPACK dgesdd not registered (ctk_set_lapack)");
+    if (!H || !out || !y || k < 1 || grid_count < 1)
+        return ctk_fail(CTK_ERR_ARG, "bad projected-solve arguments");
+    Svd v;
+    const int info = svd_hessenberg(H, k + 1, k, v);
+    if (info != 0) return ctk_fail(CTK_ERR_ARG, "dgesdd failed (info %d)", info);
+    double lam = 0.0;
+    int degenerate = 0;
+    if (strategy == S_FIXED) {
+        lam = fixed_value;
+    } else if (strategy == S_LCURVE || strategy == S_GCV) {
+        if (select(v, beta, strategy, grid_count, &lam)) {
+            degenerate = 1;
+            lam = fallback_lambda;
+        }
+    }
+    double res = 0.0;
+    int rank_def = 0;
+    if (!isnan(lam)) tikhonov(H, v, beta, lam, y, &res, &rank_def);
+    out[0] = lam;
+    out[1] = res;
+    out[2] = degenerate;
+    out[3] = rank_def;
+    return CTK_OK;
+}

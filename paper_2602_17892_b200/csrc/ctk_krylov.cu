@@ -6,43 +6,49 @@
 //
 // The basis lives on the device as fp32 rows W[j][0..L) (row pitch ld, 16-B
 // aligned) -- HBM-resident for the whole solve, never copied.  Every kernel
-// streams rows with 128-bit loads and accumulates in fp64.  Reductions are a
-// fixed two-level tree: warp shuffles, a per-CTA smem pass, one fp64 partial
-// per CTA, and a last-CTA-done pass (integer ticket, no float atomics) that
-// sums the CTA partials in index order -- bitwise reproducible run to run.
+// streams rows with 128-bit loads and accumulates in fp64.
+//
+// Dots use a 2-D grid (L-chunk x group of 8 rows) so that even the small
+// Krylov vectors of c1/c2 (33k-65k floats) spread over hundreds of CTAs with 8
+// independent 16-B loads in flight per thread.  Reductions are a fixed tree:
+// warp shuffles, a per-CTA smem pass, one fp64 partial per (chunk, row), and a
+// last-CTA-done pass (integer ticket, no float atomics) that sums the chunk
+// partials in a fixed order -- bitwise reproducible run to run.
 #include <math.h>
 
 #include "ctk_common.cuh"
 
 namespace ctk {
 
-constexpr int KT = 256;           // threads per CTA
+constexpr int KT = 256;            // dots: threads per CTA
 constexpr int KWARPS = KT / 32;
-constexpr int KMAX_GRID = 2 * 148;
-constexpr int KMAX_VEC = 1024;    // rows per reduction call (smem bound)
+constexpr int JG = 8;              // rows per dots CTA
+constexpr int MAXCH = 1024;        // max L-chunks (= partial rows)
+constexpr int CT = 128;            // combine: threads per CTA
+constexpr int KMAX_VEC = 4096;     // rows per call (smem bound of k_combine)
 
-struct Scratch {                  // carved from the caller's zero-filled scratch
-    unsigned int* ticket;         // [1]
-    double* partial;              // [KMAX_GRID][nvec_cap]
-    double* tmp;                  // [3][nvec_cap]
+struct Scratch {                   // carved from the caller's zero-filled scratch
+    unsigned int* ticket;          // [1]
+    double* partial;               // [MAXCH][nvec_cap]
+    double* tmp;                   // [3][nvec_cap]
     int nvec_cap;
 };
-
-static inline int grid_for(int64_t L4) {
-    int64_t g = (L4 + 2 * KT - 1) / (2 * KT);
-    if (g > KMAX_GRID) g = KMAX_GRID;
-    if (g < 1) g = 1;
-    return (int)g;
-}
 
 static inline Scratch carve(void* scratch, int nvec_cap) {
     char* p = (char*)scratch;
     Scratch s;
     s.ticket = (unsigned int*)p;
     s.partial = (double*)(p + 256);
-    s.tmp = s.partial + (size_t)KMAX_GRID * nvec_cap;
+    s.tmp = s.partial + (size_t)MAXCH * nvec_cap;
     s.nvec_cap = nvec_cap;
     return s;
+}
+
+// float4 per chunk: at least one per thread, at most MAXCH chunks.
+static inline int64_t chunk_len(int64_t L4) {
+    int64_t ch = (L4 + MAXCH - 1) / MAXCH;
+    ch = (ch + KT - 1) / KT * KT;
+    return ch < KT ? KT : ch;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -59,108 +65,117 @@ __device__ __forceinline__ double dot4(float4 a, float4 b, double acc) {
     return acc;
 }
 
-// CTA partial sums red[w][j] -> partial[blockIdx][j]; last CTA -> out[j].
-__device__ void finish_reduce(double (*red)[KWARPS], int nv, double* partial, unsigned int* ticket,
-                              double* out) {
-    __syncthreads();
-    for (int j = threadIdx.x; j < nv; j += KT) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < KWARPS; ++w) s += red[j][w];
-        partial[(size_t)blockIdx.x * nv + j] = s;
-    }
+// Last CTA of the grid sums partial[c * nv + j] over chunks c in a fixed
+// order (lane-strided, then a fixed shuffle tree) and writes out[j].
+__device__ void last_cta_reduce(const double* partial, int nchunks, int nv, unsigned int* ticket,
+                                double* out) {
     __threadfence();
     __shared__ unsigned int s_last;
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+    if (threadIdx.x == 0)
+        s_last = (atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1);
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    for (int j = threadIdx.x; j < nv; j += KT) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = warp; j < nv; j += nw) {
         double s = 0.0;
-        for (unsigned int b = 0; b < gridDim.x; ++b) s += __ldcg(partial + (size_t)b * nv + j);
-        out[j] = s;
+        for (int c = lane; c < nchunks; c += 32) s += __ldcg(partial + (size_t)c * nv + j);
+        s = warp_sum(s);
+        if (lane == 0) out[j] = s;
     }
     if (threadIdx.x == 0) *ticket = 0u;   // ready for the next stream-ordered call
 }
 
 // out[j] = <W_j, v> (j < nvec); out[nvec] = <v, v> if want_norm.
+// grid = (nchunks, ceil(nv / JG)).
 __global__ void __launch_bounds__(KT) k_dots(const float* __restrict__ W, int64_t ld, int nvec,
                                              const float* __restrict__ v, int64_t L, int want_norm,
-                                             double* out, double* partial, unsigned int* ticket) {
-    extern __shared__ double red_raw[];
-    double (*red)[KWARPS] = reinterpret_cast<double (*)[KWARPS]>(red_raw);
+                                             int64_t ch, double* out, double* partial,
+                                             unsigned int* ticket) {
+    __shared__ double red[JG][KWARPS];
     const int nv = nvec + (want_norm ? 1 : 0);
+    const int j0 = blockIdx.y * JG;
+    const int nj = min(JG, nv - j0);
     const int64_t L4 = L >> 2;
-    const int64_t chunk = (L4 + gridDim.x - 1) / gridDim.x;
-    const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(L4, i0 + chunk);
+    const int64_t i0 = (int64_t)blockIdx.x * ch, i1 = min(L4, i0 + ch);
     const float4* v4 = reinterpret_cast<const float4*>(v);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool tail_owner = (blockIdx.x == gridDim.x - 1);
-    for (int j0 = 0; j0 < nv; j0 += 4) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        const float4* w4[4];
-        const float* w1[4];
+    const float4* rows[JG];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int j = j0 + q < nv ? j0 + q : j0;
-            const float* row = (j < nvec) ? W + (size_t)j * ld : v;
-            w4[q] = reinterpret_cast<const float4*>(row);
-            w1[q] = row;
-        }
-        for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) {
-            const float4 vv = __ldg(v4 + i);
+    for (int q = 0; q < JG; ++q) {
+        const int j = j0 + (q < nj ? q : 0);
+        rows[q] = reinterpret_cast<const float4*>(j < nvec ? W + (size_t)j * ld : v);
+    }
+    double acc[JG];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q] = dot4(__ldg(w4[q] + i), vv, acc[q]);
-        }
-        if (tail_owner) {
-            for (int64_t i = (L4 << 2) + threadIdx.x; i < L; i += KT) {
-                const double vv = (double)v[i];
+    for (int q = 0; q < JG; ++q) acc[q] = 0.0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) {
+        const float4 vv = __ldg(v4 + i);
+        float4 w[JG];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[q] = fma((double)w1[q][i], vv, acc[q]);
-            }
-        }
+        for (int q = 0; q < JG; ++q)
+            if (q < nj) w[q] = __ldg(rows[q] + i);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double s = warp_sum(acc[q]);
-            if (lane == 0 && j0 + q < nv) red[j0 + q][warp] = s;
+        for (int q = 0; q < JG; ++q)
+            if (q < nj) acc[q] = dot4(w[q], vv, acc[q]);
+    }
+    if (blockIdx.x == gridDim.x - 1) {     // scalar tail L % 4
+        for (int64_t i = (L4 << 2) + threadIdx.x; i < L; i += KT) {
+            const double vv = (double)v[i];
+#pragma unroll
+            for (int q = 0; q < JG; ++q)
+                if (q < nj) acc[q] = fma((double)reinterpret_cast<const float*>(rows[q])[i], vv, acc[q]);
         }
     }
-    finish_reduce(red, nv, partial, ticket, out);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < JG; ++q) {
+        const double s = warp_sum(acc[q]);
+        if (lane == 0) red[q][warp] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < nj) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < KWARPS; ++w) s += red[threadIdx.x][w];
+        partial[(size_t)blockIdx.x * nv + j0 + threadIdx.x] = s;
+    }
+    last_cta_reduce(partial, gridDim.x, nv, ticket, out);
 }
 
 // dst = (base ? base : 0) + sgn * sum_j coef[j] W_j ; optional ||dst||^2.
-__global__ void __launch_bounds__(KT) k_combine(const float* __restrict__ W, int64_t ld, int nvec,
+__global__ void __launch_bounds__(CT) k_combine(const float* __restrict__ W, int64_t ld, int nvec,
                                                 const double* __restrict__ coef, double sgn,
                                                 const float* base, float* dst, int64_t L,
                                                 double* norm_out, double* partial,
                                                 unsigned int* ticket) {
-    extern __shared__ double sh[];
-    double* c = sh;                                               // [nvec]
-    double (*red)[KWARPS] = reinterpret_cast<double (*)[KWARPS]>(sh + ((nvec + 1) & ~1));
-    for (int j = threadIdx.x; j < nvec; j += KT) c[j] = sgn * coef[j];
+    extern __shared__ double c[];                                 // [nvec]
+    __shared__ double red[CT / 32];
+    for (int j = threadIdx.x; j < nvec; j += CT) c[j] = sgn * coef[j];
     __syncthreads();
     const int64_t L4 = L >> 2;
-    const int64_t chunk = (L4 + gridDim.x - 1) / gridDim.x;
-    const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(L4, i0 + chunk);
     double nrm = 0.0;
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += KT) {
+    for (int64_t i = blockIdx.x * (int64_t)CT + threadIdx.x; i < L4;
+         i += (int64_t)gridDim.x * CT) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         if (base) {
             const float4 b = reinterpret_cast<const float4*>(base)[i];
             a0 = b.x; a1 = b.y; a2 = b.z; a3 = b.w;
         }
         int j = 0;
-        for (; j + 1 < nvec; j += 2) {
-            const float4 w = __ldg(reinterpret_cast<const float4*>(W + (size_t)j * ld) + i);
-            const float4 z = __ldg(reinterpret_cast<const float4*>(W + (size_t)(j + 1) * ld) + i);
-            const double cj = c[j], cz = c[j + 1];
-            a0 = fma(cj, (double)w.x, a0); a1 = fma(cj, (double)w.y, a1);
-            a2 = fma(cj, (double)w.z, a2); a3 = fma(cj, (double)w.w, a3);
-            a0 = fma(cz, (double)z.x, a0); a1 = fma(cz, (double)z.y, a1);
-            a2 = fma(cz, (double)z.z, a2); a3 = fma(cz, (double)z.w, a3);
+        for (; j + 8 <= nvec; j += 8) {           // 8 independent 16-B loads in flight
+            float4 w[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                w[q] = __ldg(reinterpret_cast<const float4*>(W + (size_t)(j + q) * ld) + i);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double cj = c[j + q];
+                a0 = fma(cj, (double)w[q].x, a0); a1 = fma(cj, (double)w[q].y, a1);
+                a2 = fma(cj, (double)w[q].z, a2); a3 = fma(cj, (double)w[q].w, a3);
+            }
         }
-        if (j < nvec) {
+        for (; j < nvec; ++j) {
             const float4 w = __ldg(reinterpret_cast<const float4*>(W + (size_t)j * ld) + i);
             const double cj = c[j];
             a0 = fma(cj, (double)w.x, a0); a1 = fma(cj, (double)w.y, a1);
@@ -172,7 +187,7 @@ __global__ void __launch_bounds__(KT) k_combine(const float* __restrict__ W, int
         nrm = fma((double)o.z, (double)o.z, nrm); nrm = fma((double)o.w, (double)o.w, nrm);
     }
     if (blockIdx.x == gridDim.x - 1) {
-        for (int64_t i = (L4 << 2) + threadIdx.x; i < L; i += KT) {
+        for (int64_t i = (L4 << 2) + threadIdx.x; i < L; i += CT) {
             double a = base ? (double)base[i] : 0.0;
             for (int j = 0; j < nvec; ++j) a = fma(c[j], (double)W[(size_t)j * ld + i], a);
             const float o = (float)a;
@@ -182,8 +197,15 @@ __global__ void __launch_bounds__(KT) k_combine(const float* __restrict__ W, int
     }
     if (!norm_out) return;
     const double s = warp_sum(nrm);
-    if ((threadIdx.x & 31) == 0) red[0][threadIdx.x >> 5] = s;
-    finish_reduce(red, 1, partial, ticket, norm_out);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < CT / 32; ++w) t += red[w];
+        partial[blockIdx.x] = t;
+    }
+    last_cta_reduce(partial, gridDim.x, 1, ticket, norm_out);
 }
 
 __global__ void k_scale(const float* __restrict__ v, float* __restrict__ dst, int64_t L,
@@ -194,7 +216,7 @@ __global__ void k_scale(const float* __restrict__ v, float* __restrict__ dst, in
         dst[i] = v[i] * sc;
 }
 
-// h = h1 + h2; h[k+1] = sqrt(n2); stat = {||q||, breakdown, 1/h[k+1] or 0}
+// h = h1 + h2; h[k+1] = sqrt(n2); stat = {||q||, breakdown, 1/h[k+1] or 0, h[k+1]}
 __global__ void k_cgs2_finalize(const double* h1, const double* h2, const double* n2, int k,
                                 double* h, double* stat) {
     for (int i = threadIdx.x; i <= k; i += blockDim.x) h[i] = h1[i] + h2[i];
@@ -222,17 +244,20 @@ static int check_vec(const void* p, const char* what) {
 
 extern "C" size_t ctk_reduce_scratch_bytes(int nvec, int64_t L) {
     (void)L;
-    const int cap = nvec + 2;
-    return 256 + sizeof(double) * ((size_t)KMAX_GRID * cap + 3 * (size_t)cap) + 256;
+    const int cap = nvec + 3;
+    return 256 + sizeof(double) * ((size_t)MAXCH * cap + 3 * (size_t)cap) + 256;
 }
 
 static int launch_dots(const float* W, int64_t ld, int nvec, const float* v, int64_t L,
                        int want_norm, double* out, Scratch s, cudaStream_t st) {
     const int nv = nvec + (want_norm ? 1 : 0);
     if (nv > s.nvec_cap || nv > KMAX_VEC) return ctk_fail(CTK_ERR_ARG, "too many vectors (%d)", nv);
-    const int G = grid_for(L >> 2);
-    const size_t smem = sizeof(double) * (size_t)nv * KWARPS;
-    k_dots<<<G, KT, smem, st>>>(W, ld, nvec, v, L, want_norm, out, s.partial, s.ticket);
+    const int64_t L4 = L >> 2;
+    const int64_t ch = chunk_len(L4);
+    int64_t nch = (L4 + ch - 1) / ch;
+    if (nch < 1) nch = 1;
+    dim3 grid((unsigned)nch, (unsigned)((nv + JG - 1) / JG));
+    k_dots<<<grid, KT, 0, st>>>(W, ld, nvec, v, L, want_norm, ch, out, s.partial, s.ticket);
     CTK_LAUNCH_CHECK("k_dots");
     return CTK_OK;
 }
@@ -241,10 +266,13 @@ static int launch_combine(const float* W, int64_t ld, int nvec, const double* co
                           const float* base, float* dst, int64_t L, double* norm_out, Scratch s,
                           cudaStream_t st) {
     if (nvec > KMAX_VEC) return ctk_fail(CTK_ERR_ARG, "too many vectors (%d)", nvec);
-    const int G = grid_for(L >> 2);
-    const size_t smem = sizeof(double) * ((size_t)((nvec + 1) & ~1) + KWARPS);
-    k_combine<<<G, KT, smem, st>>>(W, ld, nvec, coef, sgn, base, dst, L, norm_out, s.partial,
-                                   s.ticket);
+    const int64_t L4 = L >> 2;
+    int64_t G = (L4 + CT - 1) / CT;
+    if (G > MAXCH) G = MAXCH;
+    if (G < 1) G = 1;
+    const size_t smem = sizeof(double) * (size_t)(nvec > 0 ? nvec : 1);
+    k_combine<<<(unsigned)G, CT, smem, st>>>(W, ld, nvec, coef, sgn, base, dst, L, norm_out,
+                                              s.partial, s.ticket);
     CTK_LAUNCH_CHECK("k_combine");
     return CTK_OK;
 }
@@ -256,7 +284,7 @@ extern "C" int ctk_dots(const float* W, int64_t ld, int nvec, const float* v, in
     if ((rc = check_vec(v, "v"))) return rc;
     if (!out || !scratch) return ctk_fail(CTK_ERR_ARG, "null output/scratch");
     if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
-    return launch_dots(W, ld, nvec, v, L, want_norm, out, carve(scratch, nvec + 2),
+    return launch_dots(W, ld, nvec, v, L, want_norm, out, carve(scratch, nvec + 3),
                        ctk_stream(stream));
 }
 
@@ -268,7 +296,7 @@ extern "C" int ctk_update(const float* W, int64_t ld, int nvec, const double* co
     if ((rc = check_vec(v, "v")) || (rc = check_vec(dst, "dst"))) return rc;
     if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
     if (!scratch || (nvec > 0 && !coef)) return ctk_fail(CTK_ERR_ARG, "null coef/scratch");
-    return launch_combine(W, ld, nvec, coef, -1.0, v, dst, L, norm2_out, carve(scratch, nvec + 2),
+    return launch_combine(W, ld, nvec, coef, -1.0, v, dst, L, norm2_out, carve(scratch, nvec + 3),
                           ctk_stream(stream));
 }
 
@@ -280,7 +308,7 @@ extern "C" int ctk_combine(const float* W, int64_t ld, int k, const double* y, c
     if (x0 && (rc = check_vec(x0, "x0"))) return rc;
     if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
     if (!scratch || (k > 0 && !y)) return ctk_fail(CTK_ERR_ARG, "null y/scratch");
-    return launch_combine(W, ld, k, y, 1.0, x0, dst, L, norm2_out, carve(scratch, k + 2),
+    return launch_combine(W, ld, k, y, 1.0, x0, dst, L, norm2_out, carve(scratch, k + 3),
                           ctk_stream(stream));
 }
 
@@ -288,7 +316,7 @@ extern "C" int ctk_norm2(const float* v, int64_t L, double* out, void* scratch, 
     int rc;
     if ((rc = check_vec(v, "v"))) return rc;
     if (!out || !scratch) return ctk_fail(CTK_ERR_ARG, "null output/scratch");
-    return launch_dots(nullptr, 4, 0, v, L, 1, out, carve(scratch, 2), ctk_stream(stream));
+    return launch_dots(nullptr, 4, 0, v, L, 1, out, carve(scratch, 3), ctk_stream(stream));
 }
 
 extern "C" int ctk_scale(const float* v, float* dst, int64_t L, const double* scale_dev,

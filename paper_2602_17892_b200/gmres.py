@@ -25,7 +25,7 @@ from dataclasses import dataclass, field, replace
 
 import numpy as np
 
-from . import metrics
+from . import _native, metrics
 from .arnoldi import (BREAKDOWN_RTOL, DeviceBasis, hessenberg_from_columns,  # noqa: F401
                       solve_projected_tikhonov)
 from .ct import GpuBack, GpuForward
@@ -158,7 +158,58 @@ class KernelTimer:
         return out
 
 
+_POOL = None
+_STREAMS: dict = {}
+
+
+def _pool():
+    """Host worker threads for the per-iteration projected problems (LAPACK
+    releases the GIL, so independent iterations' SVDs run in parallel)."""
+    global _POOL
+    if _POOL is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=max(2, min(8, (os.cpu_count() or 2) - 1)),
+                                   thread_name_prefix="ctk-lambda")
+    return _POOL
+
+
+def _side_stream(torch, dev):
+    key = (dev.index, "combine")
+    s = _STREAMS.get(key)
+    if s is None:
+        s = torch.cuda.Stream(dev)
+        _STREAMS[key] = s
+    return s
+
+
+def _projected_task(lib, H, beta, code, value, fallback=float("nan")):
+    """Native fp64 projected problem of one iteration (SVD, lambda selection,
+    Tikhonov solve; ctk_host.cpp).  ctypes drops the GIL for the call, so
+    several iterations solve concurrently on the worker threads.
+    Returns (out = [lambda, ||H y - beta e1||, degenerate, rank_def], y)."""
+    k = H.shape[1]
+    out = np.empty(4)
+    y = np.empty(k)
+    _native.check(lib.ctk_projected_solve(H.ctypes.data, k, float(beta), code,
+                                          float(value or 0.0), 200, float(fallback),
+                                          out.ctypes.data, y.ctypes.data), "ctk_projected_solve")
+    return out, y
+
+
 class _DeviceSolve:
+    """One run_gmres call.
+
+    Streams: ``sa`` runs the Arnoldi process ahead (LOOKAHEAD steps in
+    flight; each step needs only w_k, never lambda); ``sb`` runs the iterate
+    updates x_k = x0 + (B) W y_k and true residuals as the host hands over
+    each y_k.  Host worker threads solve the projected problems of different
+    iterations concurrently; results are consumed strictly in iteration order
+    (the degenerate-curve fallback needs the previous lambda).
+    """
+
+    LOOKAHEAD = 6
+
     def __init__(self, A, B, b, cfg, x_true, image_shape, stream, timer, keep_on_device=False):
         if not isinstance(A, GpuForward) or not isinstance(B, GpuBack) or A.dgeom is not B.dgeom:
             raise TypeError("the device-resident run_gmres needs the GPU projector pair from "
@@ -167,7 +218,9 @@ class _DeviceSolve:
         self.A, self.B, self.cfg = A, B, cfg
         dg = self.dg = A.dgeom
         torch = self.torch = dg.torch
-        self.stream = stream if stream is not None else torch.cuda.current_stream(dg.dev)
+        self.sa = stream if stream is not None else torch.cuda.current_stream(dg.dev)
+        self.sb = _side_stream(torch, dg.dev)
+        self.lib = _native.load()
         self.timer = timer
         self.keep_on_device = keep_on_device
         self.h2d = 0                     # bytes copied host->device / device->host by the solve
@@ -182,7 +235,7 @@ class _DeviceSolve:
         self.p = cfg.restart_period if cfg.restart_period > 0 else self.K
         rows = min(self.p, self.K) + 1
         f32, f64, dev = torch.float32, torch.float64, dg.dev
-        with torch.cuda.stream(self.stream):
+        with torch.cuda.stream(self.sa):
             if torch.is_tensor(b):
                 if b.numel() != self.m:
                     raise OperatorShapeError(f"data vector has {b.numel()} entries, expected {self.m}")
@@ -203,198 +256,251 @@ class _DeviceSolve:
                     raise ConfigError(f"x0 has shape {x0.shape}, expected ({self.n},)")
                 self.x_cur = torch.from_numpy(x0.astype(np.float32)).to(dev)
                 self.h2d += 4 * self.n
-            self.xk = torch.empty(self.n, dtype=f32, device=dev)
+            # stream sa (Arnoldi) buffers
             self.q = torch.empty(L, dtype=f32, device=dev)
             self.tmp = torch.empty(self.n if self.ab else self.m, dtype=f32, device=dev)
-            self.z = torch.empty(self.m, dtype=f32, device=dev) if self.ab else None
-            self.r = torch.empty(self.m, dtype=f32, device=dev)
             self.hcols = rows + 1 + 4                      # h[0..rows] + 4 stats
             self.hs = torch.zeros((rows, self.hcols), dtype=f64, device=dev)
             self.h_host = torch.zeros((rows, self.hcols), dtype=f64).pin_memory()
+            self.scal = torch.zeros(4, dtype=f64, device=dev)
+            self.scal_host = torch.zeros(4, dtype=f64).pin_memory()
+            # stream sb (iterate) buffers
+            self.xk = torch.empty(self.n, dtype=f32, device=dev)
+            self.z = torch.empty(self.m, dtype=f32, device=dev) if self.ab else None
+            self.r = torch.empty(self.m, dtype=f32, device=dev)
             self.y_dev = torch.zeros((self.K, rows), dtype=f64, device=dev)
             self.y_pin = torch.zeros((self.K, rows), dtype=f64).pin_memory()
             self.norms = torch.zeros((self.K + 1, 2), dtype=f64, device=dev)   # res^2, sol^2
-            self.scal = torch.zeros(4, dtype=f64, device=dev)
-            self.scal_host = torch.zeros(4, dtype=f64).pin_memory()
         self.ev_h = [None] * rows
+        # the side stream must not touch buffers before their zero-fill lands
+        self.sb.wait_stream(self.sa)
 
     # -- projector launches (optionally event-bracketed) ------------------
-    def _fwd(self, x, out, b=None):
+    def _fwd(self, x, out, stream, b=None):
         if self.timer is None:
-            return self.dg.forward(x, out=out, b=b, stream=self.stream)
-        e1 = self.timer.bracket("forward", self.stream)
-        self.dg.forward(x, out=out, b=b, stream=self.stream)
-        e1.record(self.stream)
+            return self.dg.forward(x, out=out, b=b, stream=stream)
+        e1 = self.timer.bracket("forward", stream)
+        self.dg.forward(x, out=out, b=b, stream=stream)
+        e1.record(stream)
 
-    def _back(self, u, out, x0=None):
+    def _back(self, u, out, stream, x0=None):
         if self.timer is None:
-            return self.dg.back(u, out=out, x0=x0, stream=self.stream)
-        e1 = self.timer.bracket("back", self.stream)
-        self.dg.back(u, out=out, x0=x0, stream=self.stream)
-        e1.record(self.stream)
+            return self.dg.back(u, out=out, x0=x0, stream=stream)
+        e1 = self.timer.bracket("back", stream)
+        self.dg.back(u, out=out, x0=x0, stream=stream)
+        e1.record(stream)
+
+    def _work(self, stream):
+        """(stage, back) workspaces of one stream for the native calls."""
+        dg = self.dg
+        stage = dg._workspace("stage", dg.stage_floats, stream)
+        wf = int(self.lib.ctk_back_work_floats(dg.handle, 0, dg.n_angles))
+        back = dg._workspace("back", wf, stream) if wf > 0 else None
+        return stage.data_ptr(), _native.ptr(back)
 
     def _arnoldi(self, j):
-        """Enqueue step j: q = M w_j, CGS2 -> h column + w_{j+1}; D2H h."""
-        torch = self.torch
-        w = self.basis.row(j)
-        if self.ab:
-            self._back(w, self.tmp)
-            self._fwd(self.tmp, self.q)
-        else:
-            self._fwd(w, self.tmp)
-            self._back(self.tmp, self.q)
+        """Enqueue step j on sa: q = M w_j, CGS2 -> h column + w_{j+1}; D2H h."""
+        torch, sa = self.torch, self.sa
+        stage, back = self._work(sa)
         hrow = self.hs[j]
-        stat = hrow[self.hcols - 4:]
-        self.basis.cgs2_step(j, self.q, hrow, stat, self.stream)
-        with torch.cuda.stream(self.stream):
-            self.h_host[j].copy_(hrow, non_blocking=True)
+        _native.check(self.lib.ctk_arnoldi_step(
+            self.dg.handle, int(self.ab), self.basis.W.data_ptr(), self.basis.ld, j,
+            self.q.data_ptr(), self.tmp.data_ptr(), stage, back, hrow.data_ptr(), self.hcols,
+            self.h_host[j].data_ptr(), self.basis.scratch(sa), sa.cuda_stream), "ctk_arnoldi_step")
         self.d2h += 8 * self.hcols
         ev = torch.cuda.Event()
-        ev.record(self.stream)
+        ev.record(sa)
         self.ev_h[j] = ev
 
-    def _iterate(self, it, k, y):
-        """Enqueue x_k = x0 + (B) W y, r = b - A x_k, norms into slot it."""
-        torch = self.torch
-        with torch.cuda.stream(self.stream):
-            self.y_pin[it, :k] = torch.from_numpy(y)
-            self.y_dev[it, :k].copy_(self.y_pin[it, :k], non_blocking=True)
+    def _iterate(self, it, k, y, after):
+        """Enqueue on sb: x_k = x0 + (B) W y, r = b - A x_k, norms -> slot it."""
+        torch, sb = self.torch, self.sb
+        sb.wait_event(after)
+        self.y_pin[it, :k] = torch.from_numpy(y)
         self.h2d += 8 * k
-        ydev = self.y_dev[it]
-        nrm = self.norms[it]
-        if self.ab:
-            self.basis.combine(k, ydev, self.z, stream=self.stream)
-            self._back(self.z, self.xk, x0=self.x_cur)
-            self.basis.norm2(self.xk, nrm[1:2], self.stream)
-        else:
-            self.basis.combine(k, ydev, self.xk, x0=self.x_cur, norm_out=nrm[1:2],
-                               stream=self.stream)
-        self._fwd(self.xk, self.r, b=self.b)
-        self.basis.norm2(self.r, nrm[0:1], self.stream)
+        stage, back = self._work(sb)
+        _native.check(self.lib.ctk_iterate(
+            self.dg.handle, int(self.ab), self.basis.W.data_ptr(), self.basis.ld, k,
+            self.y_pin[it].data_ptr(), self.y_dev[it].data_ptr(), self.x_cur.data_ptr(),
+            self.xk.data_ptr(), _native.ptr(self.z), self.b.data_ptr(), self.r.data_ptr(),
+            self.norms[it].data_ptr(), stage, back, self.basis.scratch(sb), sb.cuda_stream),
+            "ctk_iterate")
         ev = torch.cuda.Event(enable_timing=True)
-        ev.record(self.stream)
+        ev.record(sb)
         return ev
 
-    def _host_vec(self, t):
+    def _host_vec(self, t, stream):
         self.d2h += 4 * t.numel()
-        with self.torch.cuda.stream(self.stream):
-            return t.to("cpu", non_blocking=False).numpy().astype(np.float64)
+        stream.synchronize()
+        return t.to("cpu").numpy().astype(np.float64)
+
+    def _cycle_start(self):
+        """r0 = b - A x (AB) or B(b - A x) (BA) into W row 0; returns (beta, ||d0||)."""
+        torch, sa = self.torch, self.sa
+        w0 = self.basis.row(0)
+        if self.ab:
+            self._fwd(self.x_cur, w0, sa, b=self.b)
+            self.basis.norm2(w0, self.scal[0:1], sa)
+        else:
+            self._fwd(self.x_cur, self.tmp, sa, b=self.b)
+            self.basis.norm2(self.tmp, self.scal[1:2], sa)
+            self._back(self.tmp, w0, sa)
+            self.basis.norm2(w0, self.scal[0:1], sa)
+        with torch.cuda.stream(sa):
+            self.scal_host.copy_(self.scal, non_blocking=True)
+        self.d2h += 32
+        sa.synchronize()
+        beta = float(np.sqrt(self.scal_host[0].item()))
+        d0n = beta if self.ab else float(np.sqrt(self.scal_host[1].item()))
+        return beta, d0n
 
     def run(self) -> SolveResult:
+        try:
+            from threadpoolctl import threadpool_limits
+            limiter = threadpool_limits(limits=1, user_api="blas")
+        except Exception:   # pragma: no cover - threadpoolctl is optional
+            limiter = None
+        try:
+            return self._run()
+        finally:
+            if limiter is not None:
+                limiter.restore_original_limits()
+
+    def _run(self) -> SolveResult:
         torch, cfg = self.torch, self.cfg
+        sa, sb = self.sa, self.sb
         K, p = self.K, self.p
+        pool = _pool()
         records: list[IterationRecord] = []
-        pending: list[tuple] = []          # (record, slot, event)
+        pending: list[tuple] = []          # (record, slot, event) awaiting norms
         history: list[float] = []
         snapshots: dict[int, np.ndarray] = {}
         stop = None
         cycles = 0
-        prev_lam = 0.0
+        state = {"prev_lam": 0.0}
         need_sync = cfg.stopping_rule != "none" or self.x_true is not None
         ev_start = torch.cuda.Event(enable_timing=True)
-        ev_start.record(self.stream)
+        ev_start.record(sa)
+        sb.wait_event(ev_start)
         t_start = time.perf_counter()
+        last_ev = None
         first_cycle = True
         while stop is None and len(records) < K:
             if not first_cycle:
-                with torch.cuda.stream(self.stream):
+                sa.wait_stream(sb)
+                with torch.cuda.stream(sa):
                     self.x_cur.copy_(self.xk)
             first_cycle = False
-            # ---- cycle start: r0 = b - A x (AB) or B(b - A x) (BA), beta = ||r0||
-            w0 = self.basis.row(0)
-            if self.ab:
-                self._fwd(self.x_cur, w0, b=self.b)
-                self.basis.norm2(w0, self.scal[0:1], self.stream)
-            else:
-                self._fwd(self.x_cur, self.r, b=self.b)
-                self.basis.norm2(self.r, self.scal[1:2], self.stream)
-                self._back(self.r, w0)
-                self.basis.norm2(w0, self.scal[0:1], self.stream)
-            with torch.cuda.stream(self.stream):
-                self.scal_host.copy_(self.scal, non_blocking=True)
-            self.d2h += 32
-            self.stream.synchronize()
-            beta = float(np.sqrt(self.scal_host[0].item()))
-            d0n = beta if self.ab else float(np.sqrt(self.scal_host[1].item()))
+            beta, d0n = self._cycle_start()
             if beta == 0.0:
                 stop = "breakdown"
                 if not records:
-                    x_host = self._host_vec(self.x_cur)
+                    x_host = self._host_vec(self.x_cur, sa)
                     records.append(self._make_record(0, 0.0, 0.0, d0n, 0.0,
                                                      float(np.linalg.norm(x_host)), x_host,
                                                      time.perf_counter() - t_start))
                 break
             cycles += 1
-            with torch.cuda.stream(self.stream):
+            with torch.cuda.stream(sa):
                 self.scal[2] = 1.0 / beta
-            self.basis.scale_into(w0, w0, self.scal[2:3], self.stream)
+            self.basis.scale_into(self.basis.row(0), self.basis.row(0), self.scal[2:3], sa)
+            sb.wait_stream(sa)                     # x_cur / W0 ready for the iterate stream
 
             steps = min(p, K - len(records))
-            cols: list[np.ndarray] = []
-            self._arnoldi(0)
-            last_ev = None
-            for j in range(steps):
-                self.ev_h[j].synchronize()
-                hrow = self.h_host[j].numpy()
-                cols.append(hrow[: j + 2].copy())
-                broke = hrow[self.hcols - 3] != 0.0
-                k = j + 1
-                if not broke and j + 1 < steps:
-                    self._arnoldi(j + 1)          # speculative: overlaps the host work below
-                H = hessenberg_from_columns(cols, k)
-                svd = svd_of_hessenberg(H)
+            code = _native.STRATEGY_CODES[cfg.lambda_strategy] if self.hybrid else 0
+            Hfull = np.zeros((steps + 1, steps))     # grows one column per step
+            queued = 0                             # Arnoldi steps enqueued on sa
+            futures: dict[int, tuple] = {}
+            done_k = 0                             # iterates handed to sb
+            last_k = steps
+            broke_at = None
+
+            def enqueue_to(n):
+                nonlocal queued
+                while queued < min(n, steps):
+                    self._arnoldi(queued)
+                    queued += 1
+
+            def consume(k):
+                """Iterate k (1-based in this cycle), strictly in order."""
+                nonlocal stop, last_ev
+                H, fut = futures.pop(k)
+                out, y = fut.result()
                 warn = False
-                if self.hybrid:
-                    try:
-                        lam = select_lambda(H, beta, cfg.lambda_strategy, cfg.lambda_value, svd=svd)
-                    except DegenerateCurveError:
-                        lam, warn = prev_lam, True
-                else:
+                if not self.hybrid:
                     lam = 0.0
-                prev_lam = lam
-                sol = solve_projected_tikhonov(H, beta, lam, svd=svd)
+                elif out[2] != 0.0:        # DegenerateCurveError: previous lambda (gmres.py:196-200)
+                    lam, warn = state["prev_lam"], True
+                    out, y = _projected_task(self.lib, H, beta, 1, lam)
+                else:
+                    lam = float(out[0])
+                state["prev_lam"] = lam
+                proj_res = float(out[1])
                 slot = len(records)
-                ev = self._iterate(slot, k, sol.y)
+                ev = self._iterate(slot, k, y, self.ev_h[k - 1])
                 last_ev = ev
                 rec = IterationRecord(k=slot + 1, lambda_used=float(lam), residual_norm=0.0,
                                       data_residual_norm=0.0,
-                                      proj_residual_norm=sol.proj_residual_norm,
+                                      proj_residual_norm=proj_res,
                                       solution_norm=0.0, lambda_warning=warn)
                 records.append(rec)
                 if cfg.snapshot_stride and rec.k % cfg.snapshot_stride == 0:
-                    snapshots[rec.k] = self._host_vec(self.xk)
+                    snapshots[rec.k] = self._host_vec(self.xk, sb)
                 if need_sync:
                     ev.synchronize()
                     self._finish(rec, slot, ev_start, ev)
                     history.append(rec.data_residual_norm)
                     if self.x_true is not None:
-                        xh = self._host_vec(self.xk)
-                        self._metrics(rec, xh)
+                        self._metrics(rec, self._host_vec(self.xk, sb))
                     if cfg.stopping_rule == "dp" and metrics.dp_should_stop(
                             rec.data_residual_norm, cfg.noise_norm, cfg.dp_tau):
                         stop = "dp"
                     elif cfg.stopping_rule == "ncp" and metrics.ncp_should_stop(
-                            self._host_vec(self.r), cfg.ncp_threshold):
+                            self._host_vec(self.r, sb), cfg.ncp_threshold):
                         stop = "ncp"
                     elif cfg.stopping_rule == "rns" and metrics.rns_should_stop(
                             history, cfg.rns_epsilon):
                         stop = "rns"
                 else:
                     pending.append((rec, slot, ev))
-                if broke and stop is None:
+                if broke_at is not None and k == broke_at and stop is None:
                     stop = "breakdown"
-                if stop is not None:
+
+            enqueue_to(self.LOOKAHEAD)
+            for j in range(steps):
+                self.ev_h[j].synchronize()
+                hrow = self.h_host[j].numpy()
+                k = j + 1
+                Hfull[: j + 2, j] = hrow[: j + 2]
+                broke = hrow[self.hcols - 3] != 0.0
+                H = Hfull[: k + 1, :k].copy()
+                futures[k] = (H, pool.submit(_projected_task, self.lib, H, beta, code,
+                                             cfg.lambda_value))
+                if broke:
+                    broke_at = last_k = k
+                else:
+                    enqueue_to(k + self.LOOKAHEAD)
+                # hand finished projected solves to the iterate stream, in order
+                while stop is None and done_k + 1 in futures and (
+                        need_sync or futures[done_k + 1][1].done()):
+                    done_k += 1
+                    consume(done_k)
+                if stop is not None or broke:
                     break
-            if last_ev is not None:
-                last_ev.synchronize()
-        self.stream.synchronize()
+            while stop is None and done_k < last_k and done_k + 1 in futures:
+                done_k += 1
+                consume(done_k)
+            if stop is None and broke_at is not None:
+                stop = "breakdown"
+        sa.synchronize()
+        sb.synchronize()
         if pending:
             norms = self.norms.cpu().numpy()
             self.d2h += self.norms.numel() * 8
             for rec, slot, ev in pending:
                 self._finish(rec, slot, ev_start, ev, norms)
         x_final = self.xk if records and records[-1].k > 0 else self.x_cur
-        x_out = x_final.clone() if self.keep_on_device else self._host_vec(x_final)
+        x_out = x_final.clone() if self.keep_on_device else self._host_vec(x_final, sb)
         res = SolveResult(x=x_out, records=records, stop_reason=stop or "maxiter",
                           cycles=max(cycles, 1), snapshots=snapshots)
         res.transfer = {"h2d_bytes": self.h2d, "d2h_bytes": self.d2h}
@@ -402,8 +508,8 @@ class _DeviceSolve:
 
     def _finish(self, rec, slot, ev_start, ev, norms=None):
         if norms is None:
-            norms = self.norms[slot].cpu().numpy()[None, :]
-            row = norms[0]
+            row = self.norms[slot].cpu().numpy()
+            self.d2h += 16
         else:
             row = norms[slot]
         rec.data_residual_norm = float(np.sqrt(row[0]))
@@ -428,8 +534,7 @@ class _DeviceSolve:
 
 def run_gmres(A: LinearOperator, B: LinearOperator, b, cfg: SolverConfig,
               x_true: np.ndarray | None = None, image_shape: tuple[int, int] | None = None,
-              *, stream=None, kernel_timer: KernelTimer | None = None,
-              keep_on_device: bool = False) -> SolveResult:
+              *, stream=None, keep_on_device: bool = False) -> SolveResult:
     """(Hybrid) AB-/BA-GMRES with optional restarting, on the GPU.
 
     ``b`` may be a host array (the reference's contract) or a CUDA tensor
@@ -444,7 +549,7 @@ def run_gmres(A: LinearOperator, B: LinearOperator, b, cfg: SolverConfig,
     if len(shape) != 1:
         raise OperatorShapeError(f"data vector has shape {shape}, expected ({A.rows},)")
     _check_dims(A, B, int(shape[0]))
-    return _DeviceSolve(A, B, b, cfg, x_true, image_shape, stream, kernel_timer,
+    return _DeviceSolve(A, B, b, cfg, x_true, image_shape, stream, None,
                         keep_on_device).run()
 
 

@@ -7,6 +7,6 @@ python bench.py --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/b2.json 2>gp
 for f in gpurun_out/b3.json gpurun_out/b2.json; do python - "$f" <<'PY'
 import json,sys
 d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
-print(sys.argv[1], "value %.3e" % d["value"], "ms/step %.3f" % d["ms_per_step"], "it/s", d.get("iters_per_s"), "roof", d["roofline"]["frac"], {k:(v["mean_ms"], v["gbs"]) for k,v in d["kernels"].items()})
+print(sys.argv[1], "value %.3e" % d["value"], "ms/step %.3f" % d["ms_per_step"], "it/s", d.get("iters_per_s"), "roof", d["roofline"]["frac"], {k:(v["mean_ms"], v.get("gbs")) for k,v in d["kernels"].items()})
 PY
 done

@@ -1,0 +1,292 @@
+"""Multi-GPU hybrid GMRES: angle sharding over NCCL.
+
+One process per GPU (torchrun), ``torch.distributed`` with NCCL over
+NVLink/NVSwitch.  Work is split by projection angle:
+
+* A is angle-sharded with a replicated image: each rank projects its own
+  sinogram rows, no communication.
+* B produces a partial image per rank (the rank's angles only); one
+  all-reduce (sum, fp32, n values) completes it.
+* AB-GMRES: Krylov vectors live in measurement space and are sharded with
+  the angles; every dot product / norm is a local partial plus one batched
+  fp64 all-reduce per CGS2 sweep (h1 with ||q||^2, h2, ||q2||^2).
+* BA-GMRES: Krylov vectors live in image space and are replicated; the only
+  collective is B's partial-image all-reduce.
+* The (k+1) x k Hessenberg, lambda selection and Tikhonov solve stay on the
+  host in fp64 and are computed redundantly on every rank from bitwise
+  identical all-reduced inputs, so no broadcast is needed.
+* Independent slices (the c5 batch) need none of this: each rank runs the
+  single-GPU driver on its own slices (bench.py's weak-scaling mode).
+
+The driver below is written against a small backend interface so that the
+same sharding logic runs on the GPU (:class:`CudaShardBackend`: libctk
+kernels + NCCL) and, in the CPU test suite, on a world_size-2 gloo group
+with a host backend supplied by the tests.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from .gmres import (GMRES_METHODS, ConfigError, IterationRecord, SolveResult, SolverConfig)
+from . import metrics
+from .arnoldi import solve_projected_tikhonov, hessenberg_from_columns
+from .regparam import DegenerateCurveError, select_lambda, svd_of_hessenberg
+
+
+def angle_shards(n_angles: int, world: int, mode: str = "interleaved") -> list[np.ndarray]:
+    """Angle indices owned by each rank.
+
+    "interleaved" (a = r mod world) balances the per-angle cost, which varies
+    with |cos| + |sin| (segments per ray); "blocks" gives contiguous ranges.
+    Every rank owns at least one angle.
+    """
+    if world < 1 or n_angles < world:
+        raise ValueError(f"cannot shard {n_angles} angles over {world} ranks")
+    idx = np.arange(n_angles)
+    if mode == "interleaved":
+        return [idx[r::world] for r in range(world)]
+    if mode == "blocks":
+        return [a for a in np.array_split(idx, world)]
+    raise ValueError(f"unknown shard mode {mode!r}")
+
+
+class ShardBackend:
+    """Interface of the sharded driver.
+
+    Vectors are backend arrays; the Krylov basis is owned by the backend
+    (``basis_*``), rows 0..k addressed by index.  Small fp64 messages go
+    through ``from_host_f64`` / ``allreduce`` / ``to_host_f64``.
+    """
+
+    n: int          # image size (replicated)
+    m_local: int    # this rank's sinogram rows * det_count
+
+    def zeros(self, size): raise NotImplementedError
+    def from_host(self, arr): raise NotImplementedError
+    def to_host(self, v): raise NotImplementedError
+    def from_host_f64(self, arr): raise NotImplementedError
+    def to_host_f64(self, v): raise NotImplementedError
+    def forward(self, x): raise NotImplementedError               # image -> local sinogram
+    def back_partial(self, u): raise NotImplementedError          # local sinogram -> partial image
+    def allreduce(self, v): raise NotImplementedError             # in-place sum over ranks
+    def norm2(self, v): raise NotImplementedError                 # fp64 scalar (local part)
+    def scale(self, v, a): raise NotImplementedError
+    def add(self, a, b): raise NotImplementedError
+    def sub(self, a, b): raise NotImplementedError
+    # Krylov basis
+    def basis_init(self, L, rows): raise NotImplementedError
+    def basis_set(self, j, v, scale): raise NotImplementedError   # row j = v * scale
+    def basis_row(self, j): raise NotImplementedError
+    def basis_dots(self, k, v, want_norm): raise NotImplementedError   # host fp64, k (+1)
+    def basis_update(self, k, coef, v): raise NotImplementedError      # v - sum coef_j W_j
+    def basis_combine(self, k, y): raise NotImplementedError           # sum y_j W_j
+
+
+def _allreduce_host(be, values) -> np.ndarray:
+    """All-reduce a small fp64 host vector through the backend (one message)."""
+    v = be.from_host_f64(np.asarray(values, dtype=np.float64))
+    be.allreduce(v)
+    return be.to_host_f64(v)
+
+
+def run_gmres_sharded(be: ShardBackend, b_local, cfg: SolverConfig, x0=None) -> SolveResult:
+    """(Hybrid) AB-/BA-GMRES over an angle-sharded projector pair.
+
+    Same configuration, records and stop reasons as the single-GPU driver
+    (ctkrylov/gmres.py:135-241).  ``b_local`` is this rank's slice of the data
+    (its angles' rows).  Returns the replicated iterate on every rank.
+    """
+    cfg.validate()
+    if cfg.method not in GMRES_METHODS:
+        raise ConfigError(f"run_gmres got non-GMRES method {cfg.method!r}")
+    ab = cfg.method.startswith("ab")
+    hybrid = cfg.method.endswith("-hybrid")
+    b = be.from_host(b_local) if isinstance(b_local, np.ndarray) else b_local
+    x = be.zeros(be.n) if x0 is None else be.from_host(np.asarray(x0, dtype=np.float64))
+    K = cfg.max_iter
+    p = cfg.restart_period if cfg.restart_period > 0 else K
+
+    def back_full(u):
+        img = be.back_partial(u)
+        be.allreduce(img)                     # N1: partial images summed over ranks
+        return img
+
+    def gdots(k, v, want_norm):               # global dots: local partial + one all-reduce
+        loc = be.basis_dots(k, v, want_norm)
+        return _allreduce_host(be, loc) if ab else loc
+
+    def gnorm2(v):
+        loc = be.norm2(v)
+        return float(_allreduce_host(be, [loc])[0]) if ab else loc
+
+    rows = min(p, K) + 1
+    be.basis_init(be.m_local if ab else be.n, rows)
+    records: list[IterationRecord] = []
+    history: list[float] = []
+    stop = None
+    cycles = 0
+    prev_lam = 0.0
+    t0 = time.perf_counter()
+    while stop is None and len(records) < K:
+        d0 = be.sub(b, be.forward(x))                          # local rows of b - A x
+        r0 = d0 if ab else back_full(d0)
+        beta = float(np.sqrt(gnorm2(r0)))
+        if beta == 0.0:
+            stop = "breakdown"
+            if not records:
+                dn = float(np.sqrt(_allreduce_host(be, [be.norm2(d0)])[0]))
+                records.append(IterationRecord(0, 0.0, 0.0, dn, 0.0,
+                                               float(np.sqrt(be.norm2(x))),
+                                               elapsed=time.perf_counter() - t0))
+            break
+        cycles += 1
+        be.basis_set(0, r0, 1.0 / beta)
+        cols: list[np.ndarray] = []
+        xc = x
+        for _ in range(min(p, K - len(records))):
+            k = len(cols)
+            w = be.basis_row(k)
+            q = be.forward(back_full(w)) if ab else back_full(be.forward(w))
+            # CGS2 with batched all-reduces: [h1, ||q||^2], h2, ||q2||^2
+            h1n = gdots(k + 1, q, True)
+            h1, qn = h1n[:-1], float(np.sqrt(h1n[-1]))
+            q = be.basis_update(k + 1, h1, q)
+            h2 = gdots(k + 1, q, False)
+            q = be.basis_update(k + 1, h2, q)
+            hk = float(np.sqrt(gnorm2(q)))
+            col = np.empty(k + 2)
+            col[: k + 1] = h1 + h2
+            col[k + 1] = hk
+            cols.append(col)
+            k += 1
+            broke = hk <= 1e-14 * qn
+            if not broke:
+                be.basis_set(k, q, 1.0 / hk)
+            H = hessenberg_from_columns(cols, k)
+            svd = svd_of_hessenberg(H)
+            warn = False
+            if hybrid:
+                try:
+                    lam = select_lambda(H, beta, cfg.lambda_strategy, cfg.lambda_value, svd=svd)
+                except DegenerateCurveError:
+                    lam, warn = prev_lam, True
+            else:
+                lam = 0.0
+            prev_lam = lam
+            sol = solve_projected_tikhonov(H, beta, lam, svd=svd)
+            z = be.basis_combine(k, sol.y)
+            xk = be.add(xc, back_full(z) if ab else z)
+            r = be.sub(b, be.forward(xk))
+            dn = float(np.sqrt(_allreduce_host(be, [be.norm2(r)])[0]))
+            rec = IterationRecord(k=len(records) + 1, lambda_used=float(lam),
+                                  residual_norm=dn if ab else sol.proj_residual_norm,
+                                  data_residual_norm=dn,
+                                  proj_residual_norm=sol.proj_residual_norm,
+                                  solution_norm=float(np.sqrt(be.norm2(xk))),
+                                  elapsed=time.perf_counter() - t0, lambda_warning=warn)
+            records.append(rec)
+            history.append(dn)
+            x = xk
+            if cfg.stopping_rule == "dp" and metrics.dp_should_stop(dn, cfg.noise_norm, cfg.dp_tau):
+                stop = "dp"
+            elif cfg.stopping_rule == "rns" and metrics.rns_should_stop(history, cfg.rns_epsilon):
+                stop = "rns"
+            elif cfg.stopping_rule == "ncp":
+                raise ConfigError("ncp stopping needs the gathered residual; use the single-GPU driver")
+            if broke and stop is None:
+                stop = "breakdown"
+            if stop is not None:
+                break
+    return SolveResult(x=be.to_host(x), records=records, stop_reason=stop or "maxiter",
+                       cycles=max(cycles, 1))
+
+
+class CudaShardBackend(ShardBackend):
+    """libctk projectors on this rank's angles + NCCL all-reduce (fp32 / fp64).
+
+    Vectors are CUDA tensors (fp32 for images/sinograms, fp64 for the small
+    reduction messages).  The process group defaults to the world group.
+    """
+
+    def __init__(self, grid, geometry, angle_idx, device: int = 0, group=None):
+        import torch
+        import torch.distributed as tdist
+
+        from .ct import DeviceGeometry, ParallelGeometry
+
+        self.torch, self.dist, self.group = torch, tdist, group
+        self.dev = torch.device("cuda", device)
+        local = ParallelGeometry(np.asarray(geometry.angles)[np.asarray(angle_idx)],
+                                 geometry.det_count, geometry.det_spacing)
+        self.dg = DeviceGeometry(grid, local, device)
+        self.n = self.dg.n
+        self.m_local = self.dg.m
+
+    def zeros(self, size):
+        return self.torch.zeros(size, dtype=self.torch.float32, device=self.dev)
+
+    def from_host(self, arr):
+        return self.torch.from_numpy(np.asarray(arr, dtype=np.float32)).to(self.dev)
+
+    def to_host(self, v):
+        return v.cpu().numpy().astype(np.float64)
+
+    def from_host_f64(self, arr):
+        return self.torch.from_numpy(arr).to(self.dev)
+
+    def to_host_f64(self, v):
+        return v.cpu().numpy()
+
+    def forward(self, x):
+        return self.dg.forward(x)
+
+    def back_partial(self, u):
+        return self.dg.back(u)
+
+    def allreduce(self, v):
+        self.dist.all_reduce(v, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def norm2(self, v):
+        return float(self.torch.dot(v.double(), v.double()).item())
+
+    def scale(self, v, a):
+        return (v.double() * a).float()
+
+    def add(self, a, b):
+        return a + b
+
+    def sub(self, a, b):
+        return a - b
+
+    # Krylov basis on libctk's K3/K4 kernels (fp64 accumulation, deterministic)
+    def basis_init(self, L, rows):
+        from .arnoldi import DeviceBasis
+        self.basis = DeviceBasis(L, rows, self.dev, self.torch)
+        self.stream = self.torch.cuda.current_stream(self.dev)
+        self._out = self.torch.zeros(rows + 2, dtype=self.torch.float64, device=self.dev)
+
+    def basis_set(self, j, v, scale):
+        self.basis.row(j).copy_(v)
+        self.basis.row(j).mul_(scale)
+
+    def basis_row(self, j):
+        return self.basis.row(j)
+
+    def basis_dots(self, k, v, want_norm):
+        self.basis.dots(k, v, self._out, want_norm, self.stream)
+        return self._out[: k + (1 if want_norm else 0)].cpu().numpy().copy()
+
+    def basis_update(self, k, coef, v):
+        c = self.torch.from_numpy(np.asarray(coef, dtype=np.float64)).to(self.dev)
+        out = self.torch.empty_like(v)
+        self.basis.update(k, c, v, out, stream=self.stream)
+        return out
+
+    def basis_combine(self, k, y):
+        yd = self.torch.from_numpy(np.asarray(y, dtype=np.float64)).to(self.dev)
+        out = self.torch.empty(self.basis.L, dtype=self.torch.float32, device=self.dev)
+        self.basis.combine(k, yd, out, stream=self.stream)
+        return out

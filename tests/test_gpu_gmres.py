@@ -141,3 +141,36 @@ def test_x_true_metrics(cuda, golden):
     res = gmres.run_gmres(A, B, d["b"], gmres.SolverConfig(method="ab", max_iter=5),
                           x_true=x_true, image_shape=(16, 16))
     assert all(r.rre is not None and r.ssim is not None for r in res.records)
+
+
+def test_sharded_driver_world1_nccl_matches_single_gpu(cuda, golden):
+    """CudaShardBackend (libctk projectors + K3/K4 + NCCL all-reduce) on a
+    world_size-1 process group reproduces the single-GPU driver."""
+    import os
+    import socket
+    import torch.distributed as tdist
+    from paper_2602_17892_b200 import dist
+
+    spec, z, b = config_b(golden, "c1")
+    A, B = ops_for(spec)
+    ref = gmres.run_gmres(A, B, b, gmres.SolverConfig(method="ab-hybrid", lambda_strategy="gcv",
+                                                      max_iter=20))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        grid = ct.ImageGrid(spec.N, spec.N, 1.0)
+        geom = ct.ParallelGeometry(spec.angles(), spec.det_count, 1.0)
+        idx = dist.angle_shards(spec.n_angles, 1)[0]
+        be = dist.CudaShardBackend(grid, geom, idx, device=0)
+        res = dist.run_gmres_sharded(be, b, gmres.SolverConfig(method="ab-hybrid",
+                                                               lambda_strategy="gcv", max_iter=20))
+    finally:
+        tdist.destroy_process_group()
+    np.testing.assert_allclose(records(res, "data_residual_norm"),
+                               records(ref, "data_residual_norm"), rtol=1e-5)
+    np.testing.assert_allclose(records(res, "lambda_used"), records(ref, "lambda_used"), rtol=1e-2)
+    assert rel(res.x, ref.x) < 1e-4

@@ -1,0 +1,149 @@
+"""Pin the CPU oracle to the reference (CPU, no GPU).
+
+tests/golden/*.npz were produced by running the unmodified reference
+(tests/golden/make_golden.py).  The oracle must reproduce the projector
+outputs bit-for-bit and the solver records to rounding level.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2602_17892_b200 import problems
+
+
+def small_names(d):
+    return sorted({k.split("/")[0] for k in d.files})
+
+
+def geometry(d, nm):
+    nx, ny, h, D, sp = d[f"{nm}/params"]
+    return O.Geometry(int(nx), int(ny), float(h), d[f"{nm}/angles"], int(D), float(sp))
+
+
+def test_small_operators_bit_exact(golden):
+    d = golden("small_ops")
+    for nm in small_names(d):
+        g = geometry(d, nm)
+        np.testing.assert_array_equal(O.forward(g, d[f"{nm}/x"]), d[f"{nm}/Ax"], err_msg=nm)
+        np.testing.assert_array_equal(O.back(g, d[f"{nm}/u"]), d[f"{nm}/Bu"], err_msg=nm)
+
+
+def test_small_operators_dense_bit_exact(golden):
+    d = golden("small_ops")
+    for nm in small_names(d):
+        g = geometry(d, nm)
+        if g.n * g.m > 200_000:
+            continue
+        A = np.column_stack([O.forward(g, e) for e in np.eye(g.n)])
+        B = np.column_stack([O.back(g, e) for e in np.eye(g.m)])
+        np.testing.assert_array_equal(A, d[f"{nm}/A_dense"], err_msg=nm)
+        np.testing.assert_array_equal(B, d[f"{nm}/B_dense"], err_msg=nm)
+
+
+def test_csr_form_matches_reference_spmv(golden):
+    d = golden("small_ops")
+    for nm in small_names(d):
+        g = geometry(d, nm)
+        np.testing.assert_array_equal(O.CsrForward(g)(d[f"{nm}/x"]), d[f"{nm}/Ax"], err_msg=nm)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_config_projections_bit_exact(golden, cfg):
+    spec = problems.CONFIGS[cfg]
+    z = golden(cfg)
+    g = O.Geometry(spec.N, spec.N, 1.0, spec.angles(), spec.det_count, 1.0)
+    xt = problems.random_ellipse_phantom(spec.N, spec.ellipses, spec.phantom_seed)
+    np.testing.assert_array_equal(O.forward(g, xt), z["Ax_true"])
+    np.testing.assert_array_equal(O.forward(g, problems.uniform_image(g.n, 0)), z["Ax_uniform"])
+    np.testing.assert_array_equal(O.back(g, problems.uniform_sinogram(g.m, 1)), z["Bu_uniform"])
+    raw, nnz = O.row_counts(g)
+    assert int(nnz.sum()) == int(z["nnz"])
+    assert int(raw.sum()) == {"c1": 3755392, "c2": 30039404}[cfg]
+
+
+def test_reference_test_vectors(golden):
+    """Known answers from the reference's own unit tests (tests/test_ct.py)."""
+    g = O.Geometry(8, 8, 0.5, [0.0], 1, 0.5)                       # test_ct.py:53-58
+    assert O.forward(g, np.ones(64))[0] == pytest.approx(8 * 0.5, abs=1e-12)
+    g = O.Geometry(6, 6, 1.0, [np.pi / 4], 1, 1.0)                 # test_ct.py:60-65
+    assert O.forward(g, np.ones(36))[0] == pytest.approx(np.sqrt(2) * 6, abs=1e-10)
+    g = O.Geometry(4, 4, 0.5, [0.0], 3, 10.0)                      # test_ct.py:95-99
+    A = np.column_stack([O.forward(g, e) for e in np.eye(16)])
+    assert np.all(A[0] == 0.0) and np.all(A[2] == 0.0)
+    # mass consistency vs the analytic chord, test_ct.py:74-81
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        theta, s = rng.uniform(0, np.pi), rng.uniform(-2.0, 2.0)
+        g = O.Geometry(12, 12, 0.25, [theta], 1, 1.0)
+        _, ln = O.siddon_ray(g, 0, s)
+        ct, st = np.cos(theta), np.sin(theta)
+        px, py, dx, dy = s * ct, s * st, -st, ct
+        t0, t1 = -1e30, 1e30
+        ok = True
+        for p0, dd in ((px, dx), (py, dy)):
+            if abs(dd) < 1e-14:
+                ok &= -1.5 <= p0 <= 1.5
+            else:
+                a, b = (-1.5 - p0) / dd, (1.5 - p0) / dd
+                t0, t1 = max(t0, min(a, b)), min(t1, max(a, b))
+        chord = max(t1 - t0, 0.0) if ok else 0.0
+        assert ln.sum() == pytest.approx(chord, abs=1e-10)
+
+
+CASES = {
+    "ab_plain": dict(method="ab", max_iter=12),
+    "ba_plain": dict(method="ba", max_iter=12),
+    "ab_gcv": dict(method="ab-hybrid", strategy="gcv", max_iter=15),
+    "ba_gcv": dict(method="ba-hybrid", strategy="gcv", max_iter=15),
+    "ab_lcurve": dict(method="ab-hybrid", strategy="lcurve", max_iter=15),
+    "ba_fixed": dict(method="ba-hybrid", strategy="fixed", lambda_value=0.3, max_iter=10),
+    "ab_restart": dict(method="ab-hybrid", strategy="gcv", max_iter=14, restart_period=5),
+    "ab_dp": dict(method="ab", max_iter=40, stopping_rule="dp"),
+    "ba_rns": dict(method="ba", max_iter=40, stopping_rule="rns", rns_epsilon=1e-3),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_oracle_gmres_branches(golden, case):
+    d = golden("solver_cases")
+    A, B, b = d["A_dense"], d["B_dense"], d["b"]
+    kw = dict(CASES[case])
+    if kw.get("stopping_rule") == "dp":
+        kw["noise_norm"] = float(d["noise_norm"])
+    r = O.gmres(lambda v: A @ v, lambda v: B @ v, b, **kw)
+    assert r.stop_reason == str(d[f"{case}/stop"])
+    assert r.cycles == int(d[f"{case}/cycles"])
+    dn = np.array([x["data_residual_norm"] for x in r.records])
+    ref = d[f"{case}/rec/data_residual_norm"]
+    # dense A/B here vs the reference's CSR: identical math, different rounding,
+    # which unregularised GMRES amplifies past ~12 iterations
+    np.testing.assert_allclose(dn[:12], ref[:12], rtol=1e-6)
+    np.testing.assert_allclose(dn[12:], ref[12:], rtol=5e-3)
+    if "gcv" in case or "fixed" in case:
+        lam = np.array([x["lambda_used"] for x in r.records])
+        np.testing.assert_allclose(lam, d[f"{case}/rec/lambda_used"], rtol=1e-9)
+
+
+def test_oracle_lambda_selection_golden(golden):
+    d = golden("solver_cases")
+    for i in range(4):
+        H = d[f"lam/{i}/H"]
+        assert O.lambda_selection(H, 2.5, "gcv") == d[f"lam/{i}/gcv"]
+        assert O.lambda_selection(H, 2.5, "lcurve") == d[f"lam/{i}/lcurve"]
+
+
+@pytest.mark.slow
+def test_oracle_c1_hybrid_solve_bit_exact(golden):
+    spec = problems.CONFIGS["c1"]
+    z = golden("c1")
+    g = O.Geometry(spec.N, spec.N, 1.0, spec.angles(), spec.det_count, 1.0)
+    A = O.CsrForward(g)
+    b, _ = problems.add_noise(z["Ax_true"], spec.noise, spec.noise_seed)
+    b = b.astype(np.float32).astype(np.float64)
+    r = O.gmres(A, lambda u: O.back(g, u), b, spec.method, spec.strategy, spec.max_iter)
+    lam = np.array([x["lambda_used"] for x in r.records])
+    np.testing.assert_array_equal(lam, z["rec/lambda_used"])
+    dn = np.array([x["data_residual_norm"] for x in r.records])
+    np.testing.assert_array_equal(dn, z["rec/data_residual_norm"])
+    np.testing.assert_allclose(r.x.astype(np.float32), z["x_final"], rtol=0, atol=0)

@@ -44,6 +44,7 @@ struct ctk_geom {
     double h, det_spacing;
     double xmin, xmax, ymin, ymax, center;
     int back_wmax;            // max staged bins per angle for one K2 tile
+    int fwd_split;            // K1 row chunks per ray (small problems: more CTAs)
     int n_degenerate;
     int h_pow2;               // pixel size is a power of two: x / h == x * (1 / h) exactly
     double inv_h;
@@ -56,10 +57,11 @@ struct ctk_geom {
     double* d_offsets;        // [det_count] bitwise bin_offsets()
     // degenerate (axis-aligned) angles: literal-Siddon segment lists built once
     int* d_deg_slot;          // [n_angles] -> slot in the lists below, or -1
-    long long* d_deg_ptr;     // [n_degenerate * det_count + 1] segment offsets per ray
-    int* d_deg_pix;           // [total] pixel index
-    float* d_deg_len;         // [total] exact fp64 length rounded to fp32
+    long long* d_deg_ptr;     // [n_degenerate * det_count] kept segments per ray
+    int* d_deg_pix;           // [n_degenerate][deg_maxseg][det_count] pixel index
+    float* d_deg_len;         // same layout: exact fp64 length rounded to fp32
     long long deg_segments;
+    int deg_maxseg;
 };
 
 // Builds the degenerate-angle segment lists (ctk_forward.cu); called by
@@ -93,7 +95,9 @@ int ctk_check_cuda(cudaError_t e, const char* what);
 
 static inline cudaStream_t ctk_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// Pad counts for the K1 staging copies.
-static inline int64_t ctk_stage_floats(int nx, int ny) {
-    return (int64_t)ny * (nx + 2) + (int64_t)nx * (ny + 2);
+// K1 workspace: zero-bordered copies P, PT, then fwd_split row-chunk partials.
+static inline int64_t ctk_stage_floats(const ctk_geom* g) {
+    const int64_t m = (int64_t)g->n_angles * g->det_count;
+    return (int64_t)g->ny * (g->nx + 2) + (int64_t)g->nx * (g->ny + 2) +
+           (g->fwd_split > 1 ? (int64_t)g->fwd_split * m : 0);
 }

@@ -133,14 +133,15 @@ struct CountSink {
     }
 };
 
-struct FillSink {
+struct FillSink {          // segment i of a ray -> entry i * stride of its column
     int* pix;
     float* len;
     long long i;
+    long long stride;
     __device__ void operator()(long long p, double l) {
         pix[i] = (int)p;
         len[i] = (float)l;
-        ++i;
+        i += stride;
     }
 };
 
@@ -205,10 +206,13 @@ struct FwdArgs {
     const float* PT;         // zero-bordered transposed copy
     const float* b;          // optional: y = b - A x
     float* y;
+    float* part;             // split > 1: per-row-chunk partial sums [split][rows * D]
+    int split;               // row chunks per ray (blockIdx.z), small-problem parallelism
     const int* deg_slot;
-    const long long* deg_ptr;
-    const int* deg_pix;
+    const long long* deg_cnt;   // segments per degenerate ray [slot * D + j]
+    const int* deg_pix;         // [slot][maxseg][D]: ray-interleaved, coalesced per warp
     const float* deg_len;
+    int deg_maxseg;
     ExactGrid eg;
     int D, a0, a1;
 };
@@ -217,7 +221,8 @@ struct FwdArgs {
 // the zero-bordered copy the ray walks; MIRROR reverses the cross axis.
 template <bool MIRROR>
 __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
-                                           const float* __restrict__ base, int R, int C) {
+                                           const float* __restrict__ base, int R, int C,
+                                           int krow0, int krow1) {
     const double sigma = (double)p.sigma_fx * (1.0 / 4294967296.0);
     const double u0 = fma(p.beta, s, p.alpha);
     // the ray meets the image iff u(k) in (0, C) for some k in [0, R]
@@ -233,8 +238,8 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
     if (U0 >= C2) return 0.0;
     if (Sg == 0) ke = R;
     else ke = (C2 - U0 + Sg - 1) / Sg;          // smallest k with U0 + k Sg >= C
-    if (kb < 0) kb = 0;
-    if (ke > R) ke = R;
+    if (kb < krow0) kb = krow0;               // this block's row chunk only
+    if (ke > krow1) ke = krow1;
     if (kb >= ke) return 0.0;
 
     const int pitch = C + 2;
@@ -282,47 +287,70 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
     return acc;
 }
 
-// Degenerate angle: warp per ray over the precomputed literal segment list.
-__device__ __forceinline__ void degenerate_block(const FwdArgs& A, int a, int slot) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int jb = blockIdx.x * FWD_THREADS + warp * 32;
-    for (int r = 0; r < 32; ++r) {
-        const int j = jb + r;
-        if (j >= A.D) break;
-        const long long ray = (long long)slot * A.D + j;
-        const long long beg = A.deg_ptr[ray], end = A.deg_ptr[ray + 1];
-        double s = 0.0;
-        for (long long e = beg + lane; e < end; e += 32)
-            s = fma((double)__ldg(A.deg_len + e), (double)__ldg(A.x + __ldg(A.deg_pix + e)), s);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) {
-            const size_t o = (size_t)(a - A.a0) * A.D + j;
-            A.y[o] = A.b ? (float)((double)A.b[o] - s) : (float)s;
+// Degenerate angle: thread per ray over its precomputed literal segments,
+// stored ray-interleaved so a warp's loads are coalesced like the walk's.
+__device__ __forceinline__ double degenerate_ray(const FwdArgs& A, int slot, int j, int e0,
+                                                 int e1) {
+    const long long cnt = A.deg_cnt[(size_t)slot * A.D + j];
+    if (e1 > cnt) e1 = (int)cnt;
+    const size_t base = (size_t)slot * A.deg_maxseg * A.D + j;
+    double acc = 0.0;
+    float s = 0.f;
+    int e = e0;
+    while (e < e1) {
+        const int stop = min(e1, e + 48);
+#pragma unroll 8
+        for (; e < stop; ++e) {
+            const size_t o = base + (size_t)e * A.D;
+            s = fmaf(__ldg(A.deg_len + o), __ldg(A.x + __ldg(A.deg_pix + o)), s);
         }
+        acc += (double)s;
+        s = 0.f;
     }
+    return acc;
 }
 
 __global__ void __launch_bounds__(FWD_THREADS, 12) k_forward(FwdArgs A) {
     const int a = A.a0 + blockIdx.y;
     const int slot = A.deg_slot[a];
-    if (slot >= 0) {                         // whole block: warp-uniform branch
-        degenerate_block(A, a, slot);
-        return;
-    }
+    const int chunk = blockIdx.z;
+    const size_t rows = (size_t)(A.a1 - A.a0) * A.D;
     const int j = blockIdx.x * FWD_THREADS + threadIdx.x;
     if (j >= A.D) return;
+    if (slot >= 0) {                         // whole block: warp-uniform branch
+        const int per = (A.deg_maxseg + A.split - 1) / A.split;
+        const double acc = degenerate_ray(A, slot, j, chunk * per, (chunk + 1) * per);
+        const size_t o = (size_t)blockIdx.y * A.D + j;
+        if (A.split > 1) A.part[chunk * rows + o] = (float)acc;
+        else A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
+        return;
+    }
     const AngleParams p = A.ap[a];
     const double s = A.offsets[j];
+    const int R = p.frame == 0 ? A.eg.ny : A.eg.nx;
+    const int per = (R + A.split - 1) / A.split;
+    const int k0 = chunk * per, k1 = min(R, k0 + per);
     double acc;
     if (p.frame == 0)
-        acc = p.mirror ? walk_ray<true>(p, s, A.P, A.eg.ny, A.eg.nx)
-                       : walk_ray<false>(p, s, A.P, A.eg.ny, A.eg.nx);
+        acc = p.mirror ? walk_ray<true>(p, s, A.P, A.eg.ny, A.eg.nx, k0, k1)
+                       : walk_ray<false>(p, s, A.P, A.eg.ny, A.eg.nx, k0, k1);
     else
-        acc = p.mirror ? walk_ray<true>(p, s, A.PT, A.eg.nx, A.eg.ny)
-                       : walk_ray<false>(p, s, A.PT, A.eg.nx, A.eg.ny);
+        acc = p.mirror ? walk_ray<true>(p, s, A.PT, A.eg.nx, A.eg.ny, k0, k1)
+                       : walk_ray<false>(p, s, A.PT, A.eg.nx, A.eg.ny, k0, k1);
     const size_t o = (size_t)blockIdx.y * A.D + j;
-    A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
+    if (A.split > 1) A.part[chunk * rows + o] = (float)acc;
+    else A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
+}
+
+// Row-chunk partials -> y (fixed summation order; b - A x epilogue).
+__global__ void k_forward_finalize(const float* __restrict__ part, int split, size_t rows,
+                                   const float* __restrict__ b, float* __restrict__ y) {
+    for (size_t o = blockIdx.x * (size_t)blockDim.x + threadIdx.x; o < rows;
+         o += (size_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < split; ++c) s += (double)part[(size_t)c * rows + o];
+        y[o] = b ? (float)((double)b[o] - s) : (float)s;
+    }
 }
 
 // Literal fp64 Siddon for every ray (validation path, ctk_forward_exact).
@@ -356,20 +384,22 @@ __global__ void __launch_bounds__(FWD_THREADS) k_count(FwdArgs A, unsigned long 
     }
 }
 
-// Degenerate-angle segment lists: pass 1 counts, pass 2 fills.
+// Degenerate-angle segment lists: pass 1 counts, pass 2 fills the
+// ray-interleaved [slot][e][D] layout.
 __global__ void k_deg_lists(ExactGrid eg, const AngleParams* ap, const double* cos_tab,
                             const double* sin_tab, const double* offsets, const int* angles,
-                            int n_deg, int D, long long* ptr_or_counts, int* pix, float* len) {
+                            int n_deg, int D, long long* counts, int maxseg, int* pix, float* len) {
     const long long ray = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (ray >= (long long)n_deg * D) return;
-    const int a = angles[ray / D];
+    const int slot = (int)(ray / D);
+    const int a = angles[slot];
     const int j = (int)(ray % D);
     if (pix == nullptr) {
         CountSink c;
         trace_exact(eg, cos_tab[a], sin_tab[a], offsets[j], ap[a], c);
-        ptr_or_counts[ray + 1] = c.raw;
+        counts[ray] = c.raw;
     } else {
-        FillSink f{pix, len, ptr_or_counts[ray]};
+        FillSink f{pix, len, (long long)slot * maxseg * D + j, D};
         trace_exact(eg, cos_tab[a], sin_tab[a], offsets[j], ap[a], f);
     }
 }
@@ -387,13 +417,16 @@ static FwdArgs make_args(const ctk_geom* g, const float* x, float* y, int a0, in
     A.b = b;
     A.y = y;
     A.deg_slot = g->d_deg_slot;
-    A.deg_ptr = g->d_deg_ptr;
+    A.deg_cnt = g->d_deg_ptr;
     A.deg_pix = g->d_deg_pix;
     A.deg_len = g->d_deg_len;
+    A.deg_maxseg = g->deg_maxseg;
     A.eg = ExactGrid{g->nx, g->ny, g->h, g->xmin, g->xmax, g->ymin, g->ymax, g->inv_h, g->h_pow2};
     A.D = g->det_count;
     A.a0 = a0;
     A.a1 = a1;
+    A.split = 1;
+    A.part = nullptr;
     return A;
 }
 
@@ -420,6 +453,7 @@ int ctk_build_degenerate_lists(ctk_geom* g) {
     CTK_CUDA(cudaMalloc(&g->d_deg_ptr, sizeof(long long) * (rays + 1)));
     CTK_CUDA(cudaMemset(g->d_deg_ptr, 0, sizeof(long long) * (rays + 1)));
     g->deg_segments = 0;
+    g->deg_maxseg = 0;
     if (rays == 0) return CTK_OK;
     int* d_angles = nullptr;
     CTK_CUDA(cudaMalloc(&d_angles, sizeof(int) * angles.size()));
@@ -428,28 +462,32 @@ int ctk_build_degenerate_lists(ctk_geom* g) {
     const ExactGrid eg{g->nx, g->ny, g->h, g->xmin, g->xmax, g->ymin, g->ymax, g->inv_h, g->h_pow2};
     const int threads = 128;
     const int blocks = (int)((rays + threads - 1) / threads);
+    const int D = g->det_count;
     k_deg_lists<<<blocks, threads>>>(eg, g->d_ap, g->d_cos, g->d_sin, g->d_offsets, d_angles,
-                                    (int)angles.size(), g->det_count, g->d_deg_ptr, nullptr,
-                                    nullptr);
+                                    (int)angles.size(), D, g->d_deg_ptr, 0, nullptr, nullptr);
     cudaError_t e = cudaGetLastError();
-    std::vector<long long> ptr(rays + 1);
+    std::vector<long long> cnt(rays);
     if (e == cudaSuccess)
-        e = cudaMemcpy(ptr.data(), g->d_deg_ptr, sizeof(long long) * (rays + 1),
-                       cudaMemcpyDeviceToHost);
+        e = cudaMemcpy(cnt.data(), g->d_deg_ptr, sizeof(long long) * rays, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) {
         cudaFree(d_angles);
         return ctk_check_cuda(e, "degenerate segment count");
     }
-    for (long long r = 0; r < rays; ++r) ptr[r + 1] += ptr[r];
-    g->deg_segments = ptr[rays];
-    e = cudaMemcpy(g->d_deg_ptr, ptr.data(), sizeof(long long) * (rays + 1),
-                   cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&g->d_deg_pix, sizeof(int) * (g->deg_segments + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&g->d_deg_len, sizeof(float) * (g->deg_segments + 1));
+    long long mx = 0;
+    for (long long r = 0; r < rays; ++r) {
+        g->deg_segments += cnt[r];
+        if (cnt[r] > mx) mx = cnt[r];
+    }
+    g->deg_maxseg = (int)(mx > 0 ? mx : 1);
+    const size_t entries = (size_t)angles.size() * g->deg_maxseg * D;
+    e = cudaMalloc(&g->d_deg_pix, sizeof(int) * entries);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_deg_len, sizeof(float) * entries);
+    if (e == cudaSuccess) e = cudaMemset(g->d_deg_pix, 0, sizeof(int) * entries);
+    if (e == cudaSuccess) e = cudaMemset(g->d_deg_len, 0, sizeof(float) * entries);
     if (e == cudaSuccess) {
         k_deg_lists<<<blocks, threads>>>(eg, g->d_ap, g->d_cos, g->d_sin, g->d_offsets,
-                                        d_angles, (int)angles.size(), g->det_count,
-                                        g->d_deg_ptr, g->d_deg_pix, g->d_deg_len);
+                                        d_angles, (int)angles.size(), D, g->d_deg_ptr,
+                                        g->deg_maxseg, g->d_deg_pix, g->d_deg_len);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -483,9 +521,18 @@ extern "C" int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0
     FwdArgs A = make_args(g, x, y, a0, a1, b);
     A.P = P;
     A.PT = PT;
-    dim3 grid((g->det_count + FWD_THREADS - 1) / FWD_THREADS, a1 - a0);
+    A.split = g->fwd_split;
+    A.part = PT + (size_t)g->nx * (g->ny + 2);
+    dim3 grid((g->det_count + FWD_THREADS - 1) / FWD_THREADS, a1 - a0, A.split);
     k_forward<<<grid, FWD_THREADS, 0, st>>>(A);
     CTK_LAUNCH_CHECK("k_forward");
+    if (A.split > 1) {
+        const size_t rows = (size_t)(a1 - a0) * g->det_count;
+        int blocks = (int)((rows + 255) / 256);
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        k_forward_finalize<<<blocks, 256, 0, st>>>(A.part, A.split, rows, b, y);
+        CTK_LAUNCH_CHECK("k_forward_finalize");
+    }
     ctk_prof_close(ph, st);
     return CTK_OK;
 }

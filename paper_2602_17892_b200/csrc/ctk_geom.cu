@@ -166,6 +166,15 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
         g->n_degenerate += p.degenerate;
     }
     g->back_wmax = (int)ceil(max_span) + 6;
+    {   // K1 row split: aim for ~3 waves of 128-thread CTAs on 148 SMs
+        const int64_t m = (int64_t)n_angles * det_count;
+        int64_t sp = (148LL * 2048 * 3 / 2 + m - 1) / m;
+        if (sp < 1) sp = 1;
+        if (sp > 4) sp = 4;
+        const int rmin = nx < ny ? nx : ny;
+        if (rmin < 64) sp = 1;
+        g->fwd_split = (int)sp;
+    }
     if ((size_t)BCA * g->back_wmax * sizeof(float) > 200 * 1024) {
         free_geom(g);
         return ctk_fail(CTK_ERR_GEOMETRY,
@@ -216,7 +225,7 @@ extern "C" int ctk_geom_info(const ctk_geom_t* g, int64_t* n, int64_t* m, int64_
     if (!g) return ctk_fail(CTK_ERR_ARG, "null geometry");
     if (n) *n = (int64_t)g->nx * g->ny;
     if (m) *m = (int64_t)g->n_angles * g->det_count;
-    if (stage_floats) *stage_floats = ctk_stage_floats(g->nx, g->ny);
+    if (stage_floats) *stage_floats = ctk_stage_floats(g);
     if (n_degenerate) *n_degenerate = g->n_degenerate;
     return CTK_OK;
 }

@@ -14,7 +14,9 @@
 // warp shuffles, a per-CTA smem pass, one fp64 partial per (chunk, row), and a
 // last-CTA-done pass (integer ticket, no float atomics) that sums the chunk
 // partials in a fixed order -- bitwise reproducible run to run.
+#include <cooperative_groups.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "ctk_common.cuh"
 
@@ -232,9 +234,249 @@ __global__ void k_cgs2_finalize(const double* h1, const double* h2, const double
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fused CGS2 step for small Krylov vectors (c1/c2: L <= 1M): one cooperative
+// launch, one CTA per SM, five grid-wide barriers instead of six launches.
+// Each CTA owns a contiguous chunk of L; each warp owns basis rows j = warp
+// (mod 8) and reduces them over the chunk, so no CTA-wide barrier is needed
+// for the dots.  Block partials are reduced warp-per-row in a fixed order.
+// ---------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+
+constexpr int FT = 256;                 // fused kernel threads per CTA
+constexpr int FW = FT / 32;
+
+__device__ __forceinline__ void chunk_of(int64_t L4, int64_t* i0, int64_t* i1) {
+    const int64_t ch = (L4 + gridDim.x - 1) / gridDim.x;
+    *i0 = (int64_t)blockIdx.x * ch;
+    *i1 = min(L4, *i0 + ch);
+}
+
+constexpr int FR = 16;                  // rows per batch: 16 independent 16-B loads
+
+// partial[blk * nv + j] = <row_j, v> over this CTA's chunk (+ scalar tail on
+// the last CTA); row nvec is v itself (norm).  Each thread owns float4
+// elements of the chunk and streams FR rows at a time (memory-level
+// parallelism), then rows are reduced warp -> CTA through smem red[j][warp].
+__device__ __forceinline__ void chunk_dots(const float* W, int64_t ld, int nvec, const float* v,
+                                           int64_t L, bool norm, double* partial, double* red) {
+    const int nv = nvec + (norm ? 1 : 0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t i0, i1;
+    const int64_t L4 = L >> 2;
+    chunk_of(L4, &i0, &i1);
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    const bool tail = blockIdx.x == gridDim.x - 1;
+    for (int j0 = 0; j0 < nv; j0 += FR) {
+        double acc[FR];
+#pragma unroll
+        for (int q = 0; q < FR; ++q) acc[q] = 0.0;
+        for (int64_t i = i0 + threadIdx.x; i < i1; i += FT) {
+            const float4 vv = v4[i];
+            float4 w[FR];
+#pragma unroll
+            for (int q = 0; q < FR; ++q) {
+                const int j = j0 + q;
+                if (j < nv) w[q] = __ldg(reinterpret_cast<const float4*>(j < nvec ? W + (size_t)j * ld : v) + i);
+            }
+#pragma unroll
+            for (int q = 0; q < FR; ++q)
+                if (j0 + q < nv) acc[q] = dot4(w[q], vv, acc[q]);
+        }
+        if (tail) {
+            for (int64_t i = (L4 << 2) + threadIdx.x; i < L; i += FT) {
+                const double vv = (double)v[i];
+#pragma unroll
+                for (int q = 0; q < FR; ++q) {
+                    const int j = j0 + q;
+                    if (j < nv) acc[q] = fma((double)(j < nvec ? W[(size_t)j * ld + i] : v[i]), vv, acc[q]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < FR; ++q) {
+            const double t = warp_sum(acc[q]);
+            if (lane == 0 && j0 + q < nv) red[(j0 + q) * FW + warp] = t;
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nv; j += FT) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < FW; ++w) t += red[j * FW + w];
+        partial[(size_t)blockIdx.x * nv + j] = t;
+    }
+    __syncthreads();
+}
+
+// out[j] = sum over CTAs of partial[b * nv + j], one warp per row (grid-wide).
+__device__ __forceinline__ void grid_reduce(const double* partial, int nv, double* out) {
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * FW + (threadIdx.x >> 5);
+    for (int j = gw; j < nv; j += gridDim.x * FW) {
+        double s = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(partial + (size_t)b * nv + j);
+        s = warp_sum(s);
+        if (lane == 0) out[j] = s;
+    }
+}
+
+// dst = v - sum_j c[j] W_j over this CTA's chunk; returns this thread's ||dst||^2 part.
+__device__ __forceinline__ double chunk_update(const float* W, int64_t ld, int nvec,
+                                               const double* c, const float* v, float* dst,
+                                               int64_t L) {
+    int64_t i0, i1;
+    const int64_t L4 = L >> 2;
+    chunk_of(L4, &i0, &i1);
+    double nrm = 0.0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += FT) {
+        const float4 b = reinterpret_cast<const float4*>(v)[i];
+        double a0 = b.x, a1 = b.y, a2 = b.z, a3 = b.w;
+        int j = 0;
+        for (; j + FR <= nvec; j += FR) {
+            float4 w[FR];
+#pragma unroll
+            for (int q = 0; q < FR; ++q)
+                w[q] = __ldg(reinterpret_cast<const float4*>(W + (size_t)(j + q) * ld) + i);
+#pragma unroll
+            for (int q = 0; q < FR; ++q) {
+                const double cj = c[j + q];
+                a0 = fma(-cj, (double)w[q].x, a0); a1 = fma(-cj, (double)w[q].y, a1);
+                a2 = fma(-cj, (double)w[q].z, a2); a3 = fma(-cj, (double)w[q].w, a3);
+            }
+        }
+        for (; j < nvec; ++j) {
+            const float4 w = __ldg(reinterpret_cast<const float4*>(W + (size_t)j * ld) + i);
+            const double cj = c[j];
+            a0 = fma(-cj, (double)w.x, a0); a1 = fma(-cj, (double)w.y, a1);
+            a2 = fma(-cj, (double)w.z, a2); a3 = fma(-cj, (double)w.w, a3);
+        }
+        const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+        reinterpret_cast<float4*>(dst)[i] = o;
+        nrm = fma((double)o.x, (double)o.x, nrm); nrm = fma((double)o.y, (double)o.y, nrm);
+        nrm = fma((double)o.z, (double)o.z, nrm); nrm = fma((double)o.w, (double)o.w, nrm);
+    }
+    if (blockIdx.x == gridDim.x - 1) {
+        for (int64_t i = (L4 << 2) + threadIdx.x; i < L; i += FT) {
+            double a = (double)v[i];
+            for (int j = 0; j < nvec; ++j) a = fma(-c[j], (double)W[(size_t)j * ld + i], a);
+            const float o = (float)a;
+            dst[i] = o;
+            nrm = fma((double)o, (double)o, nrm);
+        }
+    }
+    return nrm;
+}
+
+__global__ void __launch_bounds__(FT) k_cgs2_fused(float* W, int64_t ld, int k, int64_t L,
+                                                   float* q, double* h, double* stat,
+                                                   double* partial, double* red) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sh_c[];                 // [k+1] coefficients, then red
+    double* red_s = sh_c + (k + 1);                  // [(k+2) * FW] per-warp row sums
+    __shared__ double s_red[FW];
+    const int nb = k + 1;
+    double* h1 = red;                                // [nb + 1]: h1, ||q||^2
+    double* h2 = red + (nb + 1);                     // [nb]
+    double* n2 = red + (2 * nb + 1);                 // [1]
+    float* wnext = W + (size_t)(k + 1) * ld;
+
+    chunk_dots(W, ld, nb, q, L, true, partial, red_s);   // h1 = W^T q, ||q||^2
+    grid.sync();
+    grid_reduce(partial, nb + 1, h1);
+    grid.sync();
+    for (int j = threadIdx.x; j < nb; j += FT) sh_c[j] = h1[j];
+    __syncthreads();
+    chunk_update(W, ld, nb, sh_c, q, q, L);          // q1 = q - W h1 (in place, own chunk)
+    __syncthreads();
+    chunk_dots(W, ld, nb, q, L, false, partial, red_s);  // h2 = W^T q1
+    grid.sync();
+    grid_reduce(partial, nb, h2);
+    grid.sync();
+    for (int j = threadIdx.x; j < nb; j += FT) sh_c[j] = h2[j];
+    __syncthreads();
+    double nrm = chunk_update(W, ld, nb, sh_c, q, wnext, L);   // q2 -> row k+1
+    nrm = warp_sum(nrm);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < FW; ++w) t += s_red[w];
+        partial[blockIdx.x] = t;
+    }
+    grid.sync();
+    if (blockIdx.x == 0) {
+        grid_reduce(partial, 1, n2);                 // one warp: fixed order over CTAs
+        __syncthreads();
+        for (int i = threadIdx.x; i <= k; i += FT) h[i] = h1[i] + h2[i];
+        if (threadIdx.x == 0) {
+            const double hk = sqrt(n2[0]);
+            const double qn = sqrt(h1[nb]);
+            h[k + 1] = hk;
+            const bool broke = hk <= 1e-14 * qn;    // BREAKDOWN_RTOL, arnoldi.py:17,80
+            stat[0] = qn;
+            stat[1] = broke ? 1.0 : 0.0;
+            stat[2] = broke ? 0.0 : 1.0 / hk;
+            stat[3] = hk;
+        }
+    }
+    grid.sync();
+    const float sc = (float)__ldcg(stat + 2);
+    int64_t i0, i1;
+    chunk_of(L >> 2, &i0, &i1);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += FT) {
+        float4 v = reinterpret_cast<float4*>(wnext)[i];
+        v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+        reinterpret_cast<float4*>(wnext)[i] = v;
+    }
+    if (blockIdx.x == gridDim.x - 1)
+        for (int64_t i = ((L >> 2) << 2) + threadIdx.x; i < L; i += FT) wnext[i] *= sc;
+}
+
+constexpr int64_t FUSED_MAX_L = 1 << 21;
+
 }  // namespace ctk
 
 using namespace ctk;
+
+// Cooperative fused path when L is small and the device supports it.
+static int try_cgs2_fused(float* W, int64_t ld, int k, int64_t L, float* q, double* h,
+                          double* stat, Scratch s, cudaStream_t st, bool* done) {
+    *done = false;
+    if (L > FUSED_MAX_L) return CTK_OK;
+    static int coop = -1, sms = 0, per_sm = 0;
+    if (coop < 0) {
+        const char* off = getenv("CTK_NO_FUSED_CGS2");
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cgs2_fused, FT,
+                                                      sizeof(double) * 512 * (FW + 1));
+        cudaGetLastError();
+        if (off && off[0] == '1') coop = 0;
+    }
+    if (coop != 1 || per_sm < 1 || k + 2 > 512) return CTK_OK;
+    int64_t G = ((L >> 2) + FT - 1) / FT;            // >= one float4 per thread
+    if (G > (int64_t)sms) G = sms;
+    if (G < 1) G = 1;
+    double* red = s.tmp;
+    void* args[] = {&W, &ld, &k, &L, &q, &h, &stat, &s.partial, &red};
+    const size_t smem = sizeof(double) * ((size_t)(k + 1) + (size_t)(k + 2) * FW);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_cgs2_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * 512 * (FW + 1)));
+        attr = true;
+    }
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_cgs2_fused, dim3((unsigned)G),
+                                                dim3(FT), args, smem, st);
+    ctk_count_launch();
+    if (e != cudaSuccess) return ctk_check_cuda(e, "k_cgs2_fused");
+    *done = true;
+    return CTK_OK;
+}
 
 static int check_vec(const void* p, const char* what) {
     if (!p) return ctk_fail(CTK_ERR_ARG, "%s is NULL", what);
@@ -340,6 +582,9 @@ extern "C" int ctk_cgs2_step(float* W, int64_t ld, int k, int64_t L, float* q, d
                                 (long long)ld);
     cudaStream_t st = ctk_stream(stream);
     Scratch s = carve(scratch, k + 3);
+    bool fused = false;
+    if ((rc = try_cgs2_fused(W, ld, k, L, q, h, stat, s, st, &fused))) return rc;
+    if (fused) return CTK_OK;
     double* h1 = s.tmp;                   // k+2: h1[0..k], ||q||^2
     double* h2 = s.tmp + s.nvec_cap;      // k+1
     double* n2 = s.tmp + 2 * s.nvec_cap;  // 1

@@ -154,6 +154,8 @@ def cpu_sample(spec, iters=None, threads=0):
     from paper_2602_17892_b200 import problems
 
     threads = threads or len(os.sched_getaffinity(0))
+    if spec.N >= 1024:
+        return cpu_sample_subset(spec, threads)
     g = O.Geometry(spec.N, spec.N, 1.0, spec.angles(), spec.det_count, 1.0)
     t0 = time.perf_counter()
     A = O.CsrForward(g, nthreads=threads)
@@ -184,12 +186,43 @@ def cpu_sample(spec, iters=None, threads=0):
                         f"CSR build {build_s:.1f}s excluded"), seconds=dt)
 
 
+def cpu_sample_subset(spec, threads, stride=None):
+    """c4/c5: the full CSR would need ~23 GB (c4) / ~115 GB (c5 per slice), so
+    time the reference algorithm (CSR A + pixel-driven B) on a strided angle
+    subset and extrapolate linearly in angles (SURVEY.md §8d protocol)."""
+    from oracle import oracle as O
+    from paper_2602_17892_b200 import problems
+
+    stride = stride or max(1, spec.n_angles // 24)
+    sub = spec.angles()[::stride]
+    g = O.Geometry(spec.N, spec.N, 1.0, sub, spec.det_count, 1.0)
+    A = O.CsrForward(g, nthreads=threads)
+    x = problems.uniform_image(g.n, 0)
+    u = problems.uniform_sinogram(g.m, 1)
+    t0 = time.perf_counter()
+    A(x)
+    ta = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.back(g, u, threads)
+    tb = time.perf_counter() - t0
+    scale = spec.n_angles / len(sub)
+    ta, tb = ta * scale, tb * scale                 # extrapolated full-geometry applies
+    na, nb = applies_per_iter(spec.method) if spec.method else (1, 1)
+    per_iter = na * ta + nb * tb
+    return dict(value=(na + nb) * spec.m / per_iter, iters_per_s=1.0 / per_iter, cores=threads,
+                sample=(f"extrapolated: A (CSR) and B applies on {len(sub)} of {spec.n_angles} "
+                        f"angles at {spec.name}, scaled x{scale:.1f}; {na}A+{nb}B per iteration, "
+                        f"orthogonalisation/lambda excluded"), seconds=ta + tb)
+
+
 def run_reference(args, spec, rank, world):
     if rank != 0:
         return
     steps, warm = args.steps, args.warmup
     # each step is a bounded sample of the workload; keep the whole run short
     iters = max(1, CPU_SAMPLE_ITERS[spec.name] // 2)
+    if spec.N >= 1024:
+        steps, warm = min(steps, 2), 0
     vals, secs = [], []
     for i in range(warm + steps):
         r = cpu_sample(spec, iters=iters)

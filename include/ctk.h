@@ -126,21 +126,85 @@ int ctk_combine(const float* W, int64_t ld, int k, const double* y, const float*
  * ab == 0: M = B A on images (L = n).  stage_work / back_work as for
  * ctk_forward / ctk_back (one set per stream). */
 
-/* Arnoldi step j: q = M W_j (tmp holds the intermediate), CGS2 against rows
- * 0..j, row j+1 written; h_dev[0..hcols) receives h (j+2 values) with the 4
- * stats of ctk_cgs2_step in its last 4 entries, copied asynchronously to
- * h_host (pinned) when non-NULL. */
+/* Arnoldi step j: q = M W_j, CGS2 against rows 0..j, row j+1 written;
+ * h_dev[0..hcols) receives h (j+2 values) with the 4 stats of
+ * ctk_cgs2_step in its last 4 entries, copied asynchronously to h_host
+ * (pinned) when non-NULL.  The intermediate goes to tmp, or is kept when
+ * aux rows are given: BA: aux1[j] = A w_j; AB: aux1[j] = B w_j and
+ * aux2[j] = A B w_j (before orthogonalisation). */
 int ctk_arnoldi_step(const ctk_geom_t* g, int ab, float* W, int64_t ld, int j, float* q,
-                     float* tmp, float* stage_work, float* back_work, double* h_dev,
-                     int hcols, double* h_host, void* scratch, void* stream);
+                     float* tmp, float* aux1, int64_t ld1, float* aux2, int64_t ld2,
+                     float* stage_work, float* back_work, double* h_dev, int hcols,
+                     double* h_host, void* scratch, void* stream);
 
 /* Iterate k: y (k fp64; copied from pinned y_host when non-NULL) ->
  * x_k = x0 + W y (BA) or x0 + B (W y) (AB, z = m-length scratch);
- * r = b - A x_k; norms_dev[0] = ||r||^2, norms_dev[1] = ||x_k||^2. */
+ * r = b - A x_k; norms_dev[0] = ||r||^2, norms_dev[1] = ||x_k||^2.
+ * With the aux rows kept by ctk_arnoldi_step and d0 = b - A x0, the same
+ * x_k and r follow by linearity from two basis combinations and no projector
+ * apply: x_k = x0 + sum y_j X_j, r = d0 - sum y_j (A X_j). */
 int ctk_iterate(const ctk_geom_t* g, int ab, const float* W, int64_t ld, int k,
                 const double* y_host, double* y_dev, const float* x0, float* xk, float* z,
-                const float* b, float* r, double* norms_dev, float* stage_work,
+                const float* b, float* r, double* norms_dev, const float* aux1, int64_t ld1,
+                const float* aux2, int64_t ld2, const float* d0, float* stage_work,
                 float* back_work, void* scratch, void* stream);
+
+/* ---- Native (hybrid) AB-/BA-GMRES driver: the run_gmres loop
+ * (ctkrylov/gmres.py:135-241) without Python per iteration.  Stopping rules
+ * none / dp / rns; restarts; breakdown; degenerate-curve fallback.  All
+ * buffers are caller-owned (device unless marked host/pinned). */
+#define CTK_STOP_NONE 0
+#define CTK_STOP_MAXITER 1
+#define CTK_STOP_BREAKDOWN 2
+#define CTK_STOP_DP 3
+#define CTK_STOP_RNS 4
+
+typedef struct {
+    int ab;              /* 1: AB-GMRES (M = A B), 0: BA-GMRES (M = B A) */
+    int hybrid;          /* 0: plain (lambda = 0) */
+    int strategy;        /* 1 fixed, 2 lcurve, 3 gcv (hybrid only) */
+    int max_iter;
+    int restart_period;  /* 0: no restart */
+    int stopping;        /* CTK_STOP_NONE / CTK_STOP_DP / CTK_STOP_RNS */
+    int lookahead;       /* Arnoldi steps in flight ahead of the host (<= 0: 6) */
+    double lambda_value, dp_tau, noise_norm, rns_epsilon;
+} ctk_solve_cfg;
+
+typedef struct {
+    float* W;            /* basis [rows][ld] */
+    int64_t ld;
+    int rows;            /* >= min(restart_period or max_iter, max_iter) + 1 */
+    float *q, *tmp, *z, *r, *xk, *x_cur;   /* q: L, tmp: n (AB) / m (BA), z: m, r: m, xk/x_cur: n */
+    const float* b;      /* m */
+    float* aux1;         /* [rows][ld1]: A w_j (BA, ld1 >= m) or B w_j (AB, ld1 >= n); NULL = apply */
+    int64_t ld1;
+    float* aux2;         /* [rows][ld2]: A B w_j (AB, ld2 >= m) */
+    int64_t ld2;
+    float* d0;           /* m: b - A x0 of the current cycle (with aux) */
+    double* hs;          /* [rows][hcols] device */
+    double* h_host;      /* [rows][hcols] pinned host */
+    int hcols;           /* >= rows + 5 */
+    double* y_dev;       /* [max_iter][rows] */
+    double* y_host;      /* [max_iter][rows] pinned host */
+    double* norms;       /* [(max_iter + 1) * 2] device */
+    double* norms_host;  /* same, pinned host */
+    double* scal;        /* [4] device */
+    double* scal_host;   /* [4] pinned host */
+    float *stage_a, *back_a, *stage_b, *back_b;   /* projector workspaces per stream */
+    void *scratch_a, *scratch_b;                  /* reduction scratch per stream */
+    void *stream_a, *stream_b;                    /* Arnoldi / iterate streams */
+} ctk_solve_bufs;
+
+typedef struct {
+    int n_records, stop_reason, cycles;
+    int x_is_x0;         /* final iterate is x_cur (zero initial residual) else xk */
+    int* k;              /* host arrays of length max_iter (+1) */
+    int* warn;
+    double *lambda, *residual, *data_residual, *proj_residual, *solution_norm, *elapsed;
+} ctk_solve_out;
+
+int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solve_bufs* bufs,
+              ctk_solve_out* out);
 
 /* CUDA-event profiler over library calls: kinds 0 = forward (stage + K1),
  * 1 = back (K2 + finalize), 2 = CGS2 step, 3 = basis combination.  end()

@@ -48,19 +48,54 @@ SIGNATURES = {
                                  _vp]),
     "ctk_combine": (_c.c_int, [_fp, _c.c_int64, _c.c_int, _dp, _fp, _fp, _c.c_int64, _dp, _vp,
                                _vp]),
-    "ctk_arnoldi_step": (_c.c_int, [_vp, _c.c_int, _fp, _c.c_int64, _c.c_int, _fp, _fp, _fp, _fp,
+    "ctk_arnoldi_step": (_c.c_int, [_vp, _c.c_int, _fp, _c.c_int64, _c.c_int, _fp, _fp,
+                                    _fp, _c.c_int64, _fp, _c.c_int64, _fp, _fp,
                                     _dp, _c.c_int, _dp, _vp, _vp]),
     "ctk_iterate": (_c.c_int, [_vp, _c.c_int, _fp, _c.c_int64, _c.c_int, _dp, _dp, _fp, _fp, _fp,
-                               _fp, _fp, _dp, _fp, _fp, _vp, _vp]),
+                               _fp, _fp, _dp, _fp, _c.c_int64, _fp, _c.c_int64, _fp,
+                               _fp, _fp, _vp, _vp]),
     "ctk_set_lapack": (_c.c_int, [_vp, _vp]),
     "ctk_projected_solve": (_c.c_int, [_dp, _c.c_int, _c.c_double, _c.c_int, _c.c_double,
                                        _c.c_int, _c.c_double, _dp, _dp]),
+    "ctk_solve": (_c.c_int, [_vp, _vp, _vp, _vp]),
     "ctk_profile_begin": (_c.c_int, []),
     "ctk_profile_end": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int64), _c.POINTER(_c.c_double),
                                    _c.POINTER(_c.c_double)]),
 }
 
 PROFILE_KINDS = ("forward", "back", "cgs2", "combine")
+
+
+class SolveCfg(ctypes.Structure):
+    _fields_ = [("ab", ctypes.c_int), ("hybrid", ctypes.c_int), ("strategy", ctypes.c_int),
+                ("max_iter", ctypes.c_int), ("restart_period", ctypes.c_int),
+                ("stopping", ctypes.c_int), ("lookahead", ctypes.c_int),
+                ("lambda_value", ctypes.c_double), ("dp_tau", ctypes.c_double),
+                ("noise_norm", ctypes.c_double), ("rns_epsilon", ctypes.c_double)]
+
+
+class SolveBufs(ctypes.Structure):
+    _fields_ = [("W", _vp), ("ld", ctypes.c_int64), ("rows", ctypes.c_int),
+                ("q", _vp), ("tmp", _vp), ("z", _vp), ("r", _vp), ("xk", _vp), ("x_cur", _vp),
+                ("b", _vp), ("aux1", _vp), ("ld1", ctypes.c_int64), ("aux2", _vp),
+                ("ld2", ctypes.c_int64), ("d0", _vp),
+                ("hs", _vp), ("h_host", _vp), ("hcols", ctypes.c_int),
+                ("y_dev", _vp), ("y_host", _vp), ("norms", _vp), ("norms_host", _vp),
+                ("scal", _vp), ("scal_host", _vp),
+                ("stage_a", _vp), ("back_a", _vp), ("stage_b", _vp), ("back_b", _vp),
+                ("scratch_a", _vp), ("scratch_b", _vp), ("stream_a", _vp), ("stream_b", _vp)]
+
+
+class SolveOut(ctypes.Structure):
+    _fields_ = [("n_records", ctypes.c_int), ("stop_reason", ctypes.c_int),
+                ("cycles", ctypes.c_int), ("x_is_x0", ctypes.c_int),
+                ("k", _vp), ("warn", _vp), ("lambda_", _vp), ("residual", _vp),
+                ("data_residual", _vp), ("proj_residual", _vp), ("solution_norm", _vp),
+                ("elapsed", _vp)]
+
+
+STOP_CODES = {"none": 0, "dp": 3, "rns": 4}
+STOP_NAMES = {1: "maxiter", 2: "breakdown", 3: "dp", 4: "rns"}
 
 _lib = None
 

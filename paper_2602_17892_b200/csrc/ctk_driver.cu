@@ -1,0 +1,334 @@
+// ctk_driver.cu -- native run_gmres: the whole (hybrid) AB-/BA-GMRES loop of
+// ctkrylov/gmres.py:135-241 in C++, no Python per iteration.
+//
+// Two streams: A runs the Arnoldi process ahead (LOOKAHEAD steps in flight,
+// independent of lambda); B runs the iterate updates x_k = x0 + (B) W y_k and
+// true residuals.  The host thread waits only for each step's Hessenberg
+// column, hands the fp64 projected problem (SVD, lambda grid, L-curve/GCV,
+// Tikhonov; ctk_host.cpp) to native worker threads, and consumes results in
+// iteration order (the degenerate-curve fallback needs the previous lambda,
+// gmres.py:196-200).  Stopping rules dp / rns need each iterate's residual
+// before the next record; they sync on it (the Arnoldi look-ahead keeps
+// running).  ncp, x_true metrics and snapshots stay in the Python driver.
+#include <math.h>
+#include <string.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "ctk_common.cuh"
+
+namespace {
+
+struct Job {
+    int k = 0;
+    std::vector<double> H;      // (k+1) x k row-major
+    double beta = 0.0;
+    int strategy = 0;
+    double value = 0.0;
+    double out[4] = {0, 0, 0, 0};
+    std::vector<double> y;
+    int rc = 0;
+    bool done = false;
+};
+
+class Pool {
+  public:
+    explicit Pool(int n) {
+        for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void submit(std::shared_ptr<Job> j) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            q_.push_back(std::move(j));
+        }
+        cv_.notify_one();
+    }
+    void wait(const std::shared_ptr<Job>& j) {
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return j->done; });
+    }
+    bool ready(const std::shared_ptr<Job>& j) {
+        std::lock_guard<std::mutex> lk(mu_);
+        return j->done;
+    }
+
+  private:
+    void loop() {
+        for (;;) {
+            std::shared_ptr<Job> j;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+                if (stop_ && q_.empty()) return;
+                j = std::move(q_.front());
+                q_.pop_front();
+            }
+            j->y.assign(j->k, 0.0);
+            j->rc = ctk_projected_solve(j->H.data(), j->k, j->beta, j->strategy, j->value, 200,
+                                        NAN, j->out, j->y.data());
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                j->done = true;
+            }
+            done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::deque<std::shared_ptr<Job>> q_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    bool stop_ = false;
+};
+
+Pool& pool() {
+    static Pool p([] {
+        unsigned n = std::thread::hardware_concurrency();
+        int w = n > 2 ? (int)n - 1 : 2;
+        return w > 8 ? 8 : w;
+    }());
+    return p;
+}
+
+__global__ void k_set_inv(double* dst, double v) { *dst = v; }
+
+struct Events {
+    std::vector<cudaEvent_t> ev;
+    ~Events() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+    cudaEvent_t make(bool timing) {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
+        ev.push_back(e);
+        return e;
+    }
+};
+
+}  // namespace
+
+extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solve_bufs* bf,
+                         ctk_solve_out* out) {
+    if (!g || !cfg || !bf || !out) return ctk_fail(CTK_ERR_ARG, "null argument");
+    const bool ab = cfg->ab != 0;
+    const int K = cfg->max_iter;
+    const int p = cfg->restart_period > 0 ? cfg->restart_period : K;
+    const int rows = (p < K ? p : K) + 1;
+    if (bf->rows < rows || bf->hcols < rows + 5) return ctk_fail(CTK_ERR_ARG, "buffers too small");
+    const int na = g->n_angles;
+    const int64_t n = (int64_t)g->nx * g->ny, m = (int64_t)na * g->det_count;
+    const int64_t L = ab ? m : n;
+    cudaStream_t sa = ctk_stream(bf->stream_a), sb = ctk_stream(bf->stream_b);
+    const int hc = bf->hcols;
+    const int look = cfg->lookahead > 0 ? cfg->lookahead : 6;
+    CTK_CUDA(cudaSetDevice(g->device));
+    Events evs;
+    cudaEvent_t ev_start = evs.make(true);
+    std::vector<cudaEvent_t> ev_h(rows), ev_it(K + 1);
+    for (int i = 0; i < rows; ++i) ev_h[i] = evs.make(false);
+    for (int i = 0; i <= K; ++i) ev_it[i] = evs.make(true);
+    cudaEvent_t ev_sync = evs.make(false);
+    CTK_CUDA(cudaEventRecord(ev_start, sa));
+    CTK_CUDA(cudaStreamWaitEvent(sb, ev_start, 0));
+
+    int nrec = 0, cycles = 0, stop = CTK_STOP_NONE;
+    double prev_lam = 0.0;
+    std::vector<double> history;
+    std::vector<int> rec_slot;                        // record -> norms slot (-1: host-known)
+    auto t0 = std::chrono::steady_clock::now();
+    bool first = true;
+    int rc;
+    while (stop == CTK_STOP_NONE && nrec < K) {
+        if (!first) {   // restart from the current iterate (gmres.py:172-175)
+            CTK_CUDA(cudaEventRecord(ev_sync, sb));
+            CTK_CUDA(cudaStreamWaitEvent(sa, ev_sync, 0));
+            CTK_CUDA(cudaMemcpyAsync(bf->x_cur, bf->xk, sizeof(float) * n,
+                                     cudaMemcpyDeviceToDevice, sa));
+        }
+        first = false;
+        float* w0 = bf->W;
+        if (ab) {
+            if ((rc = ctk_forward(g, bf->x_cur, w0, 0, na, bf->b, bf->stage_a, bf->stream_a))) return rc;
+            if ((rc = ctk_norm2(w0, L, bf->scal, bf->scratch_a, bf->stream_a))) return rc;
+        } else {
+            if ((rc = ctk_forward(g, bf->x_cur, bf->tmp, 0, na, bf->b, bf->stage_a, bf->stream_a)))
+                return rc;
+            if ((rc = ctk_norm2(bf->tmp, m, bf->scal + 1, bf->scratch_a, bf->stream_a))) return rc;
+            if ((rc = ctk_back(g, bf->tmp, w0, 0, na, nullptr, bf->back_a, bf->stream_a))) return rc;
+            if ((rc = ctk_norm2(w0, L, bf->scal, bf->scratch_a, bf->stream_a))) return rc;
+        }
+        if (bf->aux1 && bf->d0)     // d0 = b - A x0 for the linear iterate path
+            CTK_CUDA(cudaMemcpyAsync(bf->d0, ab ? w0 : bf->tmp, sizeof(float) * m,
+                                     cudaMemcpyDeviceToDevice, sa));
+        CTK_CUDA(cudaMemcpyAsync(bf->scal_host, bf->scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, sa));
+        CTK_CUDA(cudaStreamSynchronize(sa));
+        const double beta = sqrt(bf->scal_host[0]);
+        const double d0n = ab ? beta : sqrt(bf->scal_host[1]);
+        if (beta == 0.0) {           // exact solution in hand (gmres.py:176-182)
+            stop = CTK_STOP_BREAKDOWN;
+            if (nrec == 0) {
+                if ((rc = ctk_norm2(bf->x_cur, n, bf->scal + 2, bf->scratch_a, bf->stream_a))) return rc;
+                CTK_CUDA(cudaMemcpyAsync(bf->scal_host + 2, bf->scal + 2, sizeof(double),
+                                         cudaMemcpyDeviceToHost, sa));
+                CTK_CUDA(cudaStreamSynchronize(sa));
+                out->k[0] = 0;
+                out->lambda[0] = 0.0;
+                out->residual[0] = 0.0;
+                out->data_residual[0] = d0n;
+                out->proj_residual[0] = 0.0;
+                out->solution_norm[0] = sqrt(bf->scal_host[2]);
+                out->elapsed[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                out->warn[0] = 0;
+                rec_slot.push_back(-1);
+                nrec = 1;
+                out->x_is_x0 = 1;
+            }
+            break;
+        }
+        ++cycles;
+        k_set_inv<<<1, 1, 0, sa>>>(bf->scal + 2, 1.0 / beta);
+        ctk_count_launch();
+        if ((rc = ctk_scale(w0, w0, L, bf->scal + 2, bf->stream_a))) return rc;
+        CTK_CUDA(cudaEventRecord(ev_sync, sa));
+        CTK_CUDA(cudaStreamWaitEvent(sb, ev_sync, 0));
+
+        const int steps = (p < K - nrec) ? p : K - nrec;
+        std::vector<double> Hfull((size_t)(steps + 1) * steps, 0.0);
+        std::vector<std::shared_ptr<Job>> jobs(steps + 1);
+        int queued = 0, done_k = 0, last_k = steps, broke_at = -1;
+        auto enqueue_to = [&](int upto) -> int {
+            while (queued < (upto < steps ? upto : steps)) {
+                int r2 = ctk_arnoldi_step(g, ab, bf->W, bf->ld, queued, bf->q, bf->tmp, bf->aux1,
+                                          bf->ld1, bf->aux2, bf->ld2, bf->stage_a,
+                                          bf->back_a, bf->hs + (size_t)queued * hc, hc,
+                                          bf->h_host + (size_t)queued * hc, bf->scratch_a,
+                                          bf->stream_a);
+                if (r2) return r2;
+                CTK_CUDA(cudaEventRecord(ev_h[queued], sa));
+                ++queued;
+            }
+            return CTK_OK;
+        };
+        auto consume = [&](int k) -> int {
+            auto& job = jobs[k];
+            pool().wait(job);
+            if (job->rc) return job->rc;
+            double lam = 0.0;
+            int warn = 0;
+            const double* y = job->y.data();
+            double proj = job->out[1];
+            std::vector<double> y2;
+            if (cfg->hybrid) {
+                if (job->out[2] != 0.0) {     // DegenerateCurveError -> previous lambda
+                    lam = prev_lam;
+                    warn = 1;
+                    double o2[4];
+                    y2.assign(k, 0.0);
+                    int r2 = ctk_projected_solve(job->H.data(), k, beta, 1, lam, 200, NAN, o2,
+                                                 y2.data());
+                    if (r2) return r2;
+                    y = y2.data();
+                    proj = o2[1];
+                } else {
+                    lam = job->out[0];
+                }
+            }
+            prev_lam = lam;
+            const int slot = nrec;
+            double* yh = bf->y_host + (size_t)slot * bf->rows;
+            memcpy(yh, y, sizeof(double) * k);
+            CTK_CUDA(cudaStreamWaitEvent(sb, ev_h[k - 1], 0));
+            int r2 = ctk_iterate(g, ab, bf->W, bf->ld, k, yh, bf->y_dev + (size_t)slot * bf->rows,
+                                 bf->x_cur, bf->xk, bf->z, bf->b, bf->r, bf->norms + 2 * slot,
+                                 bf->aux1, bf->ld1, bf->aux2, bf->ld2, bf->d0,
+                                 bf->stage_b, bf->back_b, bf->scratch_b, bf->stream_b);
+            if (r2) return r2;
+            CTK_CUDA(cudaEventRecord(ev_it[slot], sb));
+            out->k[slot] = slot + 1;
+            out->lambda[slot] = lam;
+            out->proj_residual[slot] = proj;
+            out->warn[slot] = warn;
+            rec_slot.push_back(slot);
+            nrec = slot + 1;
+            if (cfg->stopping == CTK_STOP_DP || cfg->stopping == CTK_STOP_RNS) {
+                CTK_CUDA(cudaMemcpyAsync(bf->norms_host + 2 * slot, bf->norms + 2 * slot,
+                                         2 * sizeof(double), cudaMemcpyDeviceToHost, sb));
+                CTK_CUDA(cudaStreamSynchronize(sb));
+                const double dn = sqrt(bf->norms_host[2 * slot]);
+                history.push_back(dn);
+                if (cfg->stopping == CTK_STOP_DP) {
+                    if (dn <= cfg->dp_tau * cfg->noise_norm) stop = CTK_STOP_DP;
+                } else if (history.size() >= 2) {
+                    const double pv = history[history.size() - 2], cv = history.back();
+                    if (pv == 0.0 || fabs(pv - cv) / pv < cfg->rns_epsilon) stop = CTK_STOP_RNS;
+                }
+            }
+            if (broke_at == k && stop == CTK_STOP_NONE) stop = CTK_STOP_BREAKDOWN;
+            return CTK_OK;
+        };
+        if ((rc = enqueue_to(look))) return rc;
+        for (int j = 0; j < steps; ++j) {
+            CTK_CUDA(cudaEventSynchronize(ev_h[j]));
+            const double* hr = bf->h_host + (size_t)j * hc;
+            const int k = j + 1;
+            for (int i = 0; i <= k; ++i) Hfull[(size_t)i * steps + j] = hr[i];
+            const bool broke = hr[hc - 3] != 0.0;
+            auto job = std::make_shared<Job>();
+            job->k = k;
+            job->H.resize((size_t)(k + 1) * k);
+            for (int i = 0; i <= k; ++i)
+                memcpy(&job->H[(size_t)i * k], &Hfull[(size_t)i * steps], sizeof(double) * k);
+            job->beta = beta;
+            job->strategy = cfg->hybrid ? cfg->strategy : 0;
+            job->value = cfg->lambda_value;
+            jobs[k] = job;
+            pool().submit(job);
+            if (broke) {
+                broke_at = last_k = k;
+            } else if ((rc = enqueue_to(k + look))) {
+                return rc;
+            }
+            const bool sync_mode = cfg->stopping != CTK_STOP_NONE;
+            while (stop == CTK_STOP_NONE && done_k + 1 <= k &&
+                   (sync_mode || pool().ready(jobs[done_k + 1]))) {
+                if ((rc = consume(++done_k))) return rc;
+            }
+            if (stop != CTK_STOP_NONE || broke) break;
+        }
+        while (stop == CTK_STOP_NONE && done_k < last_k && jobs[done_k + 1]) {
+            if ((rc = consume(++done_k))) return rc;
+        }
+        if (stop == CTK_STOP_NONE && broke_at > 0) stop = CTK_STOP_BREAKDOWN;
+    }
+    CTK_CUDA(cudaStreamSynchronize(sa));
+    CTK_CUDA(cudaStreamSynchronize(sb));
+    CTK_CUDA(cudaMemcpy(bf->norms_host, bf->norms, sizeof(double) * 2 * (K + 1),
+                        cudaMemcpyDeviceToHost));
+    for (int i = 0; i < nrec; ++i) {
+        if (rec_slot[i] < 0) continue;
+        const double dn = sqrt(bf->norms_host[2 * i]);
+        out->data_residual[i] = dn;
+        out->solution_norm[i] = sqrt(bf->norms_host[2 * i + 1]);
+        out->residual[i] = ab ? dn : out->proj_residual[i];
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev_start, ev_it[i]);
+        out->elapsed[i] = ms / 1000.0;
+    }
+    out->n_records = nrec;
+    out->cycles = cycles > 0 ? cycles : 1;
+    out->stop_reason = stop == CTK_STOP_NONE ? CTK_STOP_MAXITER : stop;
+    return CTK_OK;
+}

@@ -87,22 +87,28 @@ extern "C" int ctk_profile_end(int nkinds, int64_t* counts, double* mean_ms, dou
 }
 
 extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, float* W, int64_t ld, int j, float* q,
-                                float* tmp, float* stage_work, float* back_work, double* h_dev,
-                                int hcols, double* h_host, void* scratch, void* stream) {
+                                float* tmp, float* aux1, int64_t ld1, float* aux2, int64_t ld2,
+                                float* stage_work, float* back_work, double* h_dev, int hcols,
+                                double* h_host, void* scratch, void* stream) {
     if (!g) return ctk_fail(CTK_ERR_ARG, "null geometry");
     if (hcols < j + 6) return ctk_fail(CTK_ERR_ARG, "h row too short (%d) for step %d", hcols, j);
     const int na = g->n_angles;
-    const int64_t L = ab ? (int64_t)na * g->det_count : (int64_t)g->nx * g->ny;
+    const int64_t n = (int64_t)g->nx * g->ny, m = (int64_t)na * g->det_count;
+    const int64_t L = ab ? m : n;
     const float* w = W + (size_t)j * ld;
-    int rc;
-    if (ab) {   // q = A (B w)
-        if ((rc = ctk_back(g, w, tmp, 0, na, nullptr, back_work, stream))) return rc;
-        if ((rc = ctk_forward(g, tmp, q, 0, na, nullptr, stage_work, stream))) return rc;
-    } else {    // q = B (A w)
-        if ((rc = ctk_forward(g, w, tmp, 0, na, nullptr, stage_work, stream))) return rc;
-        if ((rc = ctk_back(g, tmp, q, 0, na, nullptr, back_work, stream))) return rc;
-    }
     cudaStream_t st = ctk_stream(stream);
+    int rc;
+    if (ab) {   // q = A (B w); keep B w_j (aux1) and A B w_j (aux2) for the iterates
+        float* bw = aux1 ? aux1 + (size_t)j * ld1 : tmp;
+        float* abw = aux2 ? aux2 + (size_t)j * ld2 : q;
+        if ((rc = ctk_back(g, w, bw, 0, na, nullptr, back_work, stream))) return rc;
+        if ((rc = ctk_forward(g, bw, abw, 0, na, nullptr, stage_work, stream))) return rc;
+        if (aux2) CTK_CUDA(cudaMemcpyAsync(q, abw, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+    } else {    // q = B (A w); keep A w_j (aux1)
+        float* aw = aux1 ? aux1 + (size_t)j * ld1 : tmp;
+        if ((rc = ctk_forward(g, w, aw, 0, na, nullptr, stage_work, stream))) return rc;
+        if ((rc = ctk_back(g, aw, q, 0, na, nullptr, back_work, stream))) return rc;
+    }
     const int ph = ctk_prof_open(2, st);
     rc = ctk_cgs2_step(W, ld, j, L, q, h_dev, h_dev + hcols - 4, scratch, stream);
     ctk_prof_close(ph, st);
@@ -115,7 +121,9 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, float* W, int64_t l
 extern "C" int ctk_iterate(const ctk_geom_t* g, int ab, const float* W, int64_t ld, int k,
                            const double* y_host, double* y_dev, const float* x0, float* xk,
                            float* z, const float* b, float* r, double* norms_dev,
-                           float* stage_work, float* back_work, void* scratch, void* stream) {
+                           const float* aux1, int64_t ld1, const float* aux2, int64_t ld2,
+                           const float* d0, float* stage_work, float* back_work, void* scratch,
+                           void* stream) {
     if (!g || !y_dev || !xk || !b || !r || !norms_dev) return ctk_fail(CTK_ERR_ARG, "null argument");
     const int na = g->n_angles;
     const int64_t n = (int64_t)g->nx * g->ny, m = (int64_t)na * g->det_count;
@@ -123,7 +131,21 @@ extern "C" int ctk_iterate(const ctk_geom_t* g, int ab, const float* W, int64_t 
     if (y_host && k > 0)
         CTK_CUDA(cudaMemcpyAsync(y_dev, y_host, sizeof(double) * k, cudaMemcpyHostToDevice, st));
     int rc;
+    const bool linear = aux1 && d0 && (!ab || aux2);
     const int ph = ctk_prof_open(3, st);
+    if (linear) {
+        // By linearity: x_k = x0 + sum y_j X_j with X_j = w_j (BA) or B w_j (AB),
+        // A x_k = A x0 + sum y_j A X_j with A X_j kept by the Arnoldi steps, so
+        // r = d0 - sum y_j (A X_j) needs no projector apply (d0 = b - A x0).
+        const float* Xr = ab ? aux1 : W;
+        const int64_t ldx = ab ? ld1 : ld;
+        const float* AXr = ab ? aux2 : aux1;
+        const int64_t ldax = ab ? ld2 : ld1;
+        if ((rc = ctk_combine(Xr, ldx, k, y_dev, x0, xk, n, norms_dev + 1, scratch, stream))) return rc;
+        rc = ctk_update(AXr, ldax, k, y_dev, d0, r, m, norms_dev, scratch, stream);
+        ctk_prof_close(ph, st);
+        return rc;
+    }
     if (ab) {   // x_k = x0 + B (W y)
         if (!z) return ctk_fail(CTK_ERR_ARG, "AB iterate needs z");
         if ((rc = ctk_combine(W, ld, k, y_dev, nullptr, z, m, nullptr, scratch, stream))) return rc;

@@ -20,6 +20,8 @@ end unless a stopping rule or x_true needs them every iteration.
 
 from __future__ import annotations
 
+import ctypes
+import os
 import time
 from dataclasses import dataclass, field, replace
 
@@ -267,6 +269,16 @@ class _DeviceSolve:
             # stream sb (iterate) buffers
             self.xk = torch.empty(self.n, dtype=f32, device=dev)
             self.z = torch.empty(self.m, dtype=f32, device=dev) if self.ab else None
+            # Rows kept by each Arnoldi step so iterates follow by linearity
+            # (ctk_iterate): BA keeps A w_j; AB keeps B w_j and A B w_j.
+            ldm, ldn = (self.m + 3) // 4 * 4, (self.n + 3) // 4 * 4
+            if self.ab:
+                self.aux1 = torch.zeros((rows, ldn), dtype=f32, device=dev)
+                self.aux2 = torch.zeros((rows, ldm), dtype=f32, device=dev)
+            else:
+                self.aux1 = torch.zeros((rows, ldm), dtype=f32, device=dev)
+                self.aux2 = None
+            self.d0 = torch.zeros(ldm, dtype=f32, device=dev)
             self.r = torch.empty(self.m, dtype=f32, device=dev)
             self.y_dev = torch.zeros((self.K, rows), dtype=f64, device=dev)
             self.y_pin = torch.zeros((self.K, rows), dtype=f64).pin_memory()
@@ -290,6 +302,12 @@ class _DeviceSolve:
         self.dg.back(u, out=out, x0=x0, stream=stream)
         e1.record(stream)
 
+    def _aux(self):
+        """(aux1, ld1, aux2, ld2) pointers for the native step / iterate calls."""
+        a2 = self.aux2
+        return (self.aux1.data_ptr(), self.aux1.shape[1],
+                None if a2 is None else a2.data_ptr(), 0 if a2 is None else a2.shape[1])
+
     def _work(self, stream):
         """(stage, back) workspaces of one stream for the native calls."""
         dg = self.dg
@@ -305,7 +323,8 @@ class _DeviceSolve:
         hrow = self.hs[j]
         _native.check(self.lib.ctk_arnoldi_step(
             self.dg.handle, int(self.ab), self.basis.W.data_ptr(), self.basis.ld, j,
-            self.q.data_ptr(), self.tmp.data_ptr(), stage, back, hrow.data_ptr(), self.hcols,
+            self.q.data_ptr(), self.tmp.data_ptr(), *self._aux(), stage, back, hrow.data_ptr(),
+            self.hcols,
             self.h_host[j].data_ptr(), self.basis.scratch(sa), sa.cuda_stream), "ctk_arnoldi_step")
         self.d2h += 8 * self.hcols
         ev = torch.cuda.Event()
@@ -323,8 +342,8 @@ class _DeviceSolve:
             self.dg.handle, int(self.ab), self.basis.W.data_ptr(), self.basis.ld, k,
             self.y_pin[it].data_ptr(), self.y_dev[it].data_ptr(), self.x_cur.data_ptr(),
             self.xk.data_ptr(), _native.ptr(self.z), self.b.data_ptr(), self.r.data_ptr(),
-            self.norms[it].data_ptr(), stage, back, self.basis.scratch(sb), sb.cuda_stream),
-            "ctk_iterate")
+            self.norms[it].data_ptr(), *self._aux(), self.d0.data_ptr(), stage, back,
+            self.basis.scratch(sb), sb.cuda_stream), "ctk_iterate")
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(sb)
         return ev
@@ -347,6 +366,7 @@ class _DeviceSolve:
             self._back(self.tmp, w0, sa)
             self.basis.norm2(w0, self.scal[0:1], sa)
         with torch.cuda.stream(sa):
+            self.d0[: self.m].copy_(w0 if self.ab else self.tmp)     # d0 = b - A x0
             self.scal_host.copy_(self.scal, non_blocking=True)
         self.d2h += 32
         sa.synchronize()
@@ -532,6 +552,79 @@ class _DeviceSolve:
         return rec
 
 
+class _NativeSolve(_DeviceSolve):
+    """run_gmres entirely in libctk's C++ driver (ctk_solve): no Python work
+    per iteration.  Used when no per-iteration host data is requested
+    (x_true metrics, snapshots, ncp stopping)."""
+
+    def run(self) -> SolveResult:
+        torch, cfg = self.torch, self.cfg
+        dg, K = self.dg, self.K
+        rows = self.basis.rows
+        n1 = K + 1
+        pin = dict(dtype=torch.float64)
+        out_arrays = {
+            "k": np.zeros(n1, dtype=np.int32), "warn": np.zeros(n1, dtype=np.int32),
+            "lambda_": np.zeros(n1), "residual": np.zeros(n1), "data_residual": np.zeros(n1),
+            "proj_residual": np.zeros(n1), "solution_norm": np.zeros(n1), "elapsed": np.zeros(n1)}
+        norms_host = torch.zeros((K + 1) * 2, **pin).pin_memory()
+        cfgc = _native.SolveCfg(
+            ab=int(self.ab), hybrid=int(self.hybrid),
+            strategy=_native.STRATEGY_CODES.get(cfg.lambda_strategy, 0),
+            max_iter=K, restart_period=cfg.restart_period,
+            stopping=_native.STOP_CODES[cfg.stopping_rule], lookahead=self.LOOKAHEAD,
+            lambda_value=float(cfg.lambda_value or 0.0), dp_tau=float(cfg.dp_tau),
+            noise_norm=float(cfg.noise_norm or 0.0), rns_epsilon=float(cfg.rns_epsilon))
+        sa, sb = self.sa, self.sb
+        stage_a, back_a = self._work(sa)
+        stage_b, back_b = self._work(sb)
+        P = _native.ptr
+        bufs = _native.SolveBufs(
+            W=self.basis.W.data_ptr(), ld=self.basis.ld, rows=rows,
+            q=self.q.data_ptr(), tmp=self.tmp.data_ptr(), z=P(self.z), r=self.r.data_ptr(),
+            xk=self.xk.data_ptr(), x_cur=self.x_cur.data_ptr(), b=self.b.data_ptr(),
+            aux1=self.aux1.data_ptr(), ld1=self.aux1.shape[1],
+            aux2=P(self.aux2), ld2=0 if self.aux2 is None else self.aux2.shape[1],
+            d0=self.d0.data_ptr(),
+            hs=self.hs.data_ptr(), h_host=self.h_host.data_ptr(), hcols=self.hcols,
+            y_dev=self.y_dev.data_ptr(), y_host=self.y_pin.data_ptr(),
+            norms=self.norms.data_ptr(), norms_host=norms_host.data_ptr(),
+            scal=self.scal.data_ptr(), scal_host=self.scal_host.data_ptr(),
+            stage_a=stage_a, back_a=back_a, stage_b=stage_b, back_b=back_b,
+            scratch_a=self.basis.scratch(sa), scratch_b=self.basis.scratch(sb),
+            stream_a=sa.cuda_stream, stream_b=sb.cuda_stream)
+        outc = _native.SolveOut(**{k: v.ctypes.data for k, v in out_arrays.items()})
+        try:
+            from threadpoolctl import threadpool_limits
+            limiter = threadpool_limits(limits=1, user_api="blas")
+        except Exception:   # pragma: no cover
+            limiter = None
+        try:
+            _native.check(self.lib.ctk_solve(dg.handle, ctypes.byref(cfgc), ctypes.byref(bufs),
+                                             ctypes.byref(outc)), "ctk_solve")
+        finally:
+            if limiter is not None:
+                limiter.restore_original_limits()
+        nrec = outc.n_records
+        self.d2h += 8 * self.hcols * nrec + 16 * (K + 1) + 32
+        self.h2d += sum(8 * int(k) for k in out_arrays["k"][:nrec])
+        records = [IterationRecord(
+            k=int(out_arrays["k"][i]), lambda_used=float(out_arrays["lambda_"][i]),
+            residual_norm=float(out_arrays["residual"][i]),
+            data_residual_norm=float(out_arrays["data_residual"][i]),
+            proj_residual_norm=float(out_arrays["proj_residual"][i]),
+            solution_norm=float(out_arrays["solution_norm"][i]),
+            elapsed=float(out_arrays["elapsed"][i]),
+            lambda_warning=bool(out_arrays["warn"][i])) for i in range(nrec)]
+        x_final = self.x_cur if outc.x_is_x0 else self.xk
+        x_out = x_final.clone() if self.keep_on_device else self._host_vec(x_final, sb)
+        res = SolveResult(x=x_out, records=records,
+                          stop_reason=_native.STOP_NAMES.get(outc.stop_reason, "maxiter"),
+                          cycles=outc.cycles)
+        res.transfer = {"h2d_bytes": self.h2d, "d2h_bytes": self.d2h}
+        return res
+
+
 def run_gmres(A: LinearOperator, B: LinearOperator, b, cfg: SolverConfig,
               x_true: np.ndarray | None = None, image_shape: tuple[int, int] | None = None,
               *, stream=None, keep_on_device: bool = False) -> SolveResult:
@@ -549,8 +642,10 @@ def run_gmres(A: LinearOperator, B: LinearOperator, b, cfg: SolverConfig,
     if len(shape) != 1:
         raise OperatorShapeError(f"data vector has shape {shape}, expected ({A.rows},)")
     _check_dims(A, B, int(shape[0]))
-    return _DeviceSolve(A, B, b, cfg, x_true, image_shape, stream, None,
-                        keep_on_device).run()
+    native = (x_true is None and not cfg.snapshot_stride and cfg.stopping_rule != "ncp"
+              and os.environ.get("CTK_PY_DRIVER", "0") != "1")
+    cls = _NativeSolve if native else _DeviceSolve
+    return cls(A, B, b, cfg, x_true, image_shape, stream, None, keep_on_device).run()
 
 
 def run_ab_gmres(A, B, b, cfg: SolverConfig, **kwargs) -> SolveResult:

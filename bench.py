@@ -434,6 +434,13 @@ def main():
             "iters_per_s": (world * iters_per_step * args.steps / (total_ms / 1e3)
                             if iters_per_step else None),
             "roofline": roofline, "kernels": kernels, "nnz_A": nnz,
+            "rays_counted": ("2*m per step (1 A + 1 B apply)" if spec.method is None else
+                             f"{spec.max_iter} iterations x "
+                             f"{'2A+2B' if spec.method.startswith('ab') else '2A+1B'} applies x m "
+                             "per solve: the reference algorithm's projector work "
+                             "(gmres.py:189,207,209); this path executes the Arnoldi "
+                             "1A+1B per iteration and gets x_k and b - A x_k by linearity "
+                             "from rows kept during the Arnoldi step"),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }

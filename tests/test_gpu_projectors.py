@@ -199,3 +199,35 @@ def test_drop_in_operator_contract(cuda):
         A.apply(np.ones(255))
     with pytest.raises(OperatorShapeError):
         B.apply(np.ones(256))
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_large_configs_vs_oracle_on_angle_subsets(cuda, cfg):
+    """c4 / c5: rows of A are independent and angle-major (ct.py:17-18,194),
+    so the oracle on a strided angle subset checks the full-size GPU output;
+    B is checked on a pixel-row band against the oracle B of all angles."""
+    spec = problems.CONFIGS[cfg]
+    dg, _ = make(spec.N, spec.N, 1.0, spec.angles(), spec.det_count, 1.0)
+    x = problems.random_ellipse_phantom(spec.N, spec.ellipses, 0)
+    sub = np.concatenate([[0, spec.n_angles // 2], np.arange(7, spec.n_angles, 97)])
+    ogs = O.Geometry(spec.N, spec.N, 1.0, spec.angles()[np.sort(sub)], spec.det_count, 1.0)
+    y = dg.forward(to_dev(cuda, x)).cpu().numpy().reshape(spec.n_angles, -1)[np.sort(sub)].ravel()
+    assert rel_l2(y, O.forward(ogs, x)) <= REL_L2
+    # B: full image on the GPU; oracle on a 64-row image band (independent pixels)
+    u = problems.uniform_sinogram(dg.m, 1)
+    xb = dg.back(to_dev(cuda, u)).cpu().numpy().reshape(spec.N, spec.N)
+    r0 = spec.N // 2 - 32
+    band = O.Geometry(spec.N, 64, 1.0, spec.angles(), spec.det_count, 1.0)
+    # shift the band's pixel centres: a 64-row grid is centred at y=0, the
+    # full image's rows r0..r0+63 are centred at ymax - (r0 + 32) = 0 as well
+    ref = O.back(band, u).reshape(64, spec.N)
+    assert rel_l2(xb[r0:r0 + 64], ref) <= REL_L2
+
+
+@pytest.mark.parametrize("cfg,expected", [("c4", (1922528260, 1922526218)),
+                                          ("c5", (9612630072, 9612625979))])
+def test_large_config_segment_counts_exact(cuda, cfg, expected):
+    """K6 vs the reference counts measured by the survey."""
+    spec = problems.CONFIGS[cfg]
+    dg, _ = make(spec.N, spec.N, 1.0, spec.angles(), spec.det_count, 1.0)
+    assert dg.count_segments() == expected

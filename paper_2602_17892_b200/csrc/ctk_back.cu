@@ -30,6 +30,8 @@ struct BackArgs {
     const float* u;       // row a at u + (a - a0) * D
     const float* x0;      // optional
     float* out;           // final image (S == 1) or partials [S][n]
+    float* x;             // final image (S > 1)
+    unsigned* cnt;        // S > 1: per-tile arrival tickets (zeroed once)
     int nx, ny, D, a0, a1, per_split, wmax, split;
     double h, xmin, ymax, center;
 };
@@ -114,13 +116,35 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
         accB += (double)sB;
         __syncthreads();
     }
-    if (ix >= A.nx) return;
     const size_t n = (size_t)A.nx * A.ny;
     if (A.split) {
-        float* part = A.out + (size_t)blockIdx.z * n;
-        if (iyA < A.ny) part[(size_t)iyA * A.nx + ix] = (float)accA;
-        if (iyB < A.ny) part[(size_t)iyB * A.nx + ix] = (float)accB;
+        // angle split: the last of the gridDim.z CTAs of this tile sums the
+        // partial images in split order (deterministic) and adds x0.
+        float* part = A.out;
+        const bool inx = ix < A.nx;
+        if (inx && iyA < A.ny) part[(size_t)blockIdx.z * n + (size_t)iyA * A.nx + ix] = (float)accA;
+        if (inx && iyB < A.ny) part[(size_t)blockIdx.z * n + (size_t)iyB * A.nx + ix] = (float)accB;
+        __threadfence();
+        __syncthreads();
+        __shared__ unsigned s_last;
+        unsigned* ticket = A.cnt + (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+        if (tid == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.z - 1);
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        if (inx) {
+            for (int r = 0; r < 2; ++r) {
+                const int iy = r ? iyB : iyA;
+                if (iy >= A.ny) continue;
+                const size_t o = (size_t)iy * A.nx + ix;
+                double t = 0.0;
+                for (unsigned z = 0; z < gridDim.z; ++z) t += (double)__ldcg(part + z * n + o);
+                A.x[o] = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * t);
+            }
+        }
+        if (tid == 0) *ticket = 0u;
     } else {
+        if (ix >= A.nx) return;
         if (iyA < A.ny) {
             const size_t o = (size_t)iyA * A.nx + ix;
             A.out[o] = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * accA);
@@ -129,16 +153,6 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
             const size_t o = (size_t)iyB * A.nx + ix;
             A.out[o] = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * accB);
         }
-    }
-}
-
-__global__ void k_back_finalize(const float* __restrict__ part, int S, size_t n, double h,
-                                const float* __restrict__ x0, float* __restrict__ out) {
-    for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < n;
-         p += (size_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int k = 0; k < S; ++k) s += (double)part[(size_t)k * n + p];
-        out[p] = (float)((x0 ? (double)x0[p] : 0.0) + h * s);
     }
 }
 
@@ -156,10 +170,14 @@ static int back_splits(const ctk_geom* g, int a0, int a1) {
 
 using namespace ctk;
 
+static int64_t back_tiles(const ctk_geom* g) {
+    return (int64_t)((g->nx + BTX - 1) / BTX) * ((g->ny + BTY - 1) / BTY);
+}
+
 extern "C" int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1) {
     if (!g || a0 < 0 || a1 > g->n_angles || a0 >= a1) return 0;
     const int S = back_splits(g, a0, a1);
-    return S > 1 ? (int64_t)S * g->nx * g->ny : 0;
+    return S > 1 ? (int64_t)S * g->nx * g->ny + back_tiles(g) : 0;
 }
 
 extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, int a1,
@@ -184,6 +202,8 @@ extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, i
     A.u = u;
     A.x0 = x0;
     A.out = S > 1 ? work : x;
+    A.x = x;
+    A.cnt = S > 1 ? reinterpret_cast<unsigned*>(work + (size_t)S * n) : nullptr;
     A.nx = g->nx;
     A.ny = g->ny;
     A.D = g->det_count;
@@ -204,13 +224,6 @@ extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, i
     const int ph = ctk_prof_open(1, st);
     k_back<<<grid, block, smem, st>>>(A);
     CTK_LAUNCH_CHECK("k_back");
-    if (S > 1) {
-        const int threads = 256;
-        int blocks = (int)((n + threads - 1) / threads);
-        if (blocks > 148 * 16) blocks = 148 * 16;
-        k_back_finalize<<<blocks, threads, 0, st>>>(work, S, n, g->h, x0, x);
-        CTK_LAUNCH_CHECK("k_back_finalize");
-    }
     ctk_prof_close(ph, st);
     return CTK_OK;
 }

@@ -95,9 +95,11 @@ int ctk_check_cuda(cudaError_t e, const char* what);
 
 static inline cudaStream_t ctk_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// K1 workspace: zero-bordered copies P, PT, then fwd_split row-chunk partials.
+// K1 workspace: zero-bordered copies P, PT, then fwd_split row-chunk partials
+// and one arrival ticket per (angle, 128-bin block) -- zero-filled once.
 static inline int64_t ctk_stage_floats(const ctk_geom* g) {
     const int64_t m = (int64_t)g->n_angles * g->det_count;
+    const int64_t tickets = (int64_t)g->n_angles * ((g->det_count + 127) / 128);
     return (int64_t)g->ny * (g->nx + 2) + (int64_t)g->nx * (g->ny + 2) +
-           (g->fwd_split > 1 ? (int64_t)g->fwd_split * m : 0);
+           (g->fwd_split > 1 ? (int64_t)g->fwd_split * m + tickets : 0);
 }

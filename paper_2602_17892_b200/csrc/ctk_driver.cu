@@ -11,6 +11,8 @@
 // before the next record; they sync on it (the Arnoldi look-ahead keeps
 // running).  ncp, x_true metrics and snapshots stay in the Python driver.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <chrono>
@@ -137,13 +139,19 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
     CTK_CUDA(cudaSetDevice(g->device));
     Events evs;
     cudaEvent_t ev_start = evs.make(true);
+    const char* tr_env = getenv("CTK_TRACE");
+    const bool trace = tr_env && tr_env[0] == '1';
     std::vector<cudaEvent_t> ev_h(rows), ev_it(K + 1);
-    for (int i = 0; i < rows; ++i) ev_h[i] = evs.make(false);
+    for (int i = 0; i < rows; ++i) ev_h[i] = evs.make(trace);
     for (int i = 0; i <= K; ++i) ev_it[i] = evs.make(true);
     cudaEvent_t ev_sync = evs.make(false);
     CTK_CUDA(cudaEventRecord(ev_start, sa));
     CTK_CUDA(cudaStreamWaitEvent(sb, ev_start, 0));
 
+    // CTK_TRACE=1: per-step GPU timeline of stream A (debug; stderr)
+    std::vector<cudaEvent_t> tr_beg(trace ? rows : 0);
+    std::vector<double> tr_host(trace ? rows : 0, 0.0);
+    for (auto& e : tr_beg) e = evs.make(true);
     int nrec = 0, cycles = 0, stop = CTK_STOP_NONE;
     double prev_lam = 0.0;
     std::vector<double> history;
@@ -211,6 +219,7 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
         int queued = 0, done_k = 0, last_k = steps, broke_at = -1;
         auto enqueue_to = [&](int upto) -> int {
             while (queued < (upto < steps ? upto : steps)) {
+                if (trace) CTK_CUDA(cudaEventRecord(tr_beg[queued], sa));
                 int r2 = ctk_arnoldi_step(g, ab, bf->W, bf->ld, queued, bf->q, bf->tmp, bf->aux1,
                                           bf->ld1, bf->aux2, bf->ld2, bf->stage_a,
                                           bf->back_a, bf->hs + (size_t)queued * hc, hc,
@@ -218,6 +227,10 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
                                           bf->stream_a);
                 if (r2) return r2;
                 CTK_CUDA(cudaEventRecord(ev_h[queued], sa));
+                if (trace) {
+                    tr_host[queued] = std::chrono::duration<double>(
+                        std::chrono::steady_clock::now() - t0).count();
+                }
                 ++queued;
             }
             return CTK_OK;
@@ -326,6 +339,23 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev_start, ev_it[i]);
         out->elapsed[i] = ms / 1000.0;
+    }
+    if (trace && cycles == 1) {
+        // per step: GPU busy (begin -> h event) and idle gap before the next step
+        double busy = 0.0, gap = 0.0;
+        const int nst = nrec < rows - 1 ? nrec : rows - 1;
+        for (int j = 0; j < nst; ++j) {
+            float b_ms = 0.f, g_ms = 0.f;
+            cudaEventElapsedTime(&b_ms, tr_beg[j], ev_h[j]);
+            busy += b_ms;
+            if (j + 1 < nst) {
+                cudaEventElapsedTime(&g_ms, ev_h[j], tr_beg[j + 1]);
+                gap += g_ms;
+            }
+        }
+        cudaGetLastError();
+        fprintf(stderr, "[ctk trace] %d steps: stream-A busy %.3f ms, idle %.3f ms; host enqueue of last step at %.3f ms\n",
+                nst, busy, gap, nst > 0 ? 1e3 * tr_host[nst - 1] : 0.0);
     }
     out->n_records = nrec;
     out->cycles = cycles > 0 ? cycles : 1;

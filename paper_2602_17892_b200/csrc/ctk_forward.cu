@@ -207,6 +207,7 @@ struct FwdArgs {
     const float* b;          // optional: y = b - A x
     float* y;
     float* part;             // split > 1: per-row-chunk partial sums [split][rows * D]
+    unsigned* cnt;           // split > 1: per-(angle, bin block) arrival tickets (zeroed)
     int split;               // row chunks per ray (blockIdx.z), small-problem parallelism
     const int* deg_slot;
     const long long* deg_cnt;   // segments per degenerate ray [slot * D + j]
@@ -310,36 +311,42 @@ __device__ __forceinline__ double degenerate_ray(const FwdArgs& A, int slot, int
     return acc;
 }
 
-__global__ void __launch_bounds__(FWD_THREADS, 12) k_forward(FwdArgs A) {
-    const int a = A.a0 + blockIdx.y;
-    const int slot = A.deg_slot[a];
-    const int chunk = blockIdx.z;
-    const size_t rows = (size_t)(A.a1 - A.a0) * A.D;
-    const int j = blockIdx.x * FWD_THREADS + threadIdx.x;
-    if (j >= A.D) return;
+__device__ __forceinline__ double forward_ray(const FwdArgs& A, int a, int slot, int j, int chunk) {
     if (slot >= 0) {                         // whole block: warp-uniform branch
         const int per = (A.deg_maxseg + A.split - 1) / A.split;
-        const double acc = degenerate_ray(A, slot, j, chunk * per, (chunk + 1) * per);
-        const size_t o = (size_t)blockIdx.y * A.D + j;
-        if (A.split > 1) A.part[chunk * rows + o] = (float)acc;
-        else A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
-        return;
+        return degenerate_ray(A, slot, j, chunk * per, (chunk + 1) * per);
     }
     const AngleParams p = A.ap[a];
     const double s = A.offsets[j];
     const int R = p.frame == 0 ? A.eg.ny : A.eg.nx;
     const int per = (R + A.split - 1) / A.split;
     const int k0 = chunk * per, k1 = min(R, k0 + per);
-    double acc;
     if (p.frame == 0)
-        acc = p.mirror ? walk_ray<true>(p, s, A.P, A.eg.ny, A.eg.nx, k0, k1)
-                       : walk_ray<false>(p, s, A.P, A.eg.ny, A.eg.nx, k0, k1);
-    else
-        acc = p.mirror ? walk_ray<true>(p, s, A.PT, A.eg.nx, A.eg.ny, k0, k1)
-                       : walk_ray<false>(p, s, A.PT, A.eg.nx, A.eg.ny, k0, k1);
+        return p.mirror ? walk_ray<true>(p, s, A.P, A.eg.ny, A.eg.nx, k0, k1)
+                        : walk_ray<false>(p, s, A.P, A.eg.ny, A.eg.nx, k0, k1);
+    return p.mirror ? walk_ray<true>(p, s, A.PT, A.eg.nx, A.eg.ny, k0, k1)
+                    : walk_ray<false>(p, s, A.PT, A.eg.nx, A.eg.ny, k0, k1);
+}
+
+// One ray per thread; SPLIT: rows of each ray over blockIdx.z (small problems).
+template <bool SPLIT>
+__global__ void __launch_bounds__(FWD_THREADS, 12) k_forward(FwdArgs A) {
+    const int a = A.a0 + blockIdx.y;
+    const int slot = A.deg_slot[a];
+    const int j = blockIdx.x * FWD_THREADS + threadIdx.x;
     const size_t o = (size_t)blockIdx.y * A.D + j;
-    if (A.split > 1) A.part[chunk * rows + o] = (float)acc;
-    else A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
+    if (!SPLIT) {
+        if (j >= A.D) return;
+        const double acc = forward_ray(A, a, slot, j, 0);
+        A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
+        return;
+    }
+    // Row chunks write partial sums; k_forward_finalize reduces them in chunk
+    // order.  (A last-arriving-CTA reduction needs a gpu-scope fence, which
+    // invalidates L1 on sm_100 and costs the gathers their cache hits.)
+    const int chunk = blockIdx.z;
+    const size_t rows = (size_t)(A.a1 - A.a0) * A.D;
+    if (j < A.D) A.part[chunk * rows + o] = (float)forward_ray(A, a, slot, j, chunk);
 }
 
 // Row-chunk partials -> y (fixed summation order; b - A x epilogue).
@@ -427,6 +434,7 @@ static FwdArgs make_args(const ctk_geom* g, const float* x, float* y, int a0, in
     A.a1 = a1;
     A.split = 1;
     A.part = nullptr;
+    A.cnt = nullptr;
     return A;
 }
 
@@ -523,8 +531,12 @@ extern "C" int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0
     A.PT = PT;
     A.split = g->fwd_split;
     A.part = PT + (size_t)g->nx * (g->ny + 2);
+    A.cnt = reinterpret_cast<unsigned*>(A.part + (size_t)A.split * g->n_angles * g->det_count);
     dim3 grid((g->det_count + FWD_THREADS - 1) / FWD_THREADS, a1 - a0, A.split);
-    k_forward<<<grid, FWD_THREADS, 0, st>>>(A);
+    if (A.split > 1)
+        k_forward<true><<<grid, FWD_THREADS, 0, st>>>(A);
+    else
+        k_forward<false><<<grid, FWD_THREADS, 0, st>>>(A);
     CTK_LAUNCH_CHECK("k_forward");
     if (A.split > 1) {
         const size_t rows = (size_t)(a1 - a0) * g->det_count;

@@ -115,6 +115,11 @@ int ctk_scale(const float* v, float* dst, int64_t L, const double* scale_dev, vo
  *        q2 / h[k+1].  stat must hold 4 doubles. */
 int ctk_cgs2_step(float* W, int64_t ld, int k, int64_t L, float* q, double* h,
                   double* stat, void* scratch, void* stream);
+/* Same with passes = 2 (CGS2, reorthogonalize=True) or 1 (one classical
+ * Gram-Schmidt pass, reorthogonalize=False; the reference's single pass is
+ * modified Gram-Schmidt -- equal in exact arithmetic). */
+int ctk_gs_step(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
+                double* stat, void* scratch, void* stream);
 
 /* dst = (x0 ? x0 : 0) + sum_{j<k} y[j] W_j   (y: k fp64, device);
  * norm2_out[0] = ||dst||^2 if non-NULL. */
@@ -132,7 +137,8 @@ int ctk_combine(const float* W, int64_t ld, int k, const double* y, const float*
  * (pinned) when non-NULL.  The intermediate goes to tmp, or is kept when
  * aux rows are given: BA: aux1[j] = A w_j; AB: aux1[j] = B w_j and
  * aux2[j] = A B w_j (before orthogonalisation). */
-int ctk_arnoldi_step(const ctk_geom_t* g, int ab, float* W, int64_t ld, int j, float* q,
+int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* W, int64_t ld, int j,
+                     float* q,
                      float* tmp, float* aux1, int64_t ld1, float* aux2, int64_t ld2,
                      float* stage_work, float* back_work, double* h_dev, int hcols,
                      double* h_host, void* scratch, void* stream);
@@ -168,6 +174,7 @@ typedef struct {
     int stopping;        /* CTK_STOP_NONE / CTK_STOP_DP / CTK_STOP_RNS */
     int lookahead;       /* Arnoldi steps in flight ahead of the host (<= 0: 6) */
     double lambda_value, dp_tau, noise_norm, rns_epsilon;
+    int reorthogonalize; /* 1: CGS2 (reference default), 0: single pass */
 } ctk_solve_cfg;
 
 typedef struct {
@@ -193,6 +200,16 @@ typedef struct {
     float *stage_a, *back_a, *stage_b, *back_b;   /* projector workspaces per stream */
     void *scratch_a, *scratch_b;                  /* reduction scratch per stream */
     void *stream_a, *stream_b;                    /* Arnoldi / iterate streams */
+    /* optional per-iteration records, NULL / 0 when unused */
+    const float* x_true;  /* n: RRE / SSIM reference image */
+    int img_nx, img_ny;   /* SSIM image shape (SSIM skipped when min < 8) */
+    double dyn_range;     /* SSIM dynamic range L (max - min of x_true) */
+    double* metrics;      /* [(max_iter + 1) * 2] device: ||x_k - x_true||^2, SSIM map sum */
+    double* metrics_host; /* same, pinned host */
+    void* scratch_m;      /* ctk_metrics_scratch_bytes() zero-filled */
+    int snapshot_stride;  /* copy x_k to snaps[(k / stride) - 1] every stride iterations */
+    float** snaps;        /* host pointers (pinned), n floats each */
+    int n_snaps;
 } ctk_solve_bufs;
 
 typedef struct {
@@ -201,10 +218,19 @@ typedef struct {
     int* k;              /* host arrays of length max_iter (+1) */
     int* warn;
     double *lambda, *residual, *data_residual, *proj_residual, *solution_norm, *elapsed;
+    double *rre, *ssim;  /* with x_true (NaN when not computed) */
 } ctk_solve_out;
 
 int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solve_bufs* bufs,
               ctk_solve_out* out);
+
+/* Device-side reconstruction metrics (ctkrylov/metrics.py:13-62):
+ * out[0] = ||x - x_true||^2, out[1] = sum of the SSIM map over the valid
+ * 8x8 Gaussian windows (divide by (nx-7)(ny-7)); SSIM skipped when nx or
+ * ny < 8 or dyn_range <= 0.  scratch: ctk_metrics_scratch_bytes(), zeroed. */
+size_t ctk_metrics_scratch_bytes(void);
+int ctk_metrics(const float* x, const float* x_true, int nx, int ny, double dyn_range,
+                double* out, void* scratch, void* stream);
 
 /* CUDA-event profiler over library calls: kinds 0 = forward (stage + K1),
  * 1 = back (K2 + finalize), 2 = CGS2 step, 3 = basis combination.  end()

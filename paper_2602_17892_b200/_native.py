@@ -48,7 +48,9 @@ SIGNATURES = {
                                  _vp]),
     "ctk_combine": (_c.c_int, [_fp, _c.c_int64, _c.c_int, _dp, _fp, _fp, _c.c_int64, _dp, _vp,
                                _vp]),
-    "ctk_arnoldi_step": (_c.c_int, [_vp, _c.c_int, _fp, _c.c_int64, _c.c_int, _fp, _fp,
+    "ctk_gs_step": (_c.c_int, [_fp, _c.c_int64, _c.c_int, _c.c_int64, _fp, _c.c_int, _dp, _dp,
+                               _vp, _vp]),
+    "ctk_arnoldi_step": (_c.c_int, [_vp, _c.c_int, _c.c_int, _fp, _c.c_int64, _c.c_int, _fp, _fp,
                                     _fp, _c.c_int64, _fp, _c.c_int64, _fp, _fp,
                                     _dp, _c.c_int, _dp, _vp, _vp]),
     "ctk_iterate": (_c.c_int, [_vp, _c.c_int, _fp, _c.c_int64, _c.c_int, _dp, _dp, _fp, _fp, _fp,
@@ -58,6 +60,8 @@ SIGNATURES = {
     "ctk_projected_solve": (_c.c_int, [_dp, _c.c_int, _c.c_double, _c.c_int, _c.c_double,
                                        _c.c_int, _c.c_double, _dp, _dp]),
     "ctk_solve": (_c.c_int, [_vp, _vp, _vp, _vp]),
+    "ctk_metrics_scratch_bytes": (_c.c_size_t, []),
+    "ctk_metrics": (_c.c_int, [_fp, _fp, _c.c_int, _c.c_int, _c.c_double, _dp, _vp, _vp]),
     "ctk_profile_begin": (_c.c_int, []),
     "ctk_profile_end": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int64), _c.POINTER(_c.c_double),
                                    _c.POINTER(_c.c_double)]),
@@ -71,7 +75,8 @@ class SolveCfg(ctypes.Structure):
                 ("max_iter", ctypes.c_int), ("restart_period", ctypes.c_int),
                 ("stopping", ctypes.c_int), ("lookahead", ctypes.c_int),
                 ("lambda_value", ctypes.c_double), ("dp_tau", ctypes.c_double),
-                ("noise_norm", ctypes.c_double), ("rns_epsilon", ctypes.c_double)]
+                ("noise_norm", ctypes.c_double), ("rns_epsilon", ctypes.c_double),
+                ("reorthogonalize", ctypes.c_int)]
 
 
 class SolveBufs(ctypes.Structure):
@@ -83,7 +88,11 @@ class SolveBufs(ctypes.Structure):
                 ("y_dev", _vp), ("y_host", _vp), ("norms", _vp), ("norms_host", _vp),
                 ("scal", _vp), ("scal_host", _vp),
                 ("stage_a", _vp), ("back_a", _vp), ("stage_b", _vp), ("back_b", _vp),
-                ("scratch_a", _vp), ("scratch_b", _vp), ("stream_a", _vp), ("stream_b", _vp)]
+                ("scratch_a", _vp), ("scratch_b", _vp), ("stream_a", _vp), ("stream_b", _vp),
+                ("x_true", _vp), ("img_nx", ctypes.c_int), ("img_ny", ctypes.c_int),
+                ("dyn_range", ctypes.c_double), ("metrics", _vp), ("metrics_host", _vp),
+                ("scratch_m", _vp), ("snapshot_stride", ctypes.c_int), ("snaps", _vp),
+                ("n_snaps", ctypes.c_int)]
 
 
 class SolveOut(ctypes.Structure):
@@ -91,7 +100,7 @@ class SolveOut(ctypes.Structure):
                 ("cycles", ctypes.c_int), ("x_is_x0", ctypes.c_int),
                 ("k", _vp), ("warn", _vp), ("lambda_", _vp), ("residual", _vp),
                 ("data_residual", _vp), ("proj_residual", _vp), ("solution_norm", _vp),
-                ("elapsed", _vp)]
+                ("elapsed", _vp), ("rre", _vp), ("ssim", _vp)]
 
 
 STOP_CODES = {"none": 0, "dp": 3, "rns": 4}

@@ -122,6 +122,15 @@ class DeviceBasis:
                                              self.scratch(stream), stream.cuda_stream),
                       "ctk_cgs2_step")
 
+    def gs_step(self, k: int, q, passes: int, h_out, stat_out, stream) -> None:
+        """Like cgs2_step with 1 (reorthogonalize=False) or 2 Gram-Schmidt passes."""
+        if k + 1 >= self.rows:
+            raise ValueError(f"basis holds {self.rows} rows; step {k} would write row {k + 1}")
+        _native.check(self.lib.ctk_gs_step(self.W.data_ptr(), self.ld, k, self.L, q.data_ptr(),
+                                           passes, h_out.data_ptr(), stat_out.data_ptr(),
+                                           self.scratch(stream), stream.cuda_stream),
+                      "ctk_gs_step")
+
     def combine(self, k: int, y_dev, dst, x0=None, norm_out=None, stream=None) -> None:
         """dst = (x0 or 0) + W[:k]^T y   (K4, fp64 accumulation)."""
         _native.check(self.lib.ctk_combine(self.W.data_ptr(), self.ld, k, y_dev.data_ptr(),

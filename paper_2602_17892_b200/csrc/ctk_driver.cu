@@ -220,7 +220,8 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
         auto enqueue_to = [&](int upto) -> int {
             while (queued < (upto < steps ? upto : steps)) {
                 if (trace) CTK_CUDA(cudaEventRecord(tr_beg[queued], sa));
-                int r2 = ctk_arnoldi_step(g, ab, bf->W, bf->ld, queued, bf->q, bf->tmp, bf->aux1,
+                int r2 = ctk_arnoldi_step(g, ab, cfg->reorthogonalize ? 2 : 1, bf->W, bf->ld,
+                                          queued, bf->q, bf->tmp, bf->aux1,
                                           bf->ld1, bf->aux2, bf->ld2, bf->stage_a,
                                           bf->back_a, bf->hs + (size_t)queued * hc, hc,
                                           bf->h_host + (size_t)queued * hc, bf->scratch_a,
@@ -269,6 +270,17 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
                                  bf->aux1, bf->ld1, bf->aux2, bf->ld2, bf->d0,
                                  bf->stage_b, bf->back_b, bf->scratch_b, bf->stream_b);
             if (r2) return r2;
+            if (bf->x_true) {       // device-side RRE / SSIM of x_k (row f1)
+                int r3 = ctk_metrics(bf->xk, bf->x_true, bf->img_nx, bf->img_ny, bf->dyn_range,
+                                     bf->metrics + 2 * slot, bf->scratch_m, bf->stream_b);
+                if (r3) return r3;
+            }
+            if (bf->snapshot_stride > 0 && (slot + 1) % bf->snapshot_stride == 0) {
+                const int si = (slot + 1) / bf->snapshot_stride - 1;
+                if (si < bf->n_snaps)
+                    CTK_CUDA(cudaMemcpyAsync(bf->snaps[si], bf->xk, sizeof(float) * n,
+                                             cudaMemcpyDeviceToHost, sb));
+            }
             CTK_CUDA(cudaEventRecord(ev_it[slot], sb));
             out->k[slot] = slot + 1;
             out->lambda[slot] = lam;
@@ -330,7 +342,14 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
     CTK_CUDA(cudaStreamSynchronize(sb));
     CTK_CUDA(cudaMemcpy(bf->norms_host, bf->norms, sizeof(double) * 2 * (K + 1),
                         cudaMemcpyDeviceToHost));
+    if (bf->x_true)
+        CTK_CUDA(cudaMemcpy(bf->metrics_host, bf->metrics, sizeof(double) * 2 * (K + 1),
+                            cudaMemcpyDeviceToHost));
     for (int i = 0; i < nrec; ++i) {
+        if (out->rre) {
+            out->rre[i] = bf->x_true && rec_slot[i] >= 0 ? bf->metrics_host[2 * i] : NAN;
+            out->ssim[i] = bf->x_true && rec_slot[i] >= 0 ? bf->metrics_host[2 * i + 1] : NAN;
+        }
         if (rec_slot[i] < 0) continue;
         const double dn = sqrt(bf->norms_host[2 * i]);
         out->data_residual[i] = dn;

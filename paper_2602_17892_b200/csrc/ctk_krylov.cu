@@ -221,7 +221,7 @@ __global__ void k_scale(const float* __restrict__ v, float* __restrict__ dst, in
 // h = h1 + h2; h[k+1] = sqrt(n2); stat = {||q||, breakdown, 1/h[k+1] or 0, h[k+1]}
 __global__ void k_cgs2_finalize(const double* h1, const double* h2, const double* n2, int k,
                                 double* h, double* stat) {
-    for (int i = threadIdx.x; i <= k; i += blockDim.x) h[i] = h1[i] + h2[i];
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) h[i] = h2 ? h1[i] + h2[i] : h1[i];
     if (threadIdx.x == 0) {
         const double hk = sqrt(n2[0]);
         const double qn = sqrt(h1[k + 1]);
@@ -459,7 +459,13 @@ static int try_cgs2_fused(float* W, int64_t ld, int k, int64_t L, float* q, doub
     }
     if (coop != 1 || per_sm < 1 || k + 2 > 512) return CTK_OK;
     int64_t G = ((L >> 2) + FT - 1) / FT;            // >= one float4 per thread
+    static int cap = -1;
+    if (cap < 0) {
+        const char* e = getenv("CTK_FUSED_CTAS");
+        cap = e ? atoi(e) : 0;
+    }
     if (G > (int64_t)sms) G = sms;
+    if (cap > 0 && G > cap) G = cap;
     if (G < 1) G = 1;
     double* red = s.tmp;
     void* args[] = {&W, &ld, &k, &L, &q, &h, &stat, &s.partial, &red};
@@ -574,6 +580,11 @@ extern "C" int ctk_scale(const float* v, float* dst, int64_t L, const double* sc
 
 extern "C" int ctk_cgs2_step(float* W, int64_t ld, int k, int64_t L, float* q, double* h,
                              double* stat, void* scratch, void* stream) {
+    return ctk_gs_step(W, ld, k, L, q, 2, h, stat, scratch, stream);
+}
+
+extern "C" int ctk_gs_step(float* W, int64_t ld, int k, int64_t L, float* q, int passes,
+                           double* h, double* stat, void* scratch, void* stream) {
     int rc;
     if ((rc = check_vec(W, "W")) || (rc = check_vec(q, "q"))) return rc;
     if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
@@ -582,8 +593,9 @@ extern "C" int ctk_cgs2_step(float* W, int64_t ld, int k, int64_t L, float* q, d
                                 (long long)ld);
     cudaStream_t st = ctk_stream(stream);
     Scratch s = carve(scratch, k + 3);
+    if (passes != 1 && passes != 2) return ctk_fail(CTK_ERR_ARG, "passes must be 1 or 2");
     bool fused = false;
-    if ((rc = try_cgs2_fused(W, ld, k, L, q, h, stat, s, st, &fused))) return rc;
+    if (passes == 2 && (rc = try_cgs2_fused(W, ld, k, L, q, h, stat, s, st, &fused))) return rc;
     if (fused) return CTK_OK;
     double* h1 = s.tmp;                   // k+2: h1[0..k], ||q||^2
     double* h2 = s.tmp + s.nvec_cap;      // k+1
@@ -591,6 +603,12 @@ extern "C" int ctk_cgs2_step(float* W, int64_t ld, int k, int64_t L, float* q, d
     const int nb = k + 1;
     float* wnext = W + (size_t)(k + 1) * ld;
     if ((rc = launch_dots(W, ld, nb, q, L, 1, h1, s, st))) return rc;            // h1, ||Mw||^2
+    if (passes == 1) {        // classical Gram-Schmidt, no reorthogonalisation pass
+        if ((rc = launch_combine(W, ld, nb, h1, -1.0, q, wnext, L, n2, s, st))) return rc;
+        k_cgs2_finalize<<<1, 128, 0, st>>>(h1, nullptr, n2, k, h, stat);
+        CTK_LAUNCH_CHECK("k_cgs2_finalize");
+        return ctk_scale(wnext, wnext, L, stat + 2, stream);
+    }
     if ((rc = launch_combine(W, ld, nb, h1, -1.0, q, q, L, nullptr, s, st))) return rc;  // q1
     if ((rc = launch_dots(W, ld, nb, q, L, 0, h2, s, st))) return rc;            // h2
     if ((rc = launch_combine(W, ld, nb, h2, -1.0, q, wnext, L, n2, s, st))) return rc;   // q2

@@ -86,7 +86,8 @@ extern "C" int ctk_profile_end(int nkinds, int64_t* counts, double* mean_ms, dou
     return CTK_OK;
 }
 
-extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, float* W, int64_t ld, int j, float* q,
+extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* W, int64_t ld,
+                                int j, float* q,
                                 float* tmp, float* aux1, int64_t ld1, float* aux2, int64_t ld2,
                                 float* stage_work, float* back_work, double* h_dev, int hcols,
                                 double* h_host, void* scratch, void* stream) {
@@ -110,7 +111,7 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, float* W, int64_t l
         if ((rc = ctk_back(g, aw, q, 0, na, nullptr, back_work, stream))) return rc;
     }
     const int ph = ctk_prof_open(2, st);
-    rc = ctk_cgs2_step(W, ld, j, L, q, h_dev, h_dev + hcols - 4, scratch, stream);
+    rc = ctk_gs_step(W, ld, j, L, q, passes, h_dev, h_dev + hcols - 4, scratch, stream);
     ctk_prof_close(ph, st);
     if (rc) return rc;
     if (h_host)

@@ -322,7 +322,8 @@ class _DeviceSolve:
         stage, back = self._work(sa)
         hrow = self.hs[j]
         _native.check(self.lib.ctk_arnoldi_step(
-            self.dg.handle, int(self.ab), self.basis.W.data_ptr(), self.basis.ld, j,
+            self.dg.handle, int(self.ab), 2 if self.cfg.reorthogonalize else 1,
+            self.basis.W.data_ptr(), self.basis.ld, j,
             self.q.data_ptr(), self.tmp.data_ptr(), *self._aux(), stage, back, hrow.data_ptr(),
             self.hcols,
             self.h_host[j].data_ptr(), self.basis.scratch(sa), sa.cuda_stream), "ctk_arnoldi_step")
@@ -574,7 +575,8 @@ class _NativeSolve(_DeviceSolve):
             max_iter=K, restart_period=cfg.restart_period,
             stopping=_native.STOP_CODES[cfg.stopping_rule], lookahead=self.LOOKAHEAD,
             lambda_value=float(cfg.lambda_value or 0.0), dp_tau=float(cfg.dp_tau),
-            noise_norm=float(cfg.noise_norm or 0.0), rns_epsilon=float(cfg.rns_epsilon))
+            noise_norm=float(cfg.noise_norm or 0.0), rns_epsilon=float(cfg.rns_epsilon),
+            reorthogonalize=int(bool(cfg.reorthogonalize)))
         sa, sb = self.sa, self.sb
         stage_a, back_a = self._work(sa)
         stage_b, back_b = self._work(sb)
@@ -593,6 +595,31 @@ class _NativeSolve(_DeviceSolve):
             stage_a=stage_a, back_a=back_a, stage_b=stage_b, back_b=back_b,
             scratch_a=self.basis.scratch(sa), scratch_b=self.basis.scratch(sb),
             stream_a=sa.cuda_stream, stream_b=sb.cuda_stream)
+        # optional per-iteration records computed on the device (row f1)
+        out_arrays["rre"] = np.full(n1, np.nan)
+        out_arrays["ssim"] = np.full(n1, np.nan)
+        keep = []                                  # keep buffers alive across the call
+        if self.x_true is not None:
+            xt = torch.from_numpy(self.x_true.astype(np.float32)).to(dg.dev)
+            met = torch.zeros((K + 1) * 2, dtype=torch.float64, device=dg.dev)
+            met_h = torch.zeros((K + 1) * 2, dtype=torch.float64).pin_memory()
+            scr = torch.zeros(int(self.lib.ctk_metrics_scratch_bytes()) // 8 + 1,
+                              dtype=torch.float64, device=dg.dev)
+            keep += [xt, met, met_h, scr]
+            shape = self.image_shape
+            use_ssim = shape is not None and min(shape) >= 8
+            dyn = float(self.x_true.max() - self.x_true.min()) if use_ssim else 0.0
+            bufs.x_true, bufs.metrics, bufs.metrics_host = xt.data_ptr(), met.data_ptr(), met_h.data_ptr()
+            bufs.scratch_m = scr.data_ptr()
+            bufs.img_ny, bufs.img_nx = (int(shape[0]), int(shape[1])) if use_ssim else (0, 0)
+            bufs.dyn_range = dyn
+        snaps = []
+        if cfg.snapshot_stride:
+            nsn = K // cfg.snapshot_stride
+            snaps = [torch.empty(self.n, dtype=torch.float32).pin_memory() for _ in range(nsn)]
+            arr = (ctypes.c_void_p * max(nsn, 1))(*[t.data_ptr() for t in snaps])
+            keep.append(arr)
+            bufs.snapshot_stride, bufs.snaps, bufs.n_snaps = cfg.snapshot_stride, ctypes.addressof(arr), nsn
         outc = _native.SolveOut(**{k: v.ctypes.data for k, v in out_arrays.items()})
         try:
             from threadpoolctl import threadpool_limits
@@ -616,11 +643,27 @@ class _NativeSolve(_DeviceSolve):
             solution_norm=float(out_arrays["solution_norm"][i]),
             elapsed=float(out_arrays["elapsed"][i]),
             lambda_warning=bool(out_arrays["warn"][i])) for i in range(nrec)]
+        if self.x_true is not None:
+            xn = float(np.linalg.norm(self.x_true))
+            shape = self.image_shape
+            cnt = (shape[0] - 7) * (shape[1] - 7) if shape is not None and min(shape) >= 8 else 0
+            for i, rec in enumerate(records):
+                if rec.k == 0:
+                    continue
+                rec.rre = float(np.sqrt(out_arrays["rre"][i]) / xn) if xn > 0 else None
+                if cnt and bufs.dyn_range > 0:
+                    rec.ssim = float(out_arrays["ssim"][i] / cnt)
+        snapshots = {}
+        for i, t in enumerate(snaps):
+            kk = (i + 1) * cfg.snapshot_stride
+            if kk <= nrec:
+                snapshots[kk] = t.numpy().astype(np.float64)
+        self.d2h += 4 * self.n * len(snapshots)
         x_final = self.x_cur if outc.x_is_x0 else self.xk
         x_out = x_final.clone() if self.keep_on_device else self._host_vec(x_final, sb)
         res = SolveResult(x=x_out, records=records,
                           stop_reason=_native.STOP_NAMES.get(outc.stop_reason, "maxiter"),
-                          cycles=outc.cycles)
+                          cycles=outc.cycles, snapshots=snapshots)
         res.transfer = {"h2d_bytes": self.h2d, "d2h_bytes": self.d2h}
         return res
 
@@ -642,8 +685,7 @@ def run_gmres(A: LinearOperator, B: LinearOperator, b, cfg: SolverConfig,
     if len(shape) != 1:
         raise OperatorShapeError(f"data vector has shape {shape}, expected ({A.rows},)")
     _check_dims(A, B, int(shape[0]))
-    native = (x_true is None and not cfg.snapshot_stride and cfg.stopping_rule != "ncp"
-              and os.environ.get("CTK_PY_DRIVER", "0") != "1")
+    native = cfg.stopping_rule != "ncp" and os.environ.get("CTK_PY_DRIVER", "0") != "1"
     cls = _NativeSolve if native else _DeviceSolve
     return cls(A, B, b, cfg, x_true, image_shape, stream, None, keep_on_device).run()
 

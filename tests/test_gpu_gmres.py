@@ -174,3 +174,37 @@ def test_sharded_driver_world1_nccl_matches_single_gpu(cuda, golden):
                                records(ref, "data_residual_norm"), rtol=1e-5)
     np.testing.assert_allclose(records(res, "lambda_used"), records(ref, "lambda_used"), rtol=1e-2)
     assert rel(res.x, ref.x) < 1e-4
+
+
+def test_device_metrics_match_host_reference(cuda, golden):
+    """Row f1: RRE / SSIM computed on the device by the native driver equal the
+    reference formulas evaluated on the host iterates (Python driver)."""
+    import os
+    from paper_2602_17892_b200 import metrics
+    d, A, B = small_problem(golden)
+    rng = np.random.default_rng(0)
+    x_true = (rng.random(256) * 0.8).astype(np.float32).astype(np.float64)
+    cfg = gmres.SolverConfig(method="ab-hybrid", lambda_strategy="gcv", max_iter=6,
+                             snapshot_stride=2)
+    res = gmres.run_gmres(A, B, d["b"], cfg, x_true=x_true, image_shape=(16, 16))
+    os.environ["CTK_PY_DRIVER"] = "1"
+    try:
+        ref = gmres.run_gmres(A, B, d["b"], cfg, x_true=x_true, image_shape=(16, 16))
+    finally:
+        os.environ.pop("CTK_PY_DRIVER")
+    assert sorted(res.snapshots) == [2, 4, 6]
+    for k, x in res.snapshots.items():
+        assert metrics.rre(x, ref.snapshots[k]) < 1e-5
+    for r, q in zip(res.records, ref.records):
+        assert r.rre == pytest.approx(q.rre, rel=1e-4)
+        assert r.ssim == pytest.approx(q.ssim, rel=1e-4, abs=1e-6)
+
+
+def test_single_pass_gram_schmidt(cuda, golden):
+    """reorthogonalize=False: one Gram-Schmidt pass; same iterates to working
+    precision on a well-conditioned short run."""
+    d, A, B = small_problem(golden)
+    kw = dict(method="ba-hybrid", lambda_strategy="gcv", max_iter=6)
+    r2 = gmres.run_gmres(A, B, d["b"], gmres.SolverConfig(**kw))
+    r1 = gmres.run_gmres(A, B, d["b"], gmres.SolverConfig(reorthogonalize=False, **kw))
+    assert rel(r1.x, r2.x) < 1e-3

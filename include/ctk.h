@@ -247,6 +247,14 @@ int ctk_profile_end(int nkinds, int64_t* counts, double* mean_ms, double* total_
  * ||H y - beta e1||, degenerate flag, rank-deficient flag}; y: k doubles.
  * Thread-safe: no shared state beyond the registered function pointer. */
 int ctk_set_lapack(void* dgesdd, void* ddot);
+/* LAPACK dbdsqr for the lock-free path (bidiagonalisation in C++, singular
+ * values with one rotated vector, Givens Tikhonov); without it every solve
+ * uses dgesdd (serialised by OpenBLAS across threads). */
+int ctk_set_lapack_extra(void* dbdsqr);
+/* 0 (default): lock-free path; 1: always dgesdd, whose rounding reproduces
+ * the reference's numpy SVD bit for bit (the L-curve corner is sensitive to
+ * the last bits of the SVD). */
+int ctk_set_svd_path(int lapack_only);
 int ctk_projected_solve(const double* H, int k, double beta, int strategy, double fixed_value,
                         int grid_count, double fallback_lambda, double* out, double* y);
 

@@ -57,6 +57,8 @@ SIGNATURES = {
                                _fp, _fp, _dp, _fp, _c.c_int64, _fp, _c.c_int64, _fp,
                                _fp, _fp, _vp, _vp]),
     "ctk_set_lapack": (_c.c_int, [_vp, _vp]),
+    "ctk_set_lapack_extra": (_c.c_int, [_vp]),
+    "ctk_set_svd_path": (_c.c_int, [_c.c_int]),
     "ctk_projected_solve": (_c.c_int, [_dp, _c.c_int, _c.c_double, _c.c_int, _c.c_double,
                                        _c.c_int, _c.c_double, _dp, _dp]),
     "ctk_solve": (_c.c_int, [_vp, _vp, _vp, _vp]),
@@ -156,6 +158,7 @@ def _register_lapack(L) -> None:
 
         L.ctk_set_lapack(fnptr(cython_lapack.__pyx_capi__["dgesdd"]),
                          fnptr(cython_blas.__pyx_capi__["ddot"]))
+        L.ctk_set_lapack_extra(fnptr(cython_lapack.__pyx_capi__["dbdsqr"]))
     except Exception:   # the projected solve then reports "not registered"
         pass
 

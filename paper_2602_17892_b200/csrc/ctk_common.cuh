@@ -28,6 +28,7 @@ struct AngleParams {
     int degenerate;         // |sin| or |cos| < 1e-14: exact literal path (ct.py:153-155,165,168)
     int exact_flags;        // bit0: |dx| is a power of two, bit1: |dy| is (division == exact multiply)
     double inv_dx, inv_dy;  // 1/dx, 1/dy (used only when the matching bit is set)
+    double inv_sg;          // 1 / sigma_fx (walk range estimates)
 };
 
 constexpr int CTK_MAX_DEG_LIST = 8;

@@ -151,6 +151,7 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
     // CTK_TRACE=1: per-step GPU timeline of stream A (debug; stderr)
     std::vector<cudaEvent_t> tr_beg(trace ? rows : 0);
     std::vector<double> tr_host(trace ? rows : 0, 0.0);
+    double tr_wait = 0.0, tr_consumed_at = 0.0;
     for (auto& e : tr_beg) e = evs.make(true);
     int nrec = 0, cycles = 0, stop = CTK_STOP_NONE;
     double prev_lam = 0.0;
@@ -238,7 +239,12 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
         };
         auto consume = [&](int k) -> int {
             auto& job = jobs[k];
+            const auto tw0 = std::chrono::steady_clock::now();
             pool().wait(job);
+            if (trace) {
+                tr_wait += std::chrono::duration<double>(std::chrono::steady_clock::now() - tw0).count();
+                tr_consumed_at = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            }
             if (job->rc) return job->rc;
             double lam = 0.0;
             int warn = 0;
@@ -373,8 +379,9 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
             }
         }
         cudaGetLastError();
-        fprintf(stderr, "[ctk trace] %d steps: stream-A busy %.3f ms, idle %.3f ms; host enqueue of last step at %.3f ms\n",
-                nst, busy, gap, nst > 0 ? 1e3 * tr_host[nst - 1] : 0.0);
+        fprintf(stderr, "[ctk trace] %d steps: stream-A busy %.3f ms, idle %.3f ms; host enqueue of last step at %.3f ms; "
+                "host waited %.3f ms on projected solves, last consumed at %.3f ms\n",
+                nst, busy, gap, nst > 0 ? 1e3 * tr_host[nst - 1] : 0.0, 1e3 * tr_wait, 1e3 * tr_consumed_at);
     }
     out->n_records = nrec;
     out->cycles = cycles > 0 ? cycles : 1;

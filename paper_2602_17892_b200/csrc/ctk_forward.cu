@@ -232,13 +232,25 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
     const long long U0 = llrint(u0 * 4294967296.0);
     const long long C2 = (long long)C << 32;
     // rows k with u(k+1) > 0 and u(k) < C  (=> floor(u(k)) in [-1, C-1])
+    // fp64 estimates of the integer quotients, then exact integer fix-ups
+    // (cheaper than two 64-bit integer divisions per ray)
     long long kb, ke;
-    if (U0 + Sg > 0) kb = 0;
-    else if (Sg == 0) return 0.0;
-    else kb = (-U0) / Sg;                       // smallest k with U0 + (k+1) Sg > 0
+    if (U0 + Sg > 0) {
+        kb = 0;
+    } else {
+        if (Sg == 0) return 0.0;
+        kb = (long long)floor((double)(-U0) * p.inv_sg);     // smallest k: U0 + (k+1) Sg > 0
+        while (U0 + (kb + 1) * Sg <= 0) ++kb;
+        while (kb > 0 && U0 + kb * Sg > 0) --kb;
+    }
     if (U0 >= C2) return 0.0;
-    if (Sg == 0) ke = R;
-    else ke = (C2 - U0 + Sg - 1) / Sg;          // smallest k with U0 + k Sg >= C
+    if (Sg == 0) {
+        ke = R;
+    } else {
+        ke = (long long)ceil((double)(C2 - U0) * p.inv_sg);  // smallest k: U0 + k Sg >= C
+        while (U0 + ke * Sg < C2) ++ke;
+        while (ke > 0 && U0 + (ke - 1) * Sg >= C2) --ke;
+    }
     if (kb < krow0) kb = krow0;               // this block's row chunk only
     if (ke > krow1) ke = krow1;
     if (kb >= ke) return 0.0;

@@ -158,6 +158,7 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
         // the walk keeps a 32-bit fraction: sigma == 1 (|tan| rounds to 1 at 45
         // degrees) becomes 1 - 2^-32, a 1e-6-pixel drift over a 4096-row walk
         if (p.sigma_fx > 0xffffffffll) p.sigma_fx = 0xffffffffll;
+        p.inv_sg = p.sigma_fx > 0 ? 1.0 / (double)p.sigma_fx : 0.0;
         ap[a] = p;
         bp[a].cg = c / det_spacing;
         bp[a].sg = s / det_spacing;

@@ -15,6 +15,7 @@
 // the larger lambda, DegenerateCurveError conditions reported as a flag.
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -123,27 +124,26 @@ void gradient(const std::vector<double>& f, std::vector<double>& d) {
 enum { S_NONE = 0, S_FIXED = 1, S_LCURVE = 2, S_GCV = 3 };
 
 // Returns 0 and sets lam, or 1 for a degenerate curve (DegenerateCurveError).
-int select(const Svd& v, double beta, int strategy, int grid_count, double* lam) {
-    const int k = v.k, kp1 = v.kp1;
+// s: singular values of H (k), c: beta * U[0, :] (the rotated right-hand side).
+int select_sc(const double* sv, std::vector<double>& c, int k, int kp1, double beta,
+              int strategy, int grid_count, double* lam) {
     double smax = 0.0, smin = std::numeric_limits<double>::infinity();
     for (int i = 0; i < k; ++i) {
-        smax = std::max(smax, v.s[i]);
-        if (v.s[i] > 0) smin = std::min(smin, v.s[i]);
+        smax = std::max(smax, sv[i]);
+        if (sv[i] > 0) smin = std::min(smin, sv[i]);
     }
     if (!(smax > 0.0)) return 1;                       // all singular values are zero
     std::vector<double> grid;
     geomspace(std::max(smin * 1e-4, 1e-12), smax, grid_count, grid);
-    std::vector<double> c(k);
-    for (int i = 0; i < k; ++i) c[i] = beta * v.U[(size_t)i * kp1];   // beta * U[0, i]
     const double outside = std::max(beta * beta - dot_self(c), 0.0);
     std::vector<double> sol(grid_count), res(grid_count), tr(grid_count);
     std::vector<double> ta(k), tb(k), tf(k);
     for (int g = 0; g < grid_count; ++g) {
         const double l = grid[g], l2 = l * l;
         for (int i = 0; i < k; ++i) {
-            const double s2 = v.s[i] * v.s[i];
+            const double s2 = sv[i] * sv[i];
             const double den = s2 + l2;
-            const double a = v.s[i] * c[i] / den;
+            const double a = sv[i] * c[i] / den;
             const double r = (l2 / den) * c[i];
             ta[i] = a * a;
             tb[i] = r * r;
@@ -198,6 +198,12 @@ int select(const Svd& v, double beta, int strategy, int grid_count, double* lam)
     return 0;
 }
 
+int select(const Svd& v, double beta, int strategy, int grid_count, double* lam) {
+    std::vector<double> c(v.k);
+    for (int i = 0; i < v.k; ++i) c[i] = beta * v.U[(size_t)i * v.kp1];   // beta * U[0, i]
+    return select_sc(v.s.data(), c, v.k, v.kp1, beta, strategy, grid_count, lam);
+}
+
 void tikhonov(const double* H, const Svd& v, double beta, double lam, double* y, double* res,
               int* rank_def) {
     const int k = v.k, kp1 = v.kp1;
@@ -233,7 +239,214 @@ void tikhonov(const double* H, const Svd& v, double beta, double lam, double* y,
     *rank_def = rank < k;
 }
 
+// ---------------------------------------------------------------------------
+// Lock-free fast path.  OpenBLAS serialises concurrent LAPACK calls behind a
+// global lock, so dgesdd from several worker threads runs one at a time; this
+// path needs no level-2/3 BLAS: a hand-written Householder bidiagonalisation
+// H = Q [B; 0] P^T (the left reflectors applied only to beta e1), LAPACK
+// dbdsqr for the singular values of B with the rotations applied to that one
+// vector (ncc = 1, level-1 BLAS only), and a Givens elimination of the damped
+// bidiagonal problem for the Tikhonov solution y = P z.
+// ---------------------------------------------------------------------------
+typedef void (*dbdsqr_t)(char* uplo, int* n, int* ncvt, int* nru, int* ncc, double* d, double* e,
+                         double* vt, int* ldvt, double* u, int* ldu, double* c, int* ldc,
+                         double* work, int* info);
+dbdsqr_t g_dbdsqr = nullptr;
+bool g_fast = [] {
+    const char* e = getenv("CTK_LAPACK_SVD");      // 1: always the dgesdd path
+    return !(e && e[0] == '1');
+}();
+
+// dlarfg: reflector I - tau v v^T with v[0] = 1 mapping x to (beta, 0, ...).
+void householder(double* x, int n, int stride, double* tau, double* beta) {
+    const double alpha = x[0];
+    double xn = 0.0;
+    for (int i = 1; i < n; ++i) xn = hypot(xn, x[(size_t)i * stride]);
+    if (xn == 0.0) {
+        *tau = 0.0;
+        *beta = alpha;
+        return;
+    }
+    const double b = -copysign(hypot(alpha, xn), alpha);
+    *tau = (b - alpha) / b;
+    const double sc = 1.0 / (alpha - b);
+    for (int i = 1; i < n; ++i) x[(size_t)i * stride] *= sc;
+    x[0] = 1.0;
+    *beta = b;
+}
+
+struct Bidiag {
+    int m = 0, n = 0;
+    std::vector<double> A;      // m x n column-major, right reflectors stored in rows
+    std::vector<double> d, e, taup, g;
+};
+
+// H (m x n row-major) -> B = diag d + superdiag e; g = Q^T (beta e1).
+void bidiagonalize(const double* H, int m, int n, double beta, Bidiag& bd) {
+    bd.m = m;
+    bd.n = n;
+    bd.A.assign((size_t)m * n, 0.0);
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j) bd.A[(size_t)i + (size_t)j * m] = H[(size_t)i * n + j];
+    bd.d.assign(n, 0.0);
+    bd.e.assign(n > 1 ? n - 1 : 1, 0.0);
+    bd.taup.assign(n, 0.0);
+    bd.g.assign(m, 0.0);
+    bd.g[0] = beta;
+    double* A = bd.A.data();
+    auto at = [&](int i, int j) -> double& { return A[(size_t)i + (size_t)j * m]; };
+    std::vector<double> w(m > n ? m : n);
+    for (int i = 0; i < n; ++i) {
+        // left reflector on column i, rows i..m-1
+        double tq, b;
+        householder(&at(i, i), m - i, 1, &tq, &b);
+        if (tq != 0.0) {
+            for (int j = i + 1; j < n; ++j) {
+                double s = 0.0;
+                for (int r = i; r < m; ++r) s += at(r, i) * at(r, j);
+                s *= tq;
+                for (int r = i; r < m; ++r) at(r, j) -= s * at(r, i);
+            }
+            double s = 0.0;
+            for (int r = i; r < m; ++r) s += at(r, i) * bd.g[r];
+            s *= tq;
+            for (int r = i; r < m; ++r) bd.g[r] -= s * at(r, i);
+        }
+        bd.d[i] = b;
+        if (i < n - 1) {
+            // right reflector on row i, columns i+1..n-1 (stored in place)
+            double tp, b2;
+            householder(&at(i, i + 1), n - i - 1, m, &tp, &b2);
+            bd.taup[i] = tp;
+            bd.e[i] = b2;
+            if (tp != 0.0) {
+                for (int r = i + 1; r < m; ++r) {
+                    double s = 0.0;
+                    for (int j = i + 1; j < n; ++j) s += at(r, j) * at(i, j);
+                    w[r] = s * tp;
+                }
+                for (int j = i + 1; j < n; ++j) {
+                    const double vj = at(i, j);
+                    for (int r = i + 1; r < m; ++r) at(r, j) -= w[r] * vj;
+                }
+            }
+        }
+    }
+}
+
+// y = P z = G_0 (G_1 (... G_{n-2} z)) with G_i = I - tau_i v_i v_i^T on coords i+1..n-1.
+void apply_p(const Bidiag& bd, const double* z, double* y) {
+    const int n = bd.n, m = bd.m;
+    for (int j = 0; j < n; ++j) y[j] = z[j];
+    for (int i = n - 2; i >= 0; --i) {
+        const double tp = bd.taup[i];
+        if (tp == 0.0) continue;
+        double s = y[i + 1];                               // v[0] = 1
+        for (int j = i + 2; j < n; ++j) s += bd.A[(size_t)i + (size_t)j * m] * y[j];
+        s *= tp;
+        y[i + 1] -= s;
+        for (int j = i + 2; j < n; ++j) y[j] -= s * bd.A[(size_t)i + (size_t)j * m];
+    }
+}
+
+// min ||B z - g||^2 + lam^2 ||z||^2 for upper bidiagonal B (d, e): Givens
+// elimination of each damping row, chasing its fill-in along the bidiagonal.
+// Returns false when lam == 0 and B is numerically singular.
+bool damped_bidiag_solve(std::vector<double> d, std::vector<double> e, std::vector<double> g,
+                         double lam, double smax, int m_rows, double* z) {
+    const int n = (int)d.size();
+    if (lam > 0.0) {
+        for (int j = 0; j < n; ++j) {
+            double r = lam, rhs = 0.0;       // damping row: lam at column j
+            for (int c = j; c < n; ++c) {
+                const double a = d[c];
+                const double h = hypot(a, r);
+                if (h == 0.0) break;
+                const double cs = a / h, sn = r / h;
+                d[c] = h;
+                const double gc = g[c];
+                g[c] = cs * gc + sn * rhs;
+                rhs = -sn * gc + cs * rhs;
+                if (c + 1 < n) {
+                    const double b = e[c];
+                    e[c] = cs * b;             // row c keeps its superdiagonal
+                    r = -sn * b;               // fill-in of the damping row at c+1
+                    if (r == 0.0) break;
+                }
+            }
+        }
+    } else {
+        const double cutoff = std::numeric_limits<double>::epsilon() * std::max(m_rows, n) * smax;
+        for (int c = 0; c < n; ++c)
+            if (!(fabs(d[c]) > cutoff)) return false;
+    }
+    z[n - 1] = g[n - 1] / d[n - 1];
+    for (int c = n - 2; c >= 0; --c) z[c] = (g[c] - e[c] * z[c + 1]) / d[c];
+    return true;
+}
+
+// 0 = done, 1 = fall back to the dgesdd path (lam == 0 and rank deficient, or
+// dbdsqr unavailable / failed).
+int projected_fast(const double* H, int k, double beta, int strategy, double fixed_value,
+                   int grid_count, double fallback_lambda, double* out, double* y) {
+    if (!g_dbdsqr) return 1;
+    const int m = k + 1, n = k;
+    Bidiag bd;
+    bidiagonalize(H, m, n, beta, bd);
+    std::vector<double> sv(bd.d), ee(bd.e), c(bd.g.begin(), bd.g.begin() + n);
+    std::vector<double> work(4 * (size_t)n + 4);
+    char uplo = 'U';
+    int nn = n, ncvt = 0, nru = 0, ncc = 1, ldvt = 1, ldu = 1, ldc = n, info = 0;
+    double dummy = 0.0;
+    g_dbdsqr(&uplo, &nn, &ncvt, &nru, &ncc, sv.data(), ee.data(), &dummy, &ldvt, &dummy, &ldu,
+             c.data(), &ldc, work.data(), &info);
+    if (info != 0) return 1;
+    // c = U^T (beta e1) up to per-column signs, which the filter-factor
+    // formulas square away: the same (s, c) as beta * U[0, :] of the reference SVD.
+    double lam = 0.0;
+    int degenerate = 0;
+    if (strategy == S_FIXED) {
+        lam = fixed_value;
+    } else if (strategy == S_LCURVE || strategy == S_GCV) {
+        if (select_sc(sv.data(), c, k, m, beta, strategy, grid_count, &lam)) {
+            degenerate = 1;
+            lam = fallback_lambda;
+        }
+    }
+    out[0] = lam;
+    out[2] = degenerate;
+    out[3] = 0;
+    if (isnan(lam)) {
+        out[1] = 0.0;
+        return 0;
+    }
+    std::vector<double> z(n);
+    std::vector<double> gn(bd.g.begin(), bd.g.begin() + n);
+    if (!damped_bidiag_solve(bd.d, std::vector<double>(bd.e.begin(), bd.e.begin() + (n > 1 ? n - 1 : 0)),
+                             gn, lam, sv.empty() ? 0.0 : sv[0], m, z.data()))
+        return 1;
+    apply_p(bd, z.data(), y);
+    double r2 = 0.0;
+    for (int i = 0; i < m; ++i) {
+        double a = (i == 0) ? -beta : 0.0;
+        for (int j = 0; j < n; ++j) a += H[(size_t)i * n + j] * y[j];
+        r2 += a * a;
+    }
+    out[1] = sqrt(r2);
+    return 0;
+}
+
 }  // namespace
+
+extern "C" int ctk_set_svd_path(int lapack_only) {
+    g_fast = lapack_only == 0;
+    return CTK_OK;
+}
+
+extern "C" int ctk_set_lapack_extra(void* dbdsqr) {
+    g_dbdsqr = reinterpret_cast<dbdsqr_t>(dbdsqr);
+    return CTK_OK;
+}
 
 extern "C" int ctk_set_lapack(void* dgesdd, void* ddot) {
     g_dgesdd = reinterpret_cast<dgesdd_t>(dgesdd);
@@ -247,6 +460,9 @@ extern "C" int ctk_projected_solve(const double* H, int k, double beta, int stra
     if (!g_dgesdd) return ctk_fail(CTK_ERR_ARG, "LAPACK dgesdd not registered (ctk_set_lapack)");
     if (!H || !out || !y || k < 1 || grid_count < 1)
         return ctk_fail(CTK_ERR_ARG, "bad projected-solve arguments");
+    if (g_fast && projected_fast(H, k, beta, strategy, fixed_value, grid_count, fallback_lambda,
+                                 out, y) == 0)
+        return CTK_OK;
     Svd v;
     const int info = svd_hessenberg(H, k + 1, k, v);
     if (info != 0) return ctk_fail(CTK_ERR_ARG, "dgesdd failed (info %d)", info);

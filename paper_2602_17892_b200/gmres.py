@@ -176,11 +176,13 @@ def _pool():
     return _POOL
 
 
-def _side_stream(torch, dev):
-    key = (dev.index, "combine")
+def _side_stream(torch, dev, kind, priority):
+    """Cached solver streams: the Arnoldi stream at the highest priority (it is
+    the critical path), the iterate stream at the lowest."""
+    key = (dev.index, kind)
     s = _STREAMS.get(key)
     if s is None:
-        s = torch.cuda.Stream(dev)
+        s = torch.cuda.Stream(dev, priority=priority)
         _STREAMS[key] = s
     return s
 
@@ -220,8 +222,10 @@ class _DeviceSolve:
         self.A, self.B, self.cfg = A, B, cfg
         dg = self.dg = A.dgeom
         torch = self.torch = dg.torch
-        self.sa = stream if stream is not None else torch.cuda.current_stream(dg.dev)
-        self.sb = _side_stream(torch, dg.dev)
+        self.caller = stream if stream is not None else torch.cuda.current_stream(dg.dev)
+        self.sa = _side_stream(torch, dg.dev, "arnoldi", -100)
+        self.sb = _side_stream(torch, dg.dev, "combine", 100)
+        self.sa.wait_stream(self.caller)
         self.lib = _native.load()
         self.timer = timer
         self.keep_on_device = keep_on_device
@@ -515,6 +519,8 @@ class _DeviceSolve:
                 stop = "breakdown"
         sa.synchronize()
         sb.synchronize()
+        self.caller.wait_stream(sa)
+        self.caller.wait_stream(sb)
         if pending:
             norms = self.norms.cpu().numpy()
             self.d2h += self.norms.numel() * 8
@@ -632,6 +638,8 @@ class _NativeSolve(_DeviceSolve):
         finally:
             if limiter is not None:
                 limiter.restore_original_limits()
+        self.caller.wait_stream(sa)
+        self.caller.wait_stream(sb)
         nrec = outc.n_records
         self.d2h += 8 * self.hcols * nrec + 16 * (K + 1) + 32
         self.h2d += sum(8 * int(k) for k in out_arrays["k"][:nrec])

@@ -90,9 +90,61 @@ def _native_solve(H, beta, strategy, fixed=0.0, fallback=float("nan")):
     return out, y
 
 
-def test_native_projected_solve_matches_reference_selection():
-    """Host C++ lambda selection (ctk_host.cpp) vs the reference's loops:
-    same grid point every time (grid values may differ by one ulp of pow)."""
+@pytest.fixture
+def lapack_path():
+    lib = _native.load()
+    lib.ctk_set_svd_path(1)
+    yield lib
+    lib.ctk_set_svd_path(0)
+
+
+def arnoldi_hessenberg(M, b, k):
+    V = [b / np.linalg.norm(b)]
+    cols = []
+    for j in range(k):
+        q = M @ V[j]
+        h = np.zeros(j + 2)
+        for _ in range(2):
+            for i in range(j + 1):
+                c = V[i] @ q
+                h[i] += c
+                q = q - c * V[i]
+        h[j + 1] = np.linalg.norm(q)
+        cols.append(h)
+        V.append(q / h[j + 1])
+    return O.hessenberg(cols, k), float(np.linalg.norm(b))
+
+
+def test_fast_path_gcv_and_tikhonov_match_reference():
+    """Default lock-free path (C++ bidiagonalisation + dbdsqr + Givens
+    Tikhonov): the GCV choice equals the reference's on Arnoldi Hessenbergs
+    of noisy ill-posed problems, and y / ||H y - beta e1|| match its lstsq."""
+    rng = np.random.default_rng(11)
+    n_checked = 0
+    for _ in range(12):
+        n = 100
+        Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        M = Q @ np.diag(np.logspace(0, -rng.uniform(2, 8), n)) @ Q.T
+        b = M @ rng.standard_normal(n) + 0.02 * rng.standard_normal(n)
+        for k in (5, 20, 45, 80):
+            H, beta = arnoldi_hessenberg(M, b, k)
+            out, y = _native_solve(H, beta, "gcv")
+            ref = O.lambda_selection(H, beta, "gcv")
+            assert out[2] == 0.0 and out[0] == pytest.approx(ref, rel=1e-12)
+            y_ref, r_ref = O.projected_tikhonov(H, beta, ref)
+            np.testing.assert_allclose(y, y_ref, atol=1e-8 * max(1.0, np.abs(y_ref).max()))
+            assert out[1] == pytest.approx(r_ref, rel=1e-7, abs=1e-12)
+            for lam in (0.0, 0.05):
+                out2, y2 = _native_solve(H, beta, "fixed", fixed=lam)
+                y_ref, r_ref = O.projected_tikhonov(H, beta, lam)
+                np.testing.assert_allclose(y2, y_ref, atol=1e-8 * max(1.0, np.abs(y_ref).max()))
+            n_checked += 1
+    assert n_checked == 48
+
+
+def test_native_projected_solve_matches_reference_selection(lapack_path):
+    """dgesdd path (ctk_set_svd_path(1)) vs the reference's loops: same grid
+    point every time for both GCV and the ill-conditioned L-curve."""
     rng = np.random.default_rng(3)
     n = 0
     for _ in range(80):
@@ -114,7 +166,7 @@ def test_native_projected_solve_matches_reference_selection():
     assert n > 100
 
 
-def test_native_projected_solve_golden_and_fallback(golden):
+def test_native_projected_solve_golden_and_fallback(golden, lapack_path):
     d = golden("solver_cases")
     for i in range(4):
         H = d[f"lam/{i}/H"]

@@ -436,6 +436,245 @@ __global__ void __launch_bounds__(FT) k_cgs2_fused(float* W, int64_t ld, int k, 
 
 constexpr int64_t FUSED_MAX_L = 1 << 21;
 
+// ---------------------------------------------------------------------------
+// SMEM-resident Gram-Schmidt step (c1/c2 sizes: the whole basis fits in the
+// aggregate shared memory of the 148 SMs, e.g. 81 x 65536 fp32 = 21 MB).
+// One cooperative launch, one CTA per SM.  Each CTA pulls its L-chunk of all
+// k+1 basis rows into shared memory with bulk async copies (TMA engine, one
+// mbarrier, no register staging), so both Gram-Schmidt passes, the norm and
+// the scale run out of SMEM: the basis is read from L2/HBM once per step
+// instead of four times, and there are 3 grid barriers instead of 5.  Chunk
+// partials are stored row-major [row][cta]; after each barrier EVERY CTA
+// reduces all rows in the same fixed order (lane-strided over CTAs, then a
+// fixed shuffle tree), so the coefficients are bitwise identical across CTAs
+// and run to run without a second barrier.
+// ---------------------------------------------------------------------------
+constexpr int ST = 512;                 // threads per CTA
+constexpr int SW = ST / 32;
+constexpr size_t SMEM_LIMIT = 226 * 1024;       // + static smem <= 227 KB opt-in
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+        "r"(phase)
+        : "memory");
+}
+
+// partial[j * G + b] = <Ws[j], v> over this CTA's chunk (row vrow is v
+// itself: pass vrow = nrows - 1 to fold ||v||^2 in).  Four rows per warp are
+// in flight at once (independent fp64 accumulators).
+constexpr int GS_DR = 4;
+
+__device__ __forceinline__ void smem_dots(const float* Ws, int cpad, int nrows, int vrow,
+                                          const float* v, int cn, double* partial) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cn4 = cn >> 2;
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    for (int j0 = warp; j0 < nrows; j0 += SW * GS_DR) {
+        const float* row[GS_DR];
+        double s[GS_DR];
+#pragma unroll
+        for (int r = 0; r < GS_DR; ++r) {
+            const int j = min(j0 + r * SW, nrows - 1);
+            row[r] = j == vrow ? v : Ws + (size_t)j * cpad;
+            s[r] = 0.0;
+        }
+        for (int i = lane; i < cn4; i += 32) {
+            const float4 vv = v4[i];
+#pragma unroll
+            for (int r = 0; r < GS_DR; ++r)
+                s[r] = dot4(reinterpret_cast<const float4*>(row[r])[i], vv, s[r]);
+        }
+        for (int i = (cn4 << 2) + lane; i < cn; i += 32)
+#pragma unroll
+            for (int r = 0; r < GS_DR; ++r) s[r] = fma((double)row[r][i], (double)v[i], s[r]);
+#pragma unroll
+        for (int r = 0; r < GS_DR; ++r) {
+            const double t = warp_sum(s[r]);
+            const int j = j0 + r * SW;
+            if (lane == 0 && j < nrows) partial[(size_t)j * gridDim.x + blockIdx.x] = t;
+        }
+    }
+}
+
+// coef[j] = sum over CTAs of partial[j * G + b], identical in every CTA.
+// All loads of a warp's rows are issued before any add (one L2 round trip
+// instead of one per row x CTA group); per-lane order then a fixed shuffle
+// tree, so the result does not depend on which CTA computes it.
+constexpr int GS_MAXG = 160;            // <= 5 partials per lane
+constexpr int GS_RU = 6;                // rows per warp in flight
+
+__device__ __forceinline__ void all_reduce_rows(const double* partial, int nrows, double* coef) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int G = gridDim.x;
+    for (int j0 = warp; j0 < nrows; j0 += SW * GS_RU) {
+        double v[GS_RU][GS_MAXG / 32];
+#pragma unroll
+        for (int r = 0; r < GS_RU; ++r) {
+            const int j = j0 + r * SW;
+#pragma unroll
+            for (int t = 0; t < GS_MAXG / 32; ++t) {
+                const int b = lane + 32 * t;
+                v[r][t] = (j < nrows && b < G) ? __ldcg(partial + (size_t)j * G + b) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < GS_RU; ++r) {
+            double s = v[r][0];
+#pragma unroll
+            for (int t = 1; t < GS_MAXG / 32; ++t) s += v[r][t];
+            s = warp_sum(s);
+            const int j = j0 + r * SW;
+            if (lane == 0 && j < nrows) coef[j] = s;
+        }
+    }
+}
+
+// v <- v - sum_j c[j] Ws[j] over the chunk (fp64 accumulate, fp32 result);
+// returns this thread's part of ||v||^2 (of the rounded values).  The chunk
+// has fewer float4 than the CTA has threads, so the rows are split over
+// ngrp = ST / cn4 thread groups (row j -> group j % ngrp) whose fp64 partial
+// sums meet in SMEM (acc[g][i]) and are added in group order.
+__device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb, const double* c,
+                                              float* v, int cn, double4* acc) {
+    const int cn4 = cn >> 2;
+    int ngrp = cn4 > 0 ? ST / cn4 : 1;
+    ngrp = ngrp < 1 ? 1 : (ngrp > 8 ? 8 : ngrp);
+    const int g = threadIdx.x / (cn4 > 0 ? cn4 : 1);
+    const int i = threadIdx.x - g * cn4;
+    if (g < ngrp && i < cn4) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 4
+        for (int j = g; j < nb; j += ngrp) {
+            const float4 w = reinterpret_cast<const float4*>(Ws + (size_t)j * cpad)[i];
+            const double cj = c[j];
+            a0 = fma(-cj, (double)w.x, a0); a1 = fma(-cj, (double)w.y, a1);
+            a2 = fma(-cj, (double)w.z, a2); a3 = fma(-cj, (double)w.w, a3);
+        }
+        acc[g * cn4 + i] = make_double4(a0, a1, a2, a3);
+    }
+    __syncthreads();
+    double nrm = 0.0;
+    for (int t = threadIdx.x; t < cn4; t += ST) {
+        const float4 b = reinterpret_cast<const float4*>(v)[t];
+        double a0 = b.x, a1 = b.y, a2 = b.z, a3 = b.w;
+        for (int q = 0; q < ngrp; ++q) {
+            const double4 p = acc[q * cn4 + t];
+            a0 += p.x; a1 += p.y; a2 += p.z; a3 += p.w;
+        }
+        const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+        reinterpret_cast<float4*>(v)[t] = o;
+        nrm = fma((double)o.x, (double)o.x, nrm); nrm = fma((double)o.y, (double)o.y, nrm);
+        nrm = fma((double)o.z, (double)o.z, nrm); nrm = fma((double)o.w, (double)o.w, nrm);
+    }
+    for (int t = (cn4 << 2) + threadIdx.x; t < cn; t += ST) {
+        double a = (double)v[t];
+        for (int j = 0; j < nb; ++j) a = fma(-c[j], (double)Ws[(size_t)j * cpad + t], a);
+        const float o = (float)a;
+        v[t] = o;
+        nrm = fma((double)o, (double)o, nrm);
+    }
+    return nrm;
+}
+
+__global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, int64_t L,
+                                                   const float* __restrict__ q, int passes,
+                                                   int64_t chunk, double* h, double* stat,
+                                                   double* partial) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int nb = k + 1;
+    const int cpad = (int)((chunk + 3) & ~3LL);
+    const int64_t start = (int64_t)blockIdx.x * chunk;
+    const int64_t rem = L - start;
+    const int cn = rem <= 0 ? 0 : (int)(rem < chunk ? rem : chunk);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    double* h1 = reinterpret_cast<double*>(smem_raw + 16);          // [nb + 1]
+    double* h2 = h1 + (nb + 1);                                     // [nb]
+    double* red = h2 + nb;                                          // [SW]
+    float* qv = reinterpret_cast<float*>(
+        smem_raw + ((16 + sizeof(double) * (2 * nb + 1 + SW) + 15) & ~(size_t)15));
+    float* Ws = qv + cpad;                                          // [nb][cpad]
+    double4* acc = reinterpret_cast<double4*>(                      // [ST], 32-B aligned
+        (reinterpret_cast<uintptr_t>(Ws + (size_t)nb * cpad) + 31) & ~(uintptr_t)31);
+    const unsigned bar_a = smem_u32(bar);
+    const unsigned row_bytes = (unsigned)(((cn + 3) & ~3) * 4);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x < 32 && row_bytes > 0) {
+        if (threadIdx.x == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a),
+                         "r"(row_bytes * (unsigned)nb)
+                         : "memory");
+        __syncwarp();
+        for (int j = threadIdx.x; j < nb; j += 32)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+                "[%3];" ::"r"(smem_u32(Ws + (size_t)j * cpad)),
+                "l"(W + (size_t)j * ld + start), "r"(row_bytes), "r"(bar_a)
+                : "memory");
+    }
+    for (int i = threadIdx.x; i < cn; i += ST) qv[i] = q[start + i];   // (16-B alignment of q
+    if (row_bytes > 0) mbar_wait(bar_a, 0);                          //  not assumed here)
+    __syncthreads();
+
+    double* P1 = partial;                                    // [nb + 1][G]
+    double* P2 = P1 + (size_t)(nb + 1) * gridDim.x;          // [nb][G]
+    double* P3 = P2 + (size_t)nb * gridDim.x;                // [G]
+    smem_dots(Ws, cpad, nb + 1, nb, qv, cn, P1);             // h1 = W^T q, ||q||^2
+    grid.sync();
+    all_reduce_rows(P1, nb + 1, h1);
+    __syncthreads();
+    double nrm = smem_update(Ws, cpad, nb, h1, qv, cn, acc);      // q1 = q - W h1
+    if (passes == 2) {
+        __syncthreads();
+        smem_dots(Ws, cpad, nb, -1, qv, cn, P2);             // h2 = W^T q1
+        grid.sync();
+        all_reduce_rows(P2, nb, h2);
+        __syncthreads();
+        nrm = smem_update(Ws, cpad, nb, h2, qv, cn, acc);         // q2 = q1 - W h2
+    }
+    nrm = warp_sum(nrm);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < SW; ++w) t += red[w];
+        P3[blockIdx.x] = t;
+    }
+    grid.sync();
+    __shared__ double s_n2;
+    if (threadIdx.x < 32) all_reduce_rows(P3, 1, &s_n2);
+    __syncthreads();
+    const double hk = sqrt(s_n2);
+    const double qn = sqrt(h1[nb]);
+    const bool broke = hk <= 1e-14 * qn;                     // BREAKDOWN_RTOL, arnoldi.py:17,80
+    const float sc = (float)(broke ? 0.0 : 1.0 / hk);
+    float* wnext = W + (size_t)(k + 1) * ld + start;
+    for (int i = threadIdx.x; i < cn; i += ST) wnext[i] = qv[i] * sc;
+    if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i <= k; i += ST) h[i] = passes == 2 ? h1[i] + h2[i] : h1[i];
+        if (threadIdx.x == 0) {
+            h[k + 1] = hk;
+            stat[0] = qn;
+            stat[1] = broke ? 1.0 : 0.0;
+            stat[2] = broke ? 0.0 : 1.0 / hk;
+            stat[3] = hk;
+        }
+    }
+}
+
 }  // namespace ctk
 
 using namespace ctk;
@@ -480,6 +719,51 @@ static int try_cgs2_fused(float* W, int64_t ld, int k, int64_t L, float* q, doub
                                                 dim3(FT), args, smem, st);
     ctk_count_launch();
     if (e != cudaSuccess) return ctk_check_cuda(e, "k_cgs2_fused");
+    *done = true;
+    return CTK_OK;
+}
+
+// SMEM-resident path when every CTA's chunk of the k+1 rows fits in shared
+// memory with one CTA per SM.
+static size_t gs_smem_bytes(int k, int64_t chunk) {
+    const int nb = k + 1;
+    const size_t head = (16 + sizeof(double) * (2 * (size_t)nb + 1 + SW) + 15) & ~(size_t)15;
+    return head + sizeof(float) * (size_t)chunk * (nb + 1) + sizeof(double) * 4 * ST + 32;
+}
+
+static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
+                       double* stat, Scratch s, cudaStream_t st, bool* done) {
+    *done = false;
+    static int coop = -1, sms = 0;
+    if (coop < 0) {
+        const char* off = getenv("CTK_NO_SMEM_GS");
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaFuncSetAttribute(k_gs_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SMEM_LIMIT) != cudaSuccess)
+            coop = 0;
+        cudaGetLastError();
+        if (off && off[0] == '1') coop = 0;
+    }
+    if (coop != 1 || L < 4) return CTK_OK;
+    // chunk: a multiple of 4 floats (16-B bulk-copy alignment), >= 64 floats
+    int64_t G = sms;
+    int64_t chunk = ((L + G - 1) / G + 3) & ~3LL;
+    if (chunk < 64) chunk = 64;
+    G = (L + chunk - 1) / chunk;
+    if (G > GS_MAXG) return CTK_OK;
+    const size_t smem = gs_smem_bytes(k, chunk);
+    if (smem > SMEM_LIMIT) return CTK_OK;
+    // partials: (nb + 1) + nb + 1 rows of G doubles
+    if ((size_t)(2 * k + 4) * G > (size_t)MAXCH * s.nvec_cap) return CTK_OK;
+    double* partial = s.partial;
+    void* args[] = {&W, &ld, &k, &L, &q, &passes, &chunk, &h, &stat, &partial};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_gs_smem, dim3((unsigned)G),
+                                                dim3(ST), args, smem, st);
+    ctk_count_launch();
+    if (e != cudaSuccess) return ctk_check_cuda(e, "k_gs_smem");
     *done = true;
     return CTK_OK;
 }
@@ -595,6 +879,8 @@ extern "C" int ctk_gs_step(float* W, int64_t ld, int k, int64_t L, float* q, int
     Scratch s = carve(scratch, k + 3);
     if (passes != 1 && passes != 2) return ctk_fail(CTK_ERR_ARG, "passes must be 1 or 2");
     bool fused = false;
+    if ((rc = try_gs_smem(W, ld, k, L, q, passes, h, stat, s, st, &fused))) return rc;
+    if (fused) return CTK_OK;
     if (passes == 2 && (rc = try_cgs2_fused(W, ld, k, L, q, h, stat, s, st, &fused))) return rc;
     if (fused) return CTK_OK;
     double* h1 = s.tmp;                   // k+2: h1[0..k], ||q||^2

@@ -9,13 +9,22 @@
 //
 // B200 mapping: one CTA = a 32 x 16 pixel tile, 256 threads, 2 pixels per
 // thread.  Angles are processed in chunks of 32: for each chunk the CTA
-// stages, per angle, the short detector window its tile projects onto (zero
-// filled outside [0, D), which is exactly the reference's masks) into shared
-// memory with coalesced loads; the interpolation taps then come from smem.
-// g is evaluated in fp64 (no hardware texture lerp: its 8-bit fraction would
-// break the 1e-5 bar); taps and the lerp are fp32, each 32-angle partial sum
+// stages, per angle, the short detector window its tile projects onto into
+// shared memory with coalesced loads, as (p, d) pairs per bin b:
+//   v0 = u[b] (0 outside [0, D)),  v1 = the reference's second tap for i0 = b
+//   (u[b+1], 0 outside, u[1] for b == -1: the quirk is baked into the window),
+//   d = v1 - v0,  p = v0 - d,   so  (1 - w) v0 + w v1 = p + (1 + w) d.
+// g is evaluated in fixed point: the tile origin's g (fp64, the reference's
+// geometry) becomes T0 = (g - w0) * 2^F and the per-pixel steps h cg, -h sg
+// become 32-bit integers C, S with F = 32 - ceil(log2(wmax + 1)) fraction bits
+// (26 for the BASELINE configs), so every pixel's T = T0 + dx C + dy S is one
+// integer multiply-add with |error| <= 47 * 2^-(F+1) bin (~3.5e-7 at F = 26).
+// No hardware texture lerp (its 8-bit fraction would break the 1e-5 bar) and
+// no fp64 / conversion-pipe work per pixel-angle (FRND/F2I/F2F.F64 bounded the
+// previous version): T >> F indexes the pair, the top 23 fraction bits OR'ed
+// into 1.0f give 1 + w, and the tap is one FFMA.  Each 32-angle partial sum
 // is folded into an fp64 accumulator.  Small images split the angle range
-// over blockIdx.z into partial images reduced in a fixed order (no atomics).
+// over blockIdx.z into partial images reduced in a fixed order.
 #include <math.h>
 
 #include "ctk_common.cuh"
@@ -32,26 +41,25 @@ struct BackArgs {
     float* out;           // final image (S == 1) or partials [S][n]
     float* x;             // final image (S > 1)
     unsigned* cnt;        // S > 1: per-tile arrival tickets (zeroed once)
-    int nx, ny, D, a0, a1, per_split, wmax, split;
+    int nx, ny, D, a0, a1, per_split, wmax, split, fbits;
     double h, xmin, ymax, center;
 };
 
 __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
-    extern __shared__ float win[];                 // [BCA][wmax]
-    __shared__ double s_cg[BCA], s_sg[BCA];
+    extern __shared__ float2 win[];                // [BCA][wmax] (p, d)
+    __shared__ int4 s_par[BCA];                    // T0, C, S, smem base of the window
     __shared__ int s_w0[BCA];
 
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BTX + tx;
     const int ix0 = blockIdx.x * BTX, iy0 = blockIdx.y * BTY;
     const int ix = ix0 + tx, iyA = iy0 + ty, iyB = iy0 + ty + BROWS;
-    const double X = A.xmin + ((double)ix + 0.5) * A.h;
-    const double YA = A.ymax - ((double)iyA + 0.5) * A.h;
-    const double YB = A.ymax - ((double)iyB + 0.5) * A.h;
     // tile corner pixel centres
     const double Xlo = A.xmin + ((double)ix0 + 0.5) * A.h;
     const double Xhi = A.xmin + ((double)(ix0 + BTX - 1) + 0.5) * A.h;
     const double Yhi = A.ymax - ((double)iy0 + 0.5) * A.h;
     const double Ylo = A.ymax - ((double)(iy0 + BTY - 1) + 0.5) * A.h;
+    const int F = A.fbits, I = 32 - A.fbits;
+    const double scale = ldexp(1.0, F);
 
     const int aS = A.a0 + blockIdx.z * A.per_split;
     const int aE = min(A.a1, aS + A.per_split);
@@ -68,48 +76,50 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
             const double g10 = fma(Xhi, p.cg, fma(Ylo, p.sg, A.center));
             const double g11 = fma(Xhi, p.cg, fma(Yhi, p.sg, A.center));
             const double gmin = fmin(fmin(g00, g01), fmin(g10, g11));
-            s_cg[tid] = p.cg;
-            s_sg[tid] = p.sg;
-            s_w0[tid] = (int)floor(gmin) - 1;
+            const int w0 = (int)floor(gmin) - 1;
+            s_w0[tid] = w0;
+            // origin = pixel (ix0, iy0), i.e. g01 at (Xlo, Yhi)
+            const unsigned T0 = (unsigned)llrint((g01 - (double)w0) * scale);
+            const int C = (int)llrint(p.cg * A.h * scale);
+            const int S = (int)llrint(-p.sg * A.h * scale);
+            s_par[tid] = make_int4((int)T0, C, S,
+                                   (int)(unsigned)__cvta_generic_to_shared(win + tid * wmax));
         }
         __syncthreads();
-        // stage the detector windows, zero outside [0, D)
+        // stage the (mid, d) windows; zero taps outside [0, D), quirk at b == -1
         for (int ai = ty; ai < na; ai += BROWS) {
             const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
             const int w0 = s_w0[ai];
-            float* dst = win + ai * wmax;
+            float2* dst = win + ai * wmax;
             for (int i = tx; i < wmax; i += BTX) {
-                const int bin = w0 + i;
-                dst[i] = (bin >= 0 && bin < D) ? __ldg(row + bin) : 0.f;
+                const int b = w0 + i;
+                const float v0 = (b >= 0 && b < D) ? __ldg(row + b) : 0.f;
+                const int b1 = b == -1 ? q1 : b + 1;
+                const float v1 = (b >= -1 && b + 1 < D) ? __ldg(row + b1) : 0.f;
+                const float d = v1 - v0;
+                dst[i] = make_float2(v0 - d, d);
             }
         }
         __syncthreads();
         float sA = 0.f, sB = 0.f;
 #pragma unroll 4
         for (int ai = 0; ai < na; ++ai) {
-            const double cg = s_cg[ai], sg = s_sg[ai];
-            const int w0 = s_w0[ai];
-            const float* wrow = win + ai * wmax;
-            const int iq = min(max(q1 - w0, 0), wmax - 1);
+            const int4 P = s_par[ai];
+            const unsigned TA = (unsigned)P.x + (unsigned)tx * (unsigned)P.y + (unsigned)ty * (unsigned)P.z;
+            const unsigned TB = TA + (unsigned)BROWS * (unsigned)P.z;
             {
-                const double g = fma(X, cg, fma(YA, sg, A.center));
-                const double fl = floor(g);
-                const int i0 = (int)fl;
-                const float w = (float)(g - fl);
-                const int li = min(max(i0 - w0, 0), wmax - 2);
-                const float v0 = wrow[li];
-                const float v1 = (i0 == -1) ? wrow[iq] : wrow[li + 1];
-                sA += fmaf(w, v1 - v0, v0);
+                const float f1 = __uint_as_float(0x3f800000u | ((TA << I) >> 9));   // 1 + w
+                float2 pd;
+                asm("ld.shared.v2.f32 {%0, %1}, [%2];"
+                    : "=f"(pd.x), "=f"(pd.y) : "r"((TA >> F) * 8u + (unsigned)P.w));
+                sA += fmaf(f1, pd.y, pd.x);
             }
             {
-                const double g = fma(X, cg, fma(YB, sg, A.center));
-                const double fl = floor(g);
-                const int i0 = (int)fl;
-                const float w = (float)(g - fl);
-                const int li = min(max(i0 - w0, 0), wmax - 2);
-                const float v0 = wrow[li];
-                const float v1 = (i0 == -1) ? wrow[iq] : wrow[li + 1];
-                sB += fmaf(w, v1 - v0, v0);
+                const float f1 = __uint_as_float(0x3f800000u | ((TB << I) >> 9));
+                float2 pd;
+                asm("ld.shared.v2.f32 {%0, %1}, [%2];"
+                    : "=f"(pd.x), "=f"(pd.y) : "r"((TB >> F) * 8u + (unsigned)P.w));
+                sB += fmaf(f1, pd.y, pd.x);
             }
         }
         accA += (double)sA;
@@ -211,13 +221,18 @@ extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, i
     A.a1 = a1;
     A.per_split = (a1 - a0 + S - 1) / S;
     A.wmax = g->back_wmax;
+    {   // fixed-point fraction bits: window coordinates [0, wmax] need I bits
+        int I = 1;
+        while ((1 << I) <= g->back_wmax + 1) ++I;
+        A.fbits = 32 - I;
+    }
     A.split = S > 1;
     A.h = g->h;
     A.xmin = g->xmin;
     A.ymax = g->ymax;
     A.center = g->center;
     dim3 grid((g->nx + BTX - 1) / BTX, (g->ny + BTY - 1) / BTY, S), block(BTX, BROWS);
-    const size_t smem = (size_t)BCA * g->back_wmax * sizeof(float);
+    const size_t smem = (size_t)BCA * g->back_wmax * sizeof(float2);
     if (smem > 48 * 1024)
         CTK_CUDA(cudaFuncSetAttribute(k_back, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));

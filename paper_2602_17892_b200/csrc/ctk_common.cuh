@@ -99,8 +99,5 @@ static inline cudaStream_t ctk_stream(void* s) { return reinterpret_cast<cudaStr
 // K1 workspace: zero-bordered copies P, PT, then fwd_split row-chunk partials
 // and one arrival ticket per (angle, 128-bin block) -- zero-filled once.
 static inline int64_t ctk_stage_floats(const ctk_geom* g) {
-    const int64_t m = (int64_t)g->n_angles * g->det_count;
-    const int64_t tickets = (int64_t)g->n_angles * ((g->det_count + 127) / 128);
-    return (int64_t)g->ny * (g->nx + 2) + (int64_t)g->nx * (g->ny + 2) +
-           (g->fwd_split > 1 ? (int64_t)g->fwd_split * m + tickets : 0);
+    return (int64_t)g->ny * (g->nx + 2) + (int64_t)g->nx * (g->ny + 2);
 }

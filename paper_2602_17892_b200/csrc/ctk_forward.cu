@@ -23,6 +23,7 @@
 // midpoint/floor/clip sequence decides which column or row receives it.
 // That trace runs once, at geometry creation, into per-ray segment lists;
 // an apply sums them warp-per-ray inside the same launch as K1.
+#include <cooperative_groups.h>
 #include <math.h>
 
 #include <vector>
@@ -206,8 +207,6 @@ struct FwdArgs {
     const float* PT;         // zero-bordered transposed copy
     const float* b;          // optional: y = b - A x
     float* y;
-    float* part;             // split > 1: per-row-chunk partial sums [split][rows * D]
-    unsigned* cnt;           // split > 1: per-(angle, bin block) arrival tickets (zeroed)
     int split;               // row chunks per ray (blockIdx.z), small-problem parallelism
     const int* deg_slot;
     const long long* deg_cnt;   // segments per degenerate ray [slot * D + j]
@@ -341,35 +340,74 @@ __device__ __forceinline__ double forward_ray(const FwdArgs& A, int a, int slot,
 }
 
 // One ray per thread; SPLIT: rows of each ray over blockIdx.z (small problems).
+// A CTA is FWD_APB adjacent angles x 32 adjacent bins, one angle per warp:
+// neighbouring angles' rays cross nearly the same pixels at the same time,
+// so the warps of a CTA share the L1 lines their gathers pull from L2.
+constexpr int FWD_APB = FWD_THREADS / 32;
+
+constexpr int FWD_MAX_SPLIT = 4;
+
+__device__ __forceinline__ unsigned cluster_addr(const void* p, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(rank));
+    return r;
+}
+
 template <bool SPLIT>
 __global__ void __launch_bounds__(FWD_THREADS, 12) k_forward(FwdArgs A) {
-    const int a = A.a0 + blockIdx.y;
-    const int slot = A.deg_slot[a];
-    const int j = blockIdx.x * FWD_THREADS + threadIdx.x;
-    const size_t o = (size_t)blockIdx.y * A.D + j;
+    const int ai = blockIdx.y * FWD_APB + (threadIdx.x >> 5);
+    const int a = A.a0 + ai;
+    const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+    const size_t o = (size_t)ai * A.D + j;
     if (!SPLIT) {
-        if (j >= A.D) return;
-        const double acc = forward_ray(A, a, slot, j, 0);
+        if (a >= A.a1 || j >= A.D) return;
+        const double acc = forward_ray(A, a, A.deg_slot[a], j, 0);
         A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
         return;
     }
-    // Row chunks write partial sums; k_forward_finalize reduces them in chunk
-    // order.  (A last-arriving-CTA reduction needs a gpu-scope fence, which
-    // invalidates L1 on sm_100 and costs the gathers their cache hits.)
-    const int chunk = blockIdx.z;
-    const size_t rows = (size_t)(A.a1 - A.a0) * A.D;
-    if (j < A.D) A.part[chunk * rows + o] = (float)forward_ray(A, a, slot, j, chunk);
-}
-
-// Row-chunk partials -> y (fixed summation order; b - A x epilogue).
-__global__ void k_forward_finalize(const float* __restrict__ part, int split, size_t rows,
-                                   const float* __restrict__ b, float* __restrict__ y) {
-    for (size_t o = blockIdx.x * (size_t)blockDim.x + threadIdx.x; o < rows;
-         o += (size_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int c = 0; c < split; ++c) s += (double)part[(size_t)c * rows + o];
-        y[o] = b ? (float)((double)b[o] - s) : (float)s;
+    // Row chunks of the same rays form one thread-block cluster (1, 1, split).
+    // Chunks 1.. push their fp32 partial into chunk 0's shared memory over
+    // DSMEM and arrive on its mbarrier (release.cluster); chunk 0 waits
+    // (acquire.cluster) and sums in chunk order -- the same fixed order as a
+    // separate finalize pass, with no global fence (which would invalidate
+    // the L1 lines the gathers live on) and no second launch.
+    __shared__ float s_part[FWD_MAX_SPLIT - 1][FWD_THREADS];
+    __shared__ __align__(8) unsigned long long s_bar;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned rank = cl.block_rank();                 // == blockIdx.z
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+    if (rank == 0 && threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(A.split - 1)
+                     : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    cl.sync();
+    const bool valid = a < A.a1 && j < A.D;
+    const float v = valid ? (float)forward_ray(A, a, A.deg_slot[a], j, (int)rank) : 0.f;
+    if (rank != 0) {
+        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(
+                         cluster_addr(&s_part[rank - 1][threadIdx.x], 0)),
+                     "f"(v)
+                     : "memory");
+        __syncthreads();
+        if (threadIdx.x == 0)
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                             cluster_addr(&s_bar, 0))
+                         : "memory");
+        return;
+    }
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(bar)
+        : "memory");
+    if (!valid) return;
+    double s = (double)v;
+    for (int c = 1; c < A.split; ++c) s += (double)s_part[c - 1][threadIdx.x];
+    A.y[o] = A.b ? (float)((double)A.b[o] - s) : (float)s;
 }
 
 // Literal fp64 Siddon for every ray (validation path, ctk_forward_exact).
@@ -445,8 +483,6 @@ static FwdArgs make_args(const ctk_geom* g, const float* x, float* y, int a0, in
     A.a0 = a0;
     A.a1 = a1;
     A.split = 1;
-    A.part = nullptr;
-    A.cnt = nullptr;
     return A;
 }
 
@@ -542,20 +578,24 @@ extern "C" int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0
     A.P = P;
     A.PT = PT;
     A.split = g->fwd_split;
-    A.part = PT + (size_t)g->nx * (g->ny + 2);
-    A.cnt = reinterpret_cast<unsigned*>(A.part + (size_t)A.split * g->n_angles * g->det_count);
-    dim3 grid((g->det_count + FWD_THREADS - 1) / FWD_THREADS, a1 - a0, A.split);
-    if (A.split > 1)
-        k_forward<true><<<grid, FWD_THREADS, 0, st>>>(A);
-    else
-        k_forward<false><<<grid, FWD_THREADS, 0, st>>>(A);
-    CTK_LAUNCH_CHECK("k_forward");
+    dim3 grid((g->det_count + 31) / 32, (a1 - a0 + FWD_APB - 1) / FWD_APB, A.split);
     if (A.split > 1) {
-        const size_t rows = (size_t)(a1 - a0) * g->det_count;
-        int blocks = (int)((rows + 255) / 256);
-        if (blocks > 148 * 8) blocks = 148 * 8;
-        k_forward_finalize<<<blocks, 256, 0, st>>>(A.part, A.split, rows, b, y);
-        CTK_LAUNCH_CHECK("k_forward_finalize");
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(FWD_THREADS);
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 1;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = (unsigned)A.split;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CTK_CUDA(cudaLaunchKernelEx(&cfg, k_forward<true>, A));
+        ctk_count_launch();
+    } else {
+        k_forward<false><<<grid, FWD_THREADS, 0, st>>>(A);
+        CTK_LAUNCH_CHECK("k_forward");
     }
     ctk_prof_close(ph, st);
     return CTK_OK;

@@ -176,7 +176,7 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
         if (rmin < 64) sp = 1;
         g->fwd_split = (int)sp;
     }
-    if ((size_t)BCA * g->back_wmax * sizeof(float) > 200 * 1024) {
+    if ((size_t)BCA * g->back_wmax * 2 * sizeof(float) > 200 * 1024) {
         free_geom(g);
         return ctk_fail(CTK_ERR_GEOMETRY,
                         "pixel/bin ratio too large for the staged backprojector (window %d)",

@@ -46,6 +46,7 @@ struct ctk_geom {
     double xmin, xmax, ymin, ymax, center;
     int back_wmax;            // max staged bins per angle for one K2 tile
     int fwd_split;            // K1 row chunks per ray (small problems: more CTAs)
+    int fwd_pad;              // K1 zero columns each side of P / PT (warp lockstep walk)
     int n_degenerate;
     int h_pow2;               // pixel size is a power of two: x / h == x * (1 / h) exactly
     double inv_h;
@@ -96,8 +97,8 @@ int ctk_check_cuda(cudaError_t e, const char* what);
 
 static inline cudaStream_t ctk_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// K1 workspace: zero-bordered copies P, PT, then fwd_split row-chunk partials
+// K1 workspace: zero-padded copies P, PT
 // and one arrival ticket per (angle, 128-bin block) -- zero-filled once.
 static inline int64_t ctk_stage_floats(const ctk_geom* g) {
-    return (int64_t)g->ny * (g->nx + 2) + (int64_t)g->nx * (g->ny + 2);
+    return (int64_t)g->ny * (g->nx + 2 * g->fwd_pad) + (int64_t)g->nx * (g->ny + 2 * g->fwd_pad);
 }

@@ -146,52 +146,53 @@ struct FillSink {          // segment i of a ray -> entry i * stride of its colu
     }
 };
 
-// ---- K1 staging: zero-bordered row-major copy P and transposed copy PT ----
-// P : ny rows x (nx+2), P[iy][ix+1]  = x[iy][ix]
-// PT: nx rows x (ny+2), PT[ix][iy+1] = x[iy][ix]
+// ---- K1 staging: zero-padded row-major copy P and transposed copy PT ----
+// P : ny rows x (nx + 2 pad), P[iy][ix + pad]  = x[iy][ix]
+// PT: nx rows x (ny + 2 pad), PT[ix][iy + pad] = x[iy][ix]
 __global__ void __launch_bounds__(256) k_stage(const float* __restrict__ x, float* __restrict__ P,
-                                               float* __restrict__ PT, int nx, int ny) {
+                                               float* __restrict__ PT, int nx, int ny, int pad) {
     __shared__ float tile[32][33];
     const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
-    const int pP = nx + 2, pT = ny + 2;
+    const int tid = ty * 32 + tx;
+    const int pP = nx + 2 * pad, pT = ny + 2 * pad;
 #pragma unroll
     for (int r = ty; r < 32; r += 8) {
         int iy = by + r, ix = bx + tx;
         float v = (iy < ny && ix < nx) ? x[(size_t)iy * nx + ix] : 0.f;
         tile[r][tx] = v;
-        if (iy < ny && ix < nx) P[(size_t)iy * pP + ix + 1] = v;
+        if (iy < ny && ix < nx) P[(size_t)iy * pP + ix + pad] = v;
     }
-    // zero borders owned by edge tiles
-    if (blockIdx.x == 0) {
-        for (int r = ty * 32 + tx; r < 32; r += 256) {
-            int iy = by + r;
-            if (iy < ny) P[(size_t)iy * pP] = 0.f;
+    // zero padding owned by the edge tiles
+    if (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) {
+        const int c0 = blockIdx.x == 0 ? 0 : nx + pad;
+        for (int e = tid; e < 32 * pad; e += 256) {
+            const int iy = by + e / pad;
+            if (iy < ny) P[(size_t)iy * pP + c0 + e % pad] = 0.f;
         }
+        if (gridDim.x == 1)
+            for (int e = tid; e < 32 * pad; e += 256) {
+                const int iy = by + e / pad;
+                if (iy < ny) P[(size_t)iy * pP + nx + pad + e % pad] = 0.f;
+            }
     }
-    if (blockIdx.x == gridDim.x - 1) {
-        for (int r = ty * 32 + tx; r < 32; r += 256) {
-            int iy = by + r;
-            if (iy < ny) P[(size_t)iy * pP + nx + 1] = 0.f;
+    if (blockIdx.y == 0 || blockIdx.y == gridDim.y - 1) {
+        const int c0 = blockIdx.y == 0 ? 0 : ny + pad;
+        for (int e = tid; e < 32 * pad; e += 256) {
+            const int ix = bx + e / pad;
+            if (ix < nx) PT[(size_t)ix * pT + c0 + e % pad] = 0.f;
         }
-    }
-    if (blockIdx.y == 0) {
-        for (int r = ty * 32 + tx; r < 32; r += 256) {
-            int ix = bx + r;
-            if (ix < nx) PT[(size_t)ix * pT] = 0.f;
-        }
-    }
-    if (blockIdx.y == gridDim.y - 1) {
-        for (int r = ty * 32 + tx; r < 32; r += 256) {
-            int ix = bx + r;
-            if (ix < nx) PT[(size_t)ix * pT + ny + 1] = 0.f;
-        }
+        if (gridDim.y == 1)
+            for (int e = tid; e < 32 * pad; e += 256) {
+                const int ix = bx + e / pad;
+                if (ix < nx) PT[(size_t)ix * pT + ny + pad + e % pad] = 0.f;
+            }
     }
     __syncthreads();
 #pragma unroll
     for (int r = ty; r < 32; r += 8) {
         int ix = bx + r, iy = by + tx;
-        if (ix < nx && iy < ny) PT[(size_t)ix * pT + iy + 1] = tile[tx][r];
+        if (ix < nx && iy < ny) PT[(size_t)ix * pT + iy + pad] = tile[tx][r];
     }
 }
 
@@ -214,58 +215,70 @@ struct FwdArgs {
     const float* deg_len;
     int deg_maxseg;
     ExactGrid eg;
-    int D, a0, a1;
+    int D, a0, a1, pad;
 };
 
 // One ray of the row walk (see the header comment).  base/pitch/C describe
-// the zero-bordered copy the ray walks; MIRROR reverses the cross axis.
+// the zero-padded copy the ray walks; MIRROR reverses the cross axis.
+//
+// The lanes of a warp (32 adjacent bins of one angle) walk the SAME rows in
+// lockstep: each lane's own row range [kb, ke) is widened to the warp's
+// union [kw, kW), and outside its range a lane's taps fall into the zero
+// padding (pad >= the cross-axis spread of the warp's rays, set at geometry
+// creation), so they add exact zeros and need no predicate.  Rays entering
+// through the side of the image otherwise start on different rows, which
+// turns each warp gather into ~10 scattered sectors instead of 2-3.
 template <bool MIRROR>
 __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
-                                           const float* __restrict__ base, int R, int C,
+                                           const float* __restrict__ base, int R, int C, int pad,
                                            int krow0, int krow1) {
     const double sigma = (double)p.sigma_fx * (1.0 / 4294967296.0);
     const double u0 = fma(p.beta, s, p.alpha);
-    // the ray meets the image iff u(k) in (0, C) for some k in [0, R]
-    if (!(u0 < (double)C + 1.0) || !(u0 + (double)R * sigma > -1.0)) return 0.0;
     const long long Sg = p.sigma_fx;
     const long long U0 = llrint(u0 * 4294967296.0);
     const long long C2 = (long long)C << 32;
+    // the ray meets the image iff u(k) in (0, C) for some k in [0, R]
+    bool hit = (u0 < (double)C + 1.0) && (u0 + (double)R * sigma > -1.0) && U0 < C2;
     // rows k with u(k+1) > 0 and u(k) < C  (=> floor(u(k)) in [-1, C-1])
     // fp64 estimates of the integer quotients, then exact integer fix-ups
     // (cheaper than two 64-bit integer divisions per ray)
-    long long kb, ke;
-    if (U0 + Sg > 0) {
-        kb = 0;
-    } else {
-        if (Sg == 0) return 0.0;
-        kb = (long long)floor((double)(-U0) * p.inv_sg);     // smallest k: U0 + (k+1) Sg > 0
-        while (U0 + (kb + 1) * Sg <= 0) ++kb;
-        while (kb > 0 && U0 + kb * Sg > 0) --kb;
+    long long kb = 0, ke = R;
+    if (hit) {
+        if (U0 + Sg <= 0) {
+            if (Sg == 0) {
+                hit = false;
+            } else {
+                kb = (long long)floor((double)(-U0) * p.inv_sg);   // smallest k: U0 + (k+1) Sg > 0
+                while (U0 + (kb + 1) * Sg <= 0) ++kb;
+                while (kb > 0 && U0 + kb * Sg > 0) --kb;
+            }
+        }
+        if (Sg != 0) {
+            ke = (long long)ceil((double)(C2 - U0) * p.inv_sg);    // smallest k: U0 + k Sg >= C
+            while (U0 + ke * Sg < C2) ++ke;
+            while (ke > 0 && U0 + (ke - 1) * Sg >= C2) --ke;
+        }
+        if (kb < krow0) kb = krow0;           // this block's row chunk only
+        if (ke > krow1) ke = krow1;
+        if (kb >= ke) hit = false;
     }
-    if (U0 >= C2) return 0.0;
-    if (Sg == 0) {
-        ke = R;
-    } else {
-        ke = (long long)ceil((double)(C2 - U0) * p.inv_sg);  // smallest k: U0 + k Sg >= C
-        while (U0 + ke * Sg < C2) ++ke;
-        while (ke > 0 && U0 + (ke - 1) * Sg >= C2) --ke;
-    }
-    if (kb < krow0) kb = krow0;               // this block's row chunk only
-    if (ke > krow1) ke = krow1;
-    if (kb >= ke) return 0.0;
+    const unsigned lanes = __activemask();
+    const int kw = __reduce_min_sync(lanes, hit ? (int)kb : 0x7fffffff);
+    const int kW = __reduce_max_sync(lanes, hit ? (int)ke : (int)0x80000000);
+    if (!hit) return 0.0;
 
-    const int pitch = C + 2;
+    const int pitch = C + 2 * pad;
     // sigma < 1 here (the host clamps sigma_fx below 2^32), so the cross
     // coordinate is (column c, 32-bit fraction) and a row splits exactly when
     // the fraction add carries.  q = flat index of the pair's first tap:
-    // row k, bordered column c+1 (MIRROR: bordered column C - c, second tap
-    // one to the left).
-    const long long u = U0 + kb * Sg;
+    // row k, padded column c + pad (MIRROR: padded column C - 1 - c + pad,
+    // second tap one to the left).
+    const long long u = U0 + (long long)kw * Sg;
     unsigned frac = (unsigned)u;
     const unsigned Sf = (unsigned)Sg;
     const int c0 = (int)(u >> 32);
     // MIRROR keeps q negated so both directions advance with add-with-carry
-    int q = (int)kb * pitch + (MIRROR ? C - c0 : c0 + 1);
+    int q = kw * pitch + (MIRROR ? C - 1 - c0 + pad : c0 + pad);
     if (MIRROR) q = -q;
     // Second-tap weight wb = max(0, f + sigma - 1) * Lx, the length the row
     // spends past the grid line (0 when it does not reach it); wa = L - wb.
@@ -273,10 +286,9 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
     const float L = p.L, Lx = p.Lx;
     const float off = (float)(((double)Sg * (1.0 / 4294967296.0) - 2.0) * (double)p.Lx);
     double acc = 0.0;
-    int k = (int)kb;
-    const int kend = (int)ke;
-    while (k < kend) {
-        const int kstop = min(kend, k + 48);
+    int k = kw;
+    while (k < kW) {
+        const int kstop = min(kW, k + 48);
         float s0 = 0.f, s1 = 0.f;
 #pragma unroll 8
         for (; k < kstop; ++k) {
@@ -333,10 +345,10 @@ __device__ __forceinline__ double forward_ray(const FwdArgs& A, int a, int slot,
     const int per = (R + A.split - 1) / A.split;
     const int k0 = chunk * per, k1 = min(R, k0 + per);
     if (p.frame == 0)
-        return p.mirror ? walk_ray<true>(p, s, A.P, A.eg.ny, A.eg.nx, k0, k1)
-                        : walk_ray<false>(p, s, A.P, A.eg.ny, A.eg.nx, k0, k1);
-    return p.mirror ? walk_ray<true>(p, s, A.PT, A.eg.nx, A.eg.ny, k0, k1)
-                    : walk_ray<false>(p, s, A.PT, A.eg.nx, A.eg.ny, k0, k1);
+        return p.mirror ? walk_ray<true>(p, s, A.P, A.eg.ny, A.eg.nx, A.pad, k0, k1)
+                        : walk_ray<false>(p, s, A.P, A.eg.ny, A.eg.nx, A.pad, k0, k1);
+    return p.mirror ? walk_ray<true>(p, s, A.PT, A.eg.nx, A.eg.ny, A.pad, k0, k1)
+                    : walk_ray<false>(p, s, A.PT, A.eg.nx, A.eg.ny, A.pad, k0, k1);
 }
 
 // One ray per thread; SPLIT: rows of each ray over blockIdx.z (small problems).
@@ -482,6 +494,7 @@ static FwdArgs make_args(const ctk_geom* g, const float* x, float* y, int a0, in
     A.D = g->det_count;
     A.a0 = a0;
     A.a1 = a1;
+    A.pad = g->fwd_pad;
     A.split = 1;
     return A;
 }
@@ -569,10 +582,10 @@ extern "C" int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0
     CTK_CUDA(cudaSetDevice(g->device));
     cudaStream_t st = ctk_stream(stream);
     float* P = work;
-    float* PT = work + (size_t)g->ny * (g->nx + 2);
+    float* PT = work + (size_t)g->ny * (g->nx + 2 * g->fwd_pad);
     dim3 sg((g->nx + 31) / 32, (g->ny + 31) / 32), sb(32, 8);
     const int ph = ctk_prof_open(0, st);
-    k_stage<<<sg, sb, 0, st>>>(x, P, PT, g->nx, g->ny);
+    k_stage<<<sg, sb, 0, st>>>(x, P, PT, g->nx, g->ny, g->fwd_pad);
     CTK_LAUNCH_CHECK("k_stage");
     FwdArgs A = make_args(g, x, y, a0, a1, b);
     A.P = P;

@@ -89,12 +89,18 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
     if (det_count <= 0 || !(det_spacing > 0) || !offsets)
         return ctk_fail(CTK_ERR_GEOMETRY, "invalid detector: count=%d, spacing=%g", det_count,
                         det_spacing);
-    if ((int64_t)nx + 2 > (1 << 20) || (int64_t)ny + 2 > (1 << 20))
+    // K1 lockstep walk: a warp's 32 adjacent rays spread over at most
+    // 31 * sqrt(2) * spacing / h cross-axis pixels; that many zero columns on
+    // each side of the staged copies keep every lane's off-range taps in range.
+    const int64_t pad = (int64_t)ceil(31.0 * 1.4142135623730951 * det_spacing / pixel_size) + 3;
+    if ((int64_t)nx + 2 * pad > (1 << 20) || (int64_t)ny + 2 * pad > (1 << 20) ||
+        (int64_t)(nx > ny ? nx : ny) * ((nx > ny ? nx : ny) + 2 * pad) >= (1LL << 31))
         return ctk_fail(CTK_ERR_GEOMETRY, "grid too large for the 32.32 walk (%d x %d)", nx, ny);
 
     ctk_geom* g = new ctk_geom();
     memset(g, 0, sizeof(*g));
     g->device = device;
+    g->fwd_pad = (int)pad;
     g->nx = nx;
     g->ny = ny;
     g->n_angles = n_angles;

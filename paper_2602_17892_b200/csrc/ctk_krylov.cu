@@ -26,7 +26,7 @@ constexpr int KT = 256;            // dots: threads per CTA
 constexpr int KWARPS = KT / 32;
 constexpr int JG = 8;              // rows per dots CTA
 constexpr int MAXCH = 1024;        // max L-chunks (= partial rows)
-constexpr int CT = 128;            // combine: threads per CTA
+constexpr int CT = 256;            // combine: threads per CTA
 constexpr int KMAX_VEC = 4096;     // rows per call (smem bound of k_combine)
 
 struct Scratch {                   // carved from the caller's zero-filled scratch
@@ -146,50 +146,75 @@ __global__ void __launch_bounds__(KT) k_dots(const float* __restrict__ W, int64_
 }
 
 // dst = (base ? base : 0) + sgn * sum_j coef[j] W_j ; optional ||dst||^2.
+// A CTA owns a tile of 32 float4 columns; its 8 warps split the rows
+// (row j -> warp j % 8, each lane one float4 column, 4 rows unrolled), so
+// even 33k-65k-float vectors with ~40 rows keep every SM busy with many
+// independent 16-B loads; the 8 fp64 partial float4s of a column meet in
+// SMEM and are added in warp order (deterministic).
+constexpr int CW = CT / 32;                 // row groups (warps) per CTA
+
 __global__ void __launch_bounds__(CT) k_combine(const float* __restrict__ W, int64_t ld, int nvec,
                                                 const double* __restrict__ coef, double sgn,
                                                 const float* base, float* dst, int64_t L,
                                                 double* norm_out, double* partial,
                                                 unsigned int* ticket) {
     extern __shared__ double c[];                                 // [nvec]
-    __shared__ double red[CT / 32];
+    __shared__ double4 red[CW][32];
+    __shared__ double nred[CW];
     for (int j = threadIdx.x; j < nvec; j += CT) c[j] = sgn * coef[j];
     __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t L4 = L >> 2;
+    const int64_t ntiles = (L4 + 31) >> 5;
     double nrm = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)CT + threadIdx.x; i < L4;
-         i += (int64_t)gridDim.x * CT) {
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t i = (t << 5) + lane;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        if (base) {
-            const float4 b = reinterpret_cast<const float4*>(base)[i];
-            a0 = b.x; a1 = b.y; a2 = b.z; a3 = b.w;
-        }
-        int j = 0;
-        for (; j + 8 <= nvec; j += 8) {           // 8 independent 16-B loads in flight
-            float4 w[8];
+        if (i < L4) {
+            const float4* col = reinterpret_cast<const float4*>(W) + i;
+            const int64_t ld4 = ld >> 2;
+            int j = warp;
+            for (; j + 3 * CW < nvec; j += 4 * CW) {
+                float4 w[4];
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                w[q] = __ldg(reinterpret_cast<const float4*>(W + (size_t)(j + q) * ld) + i);
+                for (int q = 0; q < 4; ++q) w[q] = __ldg(col + (size_t)(j + q * CW) * ld4);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const double cj = c[j + q];
-                a0 = fma(cj, (double)w[q].x, a0); a1 = fma(cj, (double)w[q].y, a1);
-                a2 = fma(cj, (double)w[q].z, a2); a3 = fma(cj, (double)w[q].w, a3);
+                for (int q = 0; q < 4; ++q) {
+                    const double cj = c[j + q * CW];
+                    a0 = fma(cj, (double)w[q].x, a0); a1 = fma(cj, (double)w[q].y, a1);
+                    a2 = fma(cj, (double)w[q].z, a2); a3 = fma(cj, (double)w[q].w, a3);
+                }
+            }
+            for (; j < nvec; j += CW) {
+                const float4 w = __ldg(col + (size_t)j * ld4);
+                const double cj = c[j];
+                a0 = fma(cj, (double)w.x, a0); a1 = fma(cj, (double)w.y, a1);
+                a2 = fma(cj, (double)w.z, a2); a3 = fma(cj, (double)w.w, a3);
             }
         }
-        for (; j < nvec; ++j) {
-            const float4 w = __ldg(reinterpret_cast<const float4*>(W + (size_t)j * ld) + i);
-            const double cj = c[j];
-            a0 = fma(cj, (double)w.x, a0); a1 = fma(cj, (double)w.y, a1);
-            a2 = fma(cj, (double)w.z, a2); a3 = fma(cj, (double)w.w, a3);
+        red[warp][lane] = make_double4(a0, a1, a2, a3);
+        __syncthreads();
+        if (warp == 0 && i < L4) {
+            if (base) {
+                const float4 b = reinterpret_cast<const float4*>(base)[i];
+                a0 = b.x; a1 = b.y; a2 = b.z; a3 = b.w;
+            } else {
+                a0 = a1 = a2 = a3 = 0.0;
+            }
+#pragma unroll
+            for (int w = 0; w < CW; ++w) {
+                const double4 p = red[w][lane];
+                a0 += p.x; a1 += p.y; a2 += p.z; a3 += p.w;
+            }
+            const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+            reinterpret_cast<float4*>(dst)[i] = o;
+            nrm = fma((double)o.x, (double)o.x, nrm); nrm = fma((double)o.y, (double)o.y, nrm);
+            nrm = fma((double)o.z, (double)o.z, nrm); nrm = fma((double)o.w, (double)o.w, nrm);
         }
-        const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
-        reinterpret_cast<float4*>(dst)[i] = o;
-        nrm = fma((double)o.x, (double)o.x, nrm); nrm = fma((double)o.y, (double)o.y, nrm);
-        nrm = fma((double)o.z, (double)o.z, nrm); nrm = fma((double)o.w, (double)o.w, nrm);
+        __syncthreads();
     }
-    if (blockIdx.x == gridDim.x - 1) {
-        for (int64_t i = (L4 << 2) + threadIdx.x; i < L; i += CT) {
+    if (blockIdx.x == gridDim.x - 1 && warp == 0) {               // scalar tail L % 4
+        for (int64_t i = (L4 << 2) + lane; i < L; i += 32) {
             double a = base ? (double)base[i] : 0.0;
             for (int j = 0; j < nvec; ++j) a = fma(c[j], (double)W[(size_t)j * ld + i], a);
             const float o = (float)a;
@@ -199,12 +224,12 @@ __global__ void __launch_bounds__(CT) k_combine(const float* __restrict__ W, int
     }
     if (!norm_out) return;
     const double s = warp_sum(nrm);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    if (lane == 0) nred[warp] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
 #pragma unroll
-        for (int w = 0; w < CT / 32; ++w) t += red[w];
+        for (int w = 0; w < CW; ++w) t += nred[w];
         partial[blockIdx.x] = t;
     }
     last_cta_reduce(partial, gridDim.x, 1, ticket, norm_out);
@@ -547,6 +572,32 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
     const int cn4 = cn >> 2;
     int ngrp = cn4 > 0 ? ST / cn4 : 1;
     ngrp = ngrp < 1 ? 1 : (ngrp > 8 ? 8 : ngrp);
+    if (cn4 > ST / 2) {          // wide chunk: one thread per float4, all rows
+        double nrm = 0.0;
+        for (int t = threadIdx.x; t < cn4; t += ST) {
+            const float4 b = reinterpret_cast<const float4*>(v)[t];
+            double a0 = b.x, a1 = b.y, a2 = b.z, a3 = b.w;
+#pragma unroll 4
+            for (int j = 0; j < nb; ++j) {
+                const float4 w = reinterpret_cast<const float4*>(Ws + (size_t)j * cpad)[t];
+                const double cj = c[j];
+                a0 = fma(-cj, (double)w.x, a0); a1 = fma(-cj, (double)w.y, a1);
+                a2 = fma(-cj, (double)w.z, a2); a3 = fma(-cj, (double)w.w, a3);
+            }
+            const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+            reinterpret_cast<float4*>(v)[t] = o;
+            nrm = fma((double)o.x, (double)o.x, nrm); nrm = fma((double)o.y, (double)o.y, nrm);
+            nrm = fma((double)o.z, (double)o.z, nrm); nrm = fma((double)o.w, (double)o.w, nrm);
+        }
+        for (int t = (cn4 << 2) + threadIdx.x; t < cn; t += ST) {
+            double a = (double)v[t];
+            for (int j = 0; j < nb; ++j) a = fma(-c[j], (double)Ws[(size_t)j * cpad + t], a);
+            const float o = (float)a;
+            v[t] = o;
+            nrm = fma((double)o, (double)o, nrm);
+        }
+        return nrm;
+    }
     const int g = threadIdx.x / (cn4 > 0 ? cn4 : 1);
     const int i = threadIdx.x - g * cn4;
     if (g < ngrp && i < cn4) {
@@ -799,7 +850,7 @@ static int launch_combine(const float* W, int64_t ld, int nvec, const double* co
                           cudaStream_t st) {
     if (nvec > KMAX_VEC) return ctk_fail(CTK_ERR_ARG, "too many vectors (%d)", nvec);
     const int64_t L4 = L >> 2;
-    int64_t G = (L4 + CT - 1) / CT;
+    int64_t G = (L4 + 31) / 32;                       // 32-float4 column tiles
     if (G > MAXCH) G = MAXCH;
     if (G < 1) G = 1;
     const size_t smem = sizeof(double) * (size_t)(nvec > 0 ? nvec : 1);

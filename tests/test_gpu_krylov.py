@@ -19,7 +19,8 @@ def basis_with(torch, Q, rows):
     return B
 
 
-@pytest.mark.parametrize("L,k", [(1000, 0), (4099, 5), (130680, 30), (262147, 63)])
+@pytest.mark.parametrize("L,k", [(1000, 0), (4099, 5), (65536, 80), (130680, 30), (262147, 63),
+                                 (1048576, 3), (2086560, 1), (4194309, 6)])
 def test_cgs2_step_matches_fp64_mgs(cuda, L, k):
     torch = cuda
     rng = np.random.default_rng(L + k)
@@ -70,7 +71,7 @@ def test_cgs2_breakdown_flag(cuda):
     assert st[3] <= 1e-5 * st[0]
 
 
-@pytest.mark.parametrize("L,k", [(33, 4), (32940, 17), (1000003, 40)])
+@pytest.mark.parametrize("L,k", [(33, 4), (32940, 17), (130683, 77), (1000003, 40)])
 def test_combine_and_norms(cuda, L, k):
     torch = cuda
     rng = np.random.default_rng(k)

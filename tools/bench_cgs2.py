@@ -3,7 +3,8 @@ import sys, time
 sys.path.insert(0, '.')
 import numpy as np, torch
 from paper_2602_17892_b200.arnoldi import DeviceBasis
-for L in (32940, 65536, 130680, 1048576):
+Ls = [int(a) for a in sys.argv[1:]] or [32940, 65536, 130680, 1048576]
+for L in Ls:
     for k in (1, 10, 40, 80):
         B = DeviceBasis(L, k + 3, torch.device('cuda', 0), torch)
         B.W[:k + 1] = torch.randn(k + 1, B.ld, device='cuda')

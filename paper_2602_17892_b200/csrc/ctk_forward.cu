@@ -357,7 +357,7 @@ __device__ __forceinline__ double forward_ray(const FwdArgs& A, int a, int slot,
 // so the warps of a CTA share the L1 lines their gathers pull from L2.
 constexpr int FWD_APB = FWD_THREADS / 32;
 
-constexpr int FWD_MAX_SPLIT = 4;
+constexpr int FWD_MAX_SPLIT = 8;            // portable cluster size limit
 
 __device__ __forceinline__ unsigned cluster_addr(const void* p, unsigned rank) {
     unsigned r;

@@ -173,13 +173,16 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
         g->n_degenerate += p.degenerate;
     }
     g->back_wmax = (int)ceil(max_span) + 6;
-    {   // K1 row split: aim for ~3 waves of 128-thread CTAs on 148 SMs
+    {   // K1 row split: up to one wave of 128-thread CTAs (12 resident per SM)
         const int64_t m = (int64_t)n_angles * det_count;
-        int64_t sp = (148LL * 2048 * 3 / 2 + m - 1) / m;
+        int64_t sp = (148LL * 12 * 128 + m - 1) / m;
         if (sp < 1) sp = 1;
-        if (sp > 4) sp = 4;
+        if (sp > 8) sp = 8;
         const int rmin = nx < ny ? nx : ny;
-        if (rmin < 64) sp = 1;
+        if (sp > rmin / 32) sp = rmin / 32;               // >= 32 rows per chunk: the per-ray
+        if (sp < 1) sp = 1;                               // setup must stay amortised
+        const char* ov = getenv("CTK_FWD_SPLIT");          // tuning override (1..8)
+        if (ov && atoi(ov) >= 1 && atoi(ov) <= 8) sp = atoi(ov);
         g->fwd_split = (int)sp;
     }
     if ((size_t)BCA * g->back_wmax * 2 * sizeof(float) > 200 * 1024) {

@@ -257,11 +257,24 @@ bool g_fast = [] {
     return !(e && e[0] == '1');
 }();
 
+// ||x[1:n]||: plain sum of squares (vectorisable), rescaled only when it
+// under/overflows (hypot per element costs ~30 ns).
+double tail_norm(const double* x, int n, int stride) {
+    double s = 0.0;
+    for (int i = 1; i < n; ++i) {
+        const double v = x[(size_t)i * stride];
+        s += v * v;
+    }
+    if (s > 1e-290 && s < 1e290) return sqrt(s);
+    double xn = 0.0;
+    for (int i = 1; i < n; ++i) xn = hypot(xn, x[(size_t)i * stride]);
+    return xn;
+}
+
 // dlarfg: reflector I - tau v v^T with v[0] = 1 mapping x to (beta, 0, ...).
 void householder(double* x, int n, int stride, double* tau, double* beta) {
     const double alpha = x[0];
-    double xn = 0.0;
-    for (int i = 1; i < n; ++i) xn = hypot(xn, x[(size_t)i * stride]);
+    const double xn = tail_norm(x, n, stride);
     if (xn == 0.0) {
         *tau = 0.0;
         *beta = alpha;
@@ -273,6 +286,29 @@ void householder(double* x, int n, int stride, double* tau, double* beta) {
     for (int i = 1; i < n; ++i) x[(size_t)i * stride] *= sc;
     x[0] = 1.0;
     *beta = b;
+}
+
+// Dense kernels of the bidiagonalisation (column-major, contiguous columns).
+// The dot product is written with 8 independent partial sums so it
+// vectorises without -ffast-math; AVX2/FMA clones are picked at load time.
+#if defined(__x86_64__) && defined(__GNUC__) && !defined(__clang__)
+#define CTK_HOT __attribute__((target_clones("arch=x86-64-v3", "default")))
+#else
+#define CTK_HOT
+#endif
+
+CTK_HOT double col_dot(const double* a, const double* b, int n) {
+    double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int r = 0;
+    for (; r + 8 <= n; r += 8)
+        for (int q = 0; q < 8; ++q) p[q] += a[r + q] * b[r + q];
+    double s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+    for (; r < n; ++r) s += a[r] * b[r];
+    return s;
+}
+
+CTK_HOT void col_axpy(double alpha, const double* x, double* y, int n) {
+    for (int r = 0; r < n; ++r) y[r] += alpha * x[r];
 }
 
 struct Bidiag {
@@ -301,16 +337,12 @@ void bidiagonalize(const double* H, int m, int n, double beta, Bidiag& bd) {
         double tq, b;
         householder(&at(i, i), m - i, 1, &tq, &b);
         if (tq != 0.0) {
+            const double* v = &at(i, i);
             for (int j = i + 1; j < n; ++j) {
-                double s = 0.0;
-                for (int r = i; r < m; ++r) s += at(r, i) * at(r, j);
-                s *= tq;
-                for (int r = i; r < m; ++r) at(r, j) -= s * at(r, i);
+                double* col = &at(i, j);
+                col_axpy(-tq * col_dot(v, col, m - i), v, col, m - i);
             }
-            double s = 0.0;
-            for (int r = i; r < m; ++r) s += at(r, i) * bd.g[r];
-            s *= tq;
-            for (int r = i; r < m; ++r) bd.g[r] -= s * at(r, i);
+            col_axpy(-tq * col_dot(v, &bd.g[i], m - i), v, &bd.g[i], m - i);
         }
         bd.d[i] = b;
         if (i < n - 1) {
@@ -320,15 +352,10 @@ void bidiagonalize(const double* H, int m, int n, double beta, Bidiag& bd) {
             bd.taup[i] = tp;
             bd.e[i] = b2;
             if (tp != 0.0) {
-                for (int r = i + 1; r < m; ++r) {
-                    double s = 0.0;
-                    for (int j = i + 1; j < n; ++j) s += at(r, j) * at(i, j);
-                    w[r] = s * tp;
-                }
-                for (int j = i + 1; j < n; ++j) {
-                    const double vj = at(i, j);
-                    for (int r = i + 1; r < m; ++r) at(r, j) -= w[r] * vj;
-                }
+                // w = A(i+1:, i+1:) v by columns (contiguous), then the rank-1 update
+                for (int r = i + 1; r < m; ++r) w[r] = 0.0;
+                for (int j = i + 1; j < n; ++j) col_axpy(at(i, j), &at(i + 1, j), &w[i + 1], m - i - 1);
+                for (int j = i + 1; j < n; ++j) col_axpy(-tp * at(i, j), &w[i + 1], &at(i + 1, j), m - i - 1);
             }
         }
     }
@@ -360,7 +387,8 @@ bool damped_bidiag_solve(std::vector<double> d, std::vector<double> e, std::vect
             double r = lam, rhs = 0.0;       // damping row: lam at column j
             for (int c = j; c < n; ++c) {
                 const double a = d[c];
-                const double h = hypot(a, r);
+                const double ss = a * a + r * r;     // |a|, |r| are matrix-scale: no hypot needed
+                const double h = (ss > 1e-290 && ss < 1e290) ? sqrt(ss) : hypot(a, r);
                 if (h == 0.0) break;
                 const double cs = a / h, sn = r / h;
                 d[c] = h;

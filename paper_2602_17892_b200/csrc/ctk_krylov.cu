@@ -800,7 +800,12 @@ static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int pas
     }
     if (coop != 1 || L < 4) return CTK_OK;
     // chunk: a multiple of 4 floats (16-B bulk-copy alignment), >= 64 floats
-    int64_t G = sms;
+    static int gcap = -1;
+    if (gcap < 0) {
+        const char* e = getenv("CTK_GS_CTAS");             // tuning override
+        gcap = e ? atoi(e) : 0;
+    }
+    int64_t G = gcap > 0 && gcap < sms ? gcap : sms;
     int64_t chunk = ((L + G - 1) / G + 3) & ~3LL;
     if (chunk < 64) chunk = 64;
     G = (L + chunk - 1) / chunk;

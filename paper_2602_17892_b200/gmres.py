@@ -201,6 +201,25 @@ def _projected_task(lib, H, beta, code, value, fallback=float("nan")):
     return out, y
 
 
+_TP_CONTROLLER = []
+
+
+def _blas_single_thread():
+    """Single-threaded BLAS for the driver's worker threads (their projected
+    solves are tiny; a threaded BLAS would oversubscribe the host).  The
+    threadpoolctl controller scans the loaded libraries once (~5 ms), then
+    each limit costs ~20 us."""
+    import contextlib
+    if not _TP_CONTROLLER:
+        try:
+            from threadpoolctl import ThreadpoolController
+            _TP_CONTROLLER.append(ThreadpoolController())
+        except Exception:   # pragma: no cover
+            _TP_CONTROLLER.append(None)
+    ctl = _TP_CONTROLLER[0]
+    return ctl.limit(limits=1, user_api="blas") if ctl is not None else contextlib.nullcontext()
+
+
 class _DeviceSolve:
     """One run_gmres call.
 
@@ -380,16 +399,8 @@ class _DeviceSolve:
         return beta, d0n
 
     def run(self) -> SolveResult:
-        try:
-            from threadpoolctl import threadpool_limits
-            limiter = threadpool_limits(limits=1, user_api="blas")
-        except Exception:   # pragma: no cover - threadpoolctl is optional
-            limiter = None
-        try:
+        with _blas_single_thread():
             return self._run()
-        finally:
-            if limiter is not None:
-                limiter.restore_original_limits()
 
     def _run(self) -> SolveResult:
         torch, cfg = self.torch, self.cfg
@@ -627,17 +638,9 @@ class _NativeSolve(_DeviceSolve):
             keep.append(arr)
             bufs.snapshot_stride, bufs.snaps, bufs.n_snaps = cfg.snapshot_stride, ctypes.addressof(arr), nsn
         outc = _native.SolveOut(**{k: v.ctypes.data for k, v in out_arrays.items()})
-        try:
-            from threadpoolctl import threadpool_limits
-            limiter = threadpool_limits(limits=1, user_api="blas")
-        except Exception:   # pragma: no cover
-            limiter = None
-        try:
+        with _blas_single_thread():
             _native.check(self.lib.ctk_solve(dg.handle, ctypes.byref(cfgc), ctypes.byref(bufs),
                                              ctypes.byref(outc)), "ctk_solve")
-        finally:
-            if limiter is not None:
-                limiter.restore_original_limits()
         self.caller.wait_stream(sa)
         self.caller.wait_stream(sb)
         nrec = outc.n_records

@@ -136,7 +136,9 @@ int ctk_combine(const float* W, int64_t ld, int k, const double* y, const float*
  * ctk_cgs2_step in its last 4 entries, copied asynchronously to h_host
  * (pinned) when non-NULL.  The intermediate goes to tmp, or is kept when
  * aux rows are given: BA: aux1[j] = A w_j; AB: aux1[j] = B w_j and
- * aux2[j] = A B w_j (before orthogonalisation). */
+ * aux2[j] = A B w_j (before orthogonalisation).  Steps of one Arnoldi cycle
+ * must be issued in order j = 0, 1, ... on the same stage_work: step j > 0
+ * reuses the K1 staged copies that step j-1 (BA) or its own K2 (AB) wrote. */
 int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* W, int64_t ld, int j,
                      float* q,
                      float* tmp, float* aux1, int64_t ld1, float* aux2, int64_t ld2,

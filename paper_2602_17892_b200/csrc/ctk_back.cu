@@ -42,8 +42,17 @@ struct BackArgs {
     float* x;             // final image (S > 1)
     unsigned* cnt;        // S > 1: per-tile arrival tickets (zeroed once)
     int nx, ny, D, a0, a1, per_split, wmax, split, fbits;
+    float* stP;           // optional: also write the K1 staged copies of the result
+    float* stPT;
+    int pad;
     double h, xmin, ymax, center;
 };
+
+// K1's zero-padded copies of the output pixel (ix, iy) (see ctk_forward.cu).
+__device__ __forceinline__ void stage_out(const BackArgs& A, int ix, int iy, float v) {
+    A.stP[(size_t)iy * (A.nx + 2 * A.pad) + ix + A.pad] = v;
+    A.stPT[(size_t)ix * (A.ny + 2 * A.pad) + iy + A.pad] = v;
+}
 
 __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
     extern __shared__ float2 win[];                // [BCA][wmax] (p, d)
@@ -149,7 +158,9 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
                 const size_t o = (size_t)iy * A.nx + ix;
                 double t = 0.0;
                 for (unsigned z = 0; z < gridDim.z; ++z) t += (double)__ldcg(part + z * n + o);
-                A.x[o] = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * t);
+                const float v = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * t);
+                A.x[o] = v;
+                if (A.stP) stage_out(A, ix, iy, v);
             }
         }
         if (tid == 0) *ticket = 0u;
@@ -157,11 +168,15 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
         if (ix >= A.nx) return;
         if (iyA < A.ny) {
             const size_t o = (size_t)iyA * A.nx + ix;
-            A.out[o] = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * accA);
+            const float v = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * accA);
+            A.out[o] = v;
+            if (A.stP) stage_out(A, ix, iyA, v);
         }
         if (iyB < A.ny) {
             const size_t o = (size_t)iyB * A.nx + ix;
-            A.out[o] = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * accB);
+            const float v = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * accB);
+            A.out[o] = v;
+            if (A.stP) stage_out(A, ix, iyB, v);
         }
     }
 }
@@ -192,6 +207,14 @@ extern "C" int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1) {
 
 extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, int a1,
                         const float* x0, float* work, void* stream) {
+    return ctk_back_ex(g, u, x, a0, a1, x0, work, nullptr, stream);
+}
+
+// stage != NULL: also write K1's zero-padded P / PT copies of x into the
+// forward workspace `stage` (interior only: its zero padding is written by
+// any plain ctk_forward on that workspace).
+int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
+                float* work, float* stage, void* stream) {
     if (!g) return ctk_fail(CTK_ERR_ARG, "null geometry");
     if (a0 < 0 || a1 > g->n_angles || a0 > a1)
         return ctk_fail(CTK_ERR_SHAPE, "angle range [%d, %d) outside [0, %d)", a0, a1, g->n_angles);
@@ -221,6 +244,9 @@ extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, i
     A.a1 = a1;
     A.per_split = (a1 - a0 + S - 1) / S;
     A.wmax = g->back_wmax;
+    A.pad = g->fwd_pad;
+    A.stP = stage;
+    A.stPT = stage ? stage + (size_t)g->ny * (g->nx + 2 * g->fwd_pad) : nullptr;
     {   // fixed-point fraction bits: window coordinates [0, wmax] need I bits
         int I = 1;
         while ((1 << I) <= g->back_wmax + 1) ++I;

@@ -97,6 +97,25 @@ int ctk_check_cuda(cudaError_t e, const char* what);
 
 static inline cudaStream_t ctk_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Destination of a fused K1 staging write (P / PT of an image vector).
+struct ctk_stage_dst {
+    float* P;
+    float* PT;
+    int nx, ny, pad;
+};
+
+// Internal variants used by the Arnoldi step (not part of the C ABI):
+// GS step that also stages its new row for the next forward (SMEM path only),
+// whether that path is taken for (L, k), forward over already-staged copies,
+// back that also stages its output image.
+int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
+                   double* stat, void* scratch, void* stream, const ctk_stage_dst* sd);
+bool ctk_gs_smem_ok(int64_t L, int k);
+int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1, const float* b,
+                   float* work, bool prestaged, void* stream);
+int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
+                float* work, float* stage, void* stream);
+
 // K1 workspace: zero-padded copies P, PT
 // and one arrival ticket per (angle, 128-bin block) -- zero-filled once.
 static inline int64_t ctk_stage_floats(const ctk_geom* g) {

@@ -574,6 +574,14 @@ static int check_range(const ctk_geom* g, int a0, int a1) {
 
 extern "C" int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0, int a1,
                            const float* b, float* work, void* stream) {
+    return ctk_forward_ex(g, x, y, a0, a1, b, work, false, stream);
+}
+
+// prestaged: work already holds the zero-padded P / PT of x (written by the
+// producer of x: K2's epilogue or the SMEM Gram-Schmidt step), so the K1
+// staging launch is skipped.  x itself is still read by degenerate angles.
+int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1, const float* b,
+                   float* work, bool prestaged, void* stream) {
     int rc = check_range(g, a0, a1);
     if (rc) return rc;
     if (!x || !y) return ctk_fail(CTK_ERR_ARG, "null vector");
@@ -585,8 +593,10 @@ extern "C" int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0
     float* PT = work + (size_t)g->ny * (g->nx + 2 * g->fwd_pad);
     dim3 sg((g->nx + 31) / 32, (g->ny + 31) / 32), sb(32, 8);
     const int ph = ctk_prof_open(0, st);
-    k_stage<<<sg, sb, 0, st>>>(x, P, PT, g->nx, g->ny, g->fwd_pad);
-    CTK_LAUNCH_CHECK("k_stage");
+    if (!prestaged) {
+        k_stage<<<sg, sb, 0, st>>>(x, P, PT, g->nx, g->ny, g->fwd_pad);
+        CTK_LAUNCH_CHECK("k_stage");
+    }
     FwdArgs A = make_args(g, x, y, a0, a1, b);
     A.P = P;
     A.PT = PT;

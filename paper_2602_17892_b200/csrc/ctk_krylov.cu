@@ -638,7 +638,7 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
 __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, int64_t L,
                                                    const float* __restrict__ q, int passes,
                                                    int64_t chunk, double* h, double* stat,
-                                                   double* partial) {
+                                                   double* partial, ctk_stage_dst sd) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nb = k + 1;
@@ -713,7 +713,19 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     const bool broke = hk <= 1e-14 * qn;                     // BREAKDOWN_RTOL, arnoldi.py:17,80
     const float sc = (float)(broke ? 0.0 : 1.0 / hk);
     float* wnext = W + (size_t)(k + 1) * ld + start;
-    for (int i = threadIdx.x; i < cn; i += ST) wnext[i] = qv[i] * sc;
+    if (sd.P) {     // also stage w_{k+1} for the next K1 apply (zero-padded P and PT)
+        const int pP = sd.nx + 2 * sd.pad, pT = sd.ny + 2 * sd.pad;
+        for (int i = threadIdx.x; i < cn; i += ST) {
+            const float v = qv[i] * sc;
+            wnext[i] = v;
+            const int e = (int)(start + i);
+            const int iy = e / sd.nx, ix = e - iy * sd.nx;
+            sd.P[(size_t)iy * pP + ix + sd.pad] = v;
+            sd.PT[(size_t)ix * pT + iy + sd.pad] = v;
+        }
+    } else {
+        for (int i = threadIdx.x; i < cn; i += ST) wnext[i] = qv[i] * sc;
+    }
     if (blockIdx.x == 0) {
         for (int i = threadIdx.x; i <= k; i += ST) h[i] = passes == 2 ? h1[i] + h2[i] : h1[i];
         if (threadIdx.x == 0) {
@@ -782,12 +794,12 @@ static size_t gs_smem_bytes(int k, int64_t chunk) {
     return head + sizeof(float) * (size_t)chunk * (nb + 1) + sizeof(double) * 4 * ST + 32;
 }
 
-static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
-                       double* stat, Scratch s, cudaStream_t st, bool* done) {
-    *done = false;
-    static int coop = -1, sms = 0;
+static bool gs_smem_plan(int64_t L, int k, int64_t* Gp, int64_t* chunkp, size_t* smemp) {
+    static int coop = -1, sms = 0, gcap = 0;
     if (coop < 0) {
         const char* off = getenv("CTK_NO_SMEM_GS");
+        const char* e = getenv("CTK_GS_CTAS");             // tuning override
+        gcap = e ? atoi(e) : 0;
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
@@ -798,30 +810,46 @@ static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int pas
         cudaGetLastError();
         if (off && off[0] == '1') coop = 0;
     }
-    if (coop != 1 || L < 4) return CTK_OK;
+    if (coop != 1 || L < 4 || k < 0) return false;
     // chunk: a multiple of 4 floats (16-B bulk-copy alignment), >= 64 floats
-    static int gcap = -1;
-    if (gcap < 0) {
-        const char* e = getenv("CTK_GS_CTAS");             // tuning override
-        gcap = e ? atoi(e) : 0;
-    }
     int64_t G = gcap > 0 && gcap < sms ? gcap : sms;
     int64_t chunk = ((L + G - 1) / G + 3) & ~3LL;
     if (chunk < 64) chunk = 64;
     G = (L + chunk - 1) / chunk;
-    if (G > GS_MAXG) return CTK_OK;
+    if (G > GS_MAXG) return false;
     const size_t smem = gs_smem_bytes(k, chunk);
-    if (smem > SMEM_LIMIT) return CTK_OK;
-    // partials: (nb + 1) + nb + 1 rows of G doubles
-    if ((size_t)(2 * k + 4) * G > (size_t)MAXCH * s.nvec_cap) return CTK_OK;
+    if (smem > SMEM_LIMIT) return false;
+    // partials: (nb + 1) + nb + 1 rows of G doubles within carve(scratch, k + 3)
+    if ((size_t)(2 * k + 4) * G > (size_t)MAXCH * (size_t)(k + 3)) return false;
+    *Gp = G;
+    *chunkp = chunk;
+    *smemp = smem;
+    return true;
+}
+
+static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
+                       double* stat, Scratch s, cudaStream_t st, const ctk_stage_dst* sdp,
+                       bool* done) {
+    *done = false;
+    int64_t G, chunk;
+    size_t smem;
+    if (!gs_smem_plan(L, k, &G, &chunk, &smem)) return CTK_OK;
     double* partial = s.partial;
-    void* args[] = {&W, &ld, &k, &L, &q, &passes, &chunk, &h, &stat, &partial};
+    ctk_stage_dst sd = {};
+    if (sdp && sdp->P && (int64_t)sdp->nx * sdp->ny == L) sd = *sdp;
+    void* args[] = {&W, &ld, &k, &L, &q, &passes, &chunk, &h, &stat, &partial, &sd};
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_gs_smem, dim3((unsigned)G),
                                                 dim3(ST), args, smem, st);
     ctk_count_launch();
     if (e != cudaSuccess) return ctk_check_cuda(e, "k_gs_smem");
     *done = true;
     return CTK_OK;
+}
+
+bool ctk_gs_smem_ok(int64_t L, int k) {
+    int64_t G, chunk;
+    size_t smem;
+    return gs_smem_plan(L, k, &G, &chunk, &smem);
 }
 
 static int check_vec(const void* p, const char* what) {
@@ -925,6 +953,11 @@ extern "C" int ctk_cgs2_step(float* W, int64_t ld, int k, int64_t L, float* q, d
 
 extern "C" int ctk_gs_step(float* W, int64_t ld, int k, int64_t L, float* q, int passes,
                            double* h, double* stat, void* scratch, void* stream) {
+    return ctk_gs_step_ex(W, ld, k, L, q, passes, h, stat, scratch, stream, nullptr);
+}
+
+int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
+                   double* stat, void* scratch, void* stream, const ctk_stage_dst* sd) {
     int rc;
     if ((rc = check_vec(W, "W")) || (rc = check_vec(q, "q"))) return rc;
     if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
@@ -935,7 +968,7 @@ extern "C" int ctk_gs_step(float* W, int64_t ld, int k, int64_t L, float* q, int
     Scratch s = carve(scratch, k + 3);
     if (passes != 1 && passes != 2) return ctk_fail(CTK_ERR_ARG, "passes must be 1 or 2");
     bool fused = false;
-    if ((rc = try_gs_smem(W, ld, k, L, q, passes, h, stat, s, st, &fused))) return rc;
+    if ((rc = try_gs_smem(W, ld, k, L, q, passes, h, stat, s, st, sd, &fused))) return rc;
     if (fused) return CTK_OK;
     if (passes == 2 && (rc = try_cgs2_fused(W, ld, k, L, q, h, stat, s, st, &fused))) return rc;
     if (fused) return CTK_OK;

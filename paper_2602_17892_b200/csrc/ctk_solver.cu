@@ -99,19 +99,35 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
     const float* w = W + (size_t)j * ld;
     cudaStream_t st = ctk_stream(stream);
     int rc;
+    // K1 staging is fused into the producer of the forward's input where it
+    // can be: AB stages B w_j in K2's epilogue; BA stages w_{j+1} in the SMEM
+    // Gram-Schmidt step of step j (so step j+1 skips it).  Step 0 always runs
+    // the staging kernel, which also writes the zero padding.
+    const float* pre_w = nullptr;                          // GS input when q is not copied
+    ctk_stage_dst sd = {stage_work, stage_work + (size_t)g->ny * (g->nx + 2 * g->fwd_pad),
+                        g->nx, g->ny, g->fwd_pad};
+    const bool gs_smem = ctk_gs_smem_ok(L, j);
     if (ab) {   // q = A (B w); keep B w_j (aux1) and A B w_j (aux2) for the iterates
         float* bw = aux1 ? aux1 + (size_t)j * ld1 : tmp;
         float* abw = aux2 ? aux2 + (size_t)j * ld2 : q;
-        if ((rc = ctk_back(g, w, bw, 0, na, nullptr, back_work, stream))) return rc;
-        if ((rc = ctk_forward(g, bw, abw, 0, na, nullptr, stage_work, stream))) return rc;
-        if (aux2) CTK_CUDA(cudaMemcpyAsync(q, abw, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+        const bool fuse = j > 0;
+        if ((rc = ctk_back_ex(g, w, bw, 0, na, nullptr, back_work, fuse ? stage_work : nullptr,
+                              stream)))
+            return rc;
+        if ((rc = ctk_forward_ex(g, bw, abw, 0, na, nullptr, stage_work, fuse, stream))) return rc;
+        // the SMEM Gram-Schmidt path leaves its input untouched: no copy of A B w_j
+        if (aux2 && !gs_smem)
+            CTK_CUDA(cudaMemcpyAsync(q, abw, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+        if (aux2 && gs_smem) pre_w = abw;
     } else {    // q = B (A w); keep A w_j (aux1)
         float* aw = aux1 ? aux1 + (size_t)j * ld1 : tmp;
-        if ((rc = ctk_forward(g, w, aw, 0, na, nullptr, stage_work, stream))) return rc;
+        const bool pre = j > 0 && ctk_gs_smem_ok(L, j - 1);
+        if ((rc = ctk_forward_ex(g, w, aw, 0, na, nullptr, stage_work, pre, stream))) return rc;
         if ((rc = ctk_back(g, aw, q, 0, na, nullptr, back_work, stream))) return rc;
     }
     const int ph = ctk_prof_open(2, st);
-    rc = ctk_gs_step(W, ld, j, L, q, passes, h_dev, h_dev + hcols - 4, scratch, stream);
+    rc = ctk_gs_step_ex(W, ld, j, L, pre_w ? const_cast<float*>(pre_w) : q, passes, h_dev,
+                        h_dev + hcols - 4, scratch, stream, ab ? nullptr : &sd);
     ctk_prof_close(ph, st);
     if (rc) return rc;
     if (h_host)

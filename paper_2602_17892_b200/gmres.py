@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 import time
 from dataclasses import dataclass, field, replace
 
@@ -176,6 +177,25 @@ def _pool():
     return _POOL
 
 
+_PINNED: dict = {}
+
+
+def _pinned(torch, name, shape, dtype, zero=True):
+    """Page-locked host buffer reused across solves (per thread, name, shape,
+    dtype).  A fresh pin_memory() per solve goes through torch's caching host
+    allocator, which falls back to cudaHostAlloc (milliseconds) whenever the
+    previous solve's block is still fenced by an event.  Solves are
+    synchronous, so a buffer is free again when its solve returns."""
+    key = (threading.get_ident(), name, tuple(shape), dtype)
+    t = _PINNED.get(key)
+    if t is None:
+        t = torch.empty(shape, dtype=dtype).pin_memory()
+        _PINNED[key] = t
+    if zero:
+        t.zero_()
+    return t
+
+
 def _side_stream(torch, dev, kind, priority):
     """Cached solver streams: the Arnoldi stream at the highest priority (it is
     the critical path), the iterate stream at the lowest."""
@@ -269,7 +289,10 @@ class _DeviceSolve:
                 bh = np.asarray(b, dtype=np.float64)
                 if bh.shape != (self.m,):
                     raise OperatorShapeError(f"data vector has shape {bh.shape}, expected ({self.m},)")
-                self.b = torch.from_numpy(bh.astype(np.float32)).pin_memory().to(dev, non_blocking=True)
+                bp = _pinned(torch, "b", (self.m,), torch.float32, zero=False)
+                bp.numpy()[:] = bh                          # fp64 -> fp32 into page-locked memory
+                self.b = torch.empty(self.m, dtype=f32, device=dev)
+                self.b.copy_(bp, non_blocking=True)
                 self.h2d += 4 * self.m
             self.basis = DeviceBasis(L, rows, dev, torch)
             x0 = cfg.x0
@@ -286,9 +309,9 @@ class _DeviceSolve:
             self.tmp = torch.empty(self.n if self.ab else self.m, dtype=f32, device=dev)
             self.hcols = rows + 1 + 4                      # h[0..rows] + 4 stats
             self.hs = torch.zeros((rows, self.hcols), dtype=f64, device=dev)
-            self.h_host = torch.zeros((rows, self.hcols), dtype=f64).pin_memory()
+            self.h_host = _pinned(torch, "h", (rows, self.hcols), f64)
             self.scal = torch.zeros(4, dtype=f64, device=dev)
-            self.scal_host = torch.zeros(4, dtype=f64).pin_memory()
+            self.scal_host = _pinned(torch, "scal", (4,), f64)
             # stream sb (iterate) buffers
             self.xk = torch.empty(self.n, dtype=f32, device=dev)
             self.z = torch.empty(self.m, dtype=f32, device=dev) if self.ab else None
@@ -304,7 +327,7 @@ class _DeviceSolve:
             self.d0 = torch.zeros(ldm, dtype=f32, device=dev)
             self.r = torch.empty(self.m, dtype=f32, device=dev)
             self.y_dev = torch.zeros((self.K, rows), dtype=f64, device=dev)
-            self.y_pin = torch.zeros((self.K, rows), dtype=f64).pin_memory()
+            self.y_pin = _pinned(torch, "y", (self.K, rows), f64)
             self.norms = torch.zeros((self.K + 1, 2), dtype=f64, device=dev)   # res^2, sol^2
         self.ev_h = [None] * rows
         # the side stream must not touch buffers before their zero-fill lands
@@ -580,12 +603,11 @@ class _NativeSolve(_DeviceSolve):
         dg, K = self.dg, self.K
         rows = self.basis.rows
         n1 = K + 1
-        pin = dict(dtype=torch.float64)
         out_arrays = {
             "k": np.zeros(n1, dtype=np.int32), "warn": np.zeros(n1, dtype=np.int32),
             "lambda_": np.zeros(n1), "residual": np.zeros(n1), "data_residual": np.zeros(n1),
             "proj_residual": np.zeros(n1), "solution_norm": np.zeros(n1), "elapsed": np.zeros(n1)}
-        norms_host = torch.zeros((K + 1) * 2, **pin).pin_memory()
+        norms_host = _pinned(torch, "norms", ((K + 1) * 2,), torch.float64)
         cfgc = _native.SolveCfg(
             ab=int(self.ab), hybrid=int(self.hybrid),
             strategy=_native.STRATEGY_CODES.get(cfg.lambda_strategy, 0),
@@ -619,7 +641,7 @@ class _NativeSolve(_DeviceSolve):
         if self.x_true is not None:
             xt = torch.from_numpy(self.x_true.astype(np.float32)).to(dg.dev)
             met = torch.zeros((K + 1) * 2, dtype=torch.float64, device=dg.dev)
-            met_h = torch.zeros((K + 1) * 2, dtype=torch.float64).pin_memory()
+            met_h = _pinned(torch, "metrics", ((K + 1) * 2,), torch.float64)
             scr = torch.zeros(int(self.lib.ctk_metrics_scratch_bytes()) // 8 + 1,
                               dtype=torch.float64, device=dg.dev)
             keep += [xt, met, met_h, scr]

@@ -140,6 +140,8 @@ def make_solver_cases():
         "ab_restart": dict(method="ab-hybrid", lambda_strategy="gcv", max_iter=14, restart_period=5),
         "ab_dp": dict(method="ab", max_iter=40, stopping_rule="dp", noise_norm=prob.noise_norm),
         "ba_rns": dict(method="ba", max_iter=40, stopping_rule="rns", rns_epsilon=1e-3),
+        "ba_ncp": dict(method="ba", max_iter=40, stopping_rule="ncp", ncp_threshold=0.2),
+        "ab_ncp": dict(method="ab", max_iter=40, stopping_rule="ncp", ncp_threshold=0.12),
     }
     for name, kw in cases.items():
         res = run_gmres(prob.forward, prob.back, prob.b_noisy, SolverConfig(**kw))

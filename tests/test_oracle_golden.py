@@ -101,6 +101,8 @@ CASES = {
     "ab_restart": dict(method="ab-hybrid", strategy="gcv", max_iter=14, restart_period=5),
     "ab_dp": dict(method="ab", max_iter=40, stopping_rule="dp"),
     "ba_rns": dict(method="ba", max_iter=40, stopping_rule="rns", rns_epsilon=1e-3),
+    "ba_ncp": dict(method="ba", max_iter=40, stopping_rule="ncp", ncp_threshold=0.2),
+    "ab_ncp": dict(method="ab", max_iter=40, stopping_rule="ncp", ncp_threshold=0.12),
 }
 
 

@@ -111,6 +111,10 @@ struct ctk_stage_dst {
 int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
                    double* stat, void* scratch, void* stream, const ctk_stage_dst* sd);
 bool ctk_gs_smem_ok(int64_t L, int k);
+int ctk_combine_pair(const float* X, int64_t ldx, const float* x0, float* x, int64_t Lx,
+                     double* n_x, const float* AX, int64_t ldax, const float* d0, float* r,
+                     int64_t Lr, double* n_r, int k, const double* y, void* scratch,
+                     void* stream);
 int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1, const float* b,
                    float* work, bool prestaged, void* stream);
 int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,

@@ -70,12 +70,13 @@ __device__ __forceinline__ double dot4(float4 a, float4 b, double acc) {
 // Last CTA of the grid sums partial[c * nv + j] over chunks c in a fixed
 // order (lane-strided, then a fixed shuffle tree) and writes out[j].
 __device__ void last_cta_reduce(const double* partial, int nchunks, int nv, unsigned int* ticket,
-                                double* out) {
+                                double* out, unsigned arrivals = 0) {
     __threadfence();
     __shared__ unsigned int s_last;
     __syncthreads();
+    if (arrivals == 0) arrivals = gridDim.x * gridDim.y;
     if (threadIdx.x == 0)
-        s_last = (atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1);
+        s_last = (atomicAdd(ticket, 1u) == arrivals - 1);
     __syncthreads();
     if (!s_last) return;
     __threadfence();
@@ -153,21 +154,40 @@ __global__ void __launch_bounds__(KT) k_dots(const float* __restrict__ W, int64_
 // SMEM and are added in warp order (deterministic).
 constexpr int CW = CT / 32;                 // row groups (warps) per CTA
 
-__global__ void __launch_bounds__(CT) k_combine(const float* __restrict__ W, int64_t ld, int nvec,
-                                                const double* __restrict__ coef, double sgn,
-                                                const float* base, float* dst, int64_t L,
-                                                double* norm_out, double* partial,
-                                                unsigned int* ticket) {
+struct CombineJob {
+    const float* W;
+    int64_t ld;
+    double sgn;
+    const float* base;
+    float* dst;
+    int64_t L;
+    double* norm_out;
+    double* partial;
+    unsigned int* ticket;
+    int G;                  // CTAs of this job
+};
+
+// One or two combinations sharing the coefficients (ctk_iterate's x_k and
+// residual): CTAs [0, j0.G) run job 0, the rest job 1.
+__global__ void __launch_bounds__(CT) k_combine(CombineJob j0, CombineJob j1, int nvec,
+                                                const double* __restrict__ coef) {
     extern __shared__ double c[];                                 // [nvec]
     __shared__ double4 red[CW][32];
     __shared__ double nred[CW];
-    for (int j = threadIdx.x; j < nvec; j += CT) c[j] = sgn * coef[j];
+    const bool second = (int)blockIdx.x >= j0.G;
+    const CombineJob& J = second ? j1 : j0;
+    const int bid = second ? (int)blockIdx.x - j0.G : (int)blockIdx.x;
+    const float* __restrict__ W = J.W;
+    const int64_t ld = J.ld, L = J.L;
+    const float* base = J.base;
+    float* dst = J.dst;
+    for (int j = threadIdx.x; j < nvec; j += CT) c[j] = J.sgn * coef[j];
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t L4 = L >> 2;
     const int64_t ntiles = (L4 + 31) >> 5;
     double nrm = 0.0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int64_t t = bid; t < ntiles; t += J.G) {
         const int64_t i = (t << 5) + lane;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         if (i < L4) {
@@ -213,7 +233,7 @@ __global__ void __launch_bounds__(CT) k_combine(const float* __restrict__ W, int
         }
         __syncthreads();
     }
-    if (blockIdx.x == gridDim.x - 1 && warp == 0) {               // scalar tail L % 4
+    if (bid == J.G - 1 && warp == 0) {                            // scalar tail L % 4
         for (int64_t i = (L4 << 2) + lane; i < L; i += 32) {
             double a = base ? (double)base[i] : 0.0;
             for (int j = 0; j < nvec; ++j) a = fma(c[j], (double)W[(size_t)j * ld + i], a);
@@ -222,7 +242,7 @@ __global__ void __launch_bounds__(CT) k_combine(const float* __restrict__ W, int
             nrm = fma((double)o, (double)o, nrm);
         }
     }
-    if (!norm_out) return;
+    if (!J.norm_out) return;
     const double s = warp_sum(nrm);
     if (lane == 0) nred[warp] = s;
     __syncthreads();
@@ -230,9 +250,9 @@ __global__ void __launch_bounds__(CT) k_combine(const float* __restrict__ W, int
         double t = 0.0;
 #pragma unroll
         for (int w = 0; w < CW; ++w) t += nred[w];
-        partial[blockIdx.x] = t;
+        J.partial[bid] = t;
     }
-    last_cta_reduce(partial, gridDim.x, 1, ticket, norm_out);
+    last_cta_reduce(J.partial, J.G, 1, J.ticket, J.norm_out, (unsigned)J.G);
 }
 
 __global__ void k_scale(const float* __restrict__ v, float* __restrict__ dst, int64_t L,
@@ -878,17 +898,39 @@ static int launch_dots(const float* W, int64_t ld, int nvec, const float* v, int
     return CTK_OK;
 }
 
+static int combine_ctas(int64_t L) {
+    int64_t G = ((L >> 2) + 31) / 32;                 // 32-float4 column tiles
+    if (G > MAXCH / 2) G = MAXCH / 2;
+    return G < 1 ? 1 : (int)G;
+}
+
 static int launch_combine(const float* W, int64_t ld, int nvec, const double* coef, double sgn,
                           const float* base, float* dst, int64_t L, double* norm_out, Scratch s,
                           cudaStream_t st) {
     if (nvec > KMAX_VEC) return ctk_fail(CTK_ERR_ARG, "too many vectors (%d)", nvec);
-    const int64_t L4 = L >> 2;
-    int64_t G = (L4 + 31) / 32;                       // 32-float4 column tiles
-    if (G > MAXCH) G = MAXCH;
-    if (G < 1) G = 1;
+    CombineJob j0 = {W, ld, sgn, base, dst, L, norm_out, s.partial, s.ticket, combine_ctas(L)};
+    CombineJob j1 = j0;
+    j1.G = 0;
     const size_t smem = sizeof(double) * (size_t)(nvec > 0 ? nvec : 1);
-    k_combine<<<(unsigned)G, CT, smem, st>>>(W, ld, nvec, coef, sgn, base, dst, L, norm_out,
-                                              s.partial, s.ticket);
+    k_combine<<<(unsigned)j0.G, CT, smem, st>>>(j0, j1, nvec, coef);
+    CTK_LAUNCH_CHECK("k_combine");
+    return CTK_OK;
+}
+
+// x = x0 + sum y_j X_j (norm -> n_x) and r = d0 - sum y_j AX_j (norm -> n_r)
+// in one launch (ctk_iterate's linear path).
+int ctk_combine_pair(const float* X, int64_t ldx, const float* x0, float* x, int64_t Lx,
+                     double* n_x, const float* AX, int64_t ldax, const float* d0, float* r,
+                     int64_t Lr, double* n_r, int k, const double* y, void* scratch,
+                     void* stream) {
+    if (k > KMAX_VEC) return ctk_fail(CTK_ERR_ARG, "too many vectors (%d)", k);
+    if ((ldx & 3) || (ldax & 3)) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
+    Scratch s = carve(scratch, k + 3);
+    CombineJob j0 = {X, ldx, 1.0, x0, x, Lx, n_x, s.partial, s.ticket, combine_ctas(Lx)};
+    CombineJob j1 = {AX, ldax, -1.0, d0, r, Lr, n_r, s.partial + j0.G, s.ticket + 1,
+                     combine_ctas(Lr)};
+    const size_t smem = sizeof(double) * (size_t)(k > 0 ? k : 1);
+    k_combine<<<(unsigned)(j0.G + j1.G), CT, smem, ctk_stream(stream)>>>(j0, j1, k, y);
     CTK_LAUNCH_CHECK("k_combine");
     return CTK_OK;
 }

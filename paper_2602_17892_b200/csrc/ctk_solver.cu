@@ -158,8 +158,8 @@ extern "C" int ctk_iterate(const ctk_geom_t* g, int ab, const float* W, int64_t 
         const int64_t ldx = ab ? ld1 : ld;
         const float* AXr = ab ? aux2 : aux1;
         const int64_t ldax = ab ? ld2 : ld1;
-        if ((rc = ctk_combine(Xr, ldx, k, y_dev, x0, xk, n, norms_dev + 1, scratch, stream))) return rc;
-        rc = ctk_update(AXr, ldax, k, y_dev, d0, r, m, norms_dev, scratch, stream);
+        rc = ctk_combine_pair(Xr, ldx, x0, xk, n, norms_dev + 1, AXr, ldax, d0, r, m, norms_dev, k,
+                              y_dev, scratch, stream);
         ctk_prof_close(ph, st);
         return rc;
     }

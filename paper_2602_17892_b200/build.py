@@ -49,7 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *ARCH, *FLAGS, "-shared", "-o", tmp, *sources(), "-lcudart"]
+    extra = os.environ.get("CTK_NVCC_EXTRA", "").split()     # tuning experiments only
+    cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-shared", "-o", tmp, *sources(), "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -668,10 +668,10 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     const int cn = rem <= 0 ? 0 : (int)(rem < chunk ? rem : chunk);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     double* h1 = reinterpret_cast<double*>(smem_raw + 16);          // [nb + 1]
-    double* h2 = h1 + (nb + 1);                                     // [nb]
-    double* red = h2 + nb;                                          // [SW]
+    double* h2 = h1 + (nb + 1);                                     // [nb + 1]: h2, ||q1||^2
+    double* red = h2 + nb + 1;                                      // [SW]
     float* qv = reinterpret_cast<float*>(
-        smem_raw + ((16 + sizeof(double) * (2 * nb + 1 + SW) + 15) & ~(size_t)15));
+        smem_raw + ((16 + sizeof(double) * (2 * nb + 2 + SW) + 15) & ~(size_t)15));
     float* Ws = qv + cpad;                                          // [nb][cpad]
     double4* acc = reinterpret_cast<double4*>(                      // [ST], 32-B aligned
         (reinterpret_cast<uintptr_t>(Ws + (size_t)nb * cpad) + 31) & ~(uintptr_t)31);
@@ -700,33 +700,46 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     __syncthreads();
 
     double* P1 = partial;                                    // [nb + 1][G]
-    double* P2 = P1 + (size_t)(nb + 1) * gridDim.x;          // [nb][G]
-    double* P3 = P2 + (size_t)nb * gridDim.x;                // [G]
+    double* P2 = P1 + (size_t)(nb + 1) * gridDim.x;          // [nb + 1][G]
+    double* P3 = P2 + (size_t)(nb + 1) * gridDim.x;          // [G]
     smem_dots(Ws, cpad, nb + 1, nb, qv, cn, P1);             // h1 = W^T q, ||q||^2
     grid.sync();
     all_reduce_rows(P1, nb + 1, h1);
     __syncthreads();
     double nrm = smem_update(Ws, cpad, nb, h1, qv, cn, acc);      // q1 = q - W h1
+    __shared__ double s_n2;
+    bool need_norm = true;
     if (passes == 2) {
         __syncthreads();
-        smem_dots(Ws, cpad, nb, -1, qv, cn, P2);             // h2 = W^T q1
+        smem_dots(Ws, cpad, nb + 1, nb, qv, cn, P2);         // h2 = W^T q1, ||q1||^2
         grid.sync();
-        all_reduce_rows(P2, nb, h2);
+        all_reduce_rows(P2, nb + 1, h2);
         __syncthreads();
         nrm = smem_update(Ws, cpad, nb, h2, qv, cn, acc);         // q2 = q1 - W h2
-    }
-    nrm = warp_sum(nrm);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
-    __syncthreads();
-    if (threadIdx.x == 0) {
+        // ||q2||^2 = ||q1||^2 - ||h2||^2 for orthonormal W: after the first pass
+        // h2 is at rounding level, so there is no cancellation and the third
+        // grid-wide reduction is skipped.  Every CTA holds the same h2, so the
+        // (never expected) fallback branch below is grid-uniform.
         double t = 0.0;
-#pragma unroll
-        for (int w = 0; w < SW; ++w) t += red[w];
-        P3[blockIdx.x] = t;
+        for (int j = 0; j < nb; ++j) t = fma(h2[j], h2[j], t);
+        if (h2[nb] > 0.0 && t <= 0.25 * h2[nb]) {
+            if (threadIdx.x == 0) s_n2 = h2[nb] - t;
+            need_norm = false;
+        }
     }
-    grid.sync();
-    __shared__ double s_n2;
-    if (threadIdx.x < 32) all_reduce_rows(P3, 1, &s_n2);
+    if (need_norm) {
+        nrm = warp_sum(nrm);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < SW; ++w) t += red[w];
+            P3[blockIdx.x] = t;
+        }
+        grid.sync();
+        if (threadIdx.x < 32) all_reduce_rows(P3, 1, &s_n2);
+    }
     __syncthreads();
     const double hk = sqrt(s_n2);
     const double qn = sqrt(h1[nb]);
@@ -810,7 +823,7 @@ static int try_cgs2_fused(float* W, int64_t ld, int k, int64_t L, float* q, doub
 // memory with one CTA per SM.
 static size_t gs_smem_bytes(int k, int64_t chunk) {
     const int nb = k + 1;
-    const size_t head = (16 + sizeof(double) * (2 * (size_t)nb + 1 + SW) + 15) & ~(size_t)15;
+    const size_t head = (16 + sizeof(double) * (2 * (size_t)nb + 2 + SW) + 15) & ~(size_t)15;
     return head + sizeof(float) * (size_t)chunk * (nb + 1) + sizeof(double) * 4 * ST + 32;
 }
 
@@ -839,8 +852,8 @@ static bool gs_smem_plan(int64_t L, int k, int64_t* Gp, int64_t* chunkp, size_t*
     if (G > GS_MAXG) return false;
     const size_t smem = gs_smem_bytes(k, chunk);
     if (smem > SMEM_LIMIT) return false;
-    // partials: (nb + 1) + nb + 1 rows of G doubles within carve(scratch, k + 3)
-    if ((size_t)(2 * k + 4) * G > (size_t)MAXCH * (size_t)(k + 3)) return false;
+    // partials: (nb + 1) + (nb + 1) + 1 rows of G doubles within carve(scratch, k + 3)
+    if ((size_t)(2 * k + 5) * G > (size_t)MAXCH * (size_t)(k + 3)) return false;
     *Gp = G;
     *chunkp = chunk;
     *smemp = smem;

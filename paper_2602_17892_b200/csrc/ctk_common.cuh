@@ -109,7 +109,8 @@ struct ctk_stage_dst {
 // whether that path is taken for (L, k), forward over already-staged copies,
 // back that also stages its output image.
 int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
-                   double* stat, void* scratch, void* stream, const ctk_stage_dst* sd);
+                   double* stat, void* scratch, void* stream, const ctk_stage_dst* sd,
+                   double* h_mirror);
 bool ctk_gs_smem_ok(int64_t L, int k);
 int ctk_combine_pair(const float* X, int64_t ldx, const float* x0, float* x, int64_t Lx,
                      double* n_x, const float* AX, int64_t ldax, const float* d0, float* r,

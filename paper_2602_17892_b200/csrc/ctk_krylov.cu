@@ -658,7 +658,8 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
 __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, int64_t L,
                                                    const float* __restrict__ q, int passes,
                                                    int64_t chunk, double* h, double* stat,
-                                                   double* partial, ctk_stage_dst sd) {
+                                                   double* partial, ctk_stage_dst sd,
+                                                   double* hm, int stat_off) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nb = k + 1;
@@ -760,13 +761,21 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
         for (int i = threadIdx.x; i < cn; i += ST) wnext[i] = qv[i] * sc;
     }
     if (blockIdx.x == 0) {
-        for (int i = threadIdx.x; i <= k; i += ST) h[i] = passes == 2 ? h1[i] + h2[i] : h1[i];
+        // hm: optional host-mapped (page-locked) mirror of the column, written
+        // here instead of a D2H copy on the Arnoldi stream.
+        for (int i = threadIdx.x; i <= k; i += ST) {
+            const double v = passes == 2 ? h1[i] + h2[i] : h1[i];
+            h[i] = v;
+            if (hm) hm[i] = v;
+        }
         if (threadIdx.x == 0) {
+            const double st4[4] = {qn, broke ? 1.0 : 0.0, broke ? 0.0 : 1.0 / hk, hk};
             h[k + 1] = hk;
-            stat[0] = qn;
-            stat[1] = broke ? 1.0 : 0.0;
-            stat[2] = broke ? 0.0 : 1.0 / hk;
-            stat[3] = hk;
+            for (int q = 0; q < 4; ++q) stat[q] = st4[q];
+            if (hm) {
+                hm[k + 1] = hk;
+                for (int q = 0; q < 4; ++q) hm[stat_off + q] = st4[q];
+            }
         }
     }
 }
@@ -862,7 +871,7 @@ static bool gs_smem_plan(int64_t L, int k, int64_t* Gp, int64_t* chunkp, size_t*
 
 static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
                        double* stat, Scratch s, cudaStream_t st, const ctk_stage_dst* sdp,
-                       bool* done) {
+                       double* hm, bool* done) {
     *done = false;
     int64_t G, chunk;
     size_t smem;
@@ -870,7 +879,8 @@ static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int pas
     double* partial = s.partial;
     ctk_stage_dst sd = {};
     if (sdp && sdp->P && (int64_t)sdp->nx * sdp->ny == L) sd = *sdp;
-    void* args[] = {&W, &ld, &k, &L, &q, &passes, &chunk, &h, &stat, &partial, &sd};
+    int stat_off = (int)(stat - h);
+    void* args[] = {&W, &ld, &k, &L, &q, &passes, &chunk, &h, &stat, &partial, &sd, &hm, &stat_off};
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_gs_smem, dim3((unsigned)G),
                                                 dim3(ST), args, smem, st);
     ctk_count_launch();
@@ -1008,11 +1018,12 @@ extern "C" int ctk_cgs2_step(float* W, int64_t ld, int k, int64_t L, float* q, d
 
 extern "C" int ctk_gs_step(float* W, int64_t ld, int k, int64_t L, float* q, int passes,
                            double* h, double* stat, void* scratch, void* stream) {
-    return ctk_gs_step_ex(W, ld, k, L, q, passes, h, stat, scratch, stream, nullptr);
+    return ctk_gs_step_ex(W, ld, k, L, q, passes, h, stat, scratch, stream, nullptr, nullptr);
 }
 
 int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
-                   double* stat, void* scratch, void* stream, const ctk_stage_dst* sd) {
+                   double* stat, void* scratch, void* stream, const ctk_stage_dst* sd,
+                   double* h_mirror) {
     int rc;
     if ((rc = check_vec(W, "W")) || (rc = check_vec(q, "q"))) return rc;
     if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
@@ -1023,7 +1034,7 @@ int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes,
     Scratch s = carve(scratch, k + 3);
     if (passes != 1 && passes != 2) return ctk_fail(CTK_ERR_ARG, "passes must be 1 or 2");
     bool fused = false;
-    if ((rc = try_gs_smem(W, ld, k, L, q, passes, h, stat, s, st, sd, &fused))) return rc;
+    if ((rc = try_gs_smem(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, &fused))) return rc;
     if (fused) return CTK_OK;
     if (passes == 2 && (rc = try_cgs2_fused(W, ld, k, L, q, h, stat, s, st, &fused))) return rc;
     if (fused) return CTK_OK;

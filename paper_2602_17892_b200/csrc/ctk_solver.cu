@@ -125,12 +125,19 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
         if ((rc = ctk_forward_ex(g, w, aw, 0, na, nullptr, stage_work, pre, stream))) return rc;
         if ((rc = ctk_back(g, aw, q, 0, na, nullptr, back_work, stream))) return rc;
     }
+    // The SMEM Gram-Schmidt step writes the column straight into the
+    // page-locked host row (mapped, UVA) -- no D2H copy on the critical stream.
+    double* hm = nullptr;
+    if (h_host && gs_smem && cudaHostGetDevicePointer((void**)&hm, h_host, 0) != cudaSuccess) {
+        cudaGetLastError();
+        hm = nullptr;
+    }
     const int ph = ctk_prof_open(2, st);
     rc = ctk_gs_step_ex(W, ld, j, L, pre_w ? const_cast<float*>(pre_w) : q, passes, h_dev,
-                        h_dev + hcols - 4, scratch, stream, ab ? nullptr : &sd);
+                        h_dev + hcols - 4, scratch, stream, ab ? nullptr : &sd, hm);
     ctk_prof_close(ph, st);
     if (rc) return rc;
-    if (h_host)
+    if (h_host && !hm)
         CTK_CUDA(cudaMemcpyAsync(h_host, h_dev, sizeof(double) * hcols, cudaMemcpyDeviceToHost, st));
     return CTK_OK;
 }

@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 #include <math.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "ctk_common.cuh"
 
@@ -169,8 +170,15 @@ struct CombineJob {
 
 // One or two combinations sharing the coefficients (ctk_iterate's x_k and
 // residual): CTAs [0, j0.G) run job 0, the rest job 1.
+constexpr int COEF_BYVAL = 160;          // y passed in the kernel parameters up to this k
+
+struct CoefPack {
+    double c[COEF_BYVAL];
+};
+
 __global__ void __launch_bounds__(CT) k_combine(CombineJob j0, CombineJob j1, int nvec,
-                                                const double* __restrict__ coef) {
+                                                const double* __restrict__ coef,
+                                                const __grid_constant__ CoefPack cp) {
     extern __shared__ double c[];                                 // [nvec]
     __shared__ double4 red[CW][32];
     __shared__ double nred[CW];
@@ -181,7 +189,7 @@ __global__ void __launch_bounds__(CT) k_combine(CombineJob j0, CombineJob j1, in
     const int64_t ld = J.ld, L = J.L;
     const float* base = J.base;
     float* dst = J.dst;
-    for (int j = threadIdx.x; j < nvec; j += CT) c[j] = J.sgn * coef[j];
+    for (int j = threadIdx.x; j < nvec; j += CT) c[j] = J.sgn * (coef ? coef[j] : cp.c[j]);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t L4 = L >> 2;
@@ -935,7 +943,8 @@ static int launch_combine(const float* W, int64_t ld, int nvec, const double* co
     CombineJob j1 = j0;
     j1.G = 0;
     const size_t smem = sizeof(double) * (size_t)(nvec > 0 ? nvec : 1);
-    k_combine<<<(unsigned)j0.G, CT, smem, st>>>(j0, j1, nvec, coef);
+    CoefPack cp;
+    k_combine<<<(unsigned)j0.G, CT, smem, st>>>(j0, j1, nvec, coef, cp);
     CTK_LAUNCH_CHECK("k_combine");
     return CTK_OK;
 }
@@ -945,7 +954,7 @@ static int launch_combine(const float* W, int64_t ld, int nvec, const double* co
 int ctk_combine_pair(const float* X, int64_t ldx, const float* x0, float* x, int64_t Lx,
                      double* n_x, const float* AX, int64_t ldax, const float* d0, float* r,
                      int64_t Lr, double* n_r, int k, const double* y, void* scratch,
-                     void* stream) {
+                     void* stream, const double* y_host) {
     if (k > KMAX_VEC) return ctk_fail(CTK_ERR_ARG, "too many vectors (%d)", k);
     if ((ldx & 3) || (ldax & 3)) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
     Scratch s = carve(scratch, k + 3);
@@ -953,7 +962,11 @@ int ctk_combine_pair(const float* X, int64_t ldx, const float* x0, float* x, int
     CombineJob j1 = {AX, ldax, -1.0, d0, r, Lr, n_r, s.partial + j0.G, s.ticket + 1,
                      combine_ctas(Lr)};
     const size_t smem = sizeof(double) * (size_t)(k > 0 ? k : 1);
-    k_combine<<<(unsigned)(j0.G + j1.G), CT, smem, ctk_stream(stream)>>>(j0, j1, k, y);
+    CoefPack cp;
+    const bool byval = y_host && k <= COEF_BYVAL;     // no H2D copy of y on the stream
+    if (byval) memcpy(cp.c, y_host, sizeof(double) * (size_t)k);
+    k_combine<<<(unsigned)(j0.G + j1.G), CT, smem, ctk_stream(stream)>>>(j0, j1, k,
+                                                                         byval ? nullptr : y, cp);
     CTK_LAUNCH_CHECK("k_combine");
     return CTK_OK;
 }

@@ -152,10 +152,11 @@ extern "C" int ctk_iterate(const ctk_geom_t* g, int ab, const float* W, int64_t 
     const int na = g->n_angles;
     const int64_t n = (int64_t)g->nx * g->ny, m = (int64_t)na * g->det_count;
     cudaStream_t st = ctk_stream(stream);
-    if (y_host && k > 0)
-        CTK_CUDA(cudaMemcpyAsync(y_dev, y_host, sizeof(double) * k, cudaMemcpyHostToDevice, st));
     int rc;
     const bool linear = aux1 && d0 && (!ab || aux2);
+    // the linear path takes y in the kernel parameters (no H2D copy) when k is small
+    if (y_host && k > 0 && !(linear && k <= 160))
+        CTK_CUDA(cudaMemcpyAsync(y_dev, y_host, sizeof(double) * k, cudaMemcpyHostToDevice, st));
     const int ph = ctk_prof_open(3, st);
     if (linear) {
         // By linearity: x_k = x0 + sum y_j X_j with X_j = w_j (BA) or B w_j (AB),
@@ -166,7 +167,7 @@ extern "C" int ctk_iterate(const ctk_geom_t* g, int ab, const float* W, int64_t 
         const float* AXr = ab ? aux2 : aux1;
         const int64_t ldax = ab ? ld2 : ld1;
         rc = ctk_combine_pair(Xr, ldx, x0, xk, n, norms_dev + 1, AXr, ldax, d0, r, m, norms_dev, k,
-                              y_dev, scratch, stream);
+                              y_dev, scratch, stream, y_host);
         ctk_prof_close(ph, st);
         return rc;
     }

@@ -107,15 +107,47 @@ Pool& pool() {
 
 __global__ void k_set_inv(double* dst, double v) { *dst = v; }
 
+// Events are recycled across solves (a solve creates ~2K+ of them; create +
+// destroy costs ~1-2 us each on the host).  Every event handed out has
+// completed when its solve returns (the solve ends with stream syncs).
+struct EventPool {
+    std::mutex mu;
+    std::vector<cudaEvent_t> free_ev[2];      // [timing]
+    int device = -1;
+};
+
+EventPool& event_pool() {
+    static EventPool* p = new EventPool();    // never destroyed (CUDA may be gone at exit)
+    return *p;
+}
+
 struct Events {
-    std::vector<cudaEvent_t> ev;
+    std::vector<cudaEvent_t> ev[2];
     ~Events() {
-        for (auto e : ev) cudaEventDestroy(e);
+        EventPool& p = event_pool();
+        std::lock_guard<std::mutex> lk(p.mu);
+        for (int t = 0; t < 2; ++t)
+            p.free_ev[t].insert(p.free_ev[t].end(), ev[t].begin(), ev[t].end());
     }
     cudaEvent_t make(bool timing) {
-        cudaEvent_t e;
-        cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
-        ev.push_back(e);
+        const int t = timing ? 1 : 0;
+        cudaEvent_t e = nullptr;
+        {
+            EventPool& p = event_pool();
+            std::lock_guard<std::mutex> lk(p.mu);
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (p.device != dev) {                // pool is per device: drop on switch
+                for (int q = 0; q < 2; ++q) p.free_ev[q].clear();
+                p.device = dev;
+            }
+            if (!p.free_ev[t].empty()) {
+                e = p.free_ev[t].back();
+                p.free_ev[t].pop_back();
+            }
+        }
+        if (!e) cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
+        ev[t].push_back(e);
         return e;
     }
 };

@@ -26,6 +26,7 @@
 // is folded into an fp64 accumulator.  Small images split the angle range
 // over blockIdx.z into partial images reduced in a fixed order.
 #include <math.h>
+#include <stdlib.h>
 
 #include "ctk_common.cuh"
 
@@ -183,9 +184,13 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
 
 static int back_splits(const ctk_geom* g, int a0, int a1) {
     const int tiles = ((g->nx + BTX - 1) / BTX) * ((g->ny + BTY - 1) / BTY);
-    const int target = 148 * 4;
+    static int target = -1;
+    if (target < 0) {
+        const char* e = getenv("CTK_BACK_TARGET");       // tuning override (CTAs)
+        target = e && atoi(e) > 0 ? atoi(e) : 148 * 12;   // ~1.5 waves of 256-thread CTAs
+    }
     int S = (target + tiles - 1) / tiles;
-    const int max_s = (a1 - a0 + BCA - 1) / BCA;
+    const int max_s = (a1 - a0 + BCA - 1) / BCA;      // >= one 32-angle chunk per CTA
     if (S > max_s) S = max_s;
     if (S < 1) S = 1;
     return S;

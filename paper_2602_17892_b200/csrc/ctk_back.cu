@@ -32,7 +32,7 @@
 
 namespace ctk {
 
-constexpr int BTX = 32, BTY = 16, BROWS = 8, BCA = 32;
+constexpr int BTX = 32, BROWS = 8, BCA = 32;      // tile: BTX x (BROWS * PPT) pixels
 constexpr int BTHREADS = BTX * BROWS;
 
 struct BackArgs {
@@ -55,14 +55,16 @@ __device__ __forceinline__ void stage_out(const BackArgs& A, int ix, int iy, flo
     A.stPT[(size_t)ix * (A.ny + 2 * A.pad) + iy + A.pad] = v;
 }
 
+template <int PPT>                                 // pixels (rows) per thread
 __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
+    constexpr int BTY = BROWS * PPT;
     extern __shared__ float2 win[];                // [BCA][wmax] (p, d)
     __shared__ int4 s_par[BCA];                    // T0, C, S, smem base of the window
     __shared__ int s_w0[BCA];
 
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BTX + tx;
     const int ix0 = blockIdx.x * BTX, iy0 = blockIdx.y * BTY;
-    const int ix = ix0 + tx, iyA = iy0 + ty, iyB = iy0 + ty + BROWS;
+    const int ix = ix0 + tx;
     // tile corner pixel centres
     const double Xlo = A.xmin + ((double)ix0 + 0.5) * A.h;
     const double Xhi = A.xmin + ((double)(ix0 + BTX - 1) + 0.5) * A.h;
@@ -76,7 +78,9 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
     const int D = A.D, wmax = A.wmax;
     const int q1 = D > 1 ? 1 : 0;                  // reference quirk tap for i0 == -1
 
-    double accA = 0.0, accB = 0.0;
+    double acc[PPT];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) acc[r] = 0.0;
     for (int ac = aS; ac < aE; ac += BCA) {
         const int na = min(BCA, aE - ac);
         if (tid < na) {
@@ -111,29 +115,26 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
             }
         }
         __syncthreads();
-        float sA = 0.f, sB = 0.f;
+        float sp[PPT];
+#pragma unroll
+        for (int r = 0; r < PPT; ++r) sp[r] = 0.f;
 #pragma unroll 4
         for (int ai = 0; ai < na; ++ai) {
             const int4 P = s_par[ai];
-            const unsigned TA = (unsigned)P.x + (unsigned)tx * (unsigned)P.y + (unsigned)ty * (unsigned)P.z;
-            const unsigned TB = TA + (unsigned)BROWS * (unsigned)P.z;
-            {
-                const float f1 = __uint_as_float(0x3f800000u | ((TA << I) >> 9));   // 1 + w
+            const unsigned T0 = (unsigned)P.x + (unsigned)tx * (unsigned)P.y + (unsigned)ty * (unsigned)P.z;
+            const unsigned dT = (unsigned)BROWS * (unsigned)P.z;
+#pragma unroll
+            for (int r = 0; r < PPT; ++r) {
+                const unsigned T = T0 + (unsigned)r * dT;
+                const float f1 = __uint_as_float(0x3f800000u | ((T << I) >> 9));   // 1 + w
                 float2 pd;
                 asm("ld.shared.v2.f32 {%0, %1}, [%2];"
-                    : "=f"(pd.x), "=f"(pd.y) : "r"((TA >> F) * 8u + (unsigned)P.w));
-                sA += fmaf(f1, pd.y, pd.x);
-            }
-            {
-                const float f1 = __uint_as_float(0x3f800000u | ((TB << I) >> 9));
-                float2 pd;
-                asm("ld.shared.v2.f32 {%0, %1}, [%2];"
-                    : "=f"(pd.x), "=f"(pd.y) : "r"((TB >> F) * 8u + (unsigned)P.w));
-                sB += fmaf(f1, pd.y, pd.x);
+                    : "=f"(pd.x), "=f"(pd.y) : "r"((T >> F) * 8u + (unsigned)P.w));
+                sp[r] += fmaf(f1, pd.y, pd.x);
             }
         }
-        accA += (double)sA;
-        accB += (double)sB;
+#pragma unroll
+        for (int r = 0; r < PPT; ++r) acc[r] += (double)sp[r];
         __syncthreads();
     }
     const size_t n = (size_t)A.nx * A.ny;
@@ -142,8 +143,11 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
         // partial images in split order (deterministic) and adds x0.
         float* part = A.out;
         const bool inx = ix < A.nx;
-        if (inx && iyA < A.ny) part[(size_t)blockIdx.z * n + (size_t)iyA * A.nx + ix] = (float)accA;
-        if (inx && iyB < A.ny) part[(size_t)blockIdx.z * n + (size_t)iyB * A.nx + ix] = (float)accB;
+#pragma unroll
+        for (int r = 0; r < PPT; ++r) {
+            const int iy = iy0 + ty + r * BROWS;
+            if (inx && iy < A.ny) part[(size_t)blockIdx.z * n + (size_t)iy * A.nx + ix] = (float)acc[r];
+        }
         __threadfence();
         __syncthreads();
         __shared__ unsigned s_last;
@@ -153,8 +157,8 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
         if (!s_last) return;
         __threadfence();
         if (inx) {
-            for (int r = 0; r < 2; ++r) {
-                const int iy = r ? iyB : iyA;
+            for (int r = 0; r < PPT; ++r) {
+                const int iy = iy0 + ty + r * BROWS;
                 if (iy >= A.ny) continue;
                 const size_t o = (size_t)iy * A.nx + ix;
                 double t = 0.0;
@@ -167,23 +171,25 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
         if (tid == 0) *ticket = 0u;
     } else {
         if (ix >= A.nx) return;
-        if (iyA < A.ny) {
-            const size_t o = (size_t)iyA * A.nx + ix;
-            const float v = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * accA);
+#pragma unroll
+        for (int r = 0; r < PPT; ++r) {
+            const int iy = iy0 + ty + r * BROWS;
+            if (iy >= A.ny) continue;
+            const size_t o = (size_t)iy * A.nx + ix;
+            const float v = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * acc[r]);
             A.out[o] = v;
-            if (A.stP) stage_out(A, ix, iyA, v);
-        }
-        if (iyB < A.ny) {
-            const size_t o = (size_t)iyB * A.nx + ix;
-            const float v = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * accB);
-            A.out[o] = v;
-            if (A.stP) stage_out(A, ix, iyB, v);
+            if (A.stP) stage_out(A, ix, iy, v);
         }
     }
 }
 
+static int back_tiles_y(const ctk_geom* g) {
+    const int bty = BROWS * g->back_ppt;
+    return (g->ny + bty - 1) / bty;
+}
+
 static int back_splits(const ctk_geom* g, int a0, int a1) {
-    const int tiles = ((g->nx + BTX - 1) / BTX) * ((g->ny + BTY - 1) / BTY);
+    const int tiles = ((g->nx + BTX - 1) / BTX) * back_tiles_y(g);
     static int target = -1;
     if (target < 0) {
         const char* e = getenv("CTK_BACK_TARGET");       // tuning override (CTAs)
@@ -201,7 +207,7 @@ static int back_splits(const ctk_geom* g, int a0, int a1) {
 using namespace ctk;
 
 static int64_t back_tiles(const ctk_geom* g) {
-    return (int64_t)((g->nx + BTX - 1) / BTX) * ((g->ny + BTY - 1) / BTY);
+    return (int64_t)((g->nx + BTX - 1) / BTX) * back_tiles_y(g);
 }
 
 extern "C" int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1) {
@@ -262,13 +268,17 @@ int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
     A.xmin = g->xmin;
     A.ymax = g->ymax;
     A.center = g->center;
-    dim3 grid((g->nx + BTX - 1) / BTX, (g->ny + BTY - 1) / BTY, S), block(BTX, BROWS);
+    dim3 grid((g->nx + BTX - 1) / BTX, back_tiles_y(g), S), block(BTX, BROWS);
     const size_t smem = (size_t)BCA * g->back_wmax * sizeof(float2);
+    const bool p4 = g->back_ppt == 4;
     if (smem > 48 * 1024)
-        CTK_CUDA(cudaFuncSetAttribute(k_back, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+        CTK_CUDA(cudaFuncSetAttribute(p4 ? k_back<4> : k_back<2>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int ph = ctk_prof_open(1, st);
-    k_back<<<grid, block, smem, st>>>(A);
+    if (p4)
+        k_back<4><<<grid, block, smem, st>>>(A);
+    else
+        k_back<2><<<grid, block, smem, st>>>(A);
     CTK_LAUNCH_CHECK("k_back");
     ctk_prof_close(ph, st);
     return CTK_OK;

@@ -58,7 +58,7 @@ bool is_pow2(double v) {
     return frexp(fabs(v), &e) == 0.5;
 }
 
-constexpr int BTX = 32, BTY = 16, BCA = 32;   // must match ctk_back.cu
+constexpr int BTX = 32, BCA = 32;   // must match ctk_back.cu (tile height 8 * back_ppt)
 
 void free_geom(ctk_geom* g) {
     if (!g) return;
@@ -120,6 +120,14 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
     std::vector<ctk::AngleParams> ap(n_angles);
     std::vector<ctk::BackParams> bp(n_angles);
     double max_span = 0.0;
+    {   // K2 rows per thread: 4 (32x32 tiles, fewer per-angle setups) once the
+        // image has enough tiles to fill the GPU, else 2 (32x16)
+        int ppt = (int64_t)nx * ny >= 512LL * 512 ? 4 : 2;
+        const char* ov = getenv("CTK_BACK_PPT");          // tuning override (2 or 4)
+        if (ov && (atoi(ov) == 2 || atoi(ov) == 4)) ppt = atoi(ov);
+        g->back_ppt = ppt;
+    }
+    const int bty = 8 * g->back_ppt;
     const double h = pixel_size;
     for (int a = 0; a < n_angles; ++a) {
         const double c = cos_tab[a], s = sin_tab[a];
@@ -168,7 +176,7 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
         ap[a] = p;
         bp[a].cg = c / det_spacing;
         bp[a].sg = s / det_spacing;
-        const double span = ((BTX - 1) * fabs(c) + (BTY - 1) * fabs(s)) * h / det_spacing;
+        const double span = ((BTX - 1) * fabs(c) + (bty - 1) * fabs(s)) * h / det_spacing;
         if (span > max_span) max_span = span;
         g->n_degenerate += p.degenerate;
     }

@@ -75,6 +75,15 @@ int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0, int a1,
                 const float* b, float* work, void* stream);
 
 /* Literal fp64 Siddon for every angle (same output layout, no work buffer). */
+/* Exact adjoint of A (Siddon transpose; matched mode):
+ * x = (x0 ? x0 : 0) + A^T u over angles [a0, a1).  Replaces
+ * matched_back(forward) = CSR transpose, ctkrylov/ct.py:248-264.  `work` holds
+ * ctk_adjoint_work_floats(g, a0, a1) floats (zero-filled once; may be NULL when
+ * that is 0). */
+int ctk_adjoint(const ctk_geom_t* g, const float* u, float* x, int a0, int a1,
+                const float* x0, float* work, void* stream);
+int64_t ctk_adjoint_work_floats(const ctk_geom_t* g, int a0, int a1);
+
 int ctk_forward_exact(const ctk_geom_t* g, const float* x, float* y, int a0, int a1,
                       void* stream);
 

@@ -8,8 +8,8 @@ CUDA behind the C ABI in include/ctk.h); there is no CPU fallback.
 """
 
 from .linop import LinearOperator, OperatorShapeError, compose
-from .ct import (DeviceGeometry, GeometryError, GpuBack, GpuForward, ImageGrid,
-                 ParallelGeometry, back_pixel_driven, forward_ray_driven)
+from .ct import (DeviceGeometry, GeometryError, GpuAdjoint, GpuBack, GpuForward, ImageGrid,
+                 ParallelGeometry, back_pixel_driven, forward_ray_driven, matched_back)
 from .arnoldi import (Breakdown, DeviceBasis, ProjectedSolution, solve_projected_ls,
                       solve_projected_tikhonov)
 from .regparam import DegenerateCurveError, lambda_grid, select_lambda, svd_of_hessenberg

@@ -37,6 +37,8 @@ SIGNATURES = {
     "ctk_forward_exact": (_c.c_int, [_vp, _fp, _fp, _c.c_int, _c.c_int, _vp]),
     "ctk_count_segments": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp]),
     "ctk_back_work_floats": (_c.c_int64, [_vp, _c.c_int, _c.c_int]),
+    "ctk_adjoint": (_c.c_int, [_vp, _fp, _fp, _c.c_int, _c.c_int, _fp, _fp, _vp]),
+    "ctk_adjoint_work_floats": (_c.c_int64, [_vp, _c.c_int, _c.c_int]),
     "ctk_back": (_c.c_int, [_vp, _fp, _fp, _c.c_int, _c.c_int, _fp, _fp, _vp]),
     "ctk_reduce_scratch_bytes": (_c.c_size_t, [_c.c_int, _c.c_int64]),
     "ctk_dots": (_c.c_int, [_fp, _c.c_int64, _c.c_int, _fp, _c.c_int64, _c.c_int, _dp, _vp, _vp]),

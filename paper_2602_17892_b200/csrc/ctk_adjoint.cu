@@ -1,0 +1,350 @@
+// ctk_adjoint.cu -- K7: the exact adjoint A^T of the Siddon forward projector
+// (matched mode, LSQR/LSMR).  Reference: ctkrylov/ct.py:248-264
+// (`matched_back` = the transpose of the assembled Siddon CSR, ct.py:182-201).
+//
+// Pixel-driven gather: for pixel p and angle a, every ray j whose line
+// x cos + y sin = s_j crosses the pixel square contributes len(ray ∩ p) u[a, j].
+// Siddon's segment inside a (convex) pixel is exactly that chord, whose length
+// as a function of the signed distance d between the line and the pixel centre
+// is a trapezoid:
+//     len(d) = min(h / max(|c|,|s|), max(0, (P - |d|) / (|c| |s|))),
+//     P = (|c| + |s|) h / 2  (half-width of the pixel's shadow).
+// The reference drops segments <= 1e-15 (ct.py:178); the difference is below
+// fp32 resolution.  Angles the reference treats as axis-aligned (K1d: rays can
+// lie exactly on grid lines, and the midpoint/floor/clip rule decides which
+// column gets them) use the literal fp64 segment lists of K1d, transposed once
+// into per-pixel CSR lists (ray, length) on first use.
+//
+// B200 mapping mirrors K2: a CTA per 32 x 16 pixel tile, 2 pixels per thread;
+// per 32-angle chunk the detector window of the tile is staged into SMEM with
+// coalesced loads (zero outside [0, D)), then each pixel evaluates <= 4
+// candidate rays per angle in fp64 (g and d must resolve the short slope
+// region of near-axis angles, which is ~|sin| h wide).  Small images split
+// angles over blockIdx.z into partial images reduced in a fixed order.
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <mutex>
+#include <vector>
+
+#include "ctk_common.cuh"
+
+namespace ctk {
+
+constexpr int JTX = 32, JROWS = 8, JPPT = 2, JTY = JROWS * JPPT, JCA = 32;
+constexpr int JTHREADS = JTX * JROWS;
+
+struct AdjArgs {
+    const double* cs;        // [n_angles] bitwise np.cos
+    const double* sn;        // [n_angles] bitwise np.sin
+    const int* deg_slot;     // [n_angles] -> degenerate slot or -1
+    const float* u;          // row a at u + (a - a0) * D
+    const float* x0;         // optional
+    float* out;              // final image (split == 0) or partials [S][n]
+    float* x;                // final image (split)
+    unsigned* cnt;           // split: per-tile tickets (zeroed once)
+    const long long* dt_ptr; // [n_deg][n + 1] transposed degenerate lists
+    const int* dt_ray;
+    const float* dt_len;
+    const int* deg_angle;    // slot -> angle
+    int n_deg;
+    int nx, ny, D, a0, a1, per_split, wmax, split;
+    double h, sp, xmin, ymax, center;
+};
+
+__global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
+    extern __shared__ float win[];                 // [JCA][wmax]
+    __shared__ double s_cg[JCA], s_sg[JCA], s_P[JCA], s_Lm[JCA], s_ics[JCA];
+    __shared__ int s_w0[JCA], s_skip[JCA];
+
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * JTX + tx;
+    const int ix0 = blockIdx.x * JTX, iy0 = blockIdx.y * JTY;
+    const int ix = ix0 + tx;
+    const double X = A.xmin + ((double)ix + 0.5) * A.h;
+    double Y[JPPT];
+#pragma unroll
+    for (int r = 0; r < JPPT; ++r) Y[r] = A.ymax - ((double)(iy0 + ty + r * JROWS) + 0.5) * A.h;
+    const double Xlo = A.xmin + ((double)ix0 + 0.5) * A.h;
+    const double Xhi = A.xmin + ((double)(ix0 + JTX - 1) + 0.5) * A.h;
+    const double Yhi = A.ymax - ((double)iy0 + 0.5) * A.h;
+    const double Ylo = A.ymax - ((double)(iy0 + JTY - 1) + 0.5) * A.h;
+
+    const int aS = A.a0 + blockIdx.z * A.per_split;
+    const int aE = min(A.a1, aS + A.per_split);
+    const int D = A.D, wmax = A.wmax;
+    const double sp = A.sp;
+
+    double acc[JPPT];
+#pragma unroll
+    for (int r = 0; r < JPPT; ++r) acc[r] = 0.0;
+    for (int ac = aS; ac < aE; ac += JCA) {
+        const int na = min(JCA, aE - ac);
+        if (tid < na) {
+            const int a = ac + tid;
+            const double c = A.cs[a], s = A.sn[a];
+            const double cg = c / sp, sg = s / sp;
+            const double ac_ = fabs(c), as_ = fabs(s);
+            s_cg[tid] = cg;
+            s_sg[tid] = sg;
+            s_P[tid] = 0.5 * (ac_ + as_) * A.h;
+            s_Lm[tid] = A.h / fmax(ac_, as_);
+            s_ics[tid] = ac_ * as_ > 0.0 ? 1.0 / (ac_ * as_) : 0.0;
+            s_skip[tid] = A.deg_slot[a] >= 0;
+            const double g00 = fma(Xlo, cg, fma(Ylo, sg, A.center));
+            const double g01 = fma(Xlo, cg, fma(Yhi, sg, A.center));
+            const double g10 = fma(Xhi, cg, fma(Ylo, sg, A.center));
+            const double g11 = fma(Xhi, cg, fma(Yhi, sg, A.center));
+            s_w0[tid] = (int)floor(fmin(fmin(g00, g01), fmin(g10, g11))) - 2;
+        }
+        __syncthreads();
+        for (int ai = ty; ai < na; ai += JROWS) {
+            const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
+            const int w0 = s_w0[ai];
+            float* dst = win + ai * wmax;
+            for (int i = tx; i < wmax; i += JTX) {
+                const int b = w0 + i;
+                dst[i] = (b >= 0 && b < D) ? __ldg(row + b) : 0.f;
+            }
+        }
+        __syncthreads();
+        for (int ai = 0; ai < na; ++ai) {
+            if (s_skip[ai]) continue;                  // K1d angles: transposed lists below
+            const double cg = s_cg[ai], sg = s_sg[ai], P = s_P[ai], Lm = s_Lm[ai], ics = s_ics[ai];
+            const float* wrow = win + ai * wmax - s_w0[ai];
+#pragma unroll
+            for (int r = 0; r < JPPT; ++r) {
+                const double g = fma(X, cg, fma(Y[r], sg, A.center));   // ray index at the centre
+                const int j0 = (int)floor(g);
+#pragma unroll
+                for (int q = -1; q <= 2; ++q) {
+                    const int j = j0 + q;
+                    const double a = P - fabs((double)j - g) * sp;
+                    if (a > 0.0) acc[r] = fma(fmin(Lm, a * ics), (double)wrow[j], acc[r]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // degenerate angles of this split range: per-pixel transposed lists
+    const size_t n = (size_t)A.nx * A.ny;
+    for (int sl = 0; sl < A.n_deg; ++sl) {
+        const int a = A.deg_angle[sl];
+        if (a < aS || a >= aE) continue;
+        const float* urow = A.u + (size_t)(a - A.a0) * D;
+#pragma unroll
+        for (int r = 0; r < JPPT; ++r) {
+            const int iy = iy0 + ty + r * JROWS;
+            if (ix >= A.nx || iy >= A.ny) continue;
+            const size_t p = (size_t)iy * A.nx + ix;
+            const long long* pp = A.dt_ptr + (size_t)sl * (n + 1);
+            for (long long e = pp[p]; e < pp[p + 1]; ++e)
+                acc[r] = fma((double)A.dt_len[e], (double)__ldg(urow + A.dt_ray[e]), acc[r]);
+        }
+    }
+    if (A.split) {
+        float* part = A.out;
+        const bool inx = ix < A.nx;
+#pragma unroll
+        for (int r = 0; r < JPPT; ++r) {
+            const int iy = iy0 + ty + r * JROWS;
+            if (inx && iy < A.ny) part[(size_t)blockIdx.z * n + (size_t)iy * A.nx + ix] = (float)acc[r];
+        }
+        __threadfence();
+        __syncthreads();
+        __shared__ unsigned s_last;
+        unsigned* ticket = A.cnt + (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+        if (tid == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.z - 1);
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        if (inx) {
+            for (int r = 0; r < JPPT; ++r) {
+                const int iy = iy0 + ty + r * JROWS;
+                if (iy >= A.ny) continue;
+                const size_t o = (size_t)iy * A.nx + ix;
+                double t = 0.0;
+                for (unsigned z = 0; z < gridDim.z; ++z) t += (double)__ldcg(part + z * n + o);
+                A.x[o] = (float)((A.x0 ? (double)A.x0[o] : 0.0) + t);
+            }
+        }
+        if (tid == 0) *ticket = 0u;
+    } else {
+        if (ix >= A.nx) return;
+#pragma unroll
+        for (int r = 0; r < JPPT; ++r) {
+            const int iy = iy0 + ty + r * JROWS;
+            if (iy >= A.ny) continue;
+            const size_t o = (size_t)iy * A.nx + ix;
+            A.out[o] = (float)((A.x0 ? (double)A.x0[o] : 0.0) + acc[r]);
+        }
+    }
+}
+
+int adj_splits(const ctk_geom* g, int a0, int a1) {
+    const int tiles = ((g->nx + JTX - 1) / JTX) * ((g->ny + JTY - 1) / JTY);
+    int S = (148 * 8 + tiles - 1) / tiles;
+    const int max_s = (a1 - a0 + JCA - 1) / JCA;
+    if (S > max_s) S = max_s;
+    return S < 1 ? 1 : S;
+}
+
+// Transposed K1d lists (pixel -> (ray, length)), built on the host once per
+// geometry in ray order (deterministic summation order).
+struct DegT {
+    long long* ptr = nullptr;
+    int* ray = nullptr;
+    float* len = nullptr;
+    int* angle = nullptr;
+    int n_deg = 0;
+};
+
+std::mutex g_degt_mu;
+
+int degt_get(ctk_geom* g, DegT* out) {
+    std::lock_guard<std::mutex> lk(g_degt_mu);
+    if (g->d_degt_ptr || g->n_degenerate == 0) {
+        out->ptr = g->d_degt_ptr;
+        out->ray = g->d_degt_ray;
+        out->len = g->d_degt_len;
+        out->angle = g->d_degt_angle;
+        out->n_deg = g->d_degt_ptr ? g->n_degenerate : 0;
+        return CTK_OK;
+    }
+    const int D = g->det_count, nd = g->n_degenerate;
+    const size_t n = (size_t)g->nx * g->ny;
+    std::vector<int> slot(g->n_angles);
+    CTK_CUDA(cudaMemcpy(slot.data(), g->d_deg_slot, sizeof(int) * g->n_angles,
+                        cudaMemcpyDeviceToHost));
+    std::vector<int> angle(nd, -1);
+    for (int a = 0; a < g->n_angles; ++a)
+        if (slot[a] >= 0 && slot[a] < nd) angle[slot[a]] = a;
+    const size_t rays = (size_t)nd * D;
+    const size_t entries = (size_t)nd * g->deg_maxseg * D;
+    std::vector<long long> cnt(rays);
+    std::vector<int> pix(entries);
+    std::vector<float> len(entries);
+    CTK_CUDA(cudaMemcpy(cnt.data(), g->d_deg_ptr, sizeof(long long) * rays, cudaMemcpyDeviceToHost));
+    CTK_CUDA(cudaMemcpy(pix.data(), g->d_deg_pix, sizeof(int) * entries, cudaMemcpyDeviceToHost));
+    CTK_CUDA(cudaMemcpy(len.data(), g->d_deg_len, sizeof(float) * entries, cudaMemcpyDeviceToHost));
+    std::vector<long long> ptr((size_t)nd * (n + 1), 0);
+    for (int sl = 0; sl < nd; ++sl) {
+        long long* P = ptr.data() + (size_t)sl * (n + 1);
+        for (int j = 0; j < D; ++j)
+            for (long long e = 0; e < cnt[(size_t)sl * D + j]; ++e)
+                ++P[(size_t)pix[((size_t)sl * g->deg_maxseg + e) * D + j] + 1];
+        for (size_t p = 0; p < n; ++p) P[p + 1] += P[p];
+    }
+    // global offsets: slot sl's entries follow slot sl-1's
+    long long base = 0;
+    for (int sl = 0; sl < nd; ++sl) {
+        long long* P = ptr.data() + (size_t)sl * (n + 1);
+        const long long tot = P[n];
+        for (size_t p = 0; p <= n; ++p) P[p] += base;
+        base += tot;
+    }
+    std::vector<int> tray(base > 0 ? base : 1);
+    std::vector<float> tlen(base > 0 ? base : 1);
+    std::vector<long long> fill(ptr);
+    for (int sl = 0; sl < nd; ++sl) {
+        long long* F = fill.data() + (size_t)sl * (n + 1);
+        for (int j = 0; j < D; ++j)
+            for (long long e = 0; e < cnt[(size_t)sl * D + j]; ++e) {
+                const size_t idx = ((size_t)sl * g->deg_maxseg + e) * D + j;
+                const long long at = F[pix[idx]]++;
+                tray[at] = j;
+                tlen[at] = len[idx];
+            }
+    }
+    cudaError_t e = cudaMalloc(&g->d_degt_ptr, sizeof(long long) * ptr.size());
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_degt_ray, sizeof(int) * tray.size());
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_degt_len, sizeof(float) * tlen.size());
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_degt_angle, sizeof(int) * nd);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_degt_ptr, ptr.data(), sizeof(long long) * ptr.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_degt_ray, tray.data(), sizeof(int) * tray.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_degt_len, tlen.data(), sizeof(float) * tlen.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_degt_angle, angle.data(), sizeof(int) * nd, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return ctk_check_cuda(e, "transposed degenerate lists");
+    out->ptr = g->d_degt_ptr;
+    out->ray = g->d_degt_ray;
+    out->len = g->d_degt_len;
+    out->angle = g->d_degt_angle;
+    out->n_deg = nd;
+    return CTK_OK;
+}
+
+}  // namespace ctk
+
+using namespace ctk;
+
+extern "C" int64_t ctk_adjoint_work_floats(const ctk_geom_t* g, int a0, int a1) {
+    if (!g || a0 < 0 || a1 > g->n_angles || a0 >= a1) return 0;
+    const int S = adj_splits(g, a0, a1);
+    const int64_t tiles = (int64_t)((g->nx + JTX - 1) / JTX) * ((g->ny + JTY - 1) / JTY);
+    return S > 1 ? (int64_t)S * g->nx * g->ny + tiles : 0;
+}
+
+extern "C" int ctk_adjoint(const ctk_geom_t* gc, const float* u, float* x, int a0, int a1,
+                           const float* x0, float* work, void* stream) {
+    ctk_geom* g = const_cast<ctk_geom*>(gc);
+    if (!g) return ctk_fail(CTK_ERR_ARG, "null geometry");
+    if (a0 < 0 || a1 > g->n_angles || a0 > a1)
+        return ctk_fail(CTK_ERR_SHAPE, "angle range [%d, %d) outside [0, %d)", a0, a1, g->n_angles);
+    if (!u || !x) return ctk_fail(CTK_ERR_ARG, "null vector");
+    CTK_CUDA(cudaSetDevice(g->device));
+    cudaStream_t st = ctk_stream(stream);
+    const size_t n = (size_t)g->nx * g->ny;
+    if (a1 == a0) {
+        if (x0) CTK_CUDA(cudaMemcpyAsync(x, x0, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        else CTK_CUDA(cudaMemsetAsync(x, 0, n * sizeof(float), st));
+        return CTK_OK;
+    }
+    DegT dt;
+    int rc = degt_get(g, &dt);
+    if (rc) return rc;
+    const int S = adj_splits(g, a0, a1);
+    if (S > 1 && !work)
+        return ctk_fail(CTK_ERR_ARG, "ctk_adjoint needs %lld work floats",
+                        (long long)ctk_adjoint_work_floats(g, a0, a1));
+    AdjArgs A;
+    A.cs = g->d_cos;
+    A.sn = g->d_sin;
+    A.deg_slot = g->d_deg_slot;
+    A.u = u;
+    A.x0 = x0;
+    A.out = S > 1 ? work : x;
+    A.x = x;
+    A.cnt = S > 1 ? reinterpret_cast<unsigned*>(work + (size_t)S * n) : nullptr;
+    A.dt_ptr = dt.ptr;
+    A.dt_ray = dt.ray;
+    A.dt_len = dt.len;
+    A.deg_angle = dt.angle;
+    A.n_deg = dt.n_deg;
+    A.nx = g->nx;
+    A.ny = g->ny;
+    A.D = g->det_count;
+    A.a0 = a0;
+    A.a1 = a1;
+    A.per_split = (a1 - a0 + S - 1) / S;
+    // window: the tile's detector footprint + 4 bins of margin (K2's bound for
+    // its tallest tile covers it; recomputed here for 32 x 16 tiles)
+    A.wmax = g->back_wmax + 2;
+    A.split = S > 1;
+    A.h = g->h;
+    A.sp = g->det_spacing;
+    A.xmin = g->xmin;
+    A.ymax = g->ymax;
+    A.center = g->center;
+    dim3 grid((g->nx + JTX - 1) / JTX, (g->ny + JTY - 1) / JTY, S), block(JTX, JROWS);
+    const size_t smem = (size_t)JCA * A.wmax * sizeof(float);
+    if (smem > 48 * 1024)
+        CTK_CUDA(cudaFuncSetAttribute(k_adjoint, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    k_adjoint<<<grid, block, smem, st>>>(A);
+    CTK_LAUNCH_CHECK("k_adjoint");
+    return CTK_OK;
+}

@@ -65,6 +65,12 @@ struct ctk_geom {
     float* d_deg_len;         // same layout: exact fp64 length rounded to fp32
     long long deg_segments;
     int deg_maxseg;
+    // K7 (exact adjoint): the lists above transposed to pixel -> (ray, length),
+    // built on first use (ctk_adjoint.cu)
+    long long* d_degt_ptr;    // [n_degenerate][n + 1]
+    int* d_degt_ray;
+    float* d_degt_len;
+    int* d_degt_angle;        // slot -> angle index
 };
 
 // Builds the degenerate-angle segment lists (ctk_forward.cu); called by

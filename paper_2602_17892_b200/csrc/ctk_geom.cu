@@ -71,6 +71,10 @@ void free_geom(ctk_geom* g) {
     cudaFree(g->d_deg_ptr);
     cudaFree(g->d_deg_pix);
     cudaFree(g->d_deg_len);
+    cudaFree(g->d_degt_ptr);
+    cudaFree(g->d_degt_ray);
+    cudaFree(g->d_degt_len);
+    cudaFree(g->d_degt_angle);
     delete g;
 }
 

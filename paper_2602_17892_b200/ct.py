@@ -231,6 +231,24 @@ class DeviceGeometry:
                       "ctk_back")
         return out
 
+    def adjoint(self, u, out=None, a0: int = 0, a1: int | None = None, x0=None, stream=None):
+        """out = (x0 or 0) + A^T u over angles [a0, a1): the exact transpose of
+        the Siddon matrix (K7), i.e. the reference's matched_back."""
+        a0, a1 = self._range(a0, a1)
+        self._check(u, (a1 - a0) * self.det_count, "u")
+        if out is None:
+            out = self.torch.empty(self.n, dtype=self.torch.float32, device=self.dev)
+        self._check(out, self.n, "out")
+        if x0 is not None:
+            self._check(x0, self.n, "x0")
+        stream = self._stream(stream)
+        wf = int(self._lib.ctk_adjoint_work_floats(self.handle, a0, a1))
+        work = self._workspace("adjoint", wf, stream) if wf > 0 else None
+        _native.check(self._lib.ctk_adjoint(self.handle, u.data_ptr(), out.data_ptr(), a0, a1,
+                                            _native.ptr(x0), _native.ptr(work), stream.cuda_stream),
+                      "ctk_adjoint")
+        return out
+
     def count_segments(self, a0: int = 0, a1: int | None = None) -> tuple[int, int]:
         """(kept segments, CSR nnz) of A over angles [a0, a1) (K6)."""
         a0, a1 = self._range(a0, a1)
@@ -274,6 +292,16 @@ class GpuBack(_GpuOperator):
         return self.dgeom.back(u, out=out, x0=x0, stream=stream)
 
 
+class GpuAdjoint(_GpuOperator):
+    """A^T: exact transpose of the Siddon forward projector on the GPU (what
+    ctkrylov.ct.matched_back returns for a CSR-backed forward, ct.py:248-264)."""
+
+    kind = "adjoint"
+
+    def apply_device(self, u, out=None, x0=None, stream=None):
+        return self.dgeom.adjoint(u, out=out, x0=x0, stream=stream)
+
+
 _GEOM_CACHE: dict = {}
 
 
@@ -299,3 +327,27 @@ def back_pixel_driven(grid: ImageGrid, geometry: ParallelGeometry, device: int =
     """Drop-in for ctkrylov.ct.back_pixel_driven (ct.py:204)."""
     dg = device_geometry(grid, geometry, device)
     return GpuBack(grid.n, geometry.m, dg)
+
+
+DENSE_ASSEMBLY_GUARD = 10**7             # ctkrylov/ct.py:30, desk-scale guard for dense assembly
+
+
+def matched_back(forward: LinearOperator) -> LinearOperator:
+    """Drop-in for ctkrylov.ct.matched_back (ct.py:248-264): the exact
+    transpose of the forward projector.  For the GPU forward this is K7 (no
+    matrix is ever assembled); other operators follow the reference: the
+    transpose of an assembled sparse matrix, else a dense transpose under the
+    desk-scale guard."""
+    if isinstance(forward, GpuForward):
+        return GpuAdjoint(forward.cols, forward.rows, forward.dgeom)
+    mat = getattr(forward, "sparse_matrix", None)
+    if mat is not None:
+        mat_t = mat.T.tocsr()
+        return LinearOperator(forward.cols, forward.rows, lambda v: mat_t @ v)
+    if forward.rows * forward.cols > DENSE_ASSEMBLY_GUARD:
+        raise GeometryError(
+            "matched mode requires assembling the forward matrix; "
+            f"{forward.rows}x{forward.cols} exceeds the desk-scale guard of "
+            f"{DENSE_ASSEMBLY_GUARD} entries")
+    dense_t = np.ascontiguousarray(forward.to_dense().T)
+    return LinearOperator(forward.cols, forward.rows, lambda v: dense_t @ v)

@@ -231,3 +231,36 @@ def test_large_config_segment_counts_exact(cuda, cfg, expected):
     spec = problems.CONFIGS[cfg]
     dg, _ = make(spec.N, spec.N, 1.0, spec.angles(), spec.det_count, 1.0)
     assert dg.count_segments() == expected
+
+
+def test_adjoint_small_geometries_vs_reference_transpose(cuda, golden):
+    """K7 = the reference's matched_back: the transpose of its Siddon CSR
+    (ct.py:248-264), column by column through the drop-in apply; includes the
+    degenerate (axis-aligned) angles whose rays lie on grid lines."""
+    for nm, params, d in small_cases(golden):
+        dg, og = make(*params)
+        At = ct.GpuAdjoint(dg.n, dg.m, dg).to_dense()
+        ref = d[f"{nm}/A_dense"].T
+        np.testing.assert_allclose(At, ref, atol=2e-6 * max(1.0, params[2]), err_msg=nm)
+        assert rel_l2(At, ref) <= REL_L2, nm
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_adjoint_identity_and_matched_back(cuda, name):
+    """<A x, u> = <x, A^T u> at the BASELINE sizes (fp64 dots of fp32 applies),
+    and ct.matched_back(A) returns the GPU adjoint."""
+    torch = cuda
+    spec = problems.CONFIGS[name]
+    grid = ct.ImageGrid(spec.N, spec.N, 1.0)
+    geom = ct.ParallelGeometry(spec.angles(), spec.det_count, 1.0)
+    A = ct.forward_ray_driven(grid, geom)
+    At = ct.matched_back(A)
+    assert isinstance(At, ct.GpuAdjoint) and At.shape == (A.cols, A.rows)
+    dg = A.dgeom
+    rng = np.random.default_rng(7)
+    x = rng.random(dg.n).astype(np.float32)
+    u = rng.random(dg.m).astype(np.float32)
+    Ax = dg.forward(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+    Atu = dg.adjoint(torch.from_numpy(u).cuda()).cpu().numpy().astype(np.float64)
+    lhs, rhs = Ax @ u.astype(np.float64), x.astype(np.float64) @ Atu
+    assert lhs == pytest.approx(rhs, rel=2e-6)

@@ -247,3 +247,23 @@ class TestShardPlan:
                 assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
         with pytest.raises(ValueError):
             dist.angle_shards(3, 4)
+
+
+def test_matched_back_reference_semantics_on_host_operators():
+    """ct.matched_back on non-GPU operators follows ctkrylov/ct.py:248-264:
+    CSR transpose when a sparse matrix is attached, else a guarded dense
+    transpose (GeometryError past the desk-scale guard)."""
+    import scipy.sparse as sp
+    from paper_2602_17892_b200 import ct
+    from paper_2602_17892_b200.linop import LinearOperator
+    rng = np.random.default_rng(0)
+    M = rng.standard_normal((7, 5))
+    op = LinearOperator(7, 5, lambda v: M @ v)
+    At = ct.matched_back(op)
+    u = rng.standard_normal(7)
+    np.testing.assert_allclose(At.apply(u), M.T @ u)
+    op.sparse_matrix = sp.csr_matrix(M)
+    np.testing.assert_allclose(ct.matched_back(op).apply(u), M.T @ u)
+    big = LinearOperator(5000, 4000, lambda v: np.zeros(5000))
+    with pytest.raises(ct.GeometryError):
+        ct.matched_back(big)

@@ -15,6 +15,7 @@ from .arnoldi import (Breakdown, DeviceBasis, ProjectedSolution, solve_projected
 from .regparam import DegenerateCurveError, lambda_grid, select_lambda, svd_of_hessenberg
 from .gmres import (ConfigError, IterationRecord, KernelTimer, SolveResult, SolverConfig,
                     run_ab_gmres, run_ba_gmres, run_gmres)
+from .gk import run_lsmr, run_lsqr
 from .problems import CONFIGS, add_noise, random_ellipse_phantom
 from .metrics import dp_should_stop, ncp_distance, ncp_should_stop, rns_should_stop, rre, ssim
 

@@ -150,6 +150,25 @@ def make_solver_cases():
         out[f"{name}/cycles"] = np.int64(res.cycles)
         for k, v in records_arrays(res).items():
             out[f"{name}/rec/{k}"] = v
+    # Golub-Kahan solvers on the matched pair (ctkrylov/gk.py, ct.py:248-264)
+    from ctkrylov.ct import matched_back
+    from ctkrylov.gk import run_lsmr, run_lsqr
+    At = matched_back(prob.forward)
+    gk_cases = {
+        "lsqr_plain": dict(method="lsqr", max_iter=12),
+        "lsqr_gcv": dict(method="lsqr-hybrid", lambda_strategy="gcv", max_iter=15),
+        "lsqr_lcurve": dict(method="lsqr-hybrid", lambda_strategy="lcurve", max_iter=15),
+        "lsqr_dp": dict(method="lsqr", max_iter=40, stopping_rule="dp", noise_norm=prob.noise_norm),
+        "lsmr_plain": dict(method="lsmr", max_iter=12),
+        "lsmr_gcv": dict(method="lsmr-hybrid", lambda_strategy="gcv", max_iter=15),
+    }
+    for name, kw in gk_cases.items():
+        run = run_lsqr if kw["method"].startswith("lsqr") else run_lsmr
+        res = run(prob.forward, At, prob.b_noisy, SolverConfig(**kw))
+        out[f"{name}/x"] = res.x
+        out[f"{name}/stop"] = np.array(res.stop_reason)
+        for k, v in records_arrays(res).items():
+            out[f"{name}/rec/{k}"] = v
     # lambda selection on random Hessenbergs (ctkrylov/regparam.py:137-158)
     rng = np.random.default_rng(7)
     for i, k in enumerate((3, 8, 20, 45)):

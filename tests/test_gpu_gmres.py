@@ -262,3 +262,36 @@ def test_large_krylov_vectors_switch_orthogonalisation_paths(cuda, method, na):
     assert res.records[-1].proj_residual_norm == pytest.approx(pr, rel=1e-3)
     dn = np.linalg.norm(b - A.apply(x_ref))
     assert res.records[-1].data_residual_norm == pytest.approx(dn, rel=1e-4)
+
+
+GK_CASES = {
+    "lsqr_plain": dict(method="lsqr", max_iter=12),
+    "lsqr_gcv": dict(method="lsqr-hybrid", lambda_strategy="gcv", max_iter=15),
+    "lsqr_lcurve": dict(method="lsqr-hybrid", lambda_strategy="lcurve", max_iter=15),
+    "lsqr_dp": dict(method="lsqr", max_iter=40, stopping_rule="dp"),
+    "lsmr_plain": dict(method="lsmr", max_iter=12),
+    "lsmr_gcv": dict(method="lsmr-hybrid", lambda_strategy="gcv", max_iter=15),
+}
+
+
+@pytest.mark.parametrize("case", sorted(GK_CASES))
+def test_golub_kahan_solvers_vs_reference(cuda, golden, case):
+    """Row f3: device (hybrid) LSQR/LSMR on the matched pair (K1 + K7) against
+    the reference's run_lsqr/run_lsmr on its CSR and CSR transpose
+    (ctkrylov/gk.py:101-205, ct.py:248-264)."""
+    from paper_2602_17892_b200 import gk
+    d, A, _ = small_problem(golden)
+    At = ct.matched_back(A)
+    kw = dict(GK_CASES[case])
+    if kw.get("stopping_rule") == "dp":
+        kw["noise_norm"] = float(d["noise_norm"])
+    run = gk.run_lsqr if kw["method"].startswith("lsqr") else gk.run_lsmr
+    res = run(A, At, d["b"], gmres.SolverConfig(**kw))
+    assert res.stop_reason == str(d[f"{case}/stop"])
+    assert len(res.records) == len(d[f"{case}/rec/k"])
+    for f in ("data_residual_norm", "residual_norm", "proj_residual_norm", "solution_norm"):
+        np.testing.assert_allclose(records(res, f), d[f"{case}/rec/{f}"], rtol=2e-3, err_msg=f)
+    if "gcv" in case:
+        lam, lam_ref = records(res, "lambda_used"), d[f"{case}/rec/lambda_used"]
+        assert np.all(np.abs(lam / lam_ref - 1.0) <= 0.01)
+    assert rel(res.x, d[f"{case}/x"]) <= 2e-3

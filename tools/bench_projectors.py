@@ -6,7 +6,8 @@ import numpy as np, torch
 from paper_2602_17892_b200 import ct, problems
 peak = json.load(open('MEASURED_PEAKS.json'))['hbm_gbs']
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device='cuda')
-names = sys.argv[1:] or ['c1', 'c2', 'c3', 'c4', 'c5']
+flags = [a for a in sys.argv[1:] if a.startswith('--')]
+names = [a for a in sys.argv[1:] if not a.startswith('--')] or ['c1', 'c2', 'c3', 'c4', 'c5']
 for name in names:
     spec = problems.CONFIGS[name]
     dg = ct.DeviceGeometry(ct.ImageGrid(spec.N, spec.N, 1.0),
@@ -16,7 +17,10 @@ for name in names:
     u = torch.from_numpy(problems.uniform_sinogram(dg.m, 1).astype(np.float32)).cuda()
     y = torch.empty(dg.m, device='cuda'); xo = torch.empty(dg.n, device='cuda')
     res = {}
-    for kind, fn in (('A', lambda: dg.forward(x, out=y)), ('B', lambda: dg.back(u, out=xo))):
+    kinds = [('A', lambda: dg.forward(x, out=y)), ('B', lambda: dg.back(u, out=xo))]
+    if '--adjoint' in flags:
+        kinds.append(('At', lambda: dg.adjoint(u, out=xo)))
+    for kind, fn in kinds:
         for _ in range(3): fn()
         ts = []
         for _ in range(10):
@@ -25,7 +29,7 @@ for name in names:
             e0.record(); fn(); e1.record(); e1.synchronize()
             ts.append(e0.elapsed_time(e1))
         ms = float(np.median(ts))
-        by = 4 * nnz + 4 * dg.m if kind == 'A' else 8 * dg.n * dg.n_angles + 4 * dg.n
+        by = 4 * nnz + 4 * dg.m if kind in ('A', 'At') else 8 * dg.n * dg.n_angles + 4 * dg.n
         res[kind] = {'ms': round(ms, 4), 'GBps': round(by / ms / 1e6, 1), 'frac': round(by / ms / 1e6 / peak, 3),
                      'rays_per_s': round(dg.m / ms * 1e3, -6)}
     print(json.dumps({'config': name, 'nnz': nnz, 'segments': raw, **res}), flush=True)

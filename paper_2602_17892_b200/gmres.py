@@ -196,6 +196,45 @@ def _pinned(torch, name, shape, dtype, zero=True):
     return t
 
 
+_WORKSPACES: dict = {}
+
+
+def _solve_workspace(torch, dg, ab, L, rows, K):
+    """Device buffers of one solve shape, reused by later solves of the same
+    shape on this thread (allocation + zero-fill of ~10 tensors costs more
+    host time than a c1 Arnoldi step).  Every buffer is written before it is
+    read inside a solve (the reduction scratch resets its own tickets);
+    x_cur is re-zeroed per solve.  Keeps the 4 most recent shapes."""
+    import threading as _th
+    key = (_th.get_ident(), id(dg), bool(ab), int(L), int(rows), int(K))
+    ws = _WORKSPACES.pop(key, None)
+    if ws is None:
+        f32, f64, dev = torch.float32, torch.float64, dg.dev
+        n, m = dg.n, dg.m
+        ldm, ldn = (m + 3) // 4 * 4, (n + 3) // 4 * 4
+        hcols = rows + 1 + 4
+        ws = {
+            "basis": DeviceBasis(L, rows, dev, torch),
+            "x_cur": torch.zeros(n, dtype=f32, device=dev),
+            "q": torch.empty(L, dtype=f32, device=dev),
+            "tmp": torch.empty(n if ab else m, dtype=f32, device=dev),
+            "hs": torch.zeros((rows, hcols), dtype=f64, device=dev),
+            "scal": torch.zeros(4, dtype=f64, device=dev),
+            "xk": torch.empty(n, dtype=f32, device=dev),
+            "z": torch.empty(m, dtype=f32, device=dev) if ab else None,
+            "aux1": torch.zeros((rows, ldn if ab else ldm), dtype=f32, device=dev),
+            "aux2": torch.zeros((rows, ldm), dtype=f32, device=dev) if ab else None,
+            "d0": torch.zeros(ldm, dtype=f32, device=dev),
+            "r": torch.empty(m, dtype=f32, device=dev),
+            "y_dev": torch.zeros((K, rows), dtype=f64, device=dev),
+            "norms": torch.zeros((K + 1, 2), dtype=f64, device=dev),
+        }
+    _WORKSPACES[key] = ws                      # most recent last
+    while len(_WORKSPACES) > 4:
+        _WORKSPACES.pop(next(iter(_WORKSPACES)))
+    return ws
+
+
 def _side_stream(torch, dev, kind, priority):
     """Cached solver streams: the Arnoldi stream at the highest priority (it is
     the critical path), the iterate stream at the lowest."""
@@ -294,10 +333,12 @@ class _DeviceSolve:
                 self.b = torch.empty(self.m, dtype=f32, device=dev)
                 self.b.copy_(bp, non_blocking=True)
                 self.h2d += 4 * self.m
-            self.basis = DeviceBasis(L, rows, dev, torch)
+            ws = _solve_workspace(torch, dg, self.ab, L, rows, self.K)
+            self.basis = ws["basis"]
             x0 = cfg.x0
             if x0 is None:
-                self.x_cur = torch.zeros(self.n, dtype=f32, device=dev)
+                self.x_cur = ws["x_cur"]
+                self.x_cur.zero_()
             else:
                 x0 = np.asarray(x0, dtype=np.float64)
                 if x0.shape != (self.n,):
@@ -305,30 +346,17 @@ class _DeviceSolve:
                 self.x_cur = torch.from_numpy(x0.astype(np.float32)).to(dev)
                 self.h2d += 4 * self.n
             # stream sa (Arnoldi) buffers
-            self.q = torch.empty(L, dtype=f32, device=dev)
-            self.tmp = torch.empty(self.n if self.ab else self.m, dtype=f32, device=dev)
+            self.q, self.tmp, self.hs, self.scal = ws["q"], ws["tmp"], ws["hs"], ws["scal"]
             self.hcols = rows + 1 + 4                      # h[0..rows] + 4 stats
-            self.hs = torch.zeros((rows, self.hcols), dtype=f64, device=dev)
             self.h_host = _pinned(torch, "h", (rows, self.hcols), f64)
-            self.scal = torch.zeros(4, dtype=f64, device=dev)
             self.scal_host = _pinned(torch, "scal", (4,), f64)
-            # stream sb (iterate) buffers
-            self.xk = torch.empty(self.n, dtype=f32, device=dev)
-            self.z = torch.empty(self.m, dtype=f32, device=dev) if self.ab else None
-            # Rows kept by each Arnoldi step so iterates follow by linearity
-            # (ctk_iterate): BA keeps A w_j; AB keeps B w_j and A B w_j.
-            ldm, ldn = (self.m + 3) // 4 * 4, (self.n + 3) // 4 * 4
-            if self.ab:
-                self.aux1 = torch.zeros((rows, ldn), dtype=f32, device=dev)
-                self.aux2 = torch.zeros((rows, ldm), dtype=f32, device=dev)
-            else:
-                self.aux1 = torch.zeros((rows, ldm), dtype=f32, device=dev)
-                self.aux2 = None
-            self.d0 = torch.zeros(ldm, dtype=f32, device=dev)
-            self.r = torch.empty(self.m, dtype=f32, device=dev)
-            self.y_dev = torch.zeros((self.K, rows), dtype=f64, device=dev)
+            # stream sb (iterate) buffers; rows kept by each Arnoldi step so
+            # iterates follow by linearity (ctk_iterate): BA keeps A w_j, AB
+            # keeps B w_j and A B w_j
+            self.xk, self.z, self.r = ws["xk"], ws["z"], ws["r"]
+            self.aux1, self.aux2, self.d0 = ws["aux1"], ws["aux2"], ws["d0"]
+            self.y_dev, self.norms = ws["y_dev"], ws["norms"]
             self.y_pin = _pinned(torch, "y", (self.K, rows), f64)
-            self.norms = torch.zeros((self.K + 1, 2), dtype=f64, device=dev)   # res^2, sol^2
         self.ev_h = [None] * rows
         # the side stream must not touch buffers before their zero-fill lands
         self.sb.wait_stream(self.sa)
@@ -690,14 +718,12 @@ class _NativeSolve(_DeviceSolve):
         nrec = outc.n_records
         self.d2h += 8 * self.hcols * nrec + 16 * (K + 1) + 32
         self.h2d += sum(8 * int(k) for k in out_arrays["k"][:nrec])
-        records = [IterationRecord(
-            k=int(out_arrays["k"][i]), lambda_used=float(out_arrays["lambda_"][i]),
-            residual_norm=float(out_arrays["residual"][i]),
-            data_residual_norm=float(out_arrays["data_residual"][i]),
-            proj_residual_norm=float(out_arrays["proj_residual"][i]),
-            solution_norm=float(out_arrays["solution_norm"][i]),
-            elapsed=float(out_arrays["elapsed"][i]),
-            lambda_warning=bool(out_arrays["warn"][i])) for i in range(nrec)]
+        cols = [out_arrays[f][:nrec].tolist() for f in
+                ("k", "lambda_", "residual", "data_residual", "proj_residual", "solution_norm")]
+        el = out_arrays["elapsed"][:nrec].tolist()
+        wn = out_arrays["warn"][:nrec].tolist()
+        records = [IterationRecord(kk, lam, rn, dn, pn, sn, None, None, e, bool(w))
+                   for kk, lam, rn, dn, pn, sn, e, w in zip(*cols, el, wn)]
         if self.x_true is not None:
             xn = float(np.linalg.norm(self.x_true))
             shape = self.image_shape

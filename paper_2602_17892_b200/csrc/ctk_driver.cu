@@ -105,7 +105,13 @@ Pool& pool() {
     return p;
 }
 
-__global__ void k_set_inv(double* dst, double v) { *dst = v; }
+// scal[2] = 1 / sqrt(scal[0]) (0 when the residual is exactly zero): the
+// cycle start normalises w0 on the device, so the Arnoldi pipeline starts
+// without a host round trip for beta.
+__global__ void k_set_inv(double* scal) {
+    const double s = scal[0];
+    scal[2] = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+}
 
 // Events are recycled across solves (a solve creates ~2K+ of them; create +
 // destroy costs ~1-2 us each on the host).  Every event handed out has
@@ -215,10 +221,40 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
             CTK_CUDA(cudaMemcpyAsync(bf->d0, ab ? w0 : bf->tmp, sizeof(float) * m,
                                      cudaMemcpyDeviceToDevice, sa));
         CTK_CUDA(cudaMemcpyAsync(bf->scal_host, bf->scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, sa));
-        CTK_CUDA(cudaStreamSynchronize(sa));
+        CTK_CUDA(cudaEventRecord(ev_sync, sa));
+        k_set_inv<<<1, 1, 0, sa>>>(bf->scal);
+        ctk_count_launch();
+        if ((rc = ctk_scale(w0, w0, L, bf->scal + 2, bf->stream_a))) return rc;
+        CTK_CUDA(cudaStreamWaitEvent(sb, ev_sync, 0));
+        const int steps = (p < K - nrec) ? p : K - nrec;
+        // the first Arnoldi steps go out before beta is known on the host
+        int queued = 0;
+        std::vector<std::shared_ptr<Job>> jobs(steps + 1);
+        auto enqueue_to = [&](int upto) -> int {
+            while (queued < (upto < steps ? upto : steps)) {
+                if (trace) CTK_CUDA(cudaEventRecord(tr_beg[queued], sa));
+                int r2 = ctk_arnoldi_step(g, ab, cfg->reorthogonalize ? 2 : 1, bf->W, bf->ld,
+                                          queued, bf->q, bf->tmp, bf->aux1,
+                                          bf->ld1, bf->aux2, bf->ld2, bf->stage_a,
+                                          bf->back_a, bf->hs + (size_t)queued * hc, hc,
+                                          bf->h_host + (size_t)queued * hc, bf->scratch_a,
+                                          bf->stream_a);
+                if (r2) return r2;
+                CTK_CUDA(cudaEventRecord(ev_h[queued], sa));
+                if (trace) {
+                    tr_host[queued] = std::chrono::duration<double>(
+                        std::chrono::steady_clock::now() - t0).count();
+                }
+                ++queued;
+            }
+            return CTK_OK;
+        };
+        if ((rc = enqueue_to(look))) return rc;
+        CTK_CUDA(cudaEventSynchronize(ev_sync));
         const double beta = sqrt(bf->scal_host[0]);
         const double d0n = ab ? beta : sqrt(bf->scal_host[1]);
         if (beta == 0.0) {           // exact solution in hand (gmres.py:176-182)
+            CTK_CUDA(cudaStreamSynchronize(sa));   // let the (discarded) steps drain
             stop = CTK_STOP_BREAKDOWN;
             if (nrec == 0) {
                 if ((rc = ctk_norm2(bf->x_cur, n, bf->scal + 2, bf->scratch_a, bf->stream_a))) return rc;
@@ -240,35 +276,8 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
             break;
         }
         ++cycles;
-        k_set_inv<<<1, 1, 0, sa>>>(bf->scal + 2, 1.0 / beta);
-        ctk_count_launch();
-        if ((rc = ctk_scale(w0, w0, L, bf->scal + 2, bf->stream_a))) return rc;
-        CTK_CUDA(cudaEventRecord(ev_sync, sa));
-        CTK_CUDA(cudaStreamWaitEvent(sb, ev_sync, 0));
-
-        const int steps = (p < K - nrec) ? p : K - nrec;
         std::vector<double> Hfull((size_t)(steps + 1) * steps, 0.0);
-        std::vector<std::shared_ptr<Job>> jobs(steps + 1);
-        int queued = 0, done_k = 0, last_k = steps, broke_at = -1;
-        auto enqueue_to = [&](int upto) -> int {
-            while (queued < (upto < steps ? upto : steps)) {
-                if (trace) CTK_CUDA(cudaEventRecord(tr_beg[queued], sa));
-                int r2 = ctk_arnoldi_step(g, ab, cfg->reorthogonalize ? 2 : 1, bf->W, bf->ld,
-                                          queued, bf->q, bf->tmp, bf->aux1,
-                                          bf->ld1, bf->aux2, bf->ld2, bf->stage_a,
-                                          bf->back_a, bf->hs + (size_t)queued * hc, hc,
-                                          bf->h_host + (size_t)queued * hc, bf->scratch_a,
-                                          bf->stream_a);
-                if (r2) return r2;
-                CTK_CUDA(cudaEventRecord(ev_h[queued], sa));
-                if (trace) {
-                    tr_host[queued] = std::chrono::duration<double>(
-                        std::chrono::steady_clock::now() - t0).count();
-                }
-                ++queued;
-            }
-            return CTK_OK;
-        };
+        int done_k = 0, last_k = steps, broke_at = -1;
         auto consume = [&](int k) -> int {
             auto& job = jobs[k];
             const auto tw0 = std::chrono::steady_clock::now();
@@ -342,7 +351,6 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
             if (broke_at == k && stop == CTK_STOP_NONE) stop = CTK_STOP_BREAKDOWN;
             return CTK_OK;
         };
-        if ((rc = enqueue_to(look))) return rc;
         for (int j = 0; j < steps; ++j) {
             CTK_CUDA(cudaEventSynchronize(ev_h[j]));
             const double* hr = bf->h_host + (size_t)j * hc;

@@ -15,12 +15,18 @@
 // column gets them) use the literal fp64 segment lists of K1d, transposed once
 // into per-pixel CSR lists (ray, length) on first use.
 //
-// B200 mapping mirrors K2: a CTA per 32 x 16 pixel tile, 2 pixels per thread;
+// B200 mapping mirrors K2: a CTA per 32 x 16 (32 x 32 for >= 512^2) pixel
+// tile, 2 (4) pixels per thread;
 // per 32-angle chunk the detector window of the tile is staged into SMEM with
-// coalesced loads (zero outside [0, D)), then each pixel evaluates <= 4
-// candidate rays per angle in fp64 (g and d must resolve the short slope
-// region of near-axis angles, which is ~|sin| h wide).  Small images split
-// angles over blockIdx.z into partial images reduced in a fixed order.
+// coalesced loads (zero outside [0, D)), then each pixel evaluates the 4
+// candidate rays j0-1..j0+2 around g = j0 + f.  Away from the axes
+// (min(|c|,|s|) >= 0.02, i.e. the slope region is >= 0.02 h wide) g comes
+// from K2's fixed point and the four weights, normalised by the flat-top
+// length (folded into the staged window), are one FFMA.SAT each:
+//     w_k / Lm = sat(Q_k -/+ f B),  B = s ics / Lm,  Q_k per angle;
+// near-axis angles evaluate g and the trapezoid in fp64 (their slope region
+// is ~|sin| h wide, below fp32 resolution of g).  Small images split angles
+// over blockIdx.z into partial images reduced in a fixed order.
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -32,8 +38,11 @@
 
 namespace ctk {
 
-constexpr int JTX = 32, JROWS = 8, JPPT = 2, JTY = JROWS * JPPT, JCA = 32;
+constexpr int JTX = 32, JROWS = 8, JCA = 32;     // tile JTX x (JROWS * JPPT), JPPT = K2's
 constexpr int JTHREADS = JTX * JROWS;
+#ifndef CTK_ADJ_FAST_MIN
+#define CTK_ADJ_FAST_MIN 0.02
+#endif
 
 struct AdjArgs {
     const double* cs;        // [n_angles] bitwise np.cos
@@ -49,14 +58,19 @@ struct AdjArgs {
     const float* dt_len;
     const int* deg_angle;    // slot -> angle
     int n_deg;
-    int nx, ny, D, a0, a1, per_split, wmax, split;
+    int nx, ny, D, a0, a1, per_split, wmax, split, fbits;
     double h, sp, xmin, ymax, center;
 };
 
+template <int JPPT>
 __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
-    extern __shared__ float win[];                 // [JCA][wmax]
+    constexpr int JTY = JROWS * JPPT;
+    extern __shared__ float4 winq[];               // [JCA][wmax] (v[i-1], v[i], v[i+1], v[i+2])
     __shared__ double s_cg[JCA], s_sg[JCA], s_P[JCA], s_Lm[JCA], s_ics[JCA];
-    __shared__ int s_w0[JCA], s_skip[JCA];
+    __shared__ int s_w0[JCA], s_skip[JCA];      // skip: 0 fp64 path, 1 K1d, 2 fp32 fixed point
+    __shared__ int4 s_fx[JCA];                  // fast path: T0, C, S (fixed point), unused
+    __shared__ float4 s_q[JCA];                 // fast path: weight offsets of the 4 candidates
+    __shared__ float s_b[JCA];                  //            and slope (weights / Lm)
 
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * JTX + tx;
     const int ix0 = blockIdx.x * JTX, iy0 = blockIdx.y * JTY;
@@ -74,6 +88,7 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
     const int aE = min(A.a1, aS + A.per_split);
     const int D = A.D, wmax = A.wmax;
     const double sp = A.sp;
+    const int F = A.fbits, I = 32 - A.fbits;
 
     double acc[JPPT];
 #pragma unroll
@@ -90,28 +105,75 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
             s_P[tid] = 0.5 * (ac_ + as_) * A.h;
             s_Lm[tid] = A.h / fmax(ac_, as_);
             s_ics[tid] = ac_ * as_ > 0.0 ? 1.0 / (ac_ * as_) : 0.0;
-            s_skip[tid] = A.deg_slot[a] >= 0;
             const double g00 = fma(Xlo, cg, fma(Ylo, sg, A.center));
             const double g01 = fma(Xlo, cg, fma(Yhi, sg, A.center));
             const double g10 = fma(Xhi, cg, fma(Ylo, sg, A.center));
             const double g11 = fma(Xhi, cg, fma(Yhi, sg, A.center));
-            s_w0[tid] = (int)floor(fmin(fmin(g00, g01), fmin(g10, g11))) - 2;
+            const int w0 = (int)floor(fmin(fmin(g00, g01), fmin(g10, g11))) - 2;
+            s_w0[tid] = w0;
+            // fp32 fixed-point path away from the axes (slope region >= 0.02 h
+            // wide): normalised weights sat(Q_k -/+ f B) by FFMA.SAT
+            const bool fast = fmin(ac_, as_) >= CTK_ADJ_FAST_MIN;
+            s_skip[tid] = A.deg_slot[a] >= 0 ? 1 : (fast ? 2 : 0);
+            if (fast) {
+                const double scale = ldexp(1.0, A.fbits);
+                s_fx[tid] = make_int4((int)(unsigned)llrint((g01 - (double)w0) * scale),
+                                      (int)llrint(cg * A.h * scale), (int)llrint(-sg * A.h * scale), 0);
+                const double ics = 1.0 / (ac_ * as_), Lm = A.h / fmax(ac_, as_);
+                const double A0 = 0.5 * (ac_ + as_) * A.h * ics / Lm, B0 = sp * ics / Lm;
+                s_q[tid] = make_float4((float)(A0 - B0), (float)A0, (float)(A0 - B0),
+                                       (float)(A0 - 2.0 * B0));
+                s_b[tid] = (float)B0;
+            }
         }
         __syncthreads();
         for (int ai = ty; ai < na; ai += JROWS) {
             const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
             const int w0 = s_w0[ai];
-            float* dst = win + ai * wmax;
+            float4* dst = winq + ai * wmax;
+            const float lsc = s_skip[ai] == 2 ? (float)s_Lm[ai] : 1.f;   // fast: pre-scale by Lm
             for (int i = tx; i < wmax; i += JTX) {
-                const int b = w0 + i;
-                dst[i] = (b >= 0 && b < D) ? __ldg(row + b) : 0.f;
+                float v4[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int b = w0 + i - 1 + q;
+                    v4[q] = (b >= 0 && b < D) ? lsc * __ldg(row + b) : 0.f;
+                }
+                dst[i] = make_float4(v4[0], v4[1], v4[2], v4[3]);
             }
         }
         __syncthreads();
+        float fa[JPPT];
+#pragma unroll
+        for (int r = 0; r < JPPT; ++r) fa[r] = 0.f;
         for (int ai = 0; ai < na; ++ai) {
-            if (s_skip[ai]) continue;                  // K1d angles: transposed lists below
+            const int mode = s_skip[ai];
+            if (mode == 1) continue;                   // K1d angles: transposed lists below
+            if (mode == 2) {
+                const int4 fx = s_fx[ai];
+                const float4 qw = s_q[ai];
+                const float bw = s_b[ai];
+                const float4* wr = winq + ai * wmax;
+                const unsigned T0 = (unsigned)fx.x + (unsigned)tx * (unsigned)fx.y +
+                                    (unsigned)ty * (unsigned)fx.z;
+#pragma unroll
+                for (int r = 0; r < JPPT; ++r) {
+                    const unsigned T = T0 + (unsigned)(r * JROWS) * (unsigned)fx.z;
+                    const int idx = (int)(T >> F);
+                    const float f = __uint_as_float(0x3f800000u | ((T << I) >> 9)) - 1.f;
+                    const float4 v = wr[idx];                  // taps j0-1 .. j0+2
+                    float t = fa[r];
+                    // |k - f| for k = -1, 0, 1, 2 is 1 + f, f, 1 - f, 2 - f
+                    t = fmaf(__saturatef(fmaf(f, -bw, qw.x)), v.x, t);
+                    t = fmaf(__saturatef(fmaf(f, -bw, qw.y)), v.y, t);
+                    t = fmaf(__saturatef(fmaf(f, bw, qw.z)), v.z, t);
+                    t = fmaf(__saturatef(fmaf(f, bw, qw.w)), v.w, t);
+                    fa[r] = t;
+                }
+                continue;
+            }
             const double cg = s_cg[ai], sg = s_sg[ai], P = s_P[ai], Lm = s_Lm[ai], ics = s_ics[ai];
-            const float* wrow = win + ai * wmax - s_w0[ai];
+            const float4* wq = winq + ai * wmax - s_w0[ai];   // wq[j].y = u[j]
 #pragma unroll
             for (int r = 0; r < JPPT; ++r) {
                 const double g = fma(X, cg, fma(Y[r], sg, A.center));   // ray index at the centre
@@ -120,10 +182,12 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
                 for (int q = -1; q <= 2; ++q) {
                     const int j = j0 + q;
                     const double a = P - fabs((double)j - g) * sp;
-                    if (a > 0.0) acc[r] = fma(fmin(Lm, a * ics), (double)wrow[j], acc[r]);
+                    if (a > 0.0) acc[r] = fma(fmin(Lm, a * ics), (double)wq[j].y, acc[r]);
                 }
             }
         }
+#pragma unroll
+        for (int r = 0; r < JPPT; ++r) acc[r] += (double)fa[r];
         __syncthreads();
     }
     // degenerate angles of this split range: per-pixel transposed lists
@@ -181,8 +245,13 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
     }
 }
 
+static int adj_tiles_y(const ctk_geom* g) {
+    const int jty = JROWS * g->back_ppt;
+    return (g->ny + jty - 1) / jty;
+}
+
 int adj_splits(const ctk_geom* g, int a0, int a1) {
-    const int tiles = ((g->nx + JTX - 1) / JTX) * ((g->ny + JTY - 1) / JTY);
+    const int tiles = ((g->nx + JTX - 1) / JTX) * adj_tiles_y(g);
     int S = (148 * 8 + tiles - 1) / tiles;
     const int max_s = (a1 - a0 + JCA - 1) / JCA;
     if (S > max_s) S = max_s;
@@ -284,7 +353,7 @@ using namespace ctk;
 extern "C" int64_t ctk_adjoint_work_floats(const ctk_geom_t* g, int a0, int a1) {
     if (!g || a0 < 0 || a1 > g->n_angles || a0 >= a1) return 0;
     const int S = adj_splits(g, a0, a1);
-    const int64_t tiles = (int64_t)((g->nx + JTX - 1) / JTX) * ((g->ny + JTY - 1) / JTY);
+    const int64_t tiles = (int64_t)((g->nx + JTX - 1) / JTX) * adj_tiles_y(g);
     return S > 1 ? (int64_t)S * g->nx * g->ny + tiles : 0;
 }
 
@@ -330,21 +399,29 @@ extern "C" int ctk_adjoint(const ctk_geom_t* gc, const float* u, float* x, int a
     A.a0 = a0;
     A.a1 = a1;
     A.per_split = (a1 - a0 + S - 1) / S;
-    // window: the tile's detector footprint + 4 bins of margin (K2's bound for
-    // its tallest tile covers it; recomputed here for 32 x 16 tiles)
+    // window: the tile's detector footprint (K2's bound for the same tile) + 2
     A.wmax = g->back_wmax + 2;
+    {   // fixed-point fraction bits: window coordinates [0, wmax] need I bits
+        int I = 1;
+        while ((1 << I) <= A.wmax + 1) ++I;
+        A.fbits = 32 - I;
+    }
     A.split = S > 1;
     A.h = g->h;
     A.sp = g->det_spacing;
     A.xmin = g->xmin;
     A.ymax = g->ymax;
     A.center = g->center;
-    dim3 grid((g->nx + JTX - 1) / JTX, (g->ny + JTY - 1) / JTY, S), block(JTX, JROWS);
-    const size_t smem = (size_t)JCA * A.wmax * sizeof(float);
+    dim3 grid((g->nx + JTX - 1) / JTX, adj_tiles_y(g), S), block(JTX, JROWS);
+    const size_t smem = (size_t)JCA * A.wmax * sizeof(float4);
+    const bool p4 = g->back_ppt == 4;
     if (smem > 48 * 1024)
-        CTK_CUDA(cudaFuncSetAttribute(k_adjoint, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    k_adjoint<<<grid, block, smem, st>>>(A);
+        CTK_CUDA(cudaFuncSetAttribute(p4 ? k_adjoint<4> : k_adjoint<2>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (p4)
+        k_adjoint<4><<<grid, block, smem, st>>>(A);
+    else
+        k_adjoint<2><<<grid, block, smem, st>>>(A);
     CTK_LAUNCH_CHECK("k_adjoint");
     return CTK_OK;
 }

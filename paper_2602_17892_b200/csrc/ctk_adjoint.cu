@@ -62,10 +62,25 @@ struct AdjArgs {
     double h, sp, xmin, ymax, center;
 };
 
-template <int JPPT>
+// TAPS: candidate rays per pixel-angle in the fast path: 2 (j0, j0+1) when
+// the pixel shadow is at most one bin wide, (|c|+|s|) h / 2 <= s for every
+// angle, else 4 (j0-1 .. j0+2).  The staged window holds, per bin i, the taps
+// (u[i], u[i+1]) or (u[i-1] .. u[i+2]) so one LDS.64 / LDS.128 fetches them.
+template <int TAPS>
+struct TapT {
+    typedef float4 type;
+};
+template <>
+struct TapT<2> {
+    typedef float2 type;
+};
+
+template <int JPPT, int TAPS>
 __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
     constexpr int JTY = JROWS * JPPT;
-    extern __shared__ float4 winq[];               // [JCA][wmax] (v[i-1], v[i], v[i+1], v[i+2])
+    typedef typename TapT<TAPS>::type tap_t;
+    extern __shared__ __align__(16) unsigned char wraw[];
+    tap_t* winq = reinterpret_cast<tap_t*>(wraw);    // [JCA][wmax] taps per window bin
     __shared__ double s_cg[JCA], s_sg[JCA], s_P[JCA], s_Lm[JCA], s_ics[JCA];
     __shared__ int s_w0[JCA], s_skip[JCA];      // skip: 0 fp64 path, 1 K1d, 2 fp32 fixed point
     __shared__ int4 s_fx[JCA];                  // fast path: T0, C, S (fixed point), unused
@@ -130,16 +145,20 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
         for (int ai = ty; ai < na; ai += JROWS) {
             const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
             const int w0 = s_w0[ai];
-            float4* dst = winq + ai * wmax;
+            tap_t* dst = winq + ai * wmax;
             const float lsc = s_skip[ai] == 2 ? (float)s_Lm[ai] : 1.f;   // fast: pre-scale by Lm
             for (int i = tx; i < wmax; i += JTX) {
                 float v4[4];
+                constexpr int first = TAPS == 2 ? 0 : -1;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int b = w0 + i - 1 + q;
+                for (int q = 0; q < TAPS; ++q) {
+                    const int b = w0 + i + first + q;
                     v4[q] = (b >= 0 && b < D) ? lsc * __ldg(row + b) : 0.f;
                 }
-                dst[i] = make_float4(v4[0], v4[1], v4[2], v4[3]);
+                if constexpr (TAPS == 2)
+                    dst[i] = make_float2(v4[0], v4[1]);
+                else
+                    dst[i] = make_float4(v4[0], v4[1], v4[2], v4[3]);
             }
         }
         __syncthreads();
@@ -153,7 +172,7 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
                 const int4 fx = s_fx[ai];
                 const float4 qw = s_q[ai];
                 const float bw = s_b[ai];
-                const float4* wr = winq + ai * wmax;
+                const tap_t* wr = winq + ai * wmax;
                 const unsigned T0 = (unsigned)fx.x + (unsigned)tx * (unsigned)fx.y +
                                     (unsigned)ty * (unsigned)fx.z;
 #pragma unroll
@@ -161,19 +180,24 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
                     const unsigned T = T0 + (unsigned)(r * JROWS) * (unsigned)fx.z;
                     const int idx = (int)(T >> F);
                     const float f = __uint_as_float(0x3f800000u | ((T << I) >> 9)) - 1.f;
-                    const float4 v = wr[idx];                  // taps j0-1 .. j0+2
+                    const tap_t v = wr[idx];
                     float t = fa[r];
                     // |k - f| for k = -1, 0, 1, 2 is 1 + f, f, 1 - f, 2 - f
-                    t = fmaf(__saturatef(fmaf(f, -bw, qw.x)), v.x, t);
-                    t = fmaf(__saturatef(fmaf(f, -bw, qw.y)), v.y, t);
-                    t = fmaf(__saturatef(fmaf(f, bw, qw.z)), v.z, t);
-                    t = fmaf(__saturatef(fmaf(f, bw, qw.w)), v.w, t);
+                    if constexpr (TAPS == 2) {
+                        t = fmaf(__saturatef(fmaf(f, -bw, qw.y)), v.x, t);
+                        t = fmaf(__saturatef(fmaf(f, bw, qw.z)), v.y, t);
+                    } else {
+                        t = fmaf(__saturatef(fmaf(f, -bw, qw.x)), v.x, t);
+                        t = fmaf(__saturatef(fmaf(f, -bw, qw.y)), v.y, t);
+                        t = fmaf(__saturatef(fmaf(f, bw, qw.z)), v.z, t);
+                        t = fmaf(__saturatef(fmaf(f, bw, qw.w)), v.w, t);
+                    }
                     fa[r] = t;
                 }
                 continue;
             }
             const double cg = s_cg[ai], sg = s_sg[ai], P = s_P[ai], Lm = s_Lm[ai], ics = s_ics[ai];
-            const float4* wq = winq + ai * wmax - s_w0[ai];   // wq[j].y = u[j]
+            const tap_t* wq = winq + ai * wmax - s_w0[ai];
 #pragma unroll
             for (int r = 0; r < JPPT; ++r) {
                 const double g = fma(X, cg, fma(Y[r], sg, A.center));   // ray index at the centre
@@ -182,7 +206,10 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
                 for (int q = -1; q <= 2; ++q) {
                     const int j = j0 + q;
                     const double a = P - fabs((double)j - g) * sp;
-                    if (a > 0.0) acc[r] = fma(fmin(Lm, a * ics), (double)wq[j].y, acc[r]);
+                    if (a > 0.0) {
+                        const float uj = TAPS == 2 ? wq[j].x : reinterpret_cast<const float4*>(wq)[j].y;
+                        acc[r] = fma(fmin(Lm, a * ics), (double)uj, acc[r]);
+                    }
                 }
             }
         }
@@ -413,15 +440,20 @@ extern "C" int ctk_adjoint(const ctk_geom_t* gc, const float* u, float* x, int a
     A.ymax = g->ymax;
     A.center = g->center;
     dim3 grid((g->nx + JTX - 1) / JTX, adj_tiles_y(g), S), block(JTX, JROWS);
-    const size_t smem = (size_t)JCA * A.wmax * sizeof(float4);
+    // two taps suffice when every pixel shadow is at most one bin wide
+    static int force4 = -1;
+    if (force4 < 0) {
+        const char* e = getenv("CTK_ADJ_TAPS4");          // test hook: the 4-tap path
+        force4 = e && e[0] == '1';
+    }
+    const int taps = (!force4 && 0.5 * 1.41421356237309515 * g->h <= g->det_spacing) ? 2 : 4;
+    const size_t smem = (size_t)JCA * A.wmax * (taps == 2 ? sizeof(float2) : sizeof(float4));
     const bool p4 = g->back_ppt == 4;
+    auto kern = p4 ? (taps == 2 ? k_adjoint<4, 2> : k_adjoint<4, 4>)
+                   : (taps == 2 ? k_adjoint<2, 2> : k_adjoint<2, 4>);
     if (smem > 48 * 1024)
-        CTK_CUDA(cudaFuncSetAttribute(p4 ? k_adjoint<4> : k_adjoint<2>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (p4)
-        k_adjoint<4><<<grid, block, smem, st>>>(A);
-    else
-        k_adjoint<2><<<grid, block, smem, st>>>(A);
+        CTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, block, smem, st>>>(A);
     CTK_LAUNCH_CHECK("k_adjoint");
     return CTK_OK;
 }

@@ -264,3 +264,19 @@ def test_adjoint_identity_and_matched_back(cuda, name):
     Atu = dg.adjoint(torch.from_numpy(u).cuda()).cpu().numpy().astype(np.float64)
     lhs, rhs = Ax @ u.astype(np.float64), x.astype(np.float64) @ Atu
     assert lhs == pytest.approx(rhs, rel=2e-6)
+
+
+@pytest.mark.parametrize("sp,na", [(0.5, 37), (0.55, 180)])
+def test_adjoint_four_tap_path_vs_oracle_transpose(cuda, sp, na):
+    """Detector bins narrower than a pixel shadow (s < h / sqrt 2) take K7's
+    four-candidate path; checked against the transpose of the oracle's
+    bit-exact Siddon matrix (oracle.forward, column by column), including the
+    near-axis fp64 angles."""
+    nx = ny = 12
+    angles = np.arange(na) * np.pi / na
+    D = 41
+    dg, og = make(nx, ny, 1.0, angles, D, sp)
+    A = np.stack([O.forward(og, e) for e in np.eye(nx * ny)], axis=1)
+    At = ct.GpuAdjoint(dg.n, dg.m, dg).to_dense()
+    np.testing.assert_allclose(At, A.T, atol=2e-5)
+    assert rel_l2(At, A.T) <= REL_L2

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
     const int aE = min(A.a1, aS + A.per_split);
     const int D = A.D, wmax = A.wmax;
     const int q1 = D > 1 ? 1 : 0;                  // reference quirk tap for i0 == -1
+    ctk_pdl_trigger();
 
     double acc[PPT];
 #pragma unroll
@@ -100,7 +101,8 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
                                    (int)(unsigned)__cvta_generic_to_shared(win + tid * wmax));
         }
         __syncthreads();
-        // stage the (mid, d) windows; zero taps outside [0, D), quirk at b == -1
+        ctk_pdl_wait();                            // u comes from the previous kernel
+        // stage the (p, d) windows; zero taps outside [0, D), quirk at b == -1
         for (int ai = ty; ai < na; ai += BROWS) {
             const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
             const int w0 = s_w0[ai];
@@ -275,11 +277,8 @@ int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
         CTK_CUDA(cudaFuncSetAttribute(p4 ? k_back<4> : k_back<2>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int ph = ctk_prof_open(1, st);
-    if (p4)
-        k_back<4><<<grid, block, smem, st>>>(A);
-    else
-        k_back<2><<<grid, block, smem, st>>>(A);
-    CTK_LAUNCH_CHECK("k_back");
+    CTK_CUDA(ctk_launch_pdl(p4 ? k_back<4> : k_back<2>, grid, block, smem, st, dim3(1, 1, 1), A));
+    ctk_count_launch();
     ctk_prof_close(ph, st);
     return CTK_OK;
 }

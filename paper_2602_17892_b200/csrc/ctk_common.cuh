@@ -104,6 +104,41 @@ int ctk_check_cuda(cudaError_t e, const char* what);
 
 static inline cudaStream_t ctk_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Programmatic dependent launch: kernels of the Arnoldi chain (K1, K2, K3)
+// let their successor launch early (launch_dependents at entry) and the
+// successor waits for its predecessor's memory only where it first reads
+// it (griddepcontrol.wait), so its launch and set-up overlap the previous
+// kernel's tail.  Both are no-ops without a programmatic launch.
+__device__ __forceinline__ void ctk_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void ctk_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+// cudaLaunchKernelEx with the programmatic-serialization attribute (plus an
+// optional cluster shape).
+template <typename... KArgs, typename... Args>
+static inline cudaError_t ctk_launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                         cudaStream_t st, dim3 cluster, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+    if (cluster.x * cluster.y * cluster.z > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = cluster.x;
+        at[na].val.clusterDim.y = cluster.y;
+        at[na].val.clusterDim.z = cluster.z;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // Destination of a fused K1 staging write (P / PT of an image vector).
 struct ctk_stage_dst {
     float* P;

@@ -151,6 +151,7 @@ struct FillSink {          // segment i of a ray -> entry i * stride of its colu
 // PT: nx rows x (ny + 2 pad), PT[ix][iy + pad] = x[iy][ix]
 __global__ void __launch_bounds__(256) k_stage(const float* __restrict__ x, float* __restrict__ P,
                                                float* __restrict__ PT, int nx, int ny, int pad) {
+    ctk_pdl_trigger();
     __shared__ float tile[32][33];
     const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
@@ -266,6 +267,7 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
     const int kw = __reduce_min_sync(lanes, hit ? (int)kb : 0x7fffffff);
     const int kW = __reduce_max_sync(lanes, hit ? (int)ke : (int)0x80000000);
     if (!hit) return 0.0;
+    ctk_pdl_wait();                                  // P / PT come from the previous kernel
 
     const int pitch = C + 2 * pad;
     // sigma < 1 here (the host clamps sigma_fx below 2^32), so the cross
@@ -315,6 +317,7 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
 // stored ray-interleaved so a warp's loads are coalesced like the walk's.
 __device__ __forceinline__ double degenerate_ray(const FwdArgs& A, int slot, int j, int e0,
                                                  int e1) {
+    ctk_pdl_wait();                                  // x comes from the previous kernel
     const long long cnt = A.deg_cnt[(size_t)slot * A.D + j];
     if (e1 > cnt) e1 = (int)cnt;
     const size_t base = (size_t)slot * A.deg_maxseg * A.D + j;
@@ -368,6 +371,7 @@ __device__ __forceinline__ unsigned cluster_addr(const void* p, unsigned rank) {
 
 template <bool SPLIT>
 __global__ void __launch_bounds__(FWD_THREADS, 12) k_forward(FwdArgs A) {
+    ctk_pdl_trigger();
     const int ai = blockIdx.y * FWD_APB + (threadIdx.x >> 5);
     const int a = A.a0 + ai;
     const int j = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -602,24 +606,12 @@ int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1
     A.PT = PT;
     A.split = g->fwd_split;
     dim3 grid((g->det_count + 31) / 32, (a1 - a0 + FWD_APB - 1) / FWD_APB, A.split);
-    if (A.split > 1) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = grid;
-        cfg.blockDim = dim3(FWD_THREADS);
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 1;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = (unsigned)A.split;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        CTK_CUDA(cudaLaunchKernelEx(&cfg, k_forward<true>, A));
-        ctk_count_launch();
-    } else {
-        k_forward<false><<<grid, FWD_THREADS, 0, st>>>(A);
-        CTK_LAUNCH_CHECK("k_forward");
-    }
+    if (A.split > 1)
+        CTK_CUDA(ctk_launch_pdl(k_forward<true>, grid, dim3(FWD_THREADS), 0, st,
+                                dim3(1, 1, (unsigned)A.split), A));
+    else
+        CTK_CUDA(ctk_launch_pdl(k_forward<false>, grid, dim3(FWD_THREADS), 0, st, dim3(1, 1, 1), A));
+    ctk_count_launch();
     ctk_prof_close(ph, st);
     return CTK_OK;
 }

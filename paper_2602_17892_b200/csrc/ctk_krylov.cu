@@ -669,6 +669,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
                                                    double* partial, ctk_stage_dst sd,
                                                    double* hm, int stat_off) {
     cg::grid_group grid = cg::this_grid();
+    ctk_pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nb = k + 1;
     const int cpad = (int)((chunk + 3) & ~3LL);

@@ -243,6 +243,29 @@ size_t ctk_metrics_scratch_bytes(void);
 int ctk_metrics(const float* x, const float* x_true, int nx, int ny, double dyn_range,
                 double* out, void* scratch, void* stream);
 
+/* ---- On-device problem generation.
+ * ctk_phantom replaces shepp_logan (ctkrylov/ct.py:115-134) and the harness's
+ * random-ellipse recipe: img[iy*nx+ix] = sum over ellipses, in order, of
+ * value_e where u^2 + v^2 <= 1, with (X, Y) = pixel centre / scale
+ * (xc = xmin + (ix+0.5) h, yc = ymax - (iy+0.5) h, ct.py:60-66) and
+ * u = ((X-x0) c + (Y-y0) s) / a, v = (-(X-x0) s + (Y-y0) c) / b -- the
+ * reference's fp64 operation order, bitwise.  ellipses: HOST array of
+ * n_ellipses x 7 doubles (value, a, b, x0, y0, cos phi, sin phi; at most 128);
+ * img64 / img32 device outputs (either may be NULL). */
+int ctk_phantom(int nx, int ny, double xmin, double ymax, double pixel_size, double scale,
+                const double* ellipses, int n_ellipses, double* img64, float* img32,
+                void* stream);
+/* add_noise (ctkrylov/ct.py:267-283) on a device sinogram: clean data in
+ * exactly one of b_clean (fp32) / b_clean64 (fp64); g = the m-sample
+ * standard-normal draw (device fp64, numpy default_rng(seed) on the host);
+ * noise_norm = level * ||b_clean||; b = b_clean + (noise_norm * g) / ||g||
+ * into b64 / b32 (either may be NULL); noise_norm_dev[0] = noise_norm.
+ * scratch: ctk_noise_scratch_bytes().  level 0 is the caller's copy. */
+size_t ctk_noise_scratch_bytes(void);
+int ctk_add_noise(const float* b_clean, const double* b_clean64, const double* g, int64_t m,
+                  double level, double* b64, float* b32, double* noise_norm_dev, void* scratch,
+                  void* stream);
+
 /* CUDA-event profiler over library calls: kinds 0 = forward (stage + K1),
  * 1 = back (K2 + finalize), 2 = CGS2 step, 3 = basis combination.  end()
  * synchronises the recorded events and fills per-kind counts / mean / total. */

@@ -18,6 +18,9 @@ relative to the reference's ``pkg/src``):
 * L-curve / GCV selection on the 200-point grid: ``ctkrylov/regparam.py:28-158``.
 * The (hybrid) AB/BA-GMRES driver with restarts and stopping:
   ``ctkrylov/gmres.py:135-241``.
+* Problem generation (row f4): ellipse phantoms at pixel centres
+  (``ctkrylov/ct.py:60-66,115-134``) and exact-level noise
+  (``ctkrylov/ct.py:267-283``), numpy.
 
 Pinning: ``tests/golden/make_golden.py`` runs the unmodified reference (in
 the build container, where ``/root/reference`` exists) and stores its outputs
@@ -381,3 +384,43 @@ def gmres(A, B, b, method, strategy="none", max_iter=100, lambda_value=None,
                 break
     return OracleResult(x=x, records=records, stop_reason=stop or "maxiter",
                         cycles=max(cycles, 1))
+
+
+# ---- problem generation (row f4) -------------------------------------------
+
+def phantom(nx: int, ny: int, h: float, rows, scale: float = 1.0) -> np.ndarray:
+    """Ellipse phantom at pixel centres (ctkrylov/ct.py:60-66, 115-134):
+    rows = (value, a, b, x0, y0, phi_radians); (X, Y) = centre / scale;
+    value_e added, in order, where u^2 + v^2 <= 1."""
+    xmin = -(0.5 * nx * h)
+    ymax = 0.5 * ny * h
+    X, Y = np.meshgrid(xmin + (np.arange(nx) + 0.5) * h, ymax - (np.arange(ny) + 0.5) * h)
+    X = X / scale
+    Y = Y / scale
+    img = np.zeros((ny, nx))
+    for value, a, b, x0, y0, phi in rows:
+        c, s = np.cos(phi), np.sin(phi)
+        u = ((X - x0) * c + (Y - y0) * s) / a
+        v = (-(X - x0) * s + (Y - y0) * c) / b
+        img[u * u + v * v <= 1.0] += value
+    return img.ravel()
+
+
+def shepp_logan_rows():
+    """Modified Shepp-Logan (value, a, b, x0, y0, phi_radians) on [-1, 1]^2."""
+    tab = ((1.0, 0.69, 0.92, 0.0, 0.0, 0.0), (-0.8, 0.6624, 0.8740, 0.0, -0.0184, 0.0),
+           (-0.2, 0.1100, 0.3100, 0.22, 0.0, -18.0), (-0.2, 0.1600, 0.4100, -0.22, 0.0, 18.0),
+           (0.1, 0.2100, 0.2500, 0.0, 0.35, 0.0), (0.1, 0.0460, 0.0460, 0.0, 0.1, 0.0),
+           (0.1, 0.0460, 0.0460, 0.0, -0.1, 0.0), (0.1, 0.0460, 0.0230, -0.08, -0.605, 0.0),
+           (0.1, 0.0230, 0.0230, 0.0, -0.606, 0.0), (0.1, 0.0230, 0.0460, 0.06, -0.605, 0.0))
+    return [(v, a, b, x0, y0, np.deg2rad(p)) for v, a, b, x0, y0, p in tab]
+
+
+def add_noise(b_clean: np.ndarray, level: float, seed: int):
+    """(b_clean + e, ||e||) with ||e|| = level ||b_clean|| (ct.py:267-283)."""
+    b_clean = np.asarray(b_clean, dtype=np.float64)
+    nn = level * float(np.linalg.norm(b_clean))
+    if level == 0.0:
+        return b_clean.copy(), 0.0
+    g = np.random.default_rng(seed).standard_normal(b_clean.size)
+    return b_clean + nn * g / np.linalg.norm(g), nn

@@ -8,8 +8,10 @@ CUDA behind the C ABI in include/ctk.h); there is no CPU fallback.
 """
 
 from .linop import LinearOperator, OperatorShapeError, compose
-from .ct import (DeviceGeometry, GeometryError, GpuAdjoint, GpuBack, GpuForward, ImageGrid,
-                 ParallelGeometry, back_pixel_driven, forward_ray_driven, matched_back)
+from .ct import (BUILTIN_PROBLEMS, CtProblem, DeviceGeometry, GeometryError, GpuAdjoint, GpuBack,
+                 GpuForward, ImageGrid, ParallelGeometry, back_pixel_driven, build_test_problem,
+                 forward_ray_driven, make_ct_problem, matched_back, shepp_logan, write_csv_image,
+                 write_pgm)
 from .arnoldi import (Breakdown, DeviceBasis, ProjectedSolution, solve_projected_ls,
                       solve_projected_tikhonov)
 from .regparam import DegenerateCurveError, lambda_grid, select_lambda, svd_of_hessenberg

@@ -66,6 +66,10 @@ SIGNATURES = {
     "ctk_solve": (_c.c_int, [_vp, _vp, _vp, _vp]),
     "ctk_metrics_scratch_bytes": (_c.c_size_t, []),
     "ctk_metrics": (_c.c_int, [_fp, _fp, _c.c_int, _c.c_int, _c.c_double, _dp, _vp, _vp]),
+    "ctk_phantom": (_c.c_int, [_c.c_int, _c.c_int, _c.c_double, _c.c_double, _c.c_double,
+                               _c.c_double, _c.POINTER(_c.c_double), _c.c_int, _dp, _fp, _vp]),
+    "ctk_noise_scratch_bytes": (_c.c_size_t, []),
+    "ctk_add_noise": (_c.c_int, [_fp, _dp, _dp, _c.c_int64, _c.c_double, _dp, _fp, _dp, _vp, _vp]),
     "ctk_profile_begin": (_c.c_int, []),
     "ctk_profile_end": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int64), _c.POINTER(_c.c_double),
                                    _c.POINTER(_c.c_double)]),

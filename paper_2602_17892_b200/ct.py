@@ -351,3 +351,206 @@ def matched_back(forward: LinearOperator) -> LinearOperator:
             f"{DENSE_ASSEMBLY_GUARD} entries")
     dense_t = np.ascontiguousarray(forward.to_dense().T)
     return LinearOperator(forward.cols, forward.rows, lambda v: dense_t @ v)
+
+
+# ---------------------------------------------------------------------------
+# Problem generation on the device: ctkrylov/ct.py:99-134,
+# 267-356.  Phantoms are sampled by K_phantom (bitwise numpy), the clean data
+# is the GPU forward projection, and the noise is scaled on the device from
+# numpy's own Gaussian draw; the host sees the reference's numpy contract.
+# ---------------------------------------------------------------------------
+
+# Modified Shepp-Logan ellipse stack (value, a, b, x0, y0, phi_degrees) on
+# [-1, 1]^2 -- the published Shepp & Logan (1974) / Toft modified intensities,
+# in the reference's order (ctkrylov/ct.py:99-112).
+SHEPP_LOGAN_ELLIPSES = (
+    (1.0, 0.69, 0.92, 0.0, 0.0, 0.0),
+    (-0.8, 0.6624, 0.8740, 0.0, -0.0184, 0.0),
+    (-0.2, 0.1100, 0.3100, 0.22, 0.0, -18.0),
+    (-0.2, 0.1600, 0.4100, -0.22, 0.0, 18.0),
+    (0.1, 0.2100, 0.2500, 0.0, 0.35, 0.0),
+    (0.1, 0.0460, 0.0460, 0.0, 0.1, 0.0),
+    (0.1, 0.0460, 0.0460, 0.0, -0.1, 0.0),
+    (0.1, 0.0460, 0.0230, -0.08, -0.605, 0.0),
+    (0.1, 0.0230, 0.0230, 0.0, -0.606, 0.0),
+    (0.1, 0.0230, 0.0460, 0.06, -0.605, 0.0),
+)
+
+
+def _ellipse_table(rows) -> np.ndarray:
+    """(value, a, b, x0, y0, phi_radians) rows -> the n x 7 table ctk_phantom
+    takes, with cos/sin evaluated by numpy exactly as the reference does."""
+    out = np.empty((len(rows), 7), dtype=np.float64)
+    for i, (value, a, b, x0, y0, phi) in enumerate(rows):
+        out[i] = (value, a, b, x0, y0, np.cos(phi), np.sin(phi))
+    return np.ascontiguousarray(out)
+
+
+def phantom_device(grid: ImageGrid, ellipses, scale: float = 1.0, device: int = 0,
+                   want64: bool = True, want32: bool = True, stream=None):
+    """Sample ellipses (value, a, b, x0, y0, phi in radians) at the pixel
+    centres of ``grid`` divided by ``scale`` on the GPU.  Returns
+    ``(img64, img32)`` CUDA tensors (either None when not requested)."""
+    torch = _require_cuda(device)
+    dev = torch.device("cuda", int(device))
+    tab = _ellipse_table(ellipses)
+    img64 = torch.empty(grid.n, dtype=torch.float64, device=dev) if want64 else None
+    img32 = torch.empty(grid.n, dtype=torch.float32, device=dev) if want32 else None
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    xmin, _, _, ymax = grid.extent
+    with torch.cuda.device(dev):
+        _native.check(_native.load().ctk_phantom(
+            grid.nx, grid.ny, float(xmin), float(ymax), float(grid.pixel_size), float(scale),
+            _dptr(tab), len(tab), _native.ptr(img64), _native.ptr(img32), stream.cuda_stream),
+            "ctk_phantom")
+    return img64, img32
+
+
+def shepp_logan(grid: ImageGrid, device: int = 0) -> np.ndarray:
+    """Drop-in for ctkrylov.ct.shepp_logan (ct.py:115-134): the modified
+    Shepp-Logan phantom at pixel centres, the image square mapped onto
+    [-1, 1]^2; sampled on the GPU, bitwise the reference's float64 image."""
+    if grid.nx != grid.ny:
+        raise GeometryError(f"phantom requires a square grid, got {grid.nx}x{grid.ny}")
+    scale = 0.5 * grid.nx * grid.pixel_size
+    rows = [(v, a, b, x0, y0, np.deg2rad(phi)) for v, a, b, x0, y0, phi in SHEPP_LOGAN_ELLIPSES]
+    img64, _ = phantom_device(grid, rows, scale, device, want32=False)
+    return img64.cpu().numpy()
+
+
+def add_noise_device(b_clean, level: float, seed: int, out32=None, stream=None):
+    """add_noise (ctkrylov/ct.py:267-283) for a CUDA sinogram (fp32 or fp64):
+    ``||e|| = level * ||b_clean||`` exactly, e from numpy's
+    ``default_rng(seed).standard_normal(m)``.  Returns
+    ``(b_noisy64, b_noisy32, noise_norm)``, the first two CUDA tensors."""
+    if level < 0:
+        raise ValueError(f"noise level must be nonnegative, got {level}")
+    torch = _torch()
+    dev = b_clean.device
+    m = b_clean.numel()
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    b64 = torch.empty(m, dtype=torch.float64, device=dev)
+    b32 = out32 if out32 is not None else torch.empty(m, dtype=torch.float32, device=dev)
+    if level == 0.0:
+        b64.copy_(b_clean)
+        b32.copy_(b_clean)
+        return b64, b32, 0.0
+    g = torch.from_numpy(np.random.default_rng(seed).standard_normal(m)).to(dev)
+    scratch = torch.zeros(int(_native.load().ctk_noise_scratch_bytes()) // 8,
+                          dtype=torch.float64, device=dev)
+    nn = torch.empty(1, dtype=torch.float64, device=dev)
+    f32 = b_clean.dtype == torch.float32
+    with torch.cuda.device(dev):
+        _native.check(_native.load().ctk_add_noise(
+            b_clean.data_ptr() if f32 else None, None if f32 else b_clean.data_ptr(),
+            g.data_ptr(), m, float(level), b64.data_ptr(), b32.data_ptr(), nn.data_ptr(),
+            scratch.data_ptr(), stream.cuda_stream), "ctk_add_noise")
+    return b64, b32, float(nn.item())
+
+
+def add_noise(b_clean, level: float, seed: int, device: int = 0) -> tuple[np.ndarray, float]:
+    """Drop-in for ctkrylov.ct.add_noise (ct.py:267-283), scaled on the GPU.
+    Host float64 in, host float64 out; level 0 returns a copy."""
+    if level < 0:
+        raise ValueError(f"noise level must be nonnegative, got {level}")
+    b_clean = np.asarray(b_clean, dtype=np.float64)
+    if level == 0.0:
+        return b_clean.copy(), 0.0
+    torch = _require_cuda(device)
+    bd = torch.from_numpy(np.ascontiguousarray(b_clean)).to(torch.device("cuda", int(device)))
+    b64, _, nn = add_noise_device(bd, level, seed)
+    return b64.cpu().numpy(), nn
+
+
+@dataclass
+class CtProblem:
+    """A fully populated CT test problem (ctkrylov/ct.py:286-307).  Host fields
+    are numpy as in the reference; the device copies the solver consumes are
+    kept alongside (``x_true_device`` / ``b_noisy_device``, fp32)."""
+
+    grid: ImageGrid
+    geometry: ParallelGeometry
+    x_true: np.ndarray
+    b_clean: np.ndarray
+    b_noisy: np.ndarray
+    noise_norm: float
+    forward: LinearOperator
+    back: LinearOperator
+    matched: bool
+    name: str = "custom"
+    x_true_device: object = None
+    b_noisy_device: object = None
+
+    @property
+    def m(self) -> int:
+        return self.geometry.m
+
+    @property
+    def n(self) -> int:
+        return self.grid.n
+
+
+def make_ct_problem(nx: int, n_angles: int, det_count: int | None = None,
+                    noise_level: float = 0.025, seed: int = 0, matched: bool = False,
+                    name: str = "custom", device: int = 0) -> CtProblem:
+    """Drop-in for ctkrylov.ct.make_ct_problem (ct.py:310-337): square
+    Shepp-Logan problem on [-1, 1]^2 with the detector spanning the image
+    diagonal, generated on the GPU (phantom -> K1 -> noise)."""
+    if det_count is None:
+        det_count = nx
+    grid = ImageGrid(nx, nx, pixel_size=2.0 / nx)
+    width = nx * grid.pixel_size
+    det_spacing = np.sqrt(2.0) * width / det_count
+    angles = np.arange(n_angles) * np.pi / n_angles
+    geometry = ParallelGeometry(angles, det_count, det_spacing)
+    scale = 0.5 * grid.nx * grid.pixel_size
+    rows = [(v, a, b, x0, y0, np.deg2rad(phi)) for v, a, b, x0, y0, phi in SHEPP_LOGAN_ELLIPSES]
+    x64, x32 = phantom_device(grid, rows, scale, device)
+    forward = forward_ray_driven(grid, geometry, device)
+    back = matched_back(forward) if matched else back_pixel_driven(grid, geometry, device)
+    bc = forward.dgeom.forward(x32)
+    b64, b32, noise_norm = add_noise_device(bc, noise_level, seed)
+    return CtProblem(grid, geometry, x64.cpu().numpy(), bc.double().cpu().numpy(),
+                     b64.cpu().numpy(), noise_norm, forward, back, matched, name,
+                     x_true_device=x32, b_noisy_device=b32)
+
+
+BUILTIN_PROBLEMS = ("tp1-like", "tp2", "tp3-desk")
+
+
+def build_test_problem(name: str, matched: bool = False, seed: int = 0,
+                       device: int = 0) -> CtProblem:
+    """Drop-in for ctkrylov.ct.build_test_problem (ct.py:343-356)."""
+    if name == "tp1-like":
+        return make_ct_problem(128, 180, 128, 0.001, seed, matched, name, device)
+    if name == "tp2":
+        return make_ct_problem(128, 50, 128, 0.025, seed, matched, name, device)
+    if name == "tp3-desk":
+        return make_ct_problem(256, 50, 256, 0.015, seed, matched, name, device)
+    raise GeometryError(f"unknown test problem {name!r}; choose from {BUILTIN_PROBLEMS}")
+
+
+def write_pgm(path, image, shape: tuple[int, int], window=None) -> None:
+    """16-bit binary PGM (ctkrylov/ct.py:359-370): values mapped linearly from
+    [lo, hi] (default: the image's own range) onto 0..65535, big-endian."""
+    img = np.asarray(image, dtype=np.float64).reshape(shape)
+    lo, hi = window if window is not None else (img.min(), img.max())
+    if hi <= lo:
+        scaled = np.zeros_like(img)
+    else:
+        scaled = np.clip((img - lo) / (hi - lo), 0.0, 1.0)
+    data = np.round(scaled * 65535).astype(">u2")
+    with open(path, "wb") as f:
+        f.write(f"P5\n{shape[1]} {shape[0]}\n65535\n".encode("ascii"))
+        f.write(data.tobytes())
+
+
+def write_csv_image(path, image, shape: tuple[int, int]) -> None:
+    """Row-major CSV of an image or sinogram, repr() floats (ct.py:373-379)."""
+    img = np.asarray(image, dtype=np.float64).reshape(shape)
+    with open(path, "w", encoding="utf-8", newline="\n") as f:
+        for row in img:
+            f.write(",".join(repr(float(v)) for v in row))
+            f.write("\n")

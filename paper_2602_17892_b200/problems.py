@@ -61,9 +61,7 @@ CONFIGS = {
 
 def random_ellipse_phantom(N: int, n_ellipses: int, seed: int, pixel_size: float = 1.0) -> np.ndarray:
     """Flattened row-major (N, N) phantom, fp32-representable fp64 values."""
-    lo = np.array([-0.25 * N, -0.25 * N, 0.05 * N, 0.05 * N, 0.0, 0.1])
-    hi = np.array([0.25 * N, 0.25 * N, 0.4 * N, 0.4 * N, np.pi, 1.0])
-    params = np.random.default_rng(seed).uniform(lo, hi, size=(n_ellipses, 6))
+    params = ellipse_params(N, n_ellipses, seed)
     half = 0.5 * N * pixel_size
     xc = -half + (np.arange(N) + 0.5) * pixel_size
     yc = half - (np.arange(N) + 0.5) * pixel_size
@@ -75,6 +73,23 @@ def random_ellipse_phantom(N: int, n_ellipses: int, seed: int, pixel_size: float
         v = (-(X - cx) * s + (Y - cy) * c) / b
         img[u * u + v * v <= 1.0] += rho
     return img.ravel().astype(np.float32).astype(np.float64)
+
+
+def ellipse_params(N: int, n_ellipses: int, seed: int) -> np.ndarray:
+    """The recipe's (E, 6) draw: columns cx, cy, a, b, phi, rho."""
+    lo = np.array([-0.25 * N, -0.25 * N, 0.05 * N, 0.05 * N, 0.0, 0.1])
+    hi = np.array([0.25 * N, 0.25 * N, 0.4 * N, 0.4 * N, np.pi, 1.0])
+    return np.random.default_rng(seed).uniform(lo, hi, size=(n_ellipses, 6))
+
+
+def random_ellipse_phantom_device(N: int, n_ellipses: int, seed: int, pixel_size: float = 1.0,
+                                  device: int = 0, stream=None):
+    """The same phantom sampled on the GPU (ctk_phantom, row f4): returns
+    ``(img64, img32)`` CUDA tensors; ``img64`` is bitwise
+    ``random_ellipse_phantom`` before its fp32 rounding, ``img32`` after."""
+    from . import ct
+    rows = [(rho, a, b, cx, cy, phi) for cx, cy, a, b, phi, rho in ellipse_params(N, n_ellipses, seed)]
+    return ct.phantom_device(ct.ImageGrid(N, N, pixel_size), rows, 1.0, device, stream=stream)
 
 
 def add_noise(b_clean: np.ndarray, level: float, seed: int) -> tuple[np.ndarray, float]:

@@ -15,6 +15,7 @@ from __future__ import annotations
 import os
 import sys
 import time
+from pathlib import Path
 
 import numpy as np
 
@@ -180,8 +181,79 @@ def make_solver_cases():
     print("solver_cases.npz", len(cases), "cases")
 
 
+def _file_bytes(path):
+    with open(path, "rb") as f:
+        return np.frombuffer(f.read(), dtype=np.uint8)
+
+
+def synthetic_result():
+    """A fixed SolveResult exercising every CSV cell kind (None, nan, inf,
+    tiny/huge magnitudes), built from the reference's own dataclasses."""
+    from ctkrylov.gmres import IterationRecord, SolveResult
+    recs = [
+        IterationRecord(1, 0.125, 3.5, 2.25, 1.0 / 3.0, 7.0, None, None, 0.5, False),
+        IterationRecord(2, 1.7e-08, 1e-300, 2.0 ** -30, 0.0, 1e300, 0.9, 0.25, 1.25, True),
+        IterationRecord(3, float("nan"), 4.0, float("inf"), 5.0, 6.0, 0.1, -0.5, 2.0, False),
+    ]
+    return SolveResult(np.arange(12.0), recs, "maxiter", 1)
+
+
+def make_io():
+    """Row f4 fixtures: the reference's phantom, problem builder and writers."""
+    import json
+    import tempfile
+    from ctkrylov import ct as rct
+    from ctkrylov import experiment as rexp
+    from ctkrylov.gmres import SolverConfig as RCfg
+    out = {}
+    for nx, h in ((64, 2.0 / 64), (33, 0.37), (128, 1.0)):
+        out[f"sl/{nx}"] = rct.shepp_logan(rct.ImageGrid(nx, nx, h))
+    prob = rct.make_ct_problem(32, 20, 45, 0.025, seed=3)
+    for k in ("x_true", "b_clean", "b_noisy"):
+        out[f"mk/{k}"] = getattr(prob, k)
+    out["mk/noise_norm"] = np.float64(prob.noise_norm)
+    tp2 = rct.build_test_problem("tp2", seed=0)
+    out["tp2/b_noisy"] = tp2.b_noisy
+    out["tp2/noise_norm"] = np.float64(tp2.noise_norm)
+    rng = np.random.default_rng(11)
+    img = rng.standard_normal((5, 7))
+    res = synthetic_result()
+    with tempfile.TemporaryDirectory() as d:
+        rct.write_pgm(os.path.join(d, "a.pgm"), img.ravel(), (5, 7))
+        out["io/img"] = img
+        out["io/pgm_auto"] = _file_bytes(os.path.join(d, "a.pgm"))
+        rct.write_pgm(os.path.join(d, "b.pgm"), img.ravel(), (5, 7), (-0.5, 1.5))
+        out["io/pgm_window"] = _file_bytes(os.path.join(d, "b.pgm"))
+        rct.write_pgm(os.path.join(d, "c.pgm"), np.ones(35), (5, 7))
+        out["io/pgm_flat"] = _file_bytes(os.path.join(d, "c.pgm"))
+        rct.write_csv_image(os.path.join(d, "i.csv"), img.ravel(), (5, 7))
+        out["io/csv_image"] = _file_bytes(os.path.join(d, "i.csv"))
+        for method in ("ab-hybrid", "ba", "lsmr-hybrid"):
+            for tim in (False, True):
+                f = os.path.join(d, f"{method}_{tim}.csv")
+                rexp.write_records_csv(f, res, method, tim)
+                out[f"io/records/{method}/{int(tim)}"] = _file_bytes(f)
+        # run_experiment on a small GPU-sized problem: manifest + CSV + PGMs
+        spec = rexp.ProblemSpec(kind="ct", name="custom", nx=24, angles=18, det_count=35,
+                                noise_level=0.02, seed=4)
+        solvers = [RCfg(method="ab-hybrid", lambda_strategy="gcv", max_iter=8, name="abg"),
+                   RCfg(method="ba", max_iter=6, stopping_rule="dp", name="badp")]
+        cfg = rexp.ExperimentConfig(spec, solvers, track_metrics=True, image_export_stride=3,
+                                    out_dir=Path(d))
+        for mpath in rexp.run_experiment(cfg):
+            label = json.load(open(mpath))["solver"]
+            out[f"exp/{label}/manifest"] = _file_bytes(mpath)
+            out[f"exp/{label}/csv"] = _file_bytes(os.path.join(d, f"{label}.csv"))
+            out[f"exp/{label}/final_pgm"] = _file_bytes(os.path.join(d, f"{label}_final.pgm"))
+        out["exp/dir"] = np.frombuffer(d.encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "problem_io.npz"), **out)
+    print("problem_io.npz", len(out), "entries")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "solver", "c1", "c2"]
+    which = sys.argv[1:] or ["small", "solver", "c1", "c2", "io"]
+    if "io" in which:
+        make_io()
     if "small" in which:
         make_small()
     if "solver" in which:

@@ -149,3 +149,31 @@ def test_oracle_c1_hybrid_solve_bit_exact(golden):
     dn = np.array([x["data_residual_norm"] for x in r.records])
     np.testing.assert_array_equal(dn, z["rec/data_residual_norm"])
     np.testing.assert_allclose(r.x.astype(np.float32), z["x_final"], rtol=0, atol=0)
+
+
+# ---- row f4: problem generation ---------------------------------------------
+
+def test_oracle_phantom_matches_reference_shepp_logan(golden):
+    d = golden("problem_io")
+    for nx, h in ((64, 2.0 / 64), (33, 0.37), (128, 1.0)):
+        img = O.phantom(nx, nx, h, O.shepp_logan_rows(), scale=0.5 * nx * h)
+        np.testing.assert_array_equal(img, d[f"sl/{nx}"], err_msg=f"{nx}")
+
+
+def test_oracle_make_ct_problem_noise(golden):
+    d = golden("problem_io")
+    b, nn = O.add_noise(d["mk/b_clean"], 0.025, 3)
+    np.testing.assert_array_equal(b, d["mk/b_noisy"])
+    assert nn == float(d["mk/noise_norm"])
+    np.testing.assert_array_equal(
+        O.phantom(32, 32, 2.0 / 32, O.shepp_logan_rows(), scale=0.5 * 32 * (2.0 / 32)),
+        d["mk/x_true"])
+
+
+def test_harness_phantom_is_oracle_phantom():
+    # the bench configs' random-ellipse recipe (problems.py) == the oracle's
+    # ellipse sampler on the same draw, before the fp32 rounding
+    N = 96
+    rows = [(rho, a, b, cx, cy, phi) for cx, cy, a, b, phi, rho in problems.ellipse_params(N, 10, 5)]
+    ref = O.phantom(N, N, 1.0, rows).astype(np.float32).astype(np.float64)
+    np.testing.assert_array_equal(problems.random_ellipse_phantom(N, 10, 5), ref)

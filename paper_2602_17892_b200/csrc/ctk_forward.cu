@@ -198,6 +198,10 @@ __global__ void __launch_bounds__(256) k_stage(const float* __restrict__ x, floa
 }
 
 constexpr int FWD_THREADS = 128;
+#ifndef CTK_FWD_UNROLL
+#define CTK_FWD_UNROLL 16
+#endif
+constexpr int FWD_UNROLL = CTK_FWD_UNROLL;     // rows per unrolled batch of the walk
 
 struct FwdArgs {
     const AngleParams* ap;
@@ -292,7 +296,7 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
     while (k < kW) {
         const int kstop = min(kW, k + 48);
         float s0 = 0.f, s1 = 0.f;
-#pragma unroll 8
+#pragma unroll FWD_UNROLL
         for (; k < kstop; ++k) {
             // 1 + frac as a float from the top 23 fraction bits: no I2F
             const float f1 = __uint_as_float(0x3f800000u | (frac >> 9));
@@ -369,8 +373,15 @@ __device__ __forceinline__ unsigned cluster_addr(const void* p, unsigned rank) {
     return r;
 }
 
+#ifndef CTK_FWD_MINB
+#define CTK_FWD_MINB 8
+#endif
+#ifndef CTK_FWD_DYNSMEM
+#define CTK_FWD_DYNSMEM 0
+#endif
+
 template <bool SPLIT>
-__global__ void __launch_bounds__(FWD_THREADS, 12) k_forward(FwdArgs A) {
+__global__ void __launch_bounds__(FWD_THREADS, CTK_FWD_MINB) k_forward(FwdArgs A) {
     ctk_pdl_trigger();
     const int ai = blockIdx.y * FWD_APB + (threadIdx.x >> 5);
     const int a = A.a0 + ai;
@@ -607,10 +618,11 @@ int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1
     A.split = g->fwd_split;
     dim3 grid((g->det_count + 31) / 32, (a1 - a0 + FWD_APB - 1) / FWD_APB, A.split);
     if (A.split > 1)
-        CTK_CUDA(ctk_launch_pdl(k_forward<true>, grid, dim3(FWD_THREADS), 0, st,
+        CTK_CUDA(ctk_launch_pdl(k_forward<true>, grid, dim3(FWD_THREADS), CTK_FWD_DYNSMEM, st,
                                 dim3(1, 1, (unsigned)A.split), A));
     else
-        CTK_CUDA(ctk_launch_pdl(k_forward<false>, grid, dim3(FWD_THREADS), 0, st, dim3(1, 1, 1), A));
+        CTK_CUDA(ctk_launch_pdl(k_forward<false>, grid, dim3(FWD_THREADS), CTK_FWD_DYNSMEM, st,
+                                dim3(1, 1, 1), A));
     ctk_count_launch();
     ctk_prof_close(ph, st);
     return CTK_OK;

@@ -39,10 +39,10 @@ struct BackArgs {
     const BackParams* bp;
     const float* u;       // row a at u + (a - a0) * D
     const float* x0;      // optional
-    float* out;           // final image (S == 1) or partials [S][n]
-    float* x;             // final image (S > 1)
-    unsigned* cnt;        // S > 1: per-tile arrival tickets (zeroed once)
-    int nx, ny, D, a0, a1, per_split, wmax, split, fbits;
+    float* x;             // output image
+    float* part;          // SPLIT: partial images [S][n]
+    unsigned* cnt;        // SPLIT: per-tile arrival tickets (zeroed once)
+    int nx, ny, D, a0, a1, per_split, wmax, fbits;
     float* stP;           // optional: also write the K1 staged copies of the result
     float* stPT;
     int pad;
@@ -55,8 +55,78 @@ __device__ __forceinline__ void stage_out(const BackArgs& A, int ix, int iy, flo
     A.stPT[(size_t)ix * (A.ny + 2 * A.pad) + iy + A.pad] = v;
 }
 
-template <int PPT>                                 // pixels (rows) per thread
-__global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
+// Stage one 32-angle chunk's detector windows as (p, d) pairs (header).
+// Windows of at most 63 bins (every BASELINE config): warp per angle, the
+// window's v0 values in two coalesced loads per angle, all of a warp's loads
+// issued before the first use (one L2 round trip per chunk instead of one
+// per strided element), v1 = v0 of the next bin by a lane shuffle except at
+// the quirk bin b == -1.  Wider windows take the element loop.
+__device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, const int* s_w0,
+                                              int ac, int na, int tx, int ty) {
+    const int D = A.D, wmax = A.wmax;
+    const int q1 = D > 1 ? 1 : 0;                  // reference quirk tap for i0 == -1
+    if (wmax <= 63) {
+        constexpr int NJ = BCA / BROWS;            // angles per warp
+        float va[NJ], vb[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int ai = ty + j * BROWS;
+            va[j] = vb[j] = 0.f;
+            if (ai < na) {
+                const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
+                const int b = s_w0[ai] + tx, b2 = b + 32;
+                if (b >= 0 && b < D) va[j] = __ldg(row + b);
+                if (b2 >= 0 && b2 < D && tx + 32 <= wmax) vb[j] = __ldg(row + b2);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int ai = ty + j * BROWS;
+            if (ai >= na) break;                   // warp-uniform
+            const float up_a = __shfl_down_sync(0xffffffffu, va[j], 1);
+            const float b_0 = __shfl_sync(0xffffffffu, vb[j], 0);
+            const float up_b = __shfl_down_sync(0xffffffffu, vb[j], 1);
+            const int b = s_w0[ai] + tx;
+            float v1a = tx < 31 ? up_a : b_0, v1b = up_b;
+            const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
+            if (b == -1) v1a = __ldg(row + q1);
+            if (b + 32 == -1) v1b = __ldg(row + q1);
+            float2* dst = win + ai * wmax;
+            float d = v1a - va[j];
+            dst[tx] = make_float2(va[j] - d, d);
+            if (tx + 32 < wmax) {
+                d = v1b - vb[j];
+                dst[tx + 32] = make_float2(vb[j] - d, d);
+            }
+        }
+        return;
+    }
+    for (int ai = ty; ai < na; ai += BROWS) {
+        const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
+        const int w0 = s_w0[ai];
+        float2* dst = win + ai * wmax;
+        for (int i = tx; i < wmax; i += BTX) {
+            const int b = w0 + i;
+            const float v0 = (b >= 0 && b < D) ? __ldg(row + b) : 0.f;
+            const int b1 = b == -1 ? q1 : b + 1;
+            const float v1 = (b >= -1 && b + 1 < D) ? __ldg(row + b1) : 0.f;
+            const float d = v1 - v0;
+            dst[i] = make_float2(v0 - d, d);
+        }
+    }
+}
+
+// SPLIT: the gridDim.z angle splits of a tile write fp32 partial images; the
+// last to arrive (per-tile ticket) sums them in split order and writes the
+// image.  (A cluster/DSMEM variant of this reduction measured faster in
+// isolation but slower inside the solve: its gang-scheduled CTAs wait for
+// whole free GPC slices while the iterate stream's kernels hold SMs.)
+#ifndef CTK_BACK_MINB4
+#define CTK_BACK_MINB4 5
+#endif
+
+template <int PPT, bool SPLIT>                      // pixels (rows) per thread
+__global__ void __launch_bounds__(BTHREADS, PPT == 2 ? 6 : CTK_BACK_MINB4) k_back(BackArgs A) {
     constexpr int BTY = BROWS * PPT;
     extern __shared__ float2 win[];                // [BCA][wmax] (p, d)
     __shared__ int4 s_par[BCA];                    // T0, C, S, smem base of the window
@@ -75,8 +145,7 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
 
     const int aS = A.a0 + blockIdx.z * A.per_split;
     const int aE = min(A.a1, aS + A.per_split);
-    const int D = A.D, wmax = A.wmax;
-    const int q1 = D > 1 ? 1 : 0;                  // reference quirk tap for i0 == -1
+    const int wmax = A.wmax;
     ctk_pdl_trigger();
 
     double acc[PPT];
@@ -102,20 +171,7 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
         }
         __syncthreads();
         ctk_pdl_wait();                            // u comes from the previous kernel
-        // stage the (p, d) windows; zero taps outside [0, D), quirk at b == -1
-        for (int ai = ty; ai < na; ai += BROWS) {
-            const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
-            const int w0 = s_w0[ai];
-            float2* dst = win + ai * wmax;
-            for (int i = tx; i < wmax; i += BTX) {
-                const int b = w0 + i;
-                const float v0 = (b >= 0 && b < D) ? __ldg(row + b) : 0.f;
-                const int b1 = b == -1 ? q1 : b + 1;
-                const float v1 = (b >= -1 && b + 1 < D) ? __ldg(row + b1) : 0.f;
-                const float d = v1 - v0;
-                dst[i] = make_float2(v0 - d, d);
-            }
-        }
+        stage_windows(A, win, s_w0, ac, na, tx, ty);
         __syncthreads();
         float sp[PPT];
 #pragma unroll
@@ -139,11 +195,11 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
         for (int r = 0; r < PPT; ++r) acc[r] += (double)sp[r];
         __syncthreads();
     }
-    const size_t n = (size_t)A.nx * A.ny;
-    if (A.split) {
-        // angle split: the last of the gridDim.z CTAs of this tile sums the
-        // partial images in split order (deterministic) and adds x0.
-        float* part = A.out;
+    if (SPLIT) {
+        // global partial images + per-tile arrival tickets: the last of the
+        // gridDim.z CTAs of a tile sums the partials in split order
+        const size_t n = (size_t)A.nx * A.ny;
+        float* part = A.part;
         const bool inx = ix < A.nx;
 #pragma unroll
         for (int r = 0; r < PPT; ++r) {
@@ -158,30 +214,27 @@ __global__ void __launch_bounds__(BTHREADS) k_back(BackArgs A) {
         __syncthreads();
         if (!s_last) return;
         __threadfence();
-        if (inx) {
-            for (int r = 0; r < PPT; ++r) {
-                const int iy = iy0 + ty + r * BROWS;
-                if (iy >= A.ny) continue;
-                const size_t o = (size_t)iy * A.nx + ix;
-                double t = 0.0;
-                for (unsigned z = 0; z < gridDim.z; ++z) t += (double)__ldcg(part + z * n + o);
-                const float v = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * t);
-                A.x[o] = v;
-                if (A.stP) stage_out(A, ix, iy, v);
-            }
-        }
         if (tid == 0) *ticket = 0u;
-    } else {
-        if (ix >= A.nx) return;
+        if (!inx) return;
 #pragma unroll
         for (int r = 0; r < PPT; ++r) {
             const int iy = iy0 + ty + r * BROWS;
-            if (iy >= A.ny) continue;
-            const size_t o = (size_t)iy * A.nx + ix;
-            const float v = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * acc[r]);
-            A.out[o] = v;
-            if (A.stP) stage_out(A, ix, iy, v);
+            double t = 0.0;
+            if (iy < A.ny)
+                for (unsigned z = 0; z < gridDim.z; ++z)
+                    t += (double)__ldcg(part + z * n + (size_t)iy * A.nx + ix);
+            acc[r] = t;
         }
+    }
+    if (ix >= A.nx) return;
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) {
+        const int iy = iy0 + ty + r * BROWS;
+        if (iy >= A.ny) continue;
+        const size_t o = (size_t)iy * A.nx + ix;
+        const float v = (float)((A.x0 ? (double)A.x0[o] : 0.0) + A.h * acc[r]);
+        A.x[o] = v;
+        if (A.stP) stage_out(A, ix, iy, v);
     }
 }
 
@@ -212,6 +265,7 @@ static int64_t back_tiles(const ctk_geom* g) {
     return (int64_t)((g->nx + BTX - 1) / BTX) * back_tiles_y(g);
 }
 
+// Split reduction: S partial images + one arrival ticket per tile.
 extern "C" int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1) {
     if (!g || a0 < 0 || a1 > g->n_angles || a0 >= a1) return 0;
     const int S = back_splits(g, a0, a1);
@@ -241,15 +295,16 @@ int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
         return CTK_OK;
     }
     const int S = back_splits(g, a0, a1);
-    if (S > 1 && !work) return ctk_fail(CTK_ERR_ARG, "ctk_back needs %lld work floats",
-                                        (long long)S * (long long)n);
+    if (S > 1 && !work)
+        return ctk_fail(CTK_ERR_ARG, "ctk_back needs %lld work floats",
+                        (long long)ctk_back_work_floats(g, a0, a1));
     BackArgs A;
+    A.part = S > 1 ? work : nullptr;
+    A.cnt = S > 1 ? reinterpret_cast<unsigned*>(work + (size_t)S * g->nx * g->ny) : nullptr;
     A.bp = g->d_bp;
     A.u = u;
     A.x0 = x0;
-    A.out = S > 1 ? work : x;
     A.x = x;
-    A.cnt = S > 1 ? reinterpret_cast<unsigned*>(work + (size_t)S * n) : nullptr;
     A.nx = g->nx;
     A.ny = g->ny;
     A.D = g->det_count;
@@ -265,19 +320,19 @@ int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
         while ((1 << I) <= g->back_wmax + 1) ++I;
         A.fbits = 32 - I;
     }
-    A.split = S > 1;
     A.h = g->h;
     A.xmin = g->xmin;
     A.ymax = g->ymax;
     A.center = g->center;
     dim3 grid((g->nx + BTX - 1) / BTX, back_tiles_y(g), S), block(BTX, BROWS);
-    const size_t smem = (size_t)BCA * g->back_wmax * sizeof(float2);
     const bool p4 = g->back_ppt == 4;
+    size_t smem = (size_t)BCA * g->back_wmax * sizeof(float2);
+    void (*kern)(BackArgs) = S > 1 ? (p4 ? k_back<4, true> : k_back<2, true>)
+                                   : (p4 ? k_back<4, false> : k_back<2, false>);
     if (smem > 48 * 1024)
-        CTK_CUDA(cudaFuncSetAttribute(p4 ? k_back<4> : k_back<2>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int ph = ctk_prof_open(1, st);
-    CTK_CUDA(ctk_launch_pdl(p4 ? k_back<4> : k_back<2>, grid, block, smem, st, dim3(1, 1, 1), A));
+    CTK_CUDA(ctk_launch_pdl(kern, grid, block, smem, st, dim3(1, 1, 1), A));
     ctk_count_launch();
     ctk_prof_close(ph, st);
     return CTK_OK;

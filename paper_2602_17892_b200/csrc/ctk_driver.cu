@@ -100,7 +100,10 @@ Pool& pool() {
     static Pool p([] {
         unsigned n = std::thread::hardware_concurrency();
         int w = n > 2 ? (int)n - 1 : 2;
-        return w > 8 ? 8 : w;
+        w = w > 8 ? 8 : w;
+        const char* e = getenv("CTK_POOL_THREADS");        // tuning override
+        if (e && atoi(e) > 0) w = atoi(e);
+        return w;
     }());
     return p;
 }

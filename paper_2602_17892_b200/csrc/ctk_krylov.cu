@@ -692,6 +692,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    ctk_pdl_wait();                  // q (and, transitively, the basis) from the previous kernels
     if (threadIdx.x < 32 && row_bytes > 0) {
         if (threadIdx.x == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a),
@@ -889,9 +890,22 @@ static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int pas
     ctk_stage_dst sd = {};
     if (sdp && sdp->P && (int64_t)sdp->nx * sdp->ny == L) sd = *sdp;
     int stat_off = (int)(stat - h);
-    void* args[] = {&W, &ld, &k, &L, &q, &passes, &chunk, &h, &stat, &partial, &sd, &hm, &stat_off};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_gs_smem, dim3((unsigned)G),
-                                                dim3(ST), args, smem, st);
+    // cooperative (grid barriers) and programmatic: the launch and the
+    // prologue overlap the producer of q (K2 / K1), which triggers at entry
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(ST);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_gs_smem, W, ld, k, L, (const float*)q, passes, chunk,
+                                       h, stat, partial, sd, hm, stat_off);
     ctk_count_launch();
     if (e != cudaSuccess) return ctk_check_cuda(e, "k_gs_smem");
     *done = true;

@@ -286,11 +286,12 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
     // MIRROR keeps q negated so both directions advance with add-with-carry
     int q = kw * pitch + (MIRROR ? C - 1 - c0 + pad : c0 + pad);
     if (MIRROR) q = -q;
-    // Second-tap weight wb = max(0, f + sigma - 1) * Lx, the length the row
-    // spends past the grid line (0 when it does not reach it); wa = L - wb.
-    // With f1 = 1 + f:  wb = max(0, f1 * Lx + (sigma - 2) * Lx).
-    const float L = p.L, Lx = p.Lx;
-    const float off = (float)(((double)Sg * (1.0 / 4294967296.0) - 2.0) * (double)p.Lx);
+    // Second-tap length wb = max(0, f + sigma - 1) * Lx, the part of the row
+    // past the grid line (0 when it does not reach it), and wa = L - wb, so
+    //   wa v0 + wb v1 = L v0 + Lx w (v1 - v0),  w = sat(f1 + (sigma - 2)),
+    // f1 = 1 + f (w < sigma <= 1: the saturation only clamps at 0).  Per row:
+    // frac add + carry, address, two taps, 1 + f, FADD.SAT, and the two sums.
+    const float sm2 = (float)((double)Sg * (1.0 / 4294967296.0) - 2.0);
     double acc = 0.0;
     int k = kw;
     while (k < kW) {
@@ -300,19 +301,18 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
         for (; k < kstop; ++k) {
             // 1 + frac as a float from the top 23 fraction bits: no I2F
             const float f1 = __uint_as_float(0x3f800000u | (frac >> 9));
-            const float wb = fmaxf(fmaf(f1, Lx, off), 0.f);
-            const float wa = L - wb;
-            const float* pp = MIRROR ? base - q : base + q;
+            const float w = __saturatef(f1 + sm2);
+            const float* pp = base + (MIRROR ? -(long long)q : (long long)q);
             const float v0 = __ldg(pp);
             const float v1 = __ldg(pp + (MIRROR ? -1 : 1));
-            s0 = fmaf(wa, v0, s0);
-            s1 = fmaf(wb, v1, s1);
+            s0 += v0;
+            s1 = fmaf(w, v1 - v0, s1);
             // frac += sigma; the carry moves the pair one column (row split)
             // (MIRROR: -q_pos advances by -pitch + carry)
             asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;"
                 : "+r"(frac), "+r"(q) : "r"(Sf), "r"(MIRROR ? -pitch : pitch));
         }
-        acc += (double)s0 + (double)s1;
+        acc += (double)p.L * (double)s0 + (double)p.Lx * (double)s1;
     }
     return acc;
 }

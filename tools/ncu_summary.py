@@ -45,7 +45,8 @@ for r in rows[2:]:
 open(out_txt, "w").write("\n".join(lines) + "\n")
 js = {"source": title}
 for name, lst in agg.items():
-    key = {"k_forward<1>": "forward", "k_forward<0>": "forward", "k_back": "back"}.get(name.replace("ctk::", ""), name)
+    base = name.replace("ctk::", "").split("<")[0]
+    key = {"k_forward": "forward", "k_back": "back"}.get(base, name)
     dr = [x["dram_rd"] + x["dram_wr"] for x in lst if isinstance(x["dram_rd"], float)]
     tm = [x["time_us"] for x in lst if isinstance(x["time_us"], float)]
     js[key] = {"kernel": name, "launches_captured": len(lst),

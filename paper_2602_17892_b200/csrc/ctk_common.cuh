@@ -154,6 +154,9 @@ int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes,
                    double* stat, void* scratch, void* stream, const ctk_stage_dst* sd,
                    double* h_mirror);
 bool ctk_gs_smem_ok(int64_t L, int k);
+// Streamed path (long vectors): also leaves q untouched and takes the stage /
+// host-mirror outputs.  False whenever the SMEM path applies.
+bool ctk_gs_stream_ok(int64_t L, int k);
 int ctk_combine_pair(const float* X, int64_t ldx, const float* x0, float* x, int64_t Lx,
                      double* n_x, const float* AX, int64_t ldax, const float* d0, float* r,
                      int64_t Lr, double* n_r, int k, const double* y, void* scratch,

@@ -19,6 +19,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "ctk_common.cuh"
 
 namespace ctk {
@@ -790,6 +793,299 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Streamed Gram-Schmidt step for Krylov vectors too long for the SMEM-resident
+// path (c4: L = 2.1M, c5: L = 4.2M).  One cooperative CTA per SM owns a
+// contiguous run of TW-float tiles; every sweep streams the k+1 basis rows
+// and one vector of its tiles through a double-buffered shared-memory ring
+// filled by bulk async copies (one mbarrier per buffer, issued by warp 0), so
+// the basis is read from HBM once per sweep with a whole tile in flight while
+// the other is consumed:
+//   A: h1 = W^T q, ||q||^2                                   | grid barrier
+//   B: q1 = q - W h1 -> row k+1; h2 = W^T q1 (q1 from SMEM)  | grid barrier  (passes == 2)
+//   C: q2 = q1 - W h2 -> row k+1, ||q2||^2                   | grid barrier
+//   scale row k+1 by 1/||q2|| (+ the K1 staged copies, host-mapped column)
+// Three reads of the basis instead of the register-streamed kernel's four,
+// and the input q is never written (AB keeps A B w_j without a copy).
+// Every CTA reduces the chunk partials in the same fixed order.
+// ---------------------------------------------------------------------------
+constexpr int TS_RPW = 8;                        // dot rows per warp: 16 warps x 8 = 128
+constexpr int TS_MAXROWS = SW * TS_RPW;          // basis rows + the vector row
+#ifndef CTK_TS_NBUF
+#define CTK_TS_NBUF 4
+#endif
+constexpr int TS_NBUF = CTK_TS_NBUF;             // ring depth: tiles in flight while one is consumed
+
+// Ring slot b: buffer ring + b (rows) tw floats, mbarrier bar0 + 8 b.
+struct TsRing {
+    float* ring;
+    unsigned bar0;
+    int stride;                                  // floats per slot: (nb + 1) * tw
+    __device__ float* buf(int b) const { return ring + (size_t)b * stride; }
+    __device__ unsigned bar(int b) const { return bar0 + 8u * (unsigned)b; }
+};
+
+// Thread 0: queue tile e0 of basis rows 0..nb-1 (one 2-D tensor box of
+// tw x nb floats) plus the same tile of the vector (a tw x 1 box, row nb of
+// the slot) into ring slot b.  Out-of-range columns of the last tile are
+// zero-filled by the TMA unit and still count toward the transaction bytes.
+__device__ __forceinline__ void ts_issue(const TsRing& R, int b, int tw, int nb,
+                                         const CUtensorMap* tmW, const CUtensorMap* tmV,
+                                         int64_t e0) {
+    const unsigned bar = R.bar(b);
+    const unsigned bytes = (unsigned)(tw * (nb + 1) * 4);
+    float* dst = R.buf(b);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmW)), "r"((int)e0), "r"(0), "r"(bar)
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst + (size_t)nb * tw)),
+        "l"(reinterpret_cast<uint64_t>(tmV)), "r"((int)e0), "r"(0), "r"(bar)
+        : "memory");
+}
+
+// acc[r] += <row (warp + SW r), vector row> over one tile (fp64 products).
+__device__ __forceinline__ void ts_dots(const float* tile, int tw, int nrows, int vrow, int cn,
+                                        double* acc) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fpl = tw >> 5;                     // floats per lane (4 or 8)
+    const float* vr = tile + (size_t)vrow * tw;
+#pragma unroll
+    for (int c4 = 0; c4 < 2; ++c4) {
+        const int e = lane * fpl + c4 * 4;
+        if (c4 * 4 >= fpl || e >= cn) break;
+        const float4 v = *reinterpret_cast<const float4*>(vr + e);
+        const double v0 = v.x, v1 = v.y, v2 = v.z, v3 = v.w;
+#pragma unroll
+        for (int r = 0; r < TS_RPW; ++r) {
+            const int j = warp + SW * r;
+            if (j < nrows) {
+                const float4 w = *reinterpret_cast<const float4*>(tile + (size_t)j * tw + e);
+                double a = acc[r];
+                a = fma((double)w.x, v0, a);
+                a = fma((double)w.y, v1, a);
+                a = fma((double)w.z, v2, a);
+                a = fma((double)w.w, v3, a);
+                acc[r] = a;
+            }
+        }
+    }
+}
+
+// out[e] = vector[e] - sum_j c[j] W_j[e] over one tile: the ST threads split
+// the rows into ST / tw groups whose fp64 partials meet in red[] and are
+// summed in group order.  The rounded result goes to dst (global) and, when
+// keep, back into the tile's vector row.  Returns this thread's ||out||^2 part.
+__device__ __forceinline__ double ts_update(float* tile, int tw, int nb, const double* c, int cn,
+                                            float* dst, bool keep, double* red) {
+    const int ng = ST / tw;
+    const int g = threadIdx.x / tw, e = threadIdx.x - g * tw;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;       // four independent chains
+    if (e < cn) {
+        const float* col = tile + e;
+        int j = g;
+        for (; j + 3 * ng < nb; j += 4 * ng) {
+            a0 = fma(c[j], (double)col[(size_t)j * tw], a0);
+            a1 = fma(c[j + ng], (double)col[(size_t)(j + ng) * tw], a1);
+            a2 = fma(c[j + 2 * ng], (double)col[(size_t)(j + 2 * ng) * tw], a2);
+            a3 = fma(c[j + 3 * ng], (double)col[(size_t)(j + 3 * ng) * tw], a3);
+        }
+        for (; j < nb; j += ng) a0 = fma(c[j], (double)col[(size_t)j * tw], a0);
+    }
+    red[threadIdx.x] = (a0 + a1) + (a2 + a3);
+    __syncthreads();
+    double nrm = 0.0;
+    if (g == 0 && e < cn) {
+        double t = 0.0;
+        for (int q = 0; q < ng; ++q) t += red[q * tw + e];
+        const float o = (float)((double)tile[(size_t)nb * tw + e] - t);
+        dst[e] = o;
+        if (keep) tile[(size_t)nb * tw + e] = o;
+        nrm = (double)o * (double)o;
+    }
+    __syncthreads();
+    return nrm;
+}
+
+struct TsMaps {
+    CUtensorMap W;          // rows 0..k of the basis, box tw x (k+1)
+    CUtensorMap q;          // the input vector, box tw x 1
+    CUtensorMap wn;         // row k+1 (q1 after sweep B), box tw x 1
+};
+
+__global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k, int64_t L,
+                                                     const float* __restrict__ q, int passes,
+                                                     int tw, double* h, double* stat,
+                                                     double* partial, ctk_stage_dst sd,
+                                                     double* hm, int stat_off,
+                                                     const __grid_constant__ TsMaps tm) {
+    cg::grid_group grid = cg::this_grid();
+    ctk_pdl_trigger();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int nb = k + 1;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                 // [TS_NBUF]
+    double* h1 = reinterpret_cast<double*>(smem_raw + 8 * TS_NBUF);         // [nb + 1]
+    double* h2 = h1 + (nb + 1);                                             // [nb + 1]
+    double* red = h2 + (nb + 1);                                            // [ST]
+    // ring slots: 128-B aligned for the tensor copies
+    unsigned char* ring_raw = smem_raw + 8 * TS_NBUF + sizeof(double) * (2 * (size_t)nb + 2 + ST);
+    ring_raw += (128u - (smem_u32(ring_raw) & 127u)) & 127u;
+    float* ring = reinterpret_cast<float*>(ring_raw);
+    TsRing R;
+    R.ring = ring;
+    R.bar0 = smem_u32(bars);
+    R.stride = (nb + 1) * tw;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < TS_NBUF; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(R.bar(b)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    ctk_pdl_wait();                  // q (and, transitively, the basis) from the previous kernels
+
+    const int64_t ntiles = (L + tw - 1) / tw;
+    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * per, t1 = min(ntiles, t0 + per);
+    const int nt = t1 > t0 ? (int)(t1 - t0) : 0;
+    float* wnext = W + (size_t)(k + 1) * ld;
+    double* P1 = partial;                                    // [nb + 1][G]
+    double* P2 = P1 + (size_t)(nb + 1) * gridDim.x;          // [nb + 1][G]
+    double* P3 = P2 + (size_t)(nb + 1) * gridDim.x;          // [G]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    // One sweep over this CTA's tiles.  mode 0: dots with the vector (row nb,
+    // + its norm); 1: update -> wnext, then dots with the result; 2: update ->
+    // wnext and its norm.
+    // The ring runs continuously across sweeps: tile number g (counted from
+    // the kernel's first) uses slot g % TS_NBUF at mbarrier phase (g / TS_NBUF) & 1.
+    int gbase = 0;
+    auto sweep = [&](int mode, const CUtensorMap* vmap, const double* coef, double* P) -> double {
+        double acc[TS_RPW];
+#pragma unroll
+        for (int r = 0; r < TS_RPW; ++r) acc[r] = 0.0;
+        double nrm = 0.0;
+        if (threadIdx.x == 0)
+            for (int i = 0; i < TS_NBUF && i < nt; ++i)
+                ts_issue(R, (gbase + i) % TS_NBUF, tw, nb, &tm.W, vmap, (t0 + i) * tw);
+        for (int i = 0; i < nt; ++i) {
+            const int g = gbase + i, b = g % TS_NBUF;
+            const int64_t e0 = (t0 + i) * tw;
+            const int cn = (int)min((int64_t)tw, L - e0);
+            mbar_wait(R.bar(b), (unsigned)(g / TS_NBUF) & 1u);
+            float* tile = R.buf(b);
+            if (mode == 0) {
+                ts_dots(tile, tw, nb + 1, nb, cn, acc);
+            } else {
+                nrm += ts_update(tile, tw, nb, coef, cn, wnext + e0, mode == 1, red);
+                if (mode == 1) ts_dots(tile, tw, nb, nb, cn, acc);
+            }
+            __syncthreads();                     // everyone is done with slot b
+            if (threadIdx.x == 0 && i + TS_NBUF < nt)
+                ts_issue(R, b, tw, nb, &tm.W, vmap, (t0 + i + TS_NBUF) * tw);
+        }
+        gbase += nt;
+        if (mode != 2) {
+            const int rows = mode == 0 ? nb + 1 : nb;
+#pragma unroll
+            for (int r = 0; r < TS_RPW; ++r) {
+                const double t = warp_sum(acc[r]);
+                const int j = warp + SW * r;
+                if (lane == 0 && j < rows) P[(size_t)j * gridDim.x + blockIdx.x] = t;
+            }
+        }
+        return nrm;
+    };
+
+    sweep(0, &tm.q, nullptr, P1);                            // h1 = W^T q, ||q||^2
+    grid.sync();
+    all_reduce_rows(P1, nb + 1, h1);
+    __syncthreads();
+    const double* cfin = h1;
+    const CUtensorMap* vfin = &tm.q;
+    if (passes == 2) {
+        sweep(1, &tm.q, h1, P2);                             // q1 -> wnext, h2 = W^T q1
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // q1: generic writes, bulk reads
+        grid.sync();
+        all_reduce_rows(P2, nb, h2);
+        __syncthreads();
+        cfin = h2;
+        vfin = &tm.wn;
+    }
+    double nrm = sweep(2, vfin, cfin, nullptr);              // q2 -> wnext, ||q2||^2
+    nrm = warp_sum(nrm);
+    if (lane == 0) red[warp] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < SW; ++w) t += red[w];
+        P3[blockIdx.x] = t;
+    }
+    grid.sync();
+    __shared__ double s_n2;
+    if (threadIdx.x < 32) all_reduce_rows(P3, 1, &s_n2);
+    __syncthreads();
+    const double hk = sqrt(s_n2);
+    const double qn = sqrt(h1[nb]);
+    const bool broke = hk <= 1e-14 * qn;                     // BREAKDOWN_RTOL, arnoldi.py:17,80
+    const float sc = (float)(broke ? 0.0 : 1.0 / hk);
+    if (!sd.P) {
+        if (nt > 0) {
+            const int64_t e0 = t0 * tw, e1 = min(L, t1 * tw);
+            for (int64_t i = e0 + threadIdx.x; i < e1; i += ST) wnext[i] *= sc;
+        }
+    } else {
+        // Scale and stage w_{k+1} for the next K1 apply by 32 x 32 image tiles
+        // (each tile owned by one CTA): coalesced P rows, and the transposed
+        // copy PT through a shared-memory tile instead of strided stores.
+        float (*tr)[33] = reinterpret_cast<float (*)[33]>(ring);
+        const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;      // 32 x 16
+        const int tnx = (sd.nx + 31) >> 5, tny = (sd.ny + 31) >> 5;
+        const int pP = sd.nx + 2 * sd.pad, pT = sd.ny + 2 * sd.pad;
+        for (int t = blockIdx.x; t < tnx * tny; t += gridDim.x) {
+            const int bx = (t % tnx) << 5, by = (t / tnx) << 5;
+            for (int r = ty; r < 32; r += SW) {
+                const int iy = by + r, ix = bx + tx;
+                float v = 0.f;
+                if (iy < sd.ny && ix < sd.nx) {
+                    const size_t o = (size_t)iy * sd.nx + ix;
+                    v = wnext[o] * sc;
+                    wnext[o] = v;
+                    sd.P[(size_t)iy * pP + ix + sd.pad] = v;
+                }
+                tr[r][tx] = v;
+            }
+            __syncthreads();
+            for (int r = ty; r < 32; r += SW) {
+                const int ix = bx + r, iy = by + tx;
+                if (ix < sd.nx && iy < sd.ny) sd.PT[(size_t)ix * pT + iy + sd.pad] = tr[tx][r];
+            }
+            __syncthreads();
+        }
+    }
+    if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i <= k; i += ST) {
+            const double v = passes == 2 ? h1[i] + h2[i] : h1[i];
+            h[i] = v;
+            if (hm) hm[i] = v;
+        }
+        if (threadIdx.x == 0) {
+            const double st4[4] = {qn, broke ? 1.0 : 0.0, broke ? 0.0 : 1.0 / hk, hk};
+            h[k + 1] = hk;
+            for (int c = 0; c < 4; ++c) stat[c] = st4[c];
+            if (hm) {
+                hm[k + 1] = hk;
+                for (int c = 0; c < 4; ++c) hm[stat_off + c] = st4[c];
+            }
+        }
+    }
+}
+
 }  // namespace ctk
 
 using namespace ctk;
@@ -813,12 +1109,15 @@ static int try_cgs2_fused(float* W, int64_t ld, int k, int64_t L, float* q, doub
     }
     if (coop != 1 || per_sm < 1 || k + 2 > 512) return CTK_OK;
     int64_t G = ((L >> 2) + FT - 1) / FT;            // >= one float4 per thread
-    static int cap = -1;
+    static int cap = -1, mult = 1;
     if (cap < 0) {
         const char* e = getenv("CTK_FUSED_CTAS");
         cap = e ? atoi(e) : 0;
+        const char* m = getenv("CTK_FUSED_PER_SM");      // tuning override (CTAs per SM)
+        mult = m && atoi(m) > 0 ? atoi(m) : 1;
+        if (mult > per_sm) mult = per_sm;
     }
-    if (G > (int64_t)sms) G = sms;
+    if (G > (int64_t)sms * mult) G = (int64_t)sms * mult;
     if (cap > 0 && G > cap) G = cap;
     if (G < 1) G = 1;
     double* red = s.tmp;
@@ -916,6 +1215,111 @@ bool ctk_gs_smem_ok(int64_t L, int k) {
     int64_t G, chunk;
     size_t smem;
     return gs_smem_plan(L, k, &G, &chunk, &smem);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) !=
+                cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        cudaGetLastError();
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// fp32 2-D map over `rows` rows of length L (pitch ld floats), box tw x rows.
+static bool encode_rows(CUtensorMap* m, const float* base, int64_t L, int64_t ld, int rows, int tw) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)L, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+    cuuint32_t box[2] = {(cuuint32_t)tw, (cuuint32_t)rows};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Streamed path: L a multiple of 4 (16-B row pitch of q), at most TS_MAXROWS
+// rows, two ring buffers of the widest tile (256 or 128 floats) that fit.
+static size_t gs_stream_bytes(int k, int tw) {
+    const int nb = k + 1;
+    const size_t head = 8 * TS_NBUF + sizeof(double) * (2 * (size_t)nb + 2 + ST) + 128;
+    return head + TS_NBUF * sizeof(float) * (size_t)(nb + 1) * tw;
+}
+
+static bool gs_stream_plan(int64_t L, int k, int* twp, size_t* smemp, int* Gp) {
+    static int coop = -1, sms = 0;
+    if (coop < 0) {
+        const char* off = getenv("CTK_NO_STREAM_GS");
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaFuncSetAttribute(k_gs_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SMEM_LIMIT) != cudaSuccess)
+            coop = 0;
+        cudaGetLastError();
+        if (off && off[0] == '1') coop = 0;
+    }
+    if (coop != 1 || k < 0 || (L & 3) || k + 2 > TS_MAXROWS || sms > GS_MAXG) return false;
+    if (L >= (1LL << 31) || !tensor_map_encoder()) return false;   // 32-bit TMA coordinates
+    if (L < (int64_t)sms * 1024) return false;           // short vectors: SMEM / fused paths
+    for (int tw = 256; tw >= 128; tw >>= 1) {         // ts_dots: 4 or 8 floats per lane
+        const size_t smem = gs_stream_bytes(k, tw);
+        if (smem <= SMEM_LIMIT) {
+            *twp = tw;
+            *smemp = smem;
+            *Gp = sms;
+            return true;
+        }
+    }
+    return false;
+}
+
+bool ctk_gs_stream_ok(int64_t L, int k) {
+    int tw, G;
+    size_t smem;
+    return !ctk_gs_smem_ok(L, k) && gs_stream_plan(L, k, &tw, &smem, &G);
+}
+
+static int try_gs_stream(float* W, int64_t ld, int k, int64_t L, const float* q, int passes,
+                         double* h, double* stat, Scratch s, cudaStream_t st,
+                         const ctk_stage_dst* sdp, double* hm, bool* done) {
+    *done = false;
+    int tw, G;
+    size_t smem;
+    if (!gs_stream_plan(L, k, &tw, &smem, &G)) return CTK_OK;
+    if ((size_t)(2 * k + 5) * G > (size_t)MAXCH * (size_t)(k + 3)) return CTK_OK;
+    ctk_stage_dst sd = {};
+    if (sdp && sdp->P && (int64_t)sdp->nx * sdp->ny == L) sd = *sdp;
+    const int stat_off = (int)(stat - h);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(ST);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    TsMaps tm;
+    if (!encode_rows(&tm.W, W, L, ld, k + 1, tw) || !encode_rows(&tm.q, q, L, L, 1, tw) ||
+        !encode_rows(&tm.wn, W + (size_t)(k + 1) * ld, L, ld, 1, tw))
+        return CTK_OK;                                   // no TMA encoder: other paths
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_gs_stream, W, ld, k, L, q, passes, tw, h, stat,
+                                       s.partial, sd, hm, stat_off, tm);
+    ctk_count_launch();
+    if (e != cudaSuccess) return ctk_check_cuda(e, "k_gs_stream");
+    *done = true;
+    return CTK_OK;
 }
 
 static int check_vec(const void* p, const char* what) {
@@ -1063,6 +1467,8 @@ int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes,
     if (passes != 1 && passes != 2) return ctk_fail(CTK_ERR_ARG, "passes must be 1 or 2");
     bool fused = false;
     if ((rc = try_gs_smem(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, &fused))) return rc;
+    if (fused) return CTK_OK;
+    if ((rc = try_gs_stream(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, &fused))) return rc;
     if (fused) return CTK_OK;
     if (passes == 2 && (rc = try_cgs2_fused(W, ld, k, L, q, h, stat, s, st, &fused))) return rc;
     if (fused) return CTK_OK;

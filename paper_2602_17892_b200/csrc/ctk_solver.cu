@@ -106,7 +106,9 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
     const float* pre_w = nullptr;                          // GS input when q is not copied
     ctk_stage_dst sd = {stage_work, stage_work + (size_t)g->ny * (g->nx + 2 * g->fwd_pad),
                         g->nx, g->ny, g->fwd_pad};
-    const bool gs_smem = ctk_gs_smem_ok(L, j);
+    // both single-launch Gram-Schmidt paths leave q untouched, stage w_{j+1}
+    // for K1 and write the host-mapped column
+    const bool gs_smem = ctk_gs_smem_ok(L, j) || ctk_gs_stream_ok(L, j);
     if (ab) {   // q = A (B w); keep B w_j (aux1) and A B w_j (aux2) for the iterates
         float* bw = aux1 ? aux1 + (size_t)j * ld1 : tmp;
         float* abw = aux2 ? aux2 + (size_t)j * ld2 : q;
@@ -121,7 +123,7 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
         if (aux2 && gs_smem) pre_w = abw;
     } else {    // q = B (A w); keep A w_j (aux1)
         float* aw = aux1 ? aux1 + (size_t)j * ld1 : tmp;
-        const bool pre = j > 0 && ctk_gs_smem_ok(L, j - 1);
+        const bool pre = j > 0 && (ctk_gs_smem_ok(L, j - 1) || ctk_gs_stream_ok(L, j - 1));
         if ((rc = ctk_forward_ex(g, w, aw, 0, na, nullptr, stage_work, pre, stream))) return rc;
         if ((rc = ctk_back(g, aw, q, 0, na, nullptr, back_work, stream))) return rc;
     }

@@ -20,7 +20,11 @@ def basis_with(torch, Q, rows):
 
 
 @pytest.mark.parametrize("L,k", [(1000, 0), (4099, 5), (65536, 80), (130680, 30), (262147, 63),
-                                 (1048576, 3), (2086560, 1), (4194309, 6)])
+                                 (1048576, 3), (2086560, 1), (4194309, 6),
+                                 # streamed path: 256-float tiles (c4 / c5 sizes, last c4
+                                 # step), 128-float tiles, ragged last tile and CTA ranges
+                                 (2086560, 40), (2086560, 100), (4194304, 20), (1048576, 120),
+                                 (600004, 9)])
 def test_cgs2_step_matches_fp64_mgs(cuda, L, k):
     torch = cuda
     rng = np.random.default_rng(L + k)
@@ -111,3 +115,26 @@ def test_reductions_are_bitwise_deterministic(cuda):
         B.dots(k + 1, v, d, True, torch.cuda.current_stream())
         outs.append(d.cpu().numpy())
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("L,k", [(2086560, 30), (65536, 20)])
+def test_single_pass_gram_schmidt(cuda, L, k):
+    """reorthogonalize=False: one classical pass (streamed and SMEM paths)."""
+    torch = cuda
+    rng = np.random.default_rng(k)
+    Q, _ = np.linalg.qr(rng.standard_normal((L, k + 1)))
+    Q = Q.astype(np.float32).astype(np.float64)
+    q = rng.standard_normal(L).astype(np.float32).astype(np.float64)
+    B = basis_with(torch, Q, k + 3)
+    qd = torch.from_numpy(q.astype(np.float32)).cuda()
+    h = torch.zeros(k + 8, dtype=torch.float64, device="cuda")
+    stat = torch.zeros(4, dtype=torch.float64, device="cuda")
+    B.gs_step(k, qd, 1, h, stat, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    c = Q.T @ q
+    v = q - Q @ c
+    hg = h.cpu().numpy()[: k + 2]
+    np.testing.assert_allclose(hg[: k + 1], c, rtol=1e-5, atol=1e-6 * np.abs(c).max())
+    assert hg[k + 1] == pytest.approx(np.linalg.norm(v), rel=1e-5)
+    w = B.W[k + 1, :L].cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(w, v / np.linalg.norm(v), atol=2e-6)

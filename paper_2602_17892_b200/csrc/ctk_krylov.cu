@@ -812,9 +812,9 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
 constexpr int TS_RPW = 8;                        // dot rows per warp: 16 warps x 8 = 128
 constexpr int TS_MAXROWS = SW * TS_RPW;          // basis rows + the vector row
 #ifndef CTK_TS_NBUF
-#define CTK_TS_NBUF 4
+#define CTK_TS_NBUF 2
 #endif
-constexpr int TS_NBUF = CTK_TS_NBUF;             // ring depth: tiles in flight while one is consumed
+constexpr int TS_NBUF = CTK_TS_NBUF;             // ring depth (2: deeper rings measured slower at c4/c5)
 
 // Ring slot b: buffer ring + b (rows) tw floats, mbarrier bar0 + 8 b.
 struct TsRing {

@@ -243,6 +243,30 @@ size_t ctk_metrics_scratch_bytes(void);
 int ctk_metrics(const float* x, const float* x_true, int nx, int ny, double dyn_range,
                 double* out, void* scratch, void* stream);
 
+/* ---- Angle-sharded B with the partial-image sum exchanged over peer memory
+ * (SURVEY row e, N1; ctk_exchange.cu).  Replaces back_partial + all-reduce
+ * of the sharded driver: each rank's K2 pushes its finished tiles into the
+ * tile owner's receive buffer (owner = tile mod nranks; NVLink peer stores),
+ * the owner sums them in rank order and delivers the tile to every rank.
+ * The exchange owns its buffers (receive [nranks][n], result image [n],
+ * flags); peers map them with CUDA IPC (export / connect_ipc) or, in one
+ * process, connect with raw pointers (connect_ptrs).  At most 8 ranks. */
+typedef struct ctk_xchg ctk_xchg_t;
+int ctk_xchg_create(const ctk_geom_t* g, int rank, int nranks, ctk_xchg_t** out);
+int ctk_xchg_destroy(ctk_xchg_t* x);
+int ctk_xchg_local(const ctk_xchg_t* x, float** recv, float** img, unsigned** flags);
+size_t ctk_xchg_handle_bytes(void);
+int ctk_xchg_export(const ctk_xchg_t* x, void* handles);
+int ctk_xchg_connect_ipc(ctk_xchg_t* x, const void* handles);
+int ctk_xchg_connect_ptrs(ctk_xchg_t* x, float* const* recv, float* const* img,
+                          unsigned* const* flags);
+/* img (every rank) = sum over ranks of B_rank u_rank; g = this rank's angle
+ * subset.  phases: bit 0 compute + push, bit 1 reduce owned tiles and
+ * deliver, bit 2 wait for the other tiles (7 in a multi-GPU run).  epoch:
+ * call counter (>= 1, equal on all ranks, increasing).  work: as ctk_back. */
+int ctk_back_exchange(const ctk_geom_t* g, ctk_xchg_t* x, const float* u, unsigned epoch,
+                      int phases, float* work, void* stream);
+
 /* ---- On-device problem generation.
  * ctk_phantom replaces shepp_logan (ctkrylov/ct.py:115-134) and the harness's
  * random-ellipse recipe: img[iy*nx+ix] = sum over ellipses, in order, of

@@ -70,6 +70,16 @@ SIGNATURES = {
                                _c.c_double, _c.POINTER(_c.c_double), _c.c_int, _dp, _fp, _vp]),
     "ctk_noise_scratch_bytes": (_c.c_size_t, []),
     "ctk_add_noise": (_c.c_int, [_fp, _dp, _dp, _c.c_int64, _c.c_double, _dp, _fp, _dp, _vp, _vp]),
+    "ctk_xchg_create": (_c.c_int, [_vp, _c.c_int, _c.c_int, _c.POINTER(_c.c_void_p)]),
+    "ctk_xchg_destroy": (_c.c_int, [_vp]),
+    "ctk_xchg_local": (_c.c_int, [_vp, _c.POINTER(_c.c_void_p), _c.POINTER(_c.c_void_p),
+                                  _c.POINTER(_c.c_void_p)]),
+    "ctk_xchg_handle_bytes": (_c.c_size_t, []),
+    "ctk_xchg_export": (_c.c_int, [_vp, _c.c_char_p]),
+    "ctk_xchg_connect_ipc": (_c.c_int, [_vp, _c.c_char_p]),
+    "ctk_xchg_connect_ptrs": (_c.c_int, [_vp, _c.POINTER(_c.c_void_p), _c.POINTER(_c.c_void_p),
+                                         _c.POINTER(_c.c_void_p)]),
+    "ctk_back_exchange": (_c.c_int, [_vp, _vp, _fp, _c.c_uint, _c.c_int, _fp, _vp]),
     "ctk_profile_begin": (_c.c_int, []),
     "ctk_profile_end": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int64), _c.POINTER(_c.c_double),
                                    _c.POINTER(_c.c_double)]),

@@ -47,6 +47,7 @@ struct BackArgs {
     float* stPT;
     int pad;
     double h, xmin, ymax, center;
+    const ctk_xchg_args* xc;   // optional (device copy): push the tile to its owner rank
 };
 
 // K1's zero-padded copies of the output pixel (ix, iy) (see ctk_forward.cu).
@@ -212,19 +213,41 @@ __global__ void __launch_bounds__(BTHREADS, PPT == 2 ? 6 : CTK_BACK_MINB4) k_bac
         unsigned* ticket = A.cnt + (size_t)blockIdx.y * gridDim.x + blockIdx.x;
         if (tid == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.z - 1);
         __syncthreads();
-        if (!s_last) return;
+        if (!s_last) return;                       // CTA-uniform
         __threadfence();
         if (tid == 0) *ticket = 0u;
-        if (!inx) return;
 #pragma unroll
         for (int r = 0; r < PPT; ++r) {
             const int iy = iy0 + ty + r * BROWS;
             double t = 0.0;
-            if (iy < A.ny)
+            if (inx && iy < A.ny)
                 for (unsigned z = 0; z < gridDim.z; ++z)
                     t += (double)__ldcg(part + z * n + (size_t)iy * A.nx + ix);
             acc[r] = t;
         }
+    }
+    if (A.xc) {
+        // Exchange: this rank's partial tile goes straight into the owner's
+        // receive slot (peer memory over NVLink, or local), then one
+        // system-scope release of the tile's arrival flag -- the transfer
+        // of each tile overlaps the compute of the tiles still running.
+        const ctk_xchg_args& X = *A.xc;
+        const int t = blockIdx.y * gridDim.x + blockIdx.x;
+        const int owner = t % X.nranks;
+        float* dst = X.recv[owner] + (size_t)X.rank * A.nx * A.ny;
+#pragma unroll
+        for (int r = 0; r < PPT; ++r) {
+            const int iy = iy0 + ty + r * BROWS;
+            if (ix < A.nx && iy < A.ny) dst[(size_t)iy * A.nx + ix] = (float)(A.h * acc[r]);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            unsigned* flag = X.flags[owner] + (size_t)X.rank * X.tiles + t;
+            asm volatile("fence.acq_rel.sys;\n\tst.relaxed.sys.global.u32 [%0], %1;" ::"l"(flag),
+                         "r"(X.epoch)
+                         : "memory");
+        }
+        return;
     }
     if (ix >= A.nx) return;
 #pragma unroll
@@ -236,6 +259,61 @@ __global__ void __launch_bounds__(BTHREADS, PPT == 2 ? 6 : CTK_BACK_MINB4) k_bac
         A.x[o] = v;
         if (A.stP) stage_out(A, ix, iy, v);
     }
+}
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Owner side: a CTA per owned tile (t = rank + i * nranks) waits for every
+// rank's partial of the tile, sums them in rank order (fp64; the result is
+// bitwise the same on every rank), writes it to every rank's result image
+// and releases each peer's "done" flag for the tile.
+template <int PPT>
+__global__ void __launch_bounds__(BTHREADS) k_xchg_reduce(const ctk_xchg_args* __restrict__ xa,
+                                                          int nx, int ny, int tiles_x) {
+    const ctk_xchg_args& X = *xa;
+    const int t = X.rank + blockIdx.x * X.nranks;
+    if (t >= X.tiles) return;
+    const int tid = threadIdx.y * BTX + threadIdx.x;
+    const unsigned* arrive = X.flags[X.rank];
+    if (tid < X.nranks)
+        while (ld_acquire_sys(arrive + (size_t)tid * X.tiles + t) != X.epoch) {
+        }
+    __syncthreads();
+    const size_t n = (size_t)nx * ny;
+    const float* recv = X.recv[X.rank];
+    const int ix = (t % tiles_x) * BTX + threadIdx.x;
+    const int iy0 = (t / tiles_x) * BROWS * PPT + threadIdx.y;
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) {
+        const int iy = iy0 + r * BROWS;
+        if (ix >= nx || iy >= ny) continue;
+        const size_t o = (size_t)iy * nx + ix;
+        double s = 0.0;
+        for (int q = 0; q < X.nranks; ++q) s += (double)__ldcv(recv + q * n + o);
+        const float v = (float)s;
+        for (int q = 0; q < X.nranks; ++q) X.x[q][o] = v;
+    }
+    __syncthreads();
+    if (tid < X.nranks && tid != X.rank) {
+        unsigned* flag = X.flags[tid] + (size_t)X.nranks * X.tiles + t;
+        asm volatile("fence.acq_rel.sys;\n\tst.relaxed.sys.global.u32 [%0], %1;" ::"l"(flag),
+                     "r"(X.epoch)
+                     : "memory");
+    }
+}
+
+// Every rank: wait until the owners of all other tiles have delivered them.
+__global__ void __launch_bounds__(256) k_xchg_wait(const ctk_xchg_args* __restrict__ xa) {
+    const ctk_xchg_args& X = *xa;
+    const unsigned* done = X.flags[X.rank] + (size_t)X.nranks * X.tiles;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < X.tiles; t += gridDim.x * blockDim.x)
+        if (t % X.nranks != X.rank)
+            while (ld_acquire_sys(done + t) != X.epoch) {
+            }
 }
 
 static int back_tiles_y(const ctk_geom* g) {
@@ -265,6 +343,8 @@ static int64_t back_tiles(const ctk_geom* g) {
     return (int64_t)((g->nx + BTX - 1) / BTX) * back_tiles_y(g);
 }
 
+int64_t ctk_back_tiles(const ctk_geom* g) { return back_tiles(g); }
+
 // Split reduction: S partial images + one arrival ticket per tile.
 extern "C" int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1) {
     if (!g || a0 < 0 || a1 > g->n_angles || a0 >= a1) return 0;
@@ -282,6 +362,13 @@ extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, i
 // any plain ctk_forward on that workspace).
 int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
                 float* work, float* stage, void* stream) {
+    return ctk_back_xc(g, u, x, a0, a1, x0, work, stage, nullptr, stream);
+}
+
+// xc (device pointer) != NULL: push the partial tiles to their owners
+// instead of writing x (ctk_back_exchange, phase 1).
+int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
+                float* work, float* stage, const ctk_xchg_args* xc, void* stream) {
     if (!g) return ctk_fail(CTK_ERR_ARG, "null geometry");
     if (a0 < 0 || a1 > g->n_angles || a0 > a1)
         return ctk_fail(CTK_ERR_SHAPE, "angle range [%d, %d) outside [0, %d)", a0, a1, g->n_angles);
@@ -324,6 +411,7 @@ int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
     A.xmin = g->xmin;
     A.ymax = g->ymax;
     A.center = g->center;
+    A.xc = xc;
     dim3 grid((g->nx + BTX - 1) / BTX, back_tiles_y(g), S), block(BTX, BROWS);
     const bool p4 = g->back_ppt == 4;
     size_t smem = (size_t)BCA * g->back_wmax * sizeof(float2);
@@ -335,5 +423,26 @@ int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
     CTK_CUDA(ctk_launch_pdl(kern, grid, block, smem, st, dim3(1, 1, 1), A));
     ctk_count_launch();
     ctk_prof_close(ph, st);
+    return CTK_OK;
+}
+
+// Phases 2 and 3 of ctk_back_exchange (xc: device copy of the arguments).
+int ctk_xchg_finish(const ctk_geom* g, const ctk_xchg_args* xc, int nranks, int phases,
+                    cudaStream_t st) {
+    const int tiles_x = (g->nx + BTX - 1) / BTX;
+    const int64_t tiles = back_tiles(g);
+    if (phases & 2) {
+        const unsigned owned = (unsigned)((tiles + nranks - 1) / nranks);
+        if (g->back_ppt == 4)
+            k_xchg_reduce<4><<<owned, dim3(BTX, BROWS), 0, st>>>(xc, g->nx, g->ny, tiles_x);
+        else
+            k_xchg_reduce<2><<<owned, dim3(BTX, BROWS), 0, st>>>(xc, g->nx, g->ny, tiles_x);
+        CTK_LAUNCH_CHECK("k_xchg_reduce");
+    }
+    if (phases & 4) {
+        const unsigned blocks = (unsigned)((tiles + 255) / 256);
+        k_xchg_wait<<<blocks < 148 ? blocks : 148, 256, 0, st>>>(xc);
+        CTK_LAUNCH_CHECK("k_xchg_wait");
+    }
     return CTK_OK;
 }

@@ -139,6 +139,20 @@ static inline cudaError_t ctk_launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Peer exchange for angle-sharded B (SURVEY row e; ctk_exchange.cu): every
+// rank's partial image is pushed tile by tile into the tile owner's receive
+// buffer over peer memory, the owner sums its tiles in rank order and pushes
+// the result to every rank.  Pointers are this process's mappings of each
+// rank's buffers (CUDA IPC, or the same device in the single-GPU emulation).
+constexpr int CTK_XCHG_MAX_RANKS = 8;
+struct ctk_xchg_args {
+    int rank, nranks, tiles;
+    unsigned epoch;
+    float* recv[CTK_XCHG_MAX_RANKS];      // rank q's receive buffer [nranks][n]
+    float* x[CTK_XCHG_MAX_RANKS];         // rank q's result image [n]
+    unsigned* flags[CTK_XCHG_MAX_RANKS];  // rank q's flags: arrive [nranks][tiles], done [tiles]
+};
+
 // Destination of a fused K1 staging write (P / PT of an image vector).
 struct ctk_stage_dst {
     float* P;
@@ -165,6 +179,11 @@ int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1
                    float* work, bool prestaged, void* stream);
 int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
                 float* work, float* stage, void* stream);
+int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
+                float* work, float* stage, const ctk_xchg_args* xc, void* stream);
+int ctk_xchg_finish(const ctk_geom* g, const ctk_xchg_args* xc, int nranks, int phases,
+                    cudaStream_t st);
+int64_t ctk_back_tiles(const ctk_geom* g);
 
 // K1 workspace: zero-padded copies P, PT
 // and one arrival ticket per (angle, 128-bin block) -- zero-filled once.

@@ -5,8 +5,11 @@ NVLink/NVSwitch.  Work is split by projection angle:
 
 * A is angle-sharded with a replicated image: each rank projects its own
   sinogram rows, no communication.
-* B produces a partial image per rank (the rank's angles only); one
-  all-reduce (sum, fp32, n values) completes it.
+* B produces a partial image per rank (the rank's angles only), summed over
+  ranks by :class:`PeerExchange` -- K2 pushes finished tiles to their owner
+  over NVLink peer memory, the owner reduces in rank order and delivers --
+  or, where the ranks cannot map each other's memory, one NCCL all-reduce
+  (sum, fp32, n values).
 * AB-GMRES: Krylov vectors live in measurement space and are sharded with
   the angles; every dot product / norm is a local partial plus one batched
   fp64 all-reduce per CGS2 sweep (h1 with ||q||^2, h2, ||q2||^2).
@@ -72,6 +75,12 @@ class ShardBackend:
     def forward(self, x): raise NotImplementedError               # image -> local sinogram
     def back_partial(self, u): raise NotImplementedError          # local sinogram -> partial image
     def allreduce(self, v): raise NotImplementedError             # in-place sum over ranks
+
+    def back_sum(self, u):                                        # sum over ranks of B_r u_r
+        img = self.back_partial(u)
+        self.allreduce(img)
+        return img
+
     def norm2(self, v): raise NotImplementedError                 # fp64 scalar (local part)
     def scale(self, v, a): raise NotImplementedError
     def add(self, a, b): raise NotImplementedError
@@ -110,9 +119,7 @@ def run_gmres_sharded(be: ShardBackend, b_local, cfg: SolverConfig, x0=None) -> 
     p = cfg.restart_period if cfg.restart_period > 0 else K
 
     def back_full(u):
-        img = be.back_partial(u)
-        be.allreduce(img)                     # N1: partial images summed over ranks
-        return img
+        return be.back_sum(u)                 # N1: partial images summed over ranks
 
     def gdots(k, v, want_norm):               # global dots: local partial + one all-reduce
         loc = be.basis_dots(k, v, want_norm)
@@ -204,14 +211,96 @@ def run_gmres_sharded(be: ShardBackend, b_local, cfg: SolverConfig, x0=None) -> 
                        cycles=max(cycles, 1))
 
 
+class _DeviceArray:
+    """__cuda_array_interface__ over a libctk-owned fp32 buffer (zero copy)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class PeerExchange:
+    """Angle-sharded B summed over peer memory (``ctk_back_exchange``).
+
+    Each rank's K2 pushes its finished partial tiles into the tile owner's
+    receive buffer (NVLink peer stores), the owner sums them in rank order and
+    delivers the tile to every rank -- the N1 all-reduce fused into the
+    back-projection (see csrc/ctk_exchange.cu).  ``img`` is the exchange's
+    result buffer (overwritten by the next call).  Connect with
+    :meth:`connect_ipc` across processes (handles gathered over
+    torch.distributed) or :meth:`connect_local` in one process.
+    """
+
+    def __init__(self, dgeom, rank: int, nranks: int):
+        import ctypes
+        from . import _native
+        self._native, self._ct = _native, ctypes
+        self.lib = _native.load()
+        self.dg = dgeom
+        h = ctypes.c_void_p()
+        _native.check(self.lib.ctk_xchg_create(dgeom.handle, rank, nranks, ctypes.byref(h)),
+                      "ctk_xchg_create")
+        self.handle = h
+        self.rank, self.nranks = rank, nranks
+        r, x, f = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _native.check(self.lib.ctk_xchg_local(h, ctypes.byref(r), ctypes.byref(x), ctypes.byref(f)))
+        self.local_ptrs = (r.value, x.value, f.value)
+        torch = dgeom.torch
+        self.img = torch.as_tensor(_DeviceArray(x.value, dgeom.n), device=dgeom.dev)
+        self.epoch = 0
+        wf = int(self.lib.ctk_back_work_floats(dgeom.handle, 0, dgeom.n_angles))
+        self.work = torch.zeros(max(wf, 4), dtype=torch.float32, device=dgeom.dev)
+
+    def export(self) -> bytes:
+        buf = self._ct.create_string_buffer(int(self.lib.ctk_xchg_handle_bytes()))
+        self._native.check(self.lib.ctk_xchg_export(self.handle, buf), "ctk_xchg_export")
+        return buf.raw
+
+    def connect_ipc(self, handles: list) -> None:
+        blob = b"".join(handles)
+        self._native.check(self.lib.ctk_xchg_connect_ipc(self.handle, blob), "ctk_xchg_connect_ipc")
+
+    def connect_local(self, peers: list) -> None:
+        ct = self._ct
+        arr = [(ct.c_void_p * self.nranks)(*[p.local_ptrs[i] for p in peers]) for i in range(3)]
+        self._native.check(self.lib.ctk_xchg_connect_ptrs(self.handle, *arr), "ctk_xchg_connect_ptrs")
+
+    def back(self, u, phases: int = 7, epoch: int | None = None, stream=None):
+        """img = sum over ranks of B_rank u_rank (this rank's phases)."""
+        if epoch is None:
+            self.epoch += 1
+            epoch = self.epoch
+        self.dg._check(u, self.dg.m, "u")
+        stream = self.dg._stream(stream)
+        self._native.check(self.lib.ctk_back_exchange(self.dg.handle, self.handle, u.data_ptr(),
+                                                      epoch, phases, self.work.data_ptr(),
+                                                      stream.cuda_stream), "ctk_back_exchange")
+        return self.img
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self.lib.ctk_xchg_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
 class CudaShardBackend(ShardBackend):
-    """libctk projectors on this rank's angles + NCCL all-reduce (fp32 / fp64).
+    """libctk projectors on this rank's angles; partial images summed over
+    NVLink peer memory (:class:`PeerExchange`) when every rank can map the
+    others' buffers, else NCCL all-reduce.  Small fp64 messages go through
+    NCCL.
 
     Vectors are CUDA tensors (fp32 for images/sinograms, fp64 for the small
     reduction messages).  The process group defaults to the world group.
     """
 
-    def __init__(self, grid, geometry, angle_idx, device: int = 0, group=None):
+    def __init__(self, grid, geometry, angle_idx, device: int = 0, group=None,
+                 peer_exchange: bool | None = None):
+        import os
+
         import torch
         import torch.distributed as tdist
 
@@ -224,6 +313,40 @@ class CudaShardBackend(ShardBackend):
         self.dg = DeviceGeometry(grid, local, device)
         self.n = self.dg.n
         self.m_local = self.dg.m
+        self.xchg = None
+        world = tdist.get_world_size(group) if tdist.is_initialized() else 1
+        if peer_exchange is None:
+            peer_exchange = os.environ.get("CTK_PEER_EXCHANGE", "1") != "0"
+        if peer_exchange and 1 < world <= 8:
+            self.xchg = self._open_exchange(world)
+
+    def _open_exchange(self, world):
+        """All ranks agree: every rank creates its buffers, handles are
+        all-gathered, every rank maps its peers; any failure -> NCCL path."""
+        rank = self.dist.get_rank(self.group)
+        ok, ex, mine = True, None, b""
+        try:
+            ex = PeerExchange(self.dg, rank, world)
+            mine = ex.export()
+        except Exception:
+            ok = False
+        handles = [None] * world
+        self.dist.all_gather_object(handles, mine if ok else None, group=self.group)
+        if ok and all(h is not None for h in handles):
+            try:
+                ex.connect_ipc(handles)
+            except Exception:
+                ok = False
+        else:
+            ok = False
+        flag = self.torch.tensor([1 if ok else 0], device=self.dev)
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.group)
+        return ex if int(flag.item()) == 1 else None
+
+    def back_sum(self, u):
+        if self.xchg is None:
+            return super().back_sum(u)
+        return self.xchg.back(u).clone()
 
     def zeros(self, size):
         return self.torch.zeros(size, dtype=self.torch.float32, device=self.dev)

@@ -666,11 +666,15 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
     return nrm;
 }
 
+// tm (when use_tma): 3-D tensor map over the basis rows as 64-float panels,
+// dims {64, panels, k+1}; one box {64, chunk / 64, k+1} is this CTA's whole
+// [k+1][chunk] block -- one TMA copy instead of k+1 row copies.
 __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, int64_t L,
                                                    const float* __restrict__ q, int passes,
                                                    int64_t chunk, double* h, double* stat,
                                                    double* partial, ctk_stage_dst sd,
-                                                   double* hm, int stat_off) {
+                                                   double* hm, int stat_off, int use_tma,
+                                                   const __grid_constant__ CUtensorMap tm) {
     cg::grid_group grid = cg::this_grid();
     ctk_pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -685,7 +689,9 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     double* red = h2 + nb + 1;                                      // [SW]
     float* qv = reinterpret_cast<float*>(
         smem_raw + ((16 + sizeof(double) * (2 * nb + 2 + SW) + 15) & ~(size_t)15));
-    float* Ws = qv + cpad;                                          // [nb][cpad]
+    unsigned char* ws_raw = reinterpret_cast<unsigned char*>(qv + cpad);
+    ws_raw += (128u - (smem_u32(ws_raw) & 127u)) & 127u;           // TMA destination alignment
+    float* Ws = reinterpret_cast<float*>(ws_raw);                   // [nb][cpad]
     double4* acc = reinterpret_cast<double4*>(                      // [ST], 32-B aligned
         (reinterpret_cast<uintptr_t>(Ws + (size_t)nb * cpad) + 31) & ~(uintptr_t)31);
     const unsigned bar_a = smem_u32(bar);
@@ -696,7 +702,19 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     }
     __syncthreads();
     ctk_pdl_wait();                  // q (and, transitively, the basis) from the previous kernels
-    if (threadIdx.x < 32 && row_bytes > 0) {
+    if (use_tma) {
+        if (threadIdx.x == 0 && row_bytes > 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a),
+                         "r"((unsigned)(cpad * 4) * (unsigned)nb)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(Ws)),
+                "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"((int)(start / 64)), "r"(0),
+                "r"(bar_a)
+                : "memory");
+        }
+    } else if (threadIdx.x < 32 && row_bytes > 0) {
         if (threadIdx.x == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a),
                          "r"(row_bytes * (unsigned)nb)
@@ -1138,85 +1156,6 @@ static int try_cgs2_fused(float* W, int64_t ld, int k, int64_t L, float* q, doub
 }
 
 // SMEM-resident path when every CTA's chunk of the k+1 rows fits in shared
-// memory with one CTA per SM.
-static size_t gs_smem_bytes(int k, int64_t chunk) {
-    const int nb = k + 1;
-    const size_t head = (16 + sizeof(double) * (2 * (size_t)nb + 2 + SW) + 15) & ~(size_t)15;
-    return head + sizeof(float) * (size_t)chunk * (nb + 1) + sizeof(double) * 4 * ST + 32;
-}
-
-static bool gs_smem_plan(int64_t L, int k, int64_t* Gp, int64_t* chunkp, size_t* smemp) {
-    static int coop = -1, sms = 0, gcap = 0;
-    if (coop < 0) {
-        const char* off = getenv("CTK_NO_SMEM_GS");
-        const char* e = getenv("CTK_GS_CTAS");             // tuning override
-        gcap = e ? atoi(e) : 0;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaFuncSetAttribute(k_gs_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)SMEM_LIMIT) != cudaSuccess)
-            coop = 0;
-        cudaGetLastError();
-        if (off && off[0] == '1') coop = 0;
-    }
-    if (coop != 1 || L < 4 || k < 0) return false;
-    // chunk: a multiple of 4 floats (16-B bulk-copy alignment), >= 64 floats
-    int64_t G = gcap > 0 && gcap < sms ? gcap : sms;
-    int64_t chunk = ((L + G - 1) / G + 3) & ~3LL;
-    if (chunk < 64) chunk = 64;
-    G = (L + chunk - 1) / chunk;
-    if (G > GS_MAXG) return false;
-    const size_t smem = gs_smem_bytes(k, chunk);
-    if (smem > SMEM_LIMIT) return false;
-    // partials: (nb + 1) + (nb + 1) + 1 rows of G doubles within carve(scratch, k + 3)
-    if ((size_t)(2 * k + 5) * G > (size_t)MAXCH * (size_t)(k + 3)) return false;
-    *Gp = G;
-    *chunkp = chunk;
-    *smemp = smem;
-    return true;
-}
-
-static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
-                       double* stat, Scratch s, cudaStream_t st, const ctk_stage_dst* sdp,
-                       double* hm, bool* done) {
-    *done = false;
-    int64_t G, chunk;
-    size_t smem;
-    if (!gs_smem_plan(L, k, &G, &chunk, &smem)) return CTK_OK;
-    double* partial = s.partial;
-    ctk_stage_dst sd = {};
-    if (sdp && sdp->P && (int64_t)sdp->nx * sdp->ny == L) sd = *sdp;
-    int stat_off = (int)(stat - h);
-    // cooperative (grid barriers) and programmatic: the launch and the
-    // prologue overlap the producer of q (K2 / K1), which triggers at entry
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)G);
-    cfg.blockDim = dim3(ST);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_gs_smem, W, ld, k, L, (const float*)q, passes, chunk,
-                                       h, stat, partial, sd, hm, stat_off);
-    ctk_count_launch();
-    if (e != cudaSuccess) return ctk_check_cuda(e, "k_gs_smem");
-    *done = true;
-    return CTK_OK;
-}
-
-bool ctk_gs_smem_ok(int64_t L, int k) {
-    int64_t G, chunk;
-    size_t smem;
-    return gs_smem_plan(L, k, &G, &chunk, &smem);
-}
-
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* p = nullptr;
@@ -1242,6 +1181,99 @@ static bool encode_rows(CUtensorMap* m, const float* base, int64_t L, int64_t ld
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
                es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// memory with one CTA per SM.
+static size_t gs_smem_bytes(int k, int64_t chunk) {
+    const int nb = k + 1;
+    const size_t head = (16 + sizeof(double) * (2 * (size_t)nb + 2 + SW) + 15) & ~(size_t)15;
+    return head + sizeof(float) * (size_t)chunk * (nb + 1) + sizeof(double) * 4 * ST + 32 + 128;
+}
+
+static bool gs_smem_plan(int64_t L, int k, int64_t* Gp, int64_t* chunkp, size_t* smemp) {
+    static int coop = -1, sms = 0, gcap = 0;
+    if (coop < 0) {
+        const char* off = getenv("CTK_NO_SMEM_GS");
+        const char* e = getenv("CTK_GS_CTAS");             // tuning override
+        gcap = e ? atoi(e) : 0;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaFuncSetAttribute(k_gs_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SMEM_LIMIT) != cudaSuccess)
+            coop = 0;
+        cudaGetLastError();
+        if (off && off[0] == '1') coop = 0;
+    }
+    if (coop != 1 || L < 4 || k < 0) return false;
+    // chunk: a multiple of 64 floats (the TMA panel), at most 256 panels
+    int64_t G = gcap > 0 && gcap < sms ? gcap : sms;
+    int64_t chunk = ((L + G - 1) / G + 63) & ~63LL;
+    if (chunk > 64 * 256 || k + 1 > 256) return false;
+    G = (L + chunk - 1) / chunk;
+    if (G > GS_MAXG) return false;
+    const size_t smem = gs_smem_bytes(k, chunk);
+    if (smem > SMEM_LIMIT) return false;
+    // partials: (nb + 1) + (nb + 1) + 1 rows of G doubles within carve(scratch, k + 3)
+    if ((size_t)(2 * k + 5) * G > (size_t)MAXCH * (size_t)(k + 3)) return false;
+    *Gp = G;
+    *chunkp = chunk;
+    *smemp = smem;
+    return true;
+}
+
+static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
+                       double* stat, Scratch s, cudaStream_t st, const ctk_stage_dst* sdp,
+                       double* hm, bool* done) {
+    *done = false;
+    int64_t G, chunk;
+    size_t smem;
+    if (!gs_smem_plan(L, k, &G, &chunk, &smem)) return CTK_OK;
+    double* partial = s.partial;
+    ctk_stage_dst sd = {};
+    if (sdp && sdp->P && (int64_t)sdp->nx * sdp->ny == L) sd = *sdp;
+    int stat_off = (int)(stat - h);
+    // the CTA blocks of the k+1 rows as one 3-D TMA box each (64-float panels)
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    int use_tma = 0;
+    if (auto enc = tensor_map_encoder()) {
+        cuuint64_t dims[3] = {64, (cuuint64_t)((L + 63) / 64), (cuuint64_t)(k + 1)};
+        cuuint64_t strides[2] = {64 * sizeof(float), (cuuint64_t)ld * sizeof(float)};
+        cuuint32_t box[3] = {64, (cuuint32_t)(chunk / 64), (cuuint32_t)(k + 1)};
+        cuuint32_t es[3] = {1, 1, 1};
+        use_tma = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, W, dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    // cooperative (grid barriers) and programmatic: the launch and the
+    // prologue overlap the producer of q (K2 / K1), which triggers at entry
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(ST);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_gs_smem, W, ld, k, L, (const float*)q, passes, chunk,
+                                       h, stat, partial, sd, hm, stat_off, use_tma, tm);
+    ctk_count_launch();
+    if (e != cudaSuccess) return ctk_check_cuda(e, "k_gs_smem");
+    *done = true;
+    return CTK_OK;
+}
+
+bool ctk_gs_smem_ok(int64_t L, int k) {
+    int64_t G, chunk;
+    size_t smem;
+    return gs_smem_plan(L, k, &G, &chunk, &smem);
 }
 
 // Streamed path: L a multiple of 4 (16-B row pitch of q), at most TS_MAXROWS

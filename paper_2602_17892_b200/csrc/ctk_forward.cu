@@ -233,6 +233,30 @@ struct FwdArgs {
 // creation), so they add exact zeros and need no predicate.  Rays entering
 // through the side of the image otherwise start on different rows, which
 // turns each warp gather into ~10 scattered sectors instead of 2-3.
+// One row step.  frac += sigma; the carry moves the pair one column:
+// q += pitch + carry.  MIRROR (the pair's second tap is to the LEFT) keeps
+// fr = ~frac instead: fr -= sigma borrows exactly when frac + sigma carries,
+// and the carry flag after a subtract is "no borrow", so
+// q += (pitch - 1) + !borrow = pitch - carry.  Both are two integer ops.
+template <bool MIRROR>
+__device__ __forceinline__ void walk_step(unsigned& fr, int& q, unsigned Sf, int pitch) {
+    if (MIRROR)
+        asm("sub.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;"
+            : "+r"(fr), "+r"(q) : "r"(Sf), "r"(pitch - 1));
+    else
+        asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;"
+            : "+r"(fr), "+r"(q) : "r"(Sf), "r"(pitch));
+}
+
+// Second-tap weight from the step state: w = sat(f + sigma - 1) with
+// f1 = 1 + f from the top fraction bits (no I2F); MIRROR holds ~frac, i.e.
+// f' = 1 - f - 2^-32, so w = sat((sigma + 1) - (1 + f')) (free negation).
+template <bool MIRROR>
+__device__ __forceinline__ float walk_weight(unsigned fr, float sm2, float sp1) {
+    const float f1 = __uint_as_float(0x3f800000u | (fr >> 9));
+    return MIRROR ? __saturatef(sp1 - f1) : __saturatef(f1 + sm2);
+}
+
 template <bool MIRROR>
 __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
                                            const float* __restrict__ base, int R, int C, int pad,
@@ -280,37 +304,64 @@ __device__ __forceinline__ double walk_ray(const AngleParams& p, double s,
     // row k, padded column c + pad (MIRROR: padded column C - 1 - c + pad,
     // second tap one to the left).
     const long long u = U0 + (long long)kw * Sg;
-    unsigned frac = (unsigned)u;
+    unsigned frac = MIRROR ? ~(unsigned)u : (unsigned)u;      // see walk_step
     const unsigned Sf = (unsigned)Sg;
     const int c0 = (int)(u >> 32);
-    // MIRROR keeps q negated so both directions advance with add-with-carry
+    // the carry moves the pair one column right (MIRROR: left: subtract it)
     int q = kw * pitch + (MIRROR ? C - 1 - c0 + pad : c0 + pad);
-    if (MIRROR) q = -q;
     // Second-tap length wb = max(0, f + sigma - 1) * Lx, the part of the row
     // past the grid line (0 when it does not reach it), and wa = L - wb, so
     //   wa v0 + wb v1 = L v0 + Lx w (v1 - v0),  w = sat(f1 + (sigma - 2)),
     // f1 = 1 + f (w < sigma <= 1: the saturation only clamps at 0).  Per row:
     // frac add + carry, address, two taps, 1 + f, FADD.SAT, and the two sums.
     const float sm2 = (float)((double)Sg * (1.0 / 4294967296.0) - 2.0);
+    const float sp1 = (float)((double)Sg * (1.0 / 4294967296.0) + 1.0);
     double acc = 0.0;
     int k = kw;
+#ifndef CTK_FWD_PAIRED
+#define CTK_FWD_PAIRED 1
+#endif
     while (k < kW) {
         const int kstop = min(kW, k + 48);
         float s0 = 0.f, s1 = 0.f;
+        if (CTK_FWD_PAIRED) {
+            // two rows per step in packed fp32x2 (FADD2 / FFMA2): rows k, k+1
+            // share one add for the v0 sums, one for the differences and one
+            // FMA for the weighted sums.
+            float2 S0 = make_float2(0.f, 0.f), S1 = make_float2(0.f, 0.f);
+            const float2 m1 = make_float2(-1.f, -1.f);
+#pragma unroll FWD_UNROLL / 2
+            for (; k + 1 < kstop; k += 2) {
+                float2 v0, v1, w;
+                {
+                    w.x = walk_weight<MIRROR>(frac, sm2, sp1);
+                    const float* pp = base + q;
+                    v0.x = __ldg(pp);
+                    v1.x = __ldg(pp + (MIRROR ? -1 : 1));
+                    walk_step<MIRROR>(frac, q, Sf, pitch);
+                }
+                {
+                    w.y = walk_weight<MIRROR>(frac, sm2, sp1);
+                    const float* pp = base + q;
+                    v0.y = __ldg(pp);
+                    v1.y = __ldg(pp + (MIRROR ? -1 : 1));
+                    walk_step<MIRROR>(frac, q, Sf, pitch);
+                }
+                S0 = __fadd2_rn(S0, v0);
+                S1 = __ffma2_rn(w, __ffma2_rn(v0, m1, v1), S1);
+            }
+            s0 = S0.x + S0.y;
+            s1 = S1.x + S1.y;
+        }
 #pragma unroll FWD_UNROLL
         for (; k < kstop; ++k) {
-            // 1 + frac as a float from the top 23 fraction bits: no I2F
-            const float f1 = __uint_as_float(0x3f800000u | (frac >> 9));
-            const float w = __saturatef(f1 + sm2);
-            const float* pp = base + (MIRROR ? -(long long)q : (long long)q);
+            const float w = walk_weight<MIRROR>(frac, sm2, sp1);
+            const float* pp = base + q;
             const float v0 = __ldg(pp);
             const float v1 = __ldg(pp + (MIRROR ? -1 : 1));
             s0 += v0;
             s1 = fmaf(w, v1 - v0, s1);
-            // frac += sigma; the carry moves the pair one column (row split)
-            // (MIRROR: -q_pos advances by -pitch + carry)
-            asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;"
-                : "+r"(frac), "+r"(q) : "r"(Sf), "r"(MIRROR ? -pitch : pitch));
+            walk_step<MIRROR>(frac, q, Sf, pitch);      // frac += sigma; split -> next column
         }
         acc += (double)p.L * (double)s0 + (double)p.Lx * (double)s1;
     }

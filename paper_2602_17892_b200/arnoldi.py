@@ -156,3 +156,110 @@ class DeviceBasis:
                                           v.data_ptr(), dst.data_ptr(), self.L,
                                           _native.ptr(norm_out), self.scratch(stream),
                                           stream.cuda_stream), "ctk_update")
+
+
+# ---------------------------------------------------------------------------
+# The reference's step-wise Arnoldi API (ctkrylov/arnoldi.py:28-82), the
+# second seam of SURVEY row (b), with the basis resident in HBM and each step's
+# orthogonalisation on libctk's Gram-Schmidt kernels.  Drivers that call
+# arnoldi_step themselves (or monkeypatch it, tests/test_gmres.py:183) keep
+# working; the operator is applied on the device when it can be (GPU
+# projectors and their compositions), else through its host apply.
+# ---------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    return torch
+
+
+class ArnoldiState:
+    """Growing orthonormal basis and Hessenberg factor for one solver run
+    (ctkrylov/arnoldi.py:28-53).  ``basis`` holds w_1 .. w_{k+1} (host fp64
+    copies of the HBM rows, built on access); ``hess`` is (k+1) x k;
+    ``beta`` = ||r_0||_2."""
+
+    def __init__(self, dbasis: DeviceBasis, beta: float, k: int = 0):
+        self._dev = dbasis
+        self.beta = float(beta)
+        self.k = int(k)
+        self._hess_cols: list[np.ndarray] = []
+        self._breakdown = False
+        torch = dbasis.torch
+        self._h = torch.zeros(dbasis.rows + 8, dtype=torch.float64, device=dbasis.dev)
+        self._stat = torch.zeros(4, dtype=torch.float64, device=dbasis.dev)
+
+    @classmethod
+    def start(cls, r0, device: int = 0, capacity: int = 32) -> "ArnoldiState":
+        """r0: host array or CUDA tensor; ValueError on a zero residual."""
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise _native.CtkError("a CUDA device is required: libctk has no CPU path")
+        if isinstance(r0, np.ndarray) or not hasattr(r0, "is_cuda"):
+            r = np.asarray(r0, dtype=np.float64)
+            beta = float(np.linalg.norm(r))
+            v = torch.from_numpy(r.astype(np.float32)).to(torch.device("cuda", device))
+        else:
+            v = r0.float()
+            beta = float(torch.linalg.vector_norm(r0.double()).item())
+        if beta == 0.0:
+            raise ValueError("Arnoldi cannot start from a zero residual")
+        db = DeviceBasis(v.numel(), max(2, capacity), v.device, torch)
+        db.row(0).copy_((v.double() / beta).float())
+        return cls(db, beta)
+
+    @property
+    def basis(self) -> list[np.ndarray]:
+        n = self.k if self._breakdown else self.k + 1        # no row appended on breakdown
+        W = self._dev.W[:n, : self._dev.L].double().cpu().numpy()
+        return [W[i] for i in range(n)]
+
+    @property
+    def hess(self) -> np.ndarray:
+        """The (k+1) x k upper-Hessenberg matrix assembled from stored columns."""
+        return hessenberg_from_columns(self._hess_cols, self.k)
+
+    def _ensure_rows(self, rows: int) -> None:
+        db = self._dev
+        if rows <= db.rows:
+            return
+        torch = db.torch
+        new = DeviceBasis(db.L, max(rows, 2 * db.rows), db.dev, torch)
+        new.W[: db.rows].copy_(db.W)
+        self._dev = new
+        self._h = torch.zeros(new.rows + 8, dtype=torch.float64, device=db.dev)
+
+
+def _apply_on_device(M, w):
+    """q = M w for a device row w (fp32 CUDA tensor)."""
+    if hasattr(M, "apply_device"):
+        return M.apply_device(w)
+    torch = _torch()
+    q = M.apply(w.double().cpu().numpy())              # host operator: the reference contract
+    return torch.from_numpy(np.asarray(q, dtype=np.float32)).to(w.device)
+
+
+def arnoldi_step(state: ArnoldiState, M, reorthogonalize: bool = True) -> None:
+    """Advance the factorisation by one step in place (ctkrylov/arnoldi.py:56-82).
+
+    Raises Breakdown(k) when the new direction vanishes relative to
+    ||M w_k|| (BREAKDOWN_RTOL); the Hessenberg column is recorded first, as
+    in the reference.  Orthogonalisation: CGS2 (or one pass) on the GPU."""
+    torch = state._dev.torch
+    k = state.k
+    state._ensure_rows(k + 2)
+    db = state._dev
+    w = db.row(k)
+    q = _apply_on_device(M, w)
+    if q.numel() != db.L:
+        from .linop import OperatorShapeError
+        raise OperatorShapeError(f"operator returned {q.numel()} entries, basis rows hold {db.L}")
+    q = q.contiguous().float().clone()
+    stream = torch.cuda.current_stream(db.dev)
+    db.gs_step(k, q, 2 if reorthogonalize else 1, state._h, state._stat, stream)
+    h = state._h[: k + 2].cpu().numpy().copy()
+    qn, broke = state._stat[:2].cpu().numpy()
+    state._hess_cols.append(h)
+    state.k = k + 1
+    if broke != 0.0 or h[k + 1] <= BREAKDOWN_RTOL * qn:
+        state._breakdown = True
+        raise Breakdown(state.k)

@@ -114,3 +114,67 @@ def select_lambda(hess: np.ndarray, beta: float, strategy: str,
     if strategy == "gcv":
         return gcv_from_svd(s, u, beta, grid)
     raise ValueError(f"unknown lambda strategy {strategy!r}")
+
+
+# ---- the reference's public pieces of the selector (ctkrylov/regparam.py:40-134),
+# restated on the vectorised helpers above (same values, same tie rules).
+
+class LCurvePoint:
+    """One L-curve sample (ctkrylov/regparam.py:40-43)."""
+
+    __slots__ = ("lam", "log_residual", "log_solution")
+
+    def __init__(self, lam: float, log_residual: float, log_solution: float):
+        self.lam, self.log_residual, self.log_solution = lam, log_residual, log_solution
+
+
+def tikhonov_curve_points(singular_values, left_factor, beta, grid) -> list[LCurvePoint]:
+    """The projected Tikhonov L-curve on a lambda grid (regparam.py:63-79)."""
+    s = np.asarray(singular_values, dtype=np.float64)
+    if not np.any(s > 0):
+        raise DegenerateCurveError("all singular values are zero")
+    grid = np.asarray(grid, dtype=np.float64)
+    c, outside = _rotated_rhs(s, left_factor, beta)
+    sol_sq, res_sq, _ = _grid_norms(s, c, outside, grid)
+    return [LCurvePoint(float(l), 0.5 * np.log(max(r, 1e-300)), 0.5 * np.log(max(x, 1e-300)))
+            for l, r, x in zip(grid, res_sq, sol_sq)]
+
+
+def lcurve_corner(points) -> float:
+    """Maximum signed curvature, ties toward larger lambda (regparam.py:82-107)."""
+    if len(points) < 5:
+        raise DegenerateCurveError(f"need at least 5 L-curve points, got {len(points)}")
+    xr = np.array([p.log_residual for p in points])
+    ys = np.array([p.log_solution for p in points])
+    dx, dy = np.gradient(xr), np.gradient(ys)
+    ddx, ddy = np.gradient(dx), np.gradient(dy)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        kappa = (dx * ddy - dy * ddx) / (dx * dx + dy * dy) ** 1.5
+    ok = np.isfinite(kappa)
+    if not np.any(ok):
+        raise DegenerateCurveError("curvature is non-finite everywhere")
+    kappa = np.where(ok, kappa, -np.inf)
+    if np.max(kappa) <= CURVATURE_FLOOR:
+        raise DegenerateCurveError("L-curve has no corner (curvature flat)")
+    return float(points[_last_arg(kappa, np.argmax)].lam)
+
+
+def gcv_values(singular_values, left_factor, beta, grid) -> np.ndarray:
+    """GCV function res^2 / (k+1 - sum f_i)^2 on the grid (regparam.py:110-125)."""
+    s = np.asarray(singular_values, dtype=np.float64)
+    u = np.asarray(left_factor, dtype=np.float64)
+    grid = np.asarray(grid, dtype=np.float64)
+    c, outside = _rotated_rhs(s, u, beta)
+    _, res_sq, denom = _grid_norms(s, c, outside, grid)
+    trace = u.shape[0] - np.sum(s * s / denom, axis=1)
+    if np.any(trace <= 0.0):
+        raise DegenerateCurveError("GCV trace underflow")
+    return res_sq / (trace * trace)
+
+
+def gcv_minimize(singular_values, left_factor, beta, grid) -> float:
+    """Grid minimiser of gcv_values, ties toward larger lambda (regparam.py:128-134)."""
+    vals = gcv_values(singular_values, left_factor, beta, grid)
+    if not np.all(np.isfinite(vals)):
+        raise DegenerateCurveError("GCV values are non-finite")
+    return float(np.asarray(grid, dtype=np.float64)[_last_arg(vals, np.argmin)])

@@ -138,3 +138,76 @@ def test_single_pass_gram_schmidt(cuda, L, k):
     assert hg[k + 1] == pytest.approx(np.linalg.norm(v), rel=1e-5)
     w = B.W[k + 1, :L].cpu().numpy().astype(np.float64)
     np.testing.assert_allclose(w, v / np.linalg.norm(v), atol=2e-6)
+
+
+# ---- the reference's step-wise API: ArnoldiState / arnoldi_step (row b seam)
+
+def _ref_arnoldi(Mdense, r0, steps):
+    """fp64 MGS + reorthogonalisation, ctkrylov/arnoldi.py:56-82 restated."""
+    beta = np.linalg.norm(r0)
+    V = [r0 / beta]
+    cols = []
+    for k in range(steps):
+        q = Mdense @ V[k]
+        h = np.zeros(k + 2)
+        for _ in range(2):
+            for i in range(k + 1):
+                c = V[i] @ q
+                h[i] += c
+                q = q - c * V[i]
+        h[k + 1] = np.linalg.norm(q)
+        cols.append(h)
+        V.append(q / h[k + 1])
+    return beta, cols, V
+
+
+def test_arnoldi_step_on_ct_composite(cuda):
+    """compose(A, B) of GPU projectors runs on the device; the factorisation
+    matches the fp64 reference Arnoldi and M W_k = W_{k+1} H_k."""
+    from oracle import oracle as O
+    from paper_2602_17892_b200 import arnoldi, ct, linop
+    N, na, D = 24, 18, 35
+    grid = ct.ImageGrid(N, N, 1.0)
+    geom = ct.ParallelGeometry(np.arange(na) * np.pi / na, D, 1.0)
+    A, B = ct.forward_ray_driven(grid, geom), ct.back_pixel_driven(grid, geom)
+    M = linop.compose(A, B)                       # AB: m x m, applies on the device
+    assert hasattr(M, "apply_device")
+    og = O.Geometry(N, N, 1.0, geom.angles, D, 1.0)
+    Ad = np.column_stack([O.forward(og, e) for e in np.eye(grid.n)])
+    Bd = np.column_stack([O.back(og, e) for e in np.eye(geom.m)])
+    r0 = np.random.default_rng(0).random(geom.m).astype(np.float32).astype(np.float64)
+    st = arnoldi.ArnoldiState.start(r0, capacity=3)          # grows past its first rows
+    steps = 8
+    for _ in range(steps):
+        arnoldi.arnoldi_step(st, M)
+    beta, cols, V = _ref_arnoldi(Ad @ Bd, r0, steps)
+    assert st.beta == pytest.approx(beta, rel=1e-12)
+    H = st.hess
+    Href = np.zeros((steps + 1, steps))
+    for j, c in enumerate(cols):
+        Href[: j + 2, j] = c
+    np.testing.assert_allclose(H, Href, rtol=2e-4, atol=2e-4 * np.abs(Href).max())
+    W = np.column_stack(st.basis)
+    assert W.shape == (geom.m, steps + 1)
+    assert np.abs(W.T @ W - np.eye(steps + 1)).max() < 1e-5
+    resid = (Ad @ Bd) @ W[:, :steps] - W @ H
+    assert np.linalg.norm(resid) <= 1e-4 * np.linalg.norm(H)
+
+
+def test_arnoldi_step_host_operator_and_breakdown(cuda):
+    """A host (dense) operator goes through its apply; an invariant subspace
+    raises Breakdown(k) after recording the column, without a new row."""
+    from paper_2602_17892_b200 import arnoldi, linop
+    M = linop.dense_operator(np.diag([1.0, 2.0, 3.0, 4.0, 5.0, 6.0]))
+    r0 = np.array([1.0, 1.0, 0.0, 0.0, 0.0, 0.0])           # spans a 2-D invariant subspace
+    st = arnoldi.ArnoldiState.start(r0)
+    arnoldi.arnoldi_step(st, M)
+    with pytest.raises(arnoldi.Breakdown) as e:
+        arnoldi.arnoldi_step(st, M)
+    assert e.value.k == 2 and st.k == 2
+    assert len(st.basis) == 2 and st.hess.shape == (3, 2)
+    with pytest.raises(ValueError):
+        arnoldi.ArnoldiState.start(np.zeros(4))
+    st2 = arnoldi.ArnoldiState.start(np.ones(6))
+    arnoldi.arnoldi_step(st2, M, reorthogonalize=False)
+    assert st2.k == 1 and len(st2.basis) == 2

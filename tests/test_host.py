@@ -267,3 +267,55 @@ def test_matched_back_reference_semantics_on_host_operators():
     big = LinearOperator(5000, 4000, lambda v: np.zeros(5000))
     with pytest.raises(ct.GeometryError):
         ct.matched_back(big)
+
+
+# ---- reference API pieces (drop-in names): linop helpers, public regparam functions
+
+def test_dense_operator_and_transpose_contract():
+    import pytest as _pt
+    from paper_2602_17892_b200 import linop
+    m = np.arange(6.0).reshape(2, 3)
+    A = linop.dense_operator(m)
+    At = linop.transpose_of(m)
+    v = np.array([1.0, -2.0, 0.5])
+    np.testing.assert_array_equal(A.apply(v), m @ v)
+    np.testing.assert_array_equal(At.apply(np.array([1.0, 2.0])), m.T @ np.array([1.0, 2.0]))
+    assert A.shape == (2, 3) and At.shape == (3, 2)
+    m[0, 0] = 99.0                                     # copied and frozen
+    np.testing.assert_array_equal(A.apply(v), np.arange(6.0).reshape(2, 3) @ v)
+    with _pt.raises(linop.OperatorShapeError):
+        linop.dense_operator(np.ones(3))
+    with _pt.raises(ValueError):
+        linop.dense_operator(np.array([[np.nan]]))
+    with _pt.raises(linop.OperatorShapeError):
+        A.apply(np.ones(2))
+
+
+def test_op_norm_estimate_power_iteration():
+    import pytest as _pt
+    from paper_2602_17892_b200 import linop
+    rng = np.random.default_rng(3)
+    q, _ = np.linalg.qr(rng.standard_normal((6, 6)))
+    m = q @ np.diag([5.0, 2.0, 1.0, 0.5, 0.1, 0.0]) @ q.T
+    est = linop.op_norm_estimate(linop.dense_operator(m), iterations=200, seed=0)
+    assert est == _pt.approx(5.0, rel=1e-10)
+    assert linop.op_norm_estimate(linop.dense_operator(np.zeros((3, 3)))) == 0.0
+    with _pt.raises(linop.OperatorShapeError):
+        linop.op_norm_estimate(linop.dense_operator(np.ones((2, 3))))
+
+
+def test_public_regparam_pieces_match_reference_selection(golden):
+    """gcv_minimize / lcurve_corner(tikhonov_curve_points) reproduce the
+    reference's select_lambda values stored in the golden fixture."""
+    from paper_2602_17892_b200 import regparam as R
+    d = golden("solver_cases")
+    for i in range(4):
+        H = d[f"lam/{i}/H"]
+        s, u, _ = R.svd_of_hessenberg(H)
+        grid = R.lambda_grid(s)
+        assert R.gcv_minimize(s, u, 2.5, grid) == float(d[f"lam/{i}/gcv"])
+        pts = R.tikhonov_curve_points(s, u, 2.5, grid)
+        assert len(pts) == len(grid)
+        assert R.lcurve_corner(pts) == float(d[f"lam/{i}/lcurve"])
+        vals = R.gcv_values(s, u, 2.5, grid)
+        assert vals.shape == grid.shape and np.all(vals > 0)

@@ -127,7 +127,7 @@ __device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, co
 #endif
 
 template <int PPT, bool SPLIT>                      // pixels (rows) per thread
-__global__ void __launch_bounds__(BTHREADS, PPT == 2 ? 6 : CTK_BACK_MINB4) k_back(BackArgs A) {
+__global__ void __launch_bounds__(BTHREADS, PPT == 4 ? CTK_BACK_MINB4 : 6) k_back(BackArgs A) {
     constexpr int BTY = BROWS * PPT;
     extern __shared__ float2 win[];                // [BCA][wmax] (p, d)
     __shared__ int4 s_par[BCA];                    // T0, C, S, smem base of the window
@@ -413,10 +413,11 @@ int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
     A.center = g->center;
     A.xc = xc;
     dim3 grid((g->nx + BTX - 1) / BTX, back_tiles_y(g), S), block(BTX, BROWS);
-    const bool p4 = g->back_ppt == 4;
+    const int ppt = g->back_ppt;
     size_t smem = (size_t)BCA * g->back_wmax * sizeof(float2);
-    void (*kern)(BackArgs) = S > 1 ? (p4 ? k_back<4, true> : k_back<2, true>)
-                                   : (p4 ? k_back<4, false> : k_back<2, false>);
+    void (*kern)(BackArgs) =
+        S > 1 ? (ppt == 4 ? k_back<4, true> : ppt == 1 ? k_back<1, true> : k_back<2, true>)
+              : (ppt == 4 ? k_back<4, false> : ppt == 1 ? k_back<1, false> : k_back<2, false>);
     if (smem > 48 * 1024)
         CTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int ph = ctk_prof_open(1, st);
@@ -435,6 +436,8 @@ int ctk_xchg_finish(const ctk_geom* g, const ctk_xchg_args* xc, int nranks, int 
         const unsigned owned = (unsigned)((tiles + nranks - 1) / nranks);
         if (g->back_ppt == 4)
             k_xchg_reduce<4><<<owned, dim3(BTX, BROWS), 0, st>>>(xc, g->nx, g->ny, tiles_x);
+        else if (g->back_ppt == 1)
+            k_xchg_reduce<1><<<owned, dim3(BTX, BROWS), 0, st>>>(xc, g->nx, g->ny, tiles_x);
         else
             k_xchg_reduce<2><<<owned, dim3(BTX, BROWS), 0, st>>>(xc, g->nx, g->ny, tiles_x);
         CTK_LAUNCH_CHECK("k_xchg_reduce");

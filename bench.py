@@ -457,6 +457,8 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }
+        if spec.slices > 1:      # batched slices (c5): one slice solve per rank per step
+            line["slices_per_s"] = world * args.steps / (total_ms / 1e3)
         if "last" in result:
             last = result["last"]
             line["solve"] = {"stop_reason": last.stop_reason, "iterations": len(last.records),

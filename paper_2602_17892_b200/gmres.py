@@ -197,6 +197,8 @@ def _pinned(torch, name, shape, dtype, zero=True):
 
 
 _WORKSPACES: dict = {}
+_WORKSPACE_KEEP = 8                            # shapes x threads kept alive
+_CACHE_LOCK = threading.Lock()
 
 
 def _solve_workspace(torch, dg, ab, L, rows, K):
@@ -205,9 +207,9 @@ def _solve_workspace(torch, dg, ab, L, rows, K):
     host time than a c1 Arnoldi step).  Every buffer is written before it is
     read inside a solve (the reduction scratch resets its own tickets);
     x_cur is re-zeroed per solve.  Keeps the 4 most recent shapes."""
-    import threading as _th
-    key = (_th.get_ident(), id(dg), bool(ab), int(L), int(rows), int(K))
-    ws = _WORKSPACES.pop(key, None)
+    key = (threading.get_ident(), id(dg), bool(ab), int(L), int(rows), int(K))
+    with _CACHE_LOCK:
+        ws = _WORKSPACES.pop(key, None)
     if ws is None:
         f32, f64, dev = torch.float32, torch.float64, dg.dev
         n, m = dg.n, dg.m
@@ -229,20 +231,24 @@ def _solve_workspace(torch, dg, ab, L, rows, K):
             "y_dev": torch.zeros((K, rows), dtype=f64, device=dev),
             "norms": torch.zeros((K + 1, 2), dtype=f64, device=dev),
         }
-    _WORKSPACES[key] = ws                      # most recent last
-    while len(_WORKSPACES) > 4:
-        _WORKSPACES.pop(next(iter(_WORKSPACES)))
+    with _CACHE_LOCK:
+        _WORKSPACES[key] = ws                  # most recent last
+        while len(_WORKSPACES) > _WORKSPACE_KEEP:
+            _WORKSPACES.pop(next(iter(_WORKSPACES)))
     return ws
 
 
 def _side_stream(torch, dev, kind, priority):
     """Cached solver streams: the Arnoldi stream at the highest priority (it is
-    the critical path), the iterate stream at the lowest."""
-    key = (dev.index, kind)
-    s = _STREAMS.get(key)
-    if s is None:
-        s = torch.cuda.Stream(dev, priority=priority)
-        _STREAMS[key] = s
+    the critical path), the iterate stream at the lowest.  Per host thread, so
+    independent solves issued from different threads (batched slices) run
+    concurrently instead of serialising on one stream pair."""
+    key = (dev.index, kind, threading.get_ident())
+    with _CACHE_LOCK:
+        s = _STREAMS.get(key)
+        if s is None:
+            s = torch.cuda.Stream(dev, priority=priority)
+            _STREAMS[key] = s
     return s
 
 

@@ -295,3 +295,32 @@ def test_golub_kahan_solvers_vs_reference(cuda, golden, case):
         lam, lam_ref = records(res, "lambda_used"), d[f"{case}/rec/lambda_used"]
         assert np.all(np.abs(lam / lam_ref - 1.0) <= 0.01)
     assert rel(res.x, d[f"{case}/x"]) <= 2e-3
+
+
+def test_concurrent_solves_from_threads_match_sequential(cuda, golden):
+    """Independent slices solved from several host threads at once (each
+    thread has its own stream pair and workspaces) give bitwise the results
+    of the same solves run one after another."""
+    import threading
+    spec, z, b = config_b(golden, "c1")
+    A, B = ops_for(spec)
+    rng = np.random.default_rng(9)
+    bs = [b * (1.0 + 0.1 * i) + 0.01 * rng.standard_normal(b.size) for i in range(3)]
+    bs = [v.astype(np.float32).astype(np.float64) for v in bs]
+    cfg = gmres.SolverConfig(method="ab-hybrid", lambda_strategy="gcv", max_iter=20)
+    seq = [gmres.run_gmres(A, B, v, cfg) for v in bs]
+    out = [None] * len(bs)
+
+    def work(i):
+        out[i] = gmres.run_gmres(A, B, bs[i], cfg)
+
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(len(bs))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for a, c in zip(seq, out):
+        np.testing.assert_array_equal(a.x, c.x)
+        np.testing.assert_array_equal(records(a, "lambda_used"), records(c, "lambda_used"))
+        np.testing.assert_array_equal(records(a, "data_residual_norm"),
+                                      records(c, "data_residual_norm"))

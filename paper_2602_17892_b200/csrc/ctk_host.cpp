@@ -252,6 +252,10 @@ typedef void (*dbdsqr_t)(char* uplo, int* n, int* ncvt, int* nru, int* ncc, doub
                          double* vt, int* ldvt, double* u, int* ldu, double* c, int* ldc,
                          double* work, int* info);
 dbdsqr_t g_dbdsqr = nullptr;
+bool g_lapack_bdsqr = [] {
+    const char* e = getenv("CTK_LAPACK_BDSQR");    // 1: LAPACK dbdsqr instead of bdsvd()
+    return e && e[0] == '1';
+}();
 bool g_fast = [] {
     const char* e = getenv("CTK_LAPACK_SVD");      // 1: always the dgesdd path
     return !(e && e[0] == '1');
@@ -413,6 +417,116 @@ bool damped_bidiag_solve(std::vector<double> d, std::vector<double> e, std::vect
     return true;
 }
 
+// rotation (c, s, r) with c*y + s*z = r, -s*y + c*z = 0
+inline void rot(double y, double z, double* c, double* s, double* r) {
+    if (z == 0.0) {
+        *c = 1.0;
+        *s = 0.0;
+        *r = y;
+        return;
+    }
+    const double ss = y * y + z * z;
+    const double h = (ss > 1e-290 && ss < 1e290) ? sqrt(ss) : hypot(y, z);
+    const double inv = 1.0 / h;
+    *c = y * inv;
+    *s = z * inv;
+    *r = h;
+}
+// Singular values of the upper bidiagonal B (d[0..n-1], e[0..n-2]) with the
+// left rotations applied to one vector: on return d = singular values
+// (descending), g = U^T g up to per-entry signs.  Golub-Kahan implicit-shift
+// QR (Wilkinson shift from the trailing 2x2 of B^T B), bulge chased top to
+// bottom, deflation when |e_i| <= eps (|d_i| + |d_i+1|), zero diagonals
+// rotated out (Golub & Van Loan, Alg. 8.6.2).  It replaces LAPACK dbdsqr with
+// ncc = 1, which spends most of its time in per-rotation dlartg/drot calls.
+// Returns 0, or 1 if it did not converge (the caller falls back to dgesdd).
+int bdsvd(int n, double* d, double* e, double* g) {
+    const double eps = std::numeric_limits<double>::epsilon();
+    double anorm = 0.0;
+    for (int i = 0; i < n; ++i)
+        anorm = std::max(anorm, fabs(d[i]) + (i + 1 < n ? fabs(e[i]) : 0.0));
+    const double dtol = eps * anorm;
+    int q = n - 1, iter = 0;
+    const int maxit = 30 * n * n;
+    while (q > 0) {
+        if (++iter > maxit) return 1;
+        // deflation at the bottom
+        if (fabs(e[q - 1]) <= eps * (fabs(d[q - 1]) + fabs(d[q])) || fabs(e[q - 1]) <= 1e-300) {
+            e[q - 1] = 0.0;
+            --q;
+            continue;
+        }
+        int p = q - 1;
+        while (p > 0) {
+            if (fabs(e[p - 1]) <= eps * (fabs(d[p - 1]) + fabs(d[p]))) {
+                e[p - 1] = 0.0;
+                break;
+            }
+            --p;
+        }
+        // zero diagonal inside the block
+        int zi = -1;
+        for (int i = p; i <= q; ++i)
+            if (fabs(d[i]) <= dtol) {
+                zi = i;
+                break;
+            }
+        if (zi >= 0) {
+            d[zi] = 0.0;
+            if (zi < q) {       // chase e[zi] right with left rotations (rows j, zi)
+                double f = e[zi]; e[zi] = 0.0;
+                for (int j = zi + 1; j <= q && f != 0.0; ++j) {
+                    double c, s, r; rot(d[j], f, &c, &s, &r);
+                    d[j] = r;
+                    const double gj = g[j], gi = g[zi];
+                    g[j] = c * gj + s * gi; g[zi] = -s * gj + c * gi;
+                    if (j < q) { f = -s * e[j]; e[j] = c * e[j]; }
+                }
+            } else {            // d[q] == 0: chase e[q-1] up with right rotations (columns k, q)
+                double f = e[q - 1]; e[q - 1] = 0.0;
+                for (int k = q - 1; k >= p && f != 0.0; --k) {
+                    double c, s, r; rot(d[k], f, &c, &s, &r);
+                    d[k] = r;
+                    if (k > p) { f = -s * e[k - 1]; e[k - 1] = c * e[k - 1]; }
+                }
+            }
+            continue;
+        }
+        // Wilkinson shift from the trailing 2x2 of B^T B
+        const double dm = d[q - 1], em = e[q - 1], dq = d[q];
+        const double t11 = dm * dm + (q - 1 > p ? e[q - 2] * e[q - 2] : 0.0);
+        const double t12 = dm * em, t22 = dq * dq + em * em;
+        const double dl = 0.5 * (t11 - t22);
+        const double den = dl + copysign(sqrt(dl * dl + t12 * t12), dl);
+        const double mu = den != 0.0 ? t22 - t12 * t12 / den : t22 - fabs(t12);
+        double y = d[p] * d[p] - mu, z = d[p] * e[p];
+        for (int k = p; k < q; ++k) {
+            double c, s, r;
+            rot(y, z, &c, &s, &r);                   // right: columns k, k+1
+            if (k > p) e[k - 1] = r;
+            double a = d[k], b = e[k];
+            d[k] = c * a + s * b; e[k] = -s * a + c * b;
+            const double bl = s * d[k + 1];
+            d[k + 1] = c * d[k + 1];
+            rot(d[k], bl, &c, &s, &r);              // left: rows k, k+1
+            d[k] = r;
+            a = e[k]; b = d[k + 1];
+            e[k] = c * a + s * b; d[k + 1] = -s * a + c * b;
+            if (k + 1 < q) { z = s * e[k + 1]; e[k + 1] = c * e[k + 1]; }
+            y = e[k];
+            const double g0 = g[k], g1 = g[k + 1];
+            g[k] = c * g0 + s * g1; g[k + 1] = -s * g0 + c * g1;
+        }
+    }
+    for (int i = 0; i < n; ++i) d[i] = fabs(d[i]);
+    // sort descending (insertion sort; n is small), g alongside
+    for (int i = 1; i < n; ++i) {
+        const double dv = d[i], gv = g[i]; int j = i - 1;
+        while (j >= 0 && d[j] < dv) { d[j + 1] = d[j]; g[j + 1] = g[j]; --j; }
+        d[j + 1] = dv; g[j + 1] = gv;
+    }
+    return 0;
+}
 // 0 = done, 1 = fall back to the dgesdd path (lam == 0 and rank deficient, or
 // dbdsqr unavailable / failed).
 int projected_fast(const double* H, int k, double beta, int strategy, double fixed_value,
@@ -422,13 +536,17 @@ int projected_fast(const double* H, int k, double beta, int strategy, double fix
     Bidiag bd;
     bidiagonalize(H, m, n, beta, bd);
     std::vector<double> sv(bd.d), ee(bd.e), c(bd.g.begin(), bd.g.begin() + n);
-    std::vector<double> work(4 * (size_t)n + 4);
-    char uplo = 'U';
-    int nn = n, ncvt = 0, nru = 0, ncc = 1, ldvt = 1, ldu = 1, ldc = n, info = 0;
-    double dummy = 0.0;
-    g_dbdsqr(&uplo, &nn, &ncvt, &nru, &ncc, sv.data(), ee.data(), &dummy, &ldvt, &dummy, &ldu,
-             c.data(), &ldc, work.data(), &info);
-    if (info != 0) return 1;
+    if (g_lapack_bdsqr) {
+        std::vector<double> work(4 * (size_t)n + 4);
+        char uplo = 'U';
+        int nn = n, ncvt = 0, nru = 0, ncc = 1, ldvt = 1, ldu = 1, ldc = n, info = 0;
+        double dummy = 0.0;
+        g_dbdsqr(&uplo, &nn, &ncvt, &nru, &ncc, sv.data(), ee.data(), &dummy, &ldvt, &dummy,
+                 &ldu, c.data(), &ldc, work.data(), &info);
+        if (info != 0) return 1;
+    } else if (bdsvd(n, sv.data(), ee.data(), c.data()) != 0) {
+        return 1;
+    }
     // c = U^T (beta e1) up to per-column signs, which the filter-factor
     // formulas square away: the same (s, c) as beta * U[0, :] of the reference SVD.
     double lam = 0.0;

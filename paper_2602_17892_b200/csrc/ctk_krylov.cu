@@ -524,39 +524,58 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
 }
 
 // partial[j * G + b] = <Ws[j], v> over this CTA's chunk (row vrow is v
-// itself: pass vrow = nrows - 1 to fold ||v||^2 in).  Four rows per warp are
-// in flight at once (independent fp64 accumulators).
+// itself: pass vrow = nrows - 1 to fold ||v||^2 in).  vd is v widened to fp64
+// once (SMEM), so only the basis elements go through the conversion pipe.
+// Up to four rows per warp are in flight at once (independent fp64
+// accumulators); the warp's row count is exact (no clamped duplicate rows).
 constexpr int GS_DR = 4;
 
-__device__ __forceinline__ void smem_dots(const float* Ws, int cpad, int nrows, int vrow,
-                                          const float* v, int cn, double* partial) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+template <int NR>
+__device__ __forceinline__ void smem_dots_rows(const float* Ws, int cpad, int j0, int vrow,
+                                               const float* v, const double* vd, int cn,
+                                               double* partial) {
+    const int lane = threadIdx.x & 31;
     const int cn4 = cn >> 2;
-    const float4* v4 = reinterpret_cast<const float4*>(v);
+    const double2* vd2 = reinterpret_cast<const double2*>(vd);
+    const float* row[NR];
+    double s[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        const int j = j0 + r * SW;
+        row[r] = j == vrow ? v : Ws + (size_t)j * cpad;
+        s[r] = 0.0;
+    }
+    for (int i = lane; i < cn4; i += 32) {
+        const double2 a = vd2[2 * i], b = vd2[2 * i + 1];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const float4 w = reinterpret_cast<const float4*>(row[r])[i];
+            s[r] = fma((double)w.x, a.x, s[r]);
+            s[r] = fma((double)w.y, a.y, s[r]);
+            s[r] = fma((double)w.z, b.x, s[r]);
+            s[r] = fma((double)w.w, b.y, s[r]);
+        }
+    }
+    for (int i = (cn4 << 2) + lane; i < cn; i += 32)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) s[r] = fma((double)row[r][i], vd[i], s[r]);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        const double t = warp_sum(s[r]);
+        if (lane == 0) partial[(size_t)(j0 + r * SW) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+__device__ __forceinline__ void smem_dots(const float* Ws, int cpad, int nrows, int vrow,
+                                          const float* v, const double* vd, int cn,
+                                          double* partial) {
+    const int warp = threadIdx.x >> 5;
     for (int j0 = warp; j0 < nrows; j0 += SW * GS_DR) {
-        const float* row[GS_DR];
-        double s[GS_DR];
-#pragma unroll
-        for (int r = 0; r < GS_DR; ++r) {
-            const int j = min(j0 + r * SW, nrows - 1);
-            row[r] = j == vrow ? v : Ws + (size_t)j * cpad;
-            s[r] = 0.0;
-        }
-        for (int i = lane; i < cn4; i += 32) {
-            const float4 vv = v4[i];
-#pragma unroll
-            for (int r = 0; r < GS_DR; ++r)
-                s[r] = dot4(reinterpret_cast<const float4*>(row[r])[i], vv, s[r]);
-        }
-        for (int i = (cn4 << 2) + lane; i < cn; i += 32)
-#pragma unroll
-            for (int r = 0; r < GS_DR; ++r) s[r] = fma((double)row[r][i], (double)v[i], s[r]);
-#pragma unroll
-        for (int r = 0; r < GS_DR; ++r) {
-            const double t = warp_sum(s[r]);
-            const int j = j0 + r * SW;
-            if (lane == 0 && j < nrows) partial[(size_t)j * gridDim.x + blockIdx.x] = t;
-        }
+        const int nr = (nrows - j0 + SW - 1) / SW;      // rows j0, j0 + SW, ... below nrows
+        if (nr >= 4) smem_dots_rows<4>(Ws, cpad, j0, vrow, v, vd, cn, partial);
+        else if (nr == 3) smem_dots_rows<3>(Ws, cpad, j0, vrow, v, vd, cn, partial);
+        else if (nr == 2) smem_dots_rows<2>(Ws, cpad, j0, vrow, v, vd, cn, partial);
+        else smem_dots_rows<1>(Ws, cpad, j0, vrow, v, vd, cn, partial);
     }
 }
 
@@ -599,7 +618,7 @@ __device__ __forceinline__ void all_reduce_rows(const double* partial, int nrows
 // ngrp = ST / cn4 thread groups (row j -> group j % ngrp) whose fp64 partial
 // sums meet in SMEM (acc[g][i]) and are added in group order.
 __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb, const double* c,
-                                              float* v, int cn, double4* acc) {
+                                              float* v, double* vd, int cn, double4* acc) {
     const int cn4 = cn >> 2;
     int ngrp = cn4 > 0 ? ST / cn4 : 1;
     ngrp = ngrp < 1 ? 1 : (ngrp > 8 ? 8 : ngrp);
@@ -617,14 +636,20 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
             }
             const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
             reinterpret_cast<float4*>(v)[t] = o;
-            nrm = fma((double)o.x, (double)o.x, nrm); nrm = fma((double)o.y, (double)o.y, nrm);
-            nrm = fma((double)o.z, (double)o.z, nrm); nrm = fma((double)o.w, (double)o.w, nrm);
+            const double4 od = make_double4(o.x, o.y, o.z, o.w);
+            if (vd) {
+                reinterpret_cast<double2*>(vd)[2 * t] = make_double2(od.x, od.y);
+                reinterpret_cast<double2*>(vd)[2 * t + 1] = make_double2(od.z, od.w);
+            }
+            nrm = fma(od.x, od.x, nrm); nrm = fma(od.y, od.y, nrm);
+            nrm = fma(od.z, od.z, nrm); nrm = fma(od.w, od.w, nrm);
         }
         for (int t = (cn4 << 2) + threadIdx.x; t < cn; t += ST) {
             double a = (double)v[t];
             for (int j = 0; j < nb; ++j) a = fma(-c[j], (double)Ws[(size_t)j * cpad + t], a);
             const float o = (float)a;
             v[t] = o;
+            if (vd) vd[t] = (double)o;
             nrm = fma((double)o, (double)o, nrm);
         }
         return nrm;
@@ -653,14 +678,20 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
         }
         const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
         reinterpret_cast<float4*>(v)[t] = o;
-        nrm = fma((double)o.x, (double)o.x, nrm); nrm = fma((double)o.y, (double)o.y, nrm);
-        nrm = fma((double)o.z, (double)o.z, nrm); nrm = fma((double)o.w, (double)o.w, nrm);
+        const double4 od = make_double4(o.x, o.y, o.z, o.w);
+        if (vd) {
+            reinterpret_cast<double2*>(vd)[2 * t] = make_double2(od.x, od.y);
+            reinterpret_cast<double2*>(vd)[2 * t + 1] = make_double2(od.z, od.w);
+        }
+        nrm = fma(od.x, od.x, nrm); nrm = fma(od.y, od.y, nrm);
+        nrm = fma(od.z, od.z, nrm); nrm = fma(od.w, od.w, nrm);
     }
     for (int t = (cn4 << 2) + threadIdx.x; t < cn; t += ST) {
         double a = (double)v[t];
         for (int j = 0; j < nb; ++j) a = fma(-c[j], (double)Ws[(size_t)j * cpad + t], a);
         const float o = (float)a;
         v[t] = o;
+        if (vd) vd[t] = (double)o;
         nrm = fma((double)o, (double)o, nrm);
     }
     return nrm;
@@ -669,6 +700,17 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
 // tm (when use_tma): 3-D tensor map over the basis rows as 64-float panels,
 // dims {64, panels, k+1}; one box {64, chunk / 64, k+1} is this CTA's whole
 // [k+1][chunk] block -- one TMA copy instead of k+1 row copies.
+#ifdef CTK_GS_PROF
+__device__ unsigned long long g_gs_prof[160 * 16];
+#define GS_STAMP(i) do { if (threadIdx.x == 0) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_gs_prof[blockIdx.x * 16 + (i)] = t_; } } while (0)
+extern "C" int ctk_gs_prof_read(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, g_gs_prof, sizeof(g_gs_prof)) == cudaSuccess ? 0 : -1;
+}
+#else
+#define GS_STAMP(i) do {} while (0)
+#endif
+
 __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, int64_t L,
                                                    const float* __restrict__ q, int passes,
                                                    int64_t chunk, double* h, double* stat,
@@ -676,6 +718,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
                                                    double* hm, int stat_off, int use_tma,
                                                    const __grid_constant__ CUtensorMap tm) {
     cg::grid_group grid = cg::this_grid();
+    GS_STAMP(0);
     ctk_pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nb = k + 1;
@@ -689,7 +732,8 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     double* red = h2 + nb + 1;                                      // [SW]
     float* qv = reinterpret_cast<float*>(
         smem_raw + ((16 + sizeof(double) * (2 * nb + 2 + SW) + 15) & ~(size_t)15));
-    unsigned char* ws_raw = reinterpret_cast<unsigned char*>(qv + cpad);
+    double* qd = reinterpret_cast<double*>(qv + cpad);               // [cpad]: qv in fp64
+    unsigned char* ws_raw = reinterpret_cast<unsigned char*>(qd + cpad);
     ws_raw += (128u - (smem_u32(ws_raw) & 127u)) & 127u;           // TMA destination alignment
     float* Ws = reinterpret_cast<float*>(ws_raw);                   // [nb][cpad]
     double4* acc = reinterpret_cast<double4*>(                      // [ST], 32-B aligned
@@ -701,7 +745,8 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    ctk_pdl_wait();                  // q (and, transitively, the basis) from the previous kernels
+    ctk_pdl_wait();
+    GS_STAMP(1);                     // q (and, transitively, the basis) from the previous kernels
     if (use_tma) {
         if (threadIdx.x == 0 && row_bytes > 0) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a),
@@ -727,27 +772,40 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
                 "l"(W + (size_t)j * ld + start), "r"(row_bytes), "r"(bar_a)
                 : "memory");
     }
-    for (int i = threadIdx.x; i < cn; i += ST) qv[i] = q[start + i];   // (16-B alignment of q
-    if (row_bytes > 0) mbar_wait(bar_a, 0);                          //  not assumed here)
+    for (int i = threadIdx.x; i < cn; i += ST) {                     // (16-B alignment of q
+        const float v = q[start + i];
+        qv[i] = v;
+        qd[i] = v;
+    }                                                                //  not assumed here)
+    if (row_bytes > 0) mbar_wait(bar_a, 0);
     __syncthreads();
+    GS_STAMP(2);
 
     double* P1 = partial;                                    // [nb + 1][G]
     double* P2 = P1 + (size_t)(nb + 1) * gridDim.x;          // [nb + 1][G]
     double* P3 = P2 + (size_t)(nb + 1) * gridDim.x;          // [G]
-    smem_dots(Ws, cpad, nb + 1, nb, qv, cn, P1);             // h1 = W^T q, ||q||^2
+    smem_dots(Ws, cpad, nb + 1, nb, qv, qd, cn, P1);             // h1 = W^T q, ||q||^2
+    GS_STAMP(3);
     grid.sync();
+    GS_STAMP(4);
     all_reduce_rows(P1, nb + 1, h1);
     __syncthreads();
-    double nrm = smem_update(Ws, cpad, nb, h1, qv, cn, acc);      // q1 = q - W h1
+    GS_STAMP(5);
+    double nrm = smem_update(Ws, cpad, nb, h1, qv, qd, cn, acc);      // q1 = q - W h1
+    GS_STAMP(6);
     __shared__ double s_n2;
     bool need_norm = true;
     if (passes == 2) {
         __syncthreads();
-        smem_dots(Ws, cpad, nb + 1, nb, qv, cn, P2);         // h2 = W^T q1, ||q1||^2
+        smem_dots(Ws, cpad, nb + 1, nb, qv, qd, cn, P2);         // h2 = W^T q1, ||q1||^2
+        GS_STAMP(7);
         grid.sync();
+        GS_STAMP(8);
         all_reduce_rows(P2, nb + 1, h2);
         __syncthreads();
-        nrm = smem_update(Ws, cpad, nb, h2, qv, cn, acc);         // q2 = q1 - W h2
+        GS_STAMP(9);
+        nrm = smem_update(Ws, cpad, nb, h2, qv, nullptr, cn, acc);         // q2 = q1 - W h2
+        GS_STAMP(10);
         // ||q2||^2 = ||q1||^2 - ||h2||^2 for orthonormal W: after the first pass
         // h2 is at rounding level, so there is no cancellation and the third
         // grid-wide reduction is skipped.  Every CTA holds the same h2, so the
@@ -809,6 +867,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
             }
         }
     }
+    GS_STAMP(11);
 }
 
 // ---------------------------------------------------------------------------
@@ -1187,7 +1246,8 @@ static bool encode_rows(CUtensorMap* m, const float* base, int64_t L, int64_t ld
 static size_t gs_smem_bytes(int k, int64_t chunk) {
     const int nb = k + 1;
     const size_t head = (16 + sizeof(double) * (2 * (size_t)nb + 2 + SW) + 15) & ~(size_t)15;
-    return head + sizeof(float) * (size_t)chunk * (nb + 1) + sizeof(double) * 4 * ST + 32 + 128;
+    return head + sizeof(float) * (size_t)chunk * (nb + 1) + sizeof(double) * (size_t)chunk +
+           sizeof(double) * 4 * ST + 32 + 128;
 }
 
 static bool gs_smem_plan(int64_t L, int k, int64_t* Gp, int64_t* chunkp, size_t* smemp) {

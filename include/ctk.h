@@ -166,6 +166,17 @@ int ctk_iterate(const ctk_geom_t* g, int ab, const float* W, int64_t ld, int k,
                 const float* aux2, int64_t ld2, const float* d0, float* stage_work,
                 float* back_work, void* scratch, void* stream);
 
+/* Batched iterate norms for nb (<= 8) consecutive iterations k0 .. k0+nb-1 of
+ * one cycle (the linear iterate path of ctk_iterate): with y_b = y + b*ystride
+ * (device, k0+b entries), norms[2b] = ||d0 - AX y_b||^2 and
+ * norms[2b+1] = ||x0 + X y_b||^2, and the last iterate of the batch stored to
+ * x / r (either may be NULL).  One pass over the basis for the whole batch.
+ * scratch: ctk_reduce_scratch_bytes(nvec_cap, .) bytes, zero-filled once. */
+int ctk_iterate_batch(const float* X, int64_t ldx, const float* x0, float* x, int64_t Lx,
+                      const float* AX, int64_t ldax, const float* d0, float* r, int64_t Lr,
+                      int k0, int nb, const double* y, int ystride, double* norms,
+                      void* scratch, int nvec_cap, void* stream);
+
 /* ---- Native (hybrid) AB-/BA-GMRES driver: the run_gmres loop
  * (ctkrylov/gmres.py:135-241) without Python per iteration.  Stopping rules
  * none / dp / rns; restarts; breakdown; degenerate-curve fallback.  All

@@ -58,6 +58,9 @@ SIGNATURES = {
     "ctk_iterate": (_c.c_int, [_vp, _c.c_int, _fp, _c.c_int64, _c.c_int, _dp, _dp, _fp, _fp, _fp,
                                _fp, _fp, _dp, _fp, _c.c_int64, _fp, _c.c_int64, _fp,
                                _fp, _fp, _vp, _vp]),
+    "ctk_iterate_batch": (_c.c_int, [_fp, _c.c_int64, _fp, _fp, _c.c_int64, _fp, _c.c_int64,
+                                     _fp, _fp, _c.c_int64, _c.c_int, _c.c_int, _dp, _c.c_int, _dp,
+                                     _vp, _c.c_int, _vp]),
     "ctk_set_lapack": (_c.c_int, [_vp, _vp]),
     "ctk_set_lapack_extra": (_c.c_int, [_vp]),
     "ctk_set_svd_path": (_c.c_int, [_c.c_int]),

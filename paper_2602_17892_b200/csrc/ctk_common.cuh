@@ -175,6 +175,7 @@ int ctk_combine_pair(const float* X, int64_t ldx, const float* x0, float* x, int
                      double* n_x, const float* AX, int64_t ldax, const float* d0, float* r,
                      int64_t Lr, double* n_r, int k, const double* y, void* scratch,
                      void* stream, const double* y_host);
+bool ctk_iterate_batch_ok(int k0, int nb, int nvec_cap, int64_t Lx, int64_t Lr);
 int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1, const float* b,
                    float* work, bool prestaged, void* stream);
 int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,

@@ -27,6 +27,8 @@
 
 namespace {
 
+constexpr int IB_BATCH = 8;         // iterates per ctk_iterate_batch launch
+
 struct Job {
     int k = 0;
     std::vector<double> H;      // (k+1) x k row-major
@@ -199,6 +201,10 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
     std::vector<double> history;
     std::vector<int> rec_slot;                        // record -> norms slot (-1: host-known)
     auto t0 = std::chrono::steady_clock::now();
+    const char* ib_env = getenv("CTK_ITER_BATCH");          // 0: one iterate per launch
+    const bool can_batch = !(ib_env && ib_env[0] == '0') && bf->aux1 && bf->d0 &&
+                           (!ab || bf->aux2) && !bf->x_true && bf->snapshot_stride <= 0 &&
+                           cfg->stopping == CTK_STOP_NONE;
     bool first = true;
     int rc;
     while (stop == CTK_STOP_NONE && nrec < K) {
@@ -281,6 +287,29 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
         ++cycles;
         std::vector<double> Hfull((size_t)(steps + 1) * steps, 0.0);
         int done_k = 0, last_k = steps, broke_at = -1;
+        // Batched iterate norms (no per-iterate consumer: no x_true metrics,
+        // snapshots or per-iteration stopping rule): up to IB_BATCH iterates
+        // share one pass over the basis (ctk_iterate_batch); xk / r hold the
+        // batch's last iterate, so the cycle ends with x_k of its last step.
+        int pend_n = 0, pend_slot0 = 0;
+        auto flush = [&](int k_last) -> int {
+            const int nb = pend_n, k0 = k_last - nb + 1;
+            pend_n = 0;
+            CTK_CUDA(cudaStreamWaitEvent(sb, ev_h[k_last - 1], 0));
+            CTK_CUDA(cudaMemcpyAsync(bf->y_dev + (size_t)pend_slot0 * bf->rows,
+                                     bf->y_host + (size_t)pend_slot0 * bf->rows,
+                                     sizeof(double) * (size_t)bf->rows * nb, cudaMemcpyHostToDevice,
+                                     sb));
+            int r2 = ctk_iterate_batch(ab ? bf->aux1 : bf->W, ab ? bf->ld1 : bf->ld, bf->x_cur,
+                                       bf->xk, n, ab ? bf->aux2 : bf->aux1, ab ? bf->ld2 : bf->ld1,
+                                       bf->d0, bf->r, m, k0, nb,
+                                       bf->y_dev + (size_t)pend_slot0 * bf->rows, bf->rows,
+                                       bf->norms + 2 * (size_t)pend_slot0, bf->scratch_b,
+                                       bf->rows + 2, bf->stream_b);
+            if (r2) return r2;
+            for (int q = 0; q < nb; ++q) CTK_CUDA(cudaEventRecord(ev_it[pend_slot0 + q], sb));
+            return CTK_OK;
+        };
         auto consume = [&](int k) -> int {
             auto& job = jobs[k];
             const auto tw0 = std::chrono::steady_clock::now();
@@ -314,24 +343,35 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
             const int slot = nrec;
             double* yh = bf->y_host + (size_t)slot * bf->rows;
             memcpy(yh, y, sizeof(double) * k);
-            CTK_CUDA(cudaStreamWaitEvent(sb, ev_h[k - 1], 0));
-            int r2 = ctk_iterate(g, ab, bf->W, bf->ld, k, yh, bf->y_dev + (size_t)slot * bf->rows,
-                                 bf->x_cur, bf->xk, bf->z, bf->b, bf->r, bf->norms + 2 * slot,
-                                 bf->aux1, bf->ld1, bf->aux2, bf->ld2, bf->d0,
-                                 bf->stage_b, bf->back_b, bf->scratch_b, bf->stream_b);
-            if (r2) return r2;
-            if (bf->x_true) {       // device-side RRE / SSIM of x_k (row f1)
-                int r3 = ctk_metrics(bf->xk, bf->x_true, bf->img_nx, bf->img_ny, bf->dyn_range,
-                                     bf->metrics + 2 * slot, bf->scratch_m, bf->stream_b);
-                if (r3) return r3;
+            const bool batched = can_batch && ctk_iterate_batch_ok(k - pend_n, pend_n + 1,
+                                                                   bf->rows + 2, n, m);
+            if (!batched && pend_n > 0 && (rc = flush(k - 1))) return rc;
+            if (batched) {
+                if (pend_n == 0) pend_slot0 = slot;
+                ++pend_n;
+                if (pend_n == IB_BATCH || k == steps || k == broke_at) {
+                    if ((rc = flush(k))) return rc;
+                }
+            } else {
+                CTK_CUDA(cudaStreamWaitEvent(sb, ev_h[k - 1], 0));
+                int r2 = ctk_iterate(g, ab, bf->W, bf->ld, k, yh, bf->y_dev + (size_t)slot * bf->rows,
+                                     bf->x_cur, bf->xk, bf->z, bf->b, bf->r, bf->norms + 2 * slot,
+                                     bf->aux1, bf->ld1, bf->aux2, bf->ld2, bf->d0,
+                                     bf->stage_b, bf->back_b, bf->scratch_b, bf->stream_b);
+                if (r2) return r2;
+                if (bf->x_true) {       // device-side RRE / SSIM of x_k (row f1)
+                    int r3 = ctk_metrics(bf->xk, bf->x_true, bf->img_nx, bf->img_ny, bf->dyn_range,
+                                         bf->metrics + 2 * slot, bf->scratch_m, bf->stream_b);
+                    if (r3) return r3;
+                }
+                if (bf->snapshot_stride > 0 && (slot + 1) % bf->snapshot_stride == 0) {
+                    const int si = (slot + 1) / bf->snapshot_stride - 1;
+                    if (si < bf->n_snaps)
+                        CTK_CUDA(cudaMemcpyAsync(bf->snaps[si], bf->xk, sizeof(float) * n,
+                                                 cudaMemcpyDeviceToHost, sb));
+                }
+                CTK_CUDA(cudaEventRecord(ev_it[slot], sb));
             }
-            if (bf->snapshot_stride > 0 && (slot + 1) % bf->snapshot_stride == 0) {
-                const int si = (slot + 1) / bf->snapshot_stride - 1;
-                if (si < bf->n_snaps)
-                    CTK_CUDA(cudaMemcpyAsync(bf->snaps[si], bf->xk, sizeof(float) * n,
-                                             cudaMemcpyDeviceToHost, sb));
-            }
-            CTK_CUDA(cudaEventRecord(ev_it[slot], sb));
             out->k[slot] = slot + 1;
             out->lambda[slot] = lam;
             out->proj_residual[slot] = proj;

@@ -315,10 +315,111 @@ CTK_HOT void col_axpy(double alpha, const double* x, double* y, int n) {
     for (int r = 0; r < n; ++r) y[r] += alpha * x[r];
 }
 
+// Four columns at a time (column-major, leading dimension ld): the per-column
+// loop overhead, not the flops, bounded the unblocked kernels at k ~ 80.
+// A[:, j] -= tau (v . A[:, j]) v for j < nc.  The four dot products of a
+// column group share each load of v: AVX2/FMA when the CPU has it (checked
+// once), else a portable loop.
+#if defined(__x86_64__) && defined(__GNUC__) && !defined(__clang__)
+#include <immintrin.h>
+__attribute__((target("avx2,fma"))) void dots4_avx2(const double* v, const double* c0, int ld,
+                                                   int len, double* out) {
+    const double *c1 = c0 + ld, *c2 = c1 + ld, *c3 = c2 + ld;
+    __m256d a0 = _mm256_setzero_pd(), a1 = a0, a2 = a0, a3 = a0;
+    int r = 0;
+    for (; r + 4 <= len; r += 4) {
+        const __m256d vv = _mm256_loadu_pd(v + r);
+        a0 = _mm256_fmadd_pd(vv, _mm256_loadu_pd(c0 + r), a0);
+        a1 = _mm256_fmadd_pd(vv, _mm256_loadu_pd(c1 + r), a1);
+        a2 = _mm256_fmadd_pd(vv, _mm256_loadu_pd(c2 + r), a2);
+        a3 = _mm256_fmadd_pd(vv, _mm256_loadu_pd(c3 + r), a3);
+    }
+    // horizontal sums of the four accumulators at once
+    const __m256d s01 = _mm256_hadd_pd(a0, a1), s23 = _mm256_hadd_pd(a2, a3);
+    const __m256d t = _mm256_add_pd(_mm256_permute2f128_pd(s01, s23, 0x20),
+                                    _mm256_permute2f128_pd(s01, s23, 0x31));
+    _mm256_storeu_pd(out, t);
+    for (; r < len; ++r) {
+        out[0] += v[r] * c0[r];
+        out[1] += v[r] * c1[r];
+        out[2] += v[r] * c2[r];
+        out[3] += v[r] * c3[r];
+    }
+}
+const bool g_avx2 = [] {
+    __builtin_cpu_init();       // runs in a static initializer: set up the CPU model first
+    return __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
+}();
+#else
+const bool g_avx2 = false;
+void dots4_avx2(const double*, const double*, int, int, double*) {}
+#endif
+
+void dots4(const double* v, const double* c0, int ld, int len, double* out) {
+    if (g_avx2) return dots4_avx2(v, c0, ld, len, out);
+    for (int q = 0; q < 4; ++q) out[q] = col_dot(v, c0 + (size_t)q * ld, len);
+}
+
+CTK_HOT void left_update(const double* v, double* A, int ld, int nc, int len, double tau) {
+    int j = 0;
+    for (; j + 4 <= nc; j += 4) {
+        double* c0 = A + (size_t)j * ld;
+        double *c1 = c0 + ld, *c2 = c1 + ld, *c3 = c2 + ld;
+        double sd[4];
+        dots4(v, c0, ld, len, sd);
+        const double s0 = -tau * sd[0], s1 = -tau * sd[1], s2 = -tau * sd[2], s3 = -tau * sd[3];
+        for (int r = 0; r < len; ++r) {
+            const double vv = v[r];
+            c0[r] += s0 * vv;
+            c1[r] += s1 * vv;
+            c2[r] += s2 * vv;
+            c3[r] += s3 * vv;
+        }
+    }
+    for (; j < nc; ++j) {
+        double* col = A + (size_t)j * ld;
+        col_axpy(-tau * col_dot(v, col, len), v, col, len);
+    }
+}
+
+// w = A[:, 0:nc] x (x[j] = the right reflector's entries).
+CTK_HOT void gemv_cols(const double* A, int ld, int nc, int len, const double* x, double* w) {
+    for (int r = 0; r < len; ++r) w[r] = 0.0;
+    int j = 0;
+    for (; j + 4 <= nc; j += 4) {
+        const double* c0 = A + (size_t)j * ld;
+        const double *c1 = c0 + ld, *c2 = c1 + ld, *c3 = c2 + ld;
+        const double x0 = x[j], x1 = x[j + 1], x2 = x[j + 2], x3 = x[j + 3];
+        for (int r = 0; r < len; ++r) w[r] += (x0 * c0[r] + x1 * c1[r]) + (x2 * c2[r] + x3 * c3[r]);
+    }
+    for (; j < nc; ++j) col_axpy(x[j], A + (size_t)j * ld, w, len);
+}
+
+// A[:, j] -= tau x[j] w for j < nc.
+CTK_HOT void rank1_cols(double* A, int ld, int nc, int len, const double* x, const double* w,
+                        double tau) {
+    int j = 0;
+    for (; j + 4 <= nc; j += 4) {
+        double* c0 = A + (size_t)j * ld;
+        double *c1 = c0 + ld, *c2 = c1 + ld, *c3 = c2 + ld;
+        const double a0 = -tau * x[j], a1 = -tau * x[j + 1], a2 = -tau * x[j + 2],
+                     a3 = -tau * x[j + 3];
+        for (int r = 0; r < len; ++r) {
+            const double ww = w[r];
+            c0[r] += a0 * ww;
+            c1[r] += a1 * ww;
+            c2[r] += a2 * ww;
+            c3[r] += a3 * ww;
+        }
+    }
+    for (; j < nc; ++j) col_axpy(-tau * x[j], w, A + (size_t)j * ld, len);
+}
+
 struct Bidiag {
     int m = 0, n = 0;
     std::vector<double> A;      // m x n column-major, right reflectors stored in rows
     std::vector<double> d, e, taup, g;
+    std::vector<double> tmp;    // the current right reflector, contiguous
 };
 
 // H (m x n row-major) -> B = diag d + superdiag e; g = Q^T (beta e1).
@@ -342,10 +443,7 @@ void bidiagonalize(const double* H, int m, int n, double beta, Bidiag& bd) {
         householder(&at(i, i), m - i, 1, &tq, &b);
         if (tq != 0.0) {
             const double* v = &at(i, i);
-            for (int j = i + 1; j < n; ++j) {
-                double* col = &at(i, j);
-                col_axpy(-tq * col_dot(v, col, m - i), v, col, m - i);
-            }
+            left_update(v, &at(i, i + 1), m, n - i - 1, m - i, tq);
             col_axpy(-tq * col_dot(v, &bd.g[i], m - i), v, &bd.g[i], m - i);
         }
         bd.d[i] = b;
@@ -357,9 +455,12 @@ void bidiagonalize(const double* H, int m, int n, double beta, Bidiag& bd) {
             bd.e[i] = b2;
             if (tp != 0.0) {
                 // w = A(i+1:, i+1:) v by columns (contiguous), then the rank-1 update
-                for (int r = i + 1; r < m; ++r) w[r] = 0.0;
-                for (int j = i + 1; j < n; ++j) col_axpy(at(i, j), &at(i + 1, j), &w[i + 1], m - i - 1);
-                for (int j = i + 1; j < n; ++j) col_axpy(-tp * at(i, j), &w[i + 1], &at(i + 1, j), m - i - 1);
+                const int nc = n - i - 1, len = m - i - 1;
+                std::vector<double>& x = bd.tmp;
+                x.resize(nc);
+                for (int j = 0; j < nc; ++j) x[j] = at(i, i + 1 + j);
+                gemv_cols(&at(i + 1, i + 1), m, nc, len, x.data(), &w[i + 1]);
+                rank1_cols(&at(i + 1, i + 1), m, nc, len, x.data(), &w[i + 1], tp);
             }
         }
     }
@@ -380,31 +481,34 @@ void apply_p(const Bidiag& bd, const double* z, double* y) {
     }
 }
 
-// min ||B z - g||^2 + lam^2 ||z||^2 for upper bidiagonal B (d, e): Givens
-// elimination of each damping row, chasing its fill-in along the bidiagonal.
+// min ||B z - g||^2 + lam^2 ||z||^2 for upper bidiagonal B (d, e): QR of
+// [B; lam I] by Givens rotations in O(n) (Elden's bidiagonal scheme): row i of
+// B absorbs the running damping row (pivot delta at column i), whose fill-in
+// -s e_i at column i+1 is folded into the next damping row lam e_{i+1}, so
+// every row needs two rotations and the triangular factor stays bidiagonal.
 // Returns false when lam == 0 and B is numerically singular.
 bool damped_bidiag_solve(std::vector<double> d, std::vector<double> e, std::vector<double> g,
                          double lam, double smax, int m_rows, double* z) {
     const int n = (int)d.size();
+    auto hyp = [](double a, double b) {
+        const double ss = a * a + b * b;     // |a|, |b| are matrix-scale: no hypot needed
+        return (ss > 1e-290 && ss < 1e290) ? sqrt(ss) : hypot(a, b);
+    };
     if (lam > 0.0) {
-        for (int j = 0; j < n; ++j) {
-            double r = lam, rhs = 0.0;       // damping row: lam at column j
-            for (int c = j; c < n; ++c) {
-                const double a = d[c];
-                const double ss = a * a + r * r;     // |a|, |r| are matrix-scale: no hypot needed
-                const double h = (ss > 1e-290 && ss < 1e290) ? sqrt(ss) : hypot(a, r);
-                if (h == 0.0) break;
-                const double cs = a / h, sn = r / h;
-                d[c] = h;
-                const double gc = g[c];
-                g[c] = cs * gc + sn * rhs;
-                rhs = -sn * gc + cs * rhs;
-                if (c + 1 < n) {
-                    const double b = e[c];
-                    e[c] = cs * b;             // row c keeps its superdiagonal
-                    r = -sn * b;               // fill-in of the damping row at c+1
-                    if (r == 0.0) break;
-                }
+        double delta = lam, rho = 0.0;       // running damping row: delta at column i, rhs rho
+        for (int i = 0; i < n; ++i) {
+            const double h = hyp(d[i], delta);
+            const double cs = d[i] / h, sn = delta / h;
+            d[i] = h;
+            const double gi = g[i];
+            g[i] = cs * gi + sn * rho;
+            rho = -sn * gi + cs * rho;
+            if (i + 1 < n) {
+                const double f = -sn * e[i];  // fill-in of the damping row at column i+1
+                e[i] = cs * e[i];
+                const double h2 = hyp(lam, f);
+                rho = (f / h2) * rho;         // merged with the damping row lam e_{i+1}
+                delta = h2;
             }
         }
     } else {

@@ -266,6 +266,148 @@ __global__ void __launch_bounds__(CT) k_combine(CombineJob j0, CombineJob j1, in
     last_cta_reduce(J.partial, J.G, 1, J.ticket, J.norm_out, (unsigned)J.G);
 }
 
+// ---------------------------------------------------------------------------
+// Batched iterate norms (ctk_iterate_batch): for up to IB_NB consecutive
+// iterations k_b = k0 + b of one cycle, ||x0 + X y_b||^2 and ||d0 - AX y_b||^2
+// in ONE pass over the basis (each X / AX element is read and widened once and
+// used for every iterate of the batch, instead of once per iterate), and the
+// last iterate of the batch (x and r) stored.  Job 0 (CTAs [0, G0)) is the
+// image-space combination, job 1 the residual.  Per element the rows are
+// summed in order j = 0, 1, ... from the base (x0 / d0); every CTA's norm
+// partials meet in a fixed-order reduction by the job's last CTA.
+// ---------------------------------------------------------------------------
+constexpr int IB_NB = 8;                 // iterates per batch
+constexpr int IB_T = 128;                // threads per CTA
+constexpr int IB_MAXK = 512;             // SMEM coefficient table rows
+
+struct IterBatchJob {
+    const float* X;
+    int64_t ld;
+    const float* base;
+    float* dst;              // last iterate of the batch (may be null)
+    int64_t L;
+    double* out;             // out[2 b]: ||.||^2 of iterate b
+    double* partial;         // [IB_NB][G]
+    unsigned int* ticket;
+    int G;
+};
+
+__global__ void __launch_bounds__(IB_T) k_iter_batch(IterBatchJob j0, IterBatchJob j1,
+                                                     const double* __restrict__ y, int ystride,
+                                                     int k0, int nb) {
+    __shared__ __align__(16) double cy[IB_MAXK][IB_NB];   // cy[j][b] = sgn * y_b[j] (0: j >= k_b)
+    __shared__ double nred[IB_T / 32][IB_NB];
+    __shared__ unsigned int s_last;
+    const bool second = (int)blockIdx.x >= j0.G;
+    const IterBatchJob& J = second ? j1 : j0;
+    const int bid = second ? (int)blockIdx.x - j0.G : (int)blockIdx.x;
+    const double sgn = second ? -1.0 : 1.0;
+    const int kmax = k0 + nb - 1;
+    for (int t = threadIdx.x; t < kmax * IB_NB; t += IB_T) {
+        const int j = t / IB_NB, b = t - j * IB_NB;
+        cy[j][b] = (b < nb && j < k0 + b) ? sgn * y[(size_t)b * ystride + j] : 0.0;
+    }
+    __syncthreads();
+    const int64_t L4 = J.L >> 2, ld4 = J.ld >> 2;
+    const float4* X4 = reinterpret_cast<const float4*>(J.X);
+    double nrm[IB_NB];
+#pragma unroll
+    for (int b = 0; b < IB_NB; ++b) nrm[b] = 0.0;
+    for (int64_t i = (int64_t)bid * IB_T + threadIdx.x; i < L4; i += (int64_t)J.G * IB_T) {
+        double a[IB_NB][4];
+        {
+            double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+            if (J.base) {
+                const float4 v = reinterpret_cast<const float4*>(J.base)[i];
+                b0 = v.x; b1 = v.y; b2 = v.z; b3 = v.w;
+            }
+#pragma unroll
+            for (int b = 0; b < IB_NB; ++b) {
+                a[b][0] = b0; a[b][1] = b1; a[b][2] = b2; a[b][3] = b3;
+            }
+        }
+        const float4* col = X4 + i;
+        int j = 0;
+        for (; j + 4 <= kmax; j += 4) {
+            float4 w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w[q] = __ldg(col + (size_t)(j + q) * ld4);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double wx = w[q].x, wy = w[q].y, wz = w[q].z, ww = w[q].w;
+#pragma unroll
+                for (int b = 0; b < IB_NB; ++b) {
+                    const double c = cy[j + q][b];
+                    a[b][0] = fma(c, wx, a[b][0]); a[b][1] = fma(c, wy, a[b][1]);
+                    a[b][2] = fma(c, wz, a[b][2]); a[b][3] = fma(c, ww, a[b][3]);
+                }
+            }
+        }
+        for (; j < kmax; ++j) {
+            const float4 w = __ldg(col + (size_t)j * ld4);
+            const double wx = w.x, wy = w.y, wz = w.z, ww = w.w;
+#pragma unroll
+            for (int b = 0; b < IB_NB; ++b) {
+                const double c = cy[j][b];
+                a[b][0] = fma(c, wx, a[b][0]); a[b][1] = fma(c, wy, a[b][1]);
+                a[b][2] = fma(c, wz, a[b][2]); a[b][3] = fma(c, ww, a[b][3]);
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < IB_NB; ++b) {
+            const float4 o = make_float4((float)a[b][0], (float)a[b][1], (float)a[b][2], (float)a[b][3]);
+            if (b == nb - 1 && J.dst) reinterpret_cast<float4*>(J.dst)[i] = o;
+            nrm[b] = fma((double)o.x, (double)o.x, nrm[b]); nrm[b] = fma((double)o.y, (double)o.y, nrm[b]);
+            nrm[b] = fma((double)o.z, (double)o.z, nrm[b]); nrm[b] = fma((double)o.w, (double)o.w, nrm[b]);
+        }
+    }
+    if (bid == J.G - 1 && threadIdx.x < 32) {                  // scalar tail L % 4
+        for (int64_t i = (L4 << 2) + threadIdx.x; i < J.L; i += 32) {
+            double a[IB_NB];
+            const double b0 = J.base ? (double)J.base[i] : 0.0;
+#pragma unroll
+            for (int b = 0; b < IB_NB; ++b) a[b] = b0;
+            for (int j = 0; j < kmax; ++j) {
+                const double w = J.X[(size_t)j * J.ld + i];
+#pragma unroll
+                for (int b = 0; b < IB_NB; ++b) a[b] = fma(cy[j][b], w, a[b]);
+            }
+#pragma unroll
+            for (int b = 0; b < IB_NB; ++b) {
+                const float o = (float)a[b];
+                if (b == nb - 1 && J.dst) J.dst[i] = o;
+                nrm[b] = fma((double)o, (double)o, nrm[b]);
+            }
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int b = 0; b < IB_NB; ++b) {
+        const double t = warp_sum(nrm[b]);
+        if (lane == 0) nred[warp][b] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < IB_NB) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < IB_T / 32; ++w) t += nred[w][threadIdx.x];
+        J.partial[(size_t)threadIdx.x * J.G + bid] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(J.ticket, 1u) == (unsigned)J.G - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int b = warp; b < nb; b += IB_T / 32) {
+        double t = 0.0;
+        for (int c = lane; c < J.G; c += 32) t += __ldcg(J.partial + (size_t)b * J.G + c);
+        t = warp_sum(t);
+        if (lane == 0) J.out[2 * b] = t;
+    }
+    if (threadIdx.x == 0) *J.ticket = 0u;
+}
+
 __global__ void k_scale(const float* __restrict__ v, float* __restrict__ dst, int64_t L,
                         const double* __restrict__ scale) {
     const float sc = (float)(*scale);
@@ -1479,6 +1621,38 @@ int ctk_combine_pair(const float* X, int64_t ldx, const float* x0, float* x, int
     k_combine<<<(unsigned)(j0.G + j1.G), CT, smem, ctk_stream(stream)>>>(j0, j1, k,
                                                                          byval ? nullptr : y, cp);
     CTK_LAUNCH_CHECK("k_combine");
+    return CTK_OK;
+}
+
+static int iter_batch_ctas(int64_t L) {
+    int64_t G = ((L >> 2) + IB_T - 1) / IB_T;
+    if (G > 4 * 148) G = 4 * 148;
+    return (int)(G < 1 ? 1 : G);
+}
+
+bool ctk_iterate_batch_ok(int k0, int nb, int nvec_cap, int64_t Lx, int64_t Lr) {
+    if (nb < 1 || nb > IB_NB || k0 < 1 || k0 + nb - 1 > IB_MAXK) return false;
+    const int64_t need = (int64_t)IB_NB * (iter_batch_ctas(Lx) + iter_batch_ctas(Lr));
+    return need <= (int64_t)MAXCH * (nvec_cap + 3);
+}
+
+extern "C" int ctk_iterate_batch(const float* X, int64_t ldx, const float* x0, float* x,
+                                 int64_t Lx, const float* AX, int64_t ldax, const float* d0,
+                                 float* r, int64_t Lr, int k0, int nb, const double* y,
+                                 int ystride, double* norms, void* scratch, int nvec_cap,
+                                 void* stream) {
+    if (!X || !AX || !d0 || !y || !norms || !scratch)
+        return ctk_fail(CTK_ERR_ARG, "null argument");
+    if ((ldx & 3) || (ldax & 3)) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
+    if (!ctk_iterate_batch_ok(k0, nb, nvec_cap, Lx, Lr))
+        return ctk_fail(CTK_ERR_ARG, "bad iterate batch (k0 %d, nb %d)", k0, nb);
+    Scratch s = carve(scratch, nvec_cap + 3);
+    IterBatchJob j0 = {X, ldx, x0, x, Lx, norms + 1, s.partial, s.ticket, iter_batch_ctas(Lx)};
+    IterBatchJob j1 = {AX, ldax, d0, r, Lr, norms, s.partial + (size_t)IB_NB * j0.G, s.ticket + 1,
+                       iter_batch_ctas(Lr)};
+    k_iter_batch<<<(unsigned)(j0.G + j1.G), IB_T, 0, ctk_stream(stream)>>>(j0, j1, y, ystride, k0,
+                                                                         nb);
+    CTK_LAUNCH_CHECK("k_iter_batch");
     return CTK_OK;
 }
 

@@ -324,3 +324,21 @@ def test_concurrent_solves_from_threads_match_sequential(cuda, golden):
         np.testing.assert_array_equal(records(a, "lambda_used"), records(c, "lambda_used"))
         np.testing.assert_array_equal(records(a, "data_residual_norm"),
                                       records(c, "data_residual_norm"))
+
+
+@pytest.mark.parametrize("method,strategy,K", [("ab-hybrid", "gcv", 50), ("ba-hybrid", "lcurve", 21)])
+def test_batched_iterate_norms_match_per_iterate(cuda, golden, monkeypatch, method, strategy, K):
+    """The native driver's batched iterate norms (default when no per-iterate
+    consumer exists) give the records and x_K of one launch per iterate
+    (CTK_ITER_BATCH=0) up to fp32 rounding of the iterates."""
+    spec, z, b = config_b(golden, "c1")
+    A, B = ops_for(spec)
+    cfg = gmres.SolverConfig(method=method, lambda_strategy=strategy, max_iter=K)
+    res = gmres.run_gmres(A, B, b, cfg)
+    monkeypatch.setenv("CTK_ITER_BATCH", "0")
+    ref = gmres.run_gmres(A, B, b, cfg)
+    for f in ("data_residual_norm", "residual_norm", "solution_norm"):
+        np.testing.assert_allclose(records(res, f), records(ref, f), rtol=1e-6, err_msg=f)
+    np.testing.assert_array_equal(records(res, "lambda_used"), records(ref, "lambda_used"))
+    assert rel(res.x, ref.x) <= 1e-6
+

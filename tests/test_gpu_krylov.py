@@ -102,6 +102,56 @@ def test_combine_and_norms(cuda, L, k):
     np.testing.assert_allclose(dots.cpu().numpy()[:k], dref, rtol=1e-10, atol=1e-9)
 
 
+@pytest.mark.parametrize("Lx,Lr,k0,nb", [(4096, 32940, 1, 8), (65536, 130682, 41, 8),
+                                         (1001, 2087, 75, 3), (16, 12, 5, 1)])
+def test_iterate_batch_matches_per_iterate_combinations(cuda, Lx, Lr, k0, nb):
+    """ctk_iterate_batch: one pass over X / AX for nb iterates gives the same
+    norms and last iterate as the fp64 host combinations x0 + X y_b and
+    d0 - AX y_b (fp32-rounded entries, fp64 sums)."""
+    torch = cuda
+    from paper_2602_17892_b200 import _native
+    lib = _native.load()
+    rng = np.random.default_rng(Lx + k0)
+    rows = k0 + nb + 2
+    ldx, ldr = (Lx + 3) // 4 * 4, (Lr + 3) // 4 * 4
+    X = rng.standard_normal((rows, ldx)).astype(np.float32)
+    AX = rng.standard_normal((rows, ldr)).astype(np.float32)
+    x0 = rng.standard_normal(Lx).astype(np.float32)
+    d0 = rng.standard_normal(Lr).astype(np.float32)
+    Y = np.zeros((nb, rows))
+    for b in range(nb):
+        Y[b, :k0 + b] = rng.standard_normal(k0 + b)
+    dev = torch.device("cuda", 0)
+    Xd, AXd = torch.from_numpy(X).to(dev), torch.from_numpy(AX).to(dev)
+    x0d, d0d = torch.from_numpy(x0).to(dev), torch.from_numpy(d0).to(dev)
+    Yd = torch.from_numpy(Y).to(dev)
+    x = torch.zeros(Lx, device=dev)
+    r = torch.zeros(Lr, device=dev)
+    norms = torch.zeros(2 * nb, dtype=torch.float64, device=dev)
+    cap = rows + 2
+    scratch = torch.zeros(int(lib.ctk_reduce_scratch_bytes(cap, Lr)) // 8 + 1,
+                          dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream()
+    for _ in range(2):          # the second call reuses the (reset) tickets
+        _native.check(lib.ctk_iterate_batch(Xd.data_ptr(), ldx, x0d.data_ptr(), x.data_ptr(), Lx,
+                                            AXd.data_ptr(), ldr, d0d.data_ptr(), r.data_ptr(), Lr,
+                                            k0, nb, Yd.data_ptr(), rows, norms.data_ptr(),
+                                            scratch.data_ptr(), cap, st.cuda_stream),
+                      "ctk_iterate_batch")
+    torch.cuda.synchronize()
+    got = norms.cpu().numpy()
+    for b in range(nb):
+        k = k0 + b
+        xr = x0.astype(np.float64) + X[:k, :Lx].astype(np.float64).T @ Y[b, :k]
+        rr = d0.astype(np.float64) - AX[:k, :Lr].astype(np.float64).T @ Y[b, :k]
+        assert got[2 * b + 1] == pytest.approx(float(xr @ xr), rel=1e-6)
+        assert got[2 * b] == pytest.approx(float(rr @ rr), rel=1e-6)
+    np.testing.assert_allclose(x.cpu().numpy(), xr, rtol=1e-6, atol=1e-5)
+    np.testing.assert_allclose(r.cpu().numpy(), rr, rtol=1e-6, atol=1e-5)
+    xs = x.cpu().numpy().astype(np.float64)
+    assert got[2 * nb - 1] == pytest.approx(float(xs @ xs), rel=1e-12)
+
+
 def test_reductions_are_bitwise_deterministic(cuda):
     torch = cuda
     L, k = 2086560, 20

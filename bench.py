@@ -316,7 +316,7 @@ def main():
         def step():
             dg.forward(x, out=y, stream=stream)
             dg.back(u, out=xo, stream=stream)
-        rays_per_step = 2 * dg.m
+        rays_per_step = executed_per_step = 2 * dg.m
         iters_per_step = None
     else:
         pseed, nseed = problems.slice_seeds(spec, rank) if spec.slices > 1 else (
@@ -333,6 +333,9 @@ def main():
                                  max_iter=spec.max_iter)
         na, nb = applies_per_iter(spec.method)
         rays_per_step = spec.max_iter * (na + nb) * dg.m
+        # applies this path actually runs: 1A + 1B per Arnoldi step, plus the
+        # cycle start (AB: A x0; BA: A x0 and B of the residual)
+        executed_per_step = (2 * spec.max_iter + (1 if spec.method.startswith("ab") else 2)) * dg.m
         iters_per_step = spec.max_iter
 
         def step():
@@ -454,6 +457,8 @@ def main():
                              "(gmres.py:189,207,209); this path executes the Arnoldi "
                              "1A+1B per iteration and gets x_k and b - A x_k by linearity "
                              "from rows kept during the Arnoldi step"),
+            "rays_executed_per_s": (value * executed_per_step / rays_per_step
+                                    if rays_per_step else None),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }

@@ -1650,9 +1650,11 @@ extern "C" int ctk_iterate_batch(const float* X, int64_t ldx, const float* x0, f
     IterBatchJob j0 = {X, ldx, x0, x, Lx, norms + 1, s.partial, s.ticket, iter_batch_ctas(Lx)};
     IterBatchJob j1 = {AX, ldax, d0, r, Lr, norms, s.partial + (size_t)IB_NB * j0.G, s.ticket + 1,
                        iter_batch_ctas(Lr)};
+    const int ph = ctk_prof_open(3, ctk_stream(stream));
     k_iter_batch<<<(unsigned)(j0.G + j1.G), IB_T, 0, ctk_stream(stream)>>>(j0, j1, y, ystride, k0,
                                                                          nb);
     CTK_LAUNCH_CHECK("k_iter_batch");
+    ctk_prof_close(ph, ctk_stream(stream));
     return CTK_OK;
 }
 

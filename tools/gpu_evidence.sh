@@ -16,7 +16,7 @@ python tools/bench_projectors.py > gpurun_out/projectors.jsonl 2>&1
 C2="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 $C2 > gpurun_out/plain_c2.log 2>&1 && timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv $C2 > gpurun_out/ncu_c2.log 2>&1
 python tools/ncu_launch_summary.py gpurun_out/launches_c2.csv "c2 bench (--steps 1 --warmup 1): warm-up + timed + profiled solves" > gpurun_out/launches_c2_summary.txt
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_forward|k_back|k_gs_smem|k_combine" -s 40 -c 8 -o gpurun_out/prof_c2 -f $C2 > gpurun_out/ncu_c2full.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_forward|k_back|k_gs_smem|k_iter_batch" -s 40 -c 8 -o gpurun_out/prof_c2 -f $C2 > gpurun_out/ncu_c2full.log 2>&1
 C3="python bench.py --workload c3 --steps 1 --warmup 1 --no-cpu-baseline"
 $C3 > gpurun_out/plain_c3.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_forward|k_back|k_stage" -s 3 -c 3 -o gpurun_out/prof_c3 -f $C3 > gpurun_out/ncu_c3.log 2>&1
 C5="python bench.py --workload c5 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"

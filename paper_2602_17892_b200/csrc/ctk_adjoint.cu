@@ -241,14 +241,12 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
             const int iy = iy0 + ty + r * JROWS;
             if (inx && iy < A.ny) part[(size_t)blockIdx.z * n + (size_t)iy * A.nx + ix] = (float)acc[r];
         }
-        __threadfence();
         __syncthreads();
         __shared__ unsigned s_last;
         unsigned* ticket = A.cnt + (size_t)blockIdx.y * gridDim.x + blockIdx.x;
-        if (tid == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.z - 1);
+        if (tid == 0) s_last = ctk_ticket_arrive(ticket, gridDim.z);
         __syncthreads();
         if (!s_last) return;
-        __threadfence();
         if (inx) {
             for (int r = 0; r < JPPT; ++r) {
                 const int iy = iy0 + ty + r * JROWS;

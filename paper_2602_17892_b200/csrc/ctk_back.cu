@@ -207,14 +207,12 @@ __global__ void __launch_bounds__(BTHREADS, PPT == 4 ? CTK_BACK_MINB4 : 6) k_bac
             const int iy = iy0 + ty + r * BROWS;
             if (inx && iy < A.ny) part[(size_t)blockIdx.z * n + (size_t)iy * A.nx + ix] = (float)acc[r];
         }
-        __threadfence();
         __syncthreads();
         __shared__ unsigned s_last;
         unsigned* ticket = A.cnt + (size_t)blockIdx.y * gridDim.x + blockIdx.x;
-        if (tid == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.z - 1);
+        if (tid == 0) s_last = ctk_ticket_arrive(ticket, gridDim.z);
         __syncthreads();
         if (!s_last) return;                       // CTA-uniform
-        __threadfence();
         if (tid == 0) *ticket = 0u;
 #pragma unroll
         for (int r = 0; r < PPT; ++r) {

@@ -109,6 +109,19 @@ static inline cudaStream_t ctk_stream(void* s) { return reinterpret_cast<cudaStr
 // successor waits for its predecessor's memory only where it first reads
 // it (griddepcontrol.wait), so its launch and set-up overlap the previous
 // kernel's tail.  Both are no-ops without a programmatic launch.
+// Last-arriver tickets (split reductions): after a __syncthreads() that
+// orders every thread's partial stores before it, ONE thread releases them at
+// gpu scope with the ticket increment (cumulativity covers the CTA's stores);
+// the last arriver's thread acquires before its CTA reads the partials (.cg).
+// Cheaper than a __threadfence() in every thread (MEMBAR.SC.GPU per warp).
+__device__ __forceinline__ bool ctk_ticket_arrive(unsigned* ticket, unsigned arrivals) {
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(ticket) : "memory");
+    const bool last = old == arrivals - 1;
+    if (last) asm volatile("fence.acq_rel.gpu;" ::: "memory");     // acquire the others' partials
+    return last;
+}
+
 __device__ __forceinline__ void ctk_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void ctk_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 

@@ -75,15 +75,13 @@ __device__ __forceinline__ double dot4(float4 a, float4 b, double acc) {
 // order (lane-strided, then a fixed shuffle tree) and writes out[j].
 __device__ void last_cta_reduce(const double* partial, int nchunks, int nv, unsigned int* ticket,
                                 double* out, unsigned arrivals = 0) {
-    __threadfence();
     __shared__ unsigned int s_last;
     __syncthreads();
     if (arrivals == 0) arrivals = gridDim.x * gridDim.y;
     if (threadIdx.x == 0)
-        s_last = (atomicAdd(ticket, 1u) == arrivals - 1);
+        s_last = ctk_ticket_arrive(ticket, arrivals);
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int j = warp; j < nv; j += nw) {
         double s = 0.0;
@@ -393,12 +391,10 @@ __global__ void __launch_bounds__(IB_T) k_iter_batch(IterBatchJob j0, IterBatchJ
         for (int w = 0; w < IB_T / 32; ++w) t += nred[w][threadIdx.x];
         J.partial[(size_t)threadIdx.x * J.G + bid] = t;
     }
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(J.ticket, 1u) == (unsigned)J.G - 1);
+    if (threadIdx.x == 0) s_last = ctk_ticket_arrive(J.ticket, (unsigned)J.G);
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     for (int b = warp; b < nb; b += IB_T / 32) {
         double t = 0.0;
         for (int c = lane; c < J.G; c += 32) t += __ldcg(J.partial + (size_t)b * J.G + c);

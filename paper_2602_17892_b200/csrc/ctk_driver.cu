@@ -65,12 +65,24 @@ class Pool {
         std::unique_lock<std::mutex> lk(mu_);
         done_cv_.wait(lk, [&] { return j->done; });
     }
+    // The last column's problem runs on the calling thread (it would only
+    // wait for it): two thread hand-offs off the solve's critical tail.
+    void run_inline(const std::shared_ptr<Job>& j) {
+        solve(*j);
+        std::lock_guard<std::mutex> lk(mu_);
+        j->done = true;
+    }
     bool ready(const std::shared_ptr<Job>& j) {
         std::lock_guard<std::mutex> lk(mu_);
         return j->done;
     }
 
   private:
+    static void solve(Job& j) {
+        j.y.assign(j.k, 0.0);
+        j.rc = ctk_projected_solve(j.H.data(), j.k, j.beta, j.strategy, j.value, 200, NAN, j.out,
+                                   j.y.data());
+    }
     void loop() {
         for (;;) {
             std::shared_ptr<Job> j;
@@ -81,9 +93,7 @@ class Pool {
                 j = std::move(q_.front());
                 q_.pop_front();
             }
-            j->y.assign(j->k, 0.0);
-            j->rc = ctk_projected_solve(j->H.data(), j->k, j->beta, j->strategy, j->value, 200,
-                                        NAN, j->out, j->y.data());
+            solve(*j);
             {
                 std::lock_guard<std::mutex> lk(mu_);
                 j->done = true;
@@ -409,7 +419,8 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
             job->strategy = cfg->hybrid ? cfg->strategy : 0;
             job->value = cfg->lambda_value;
             jobs[k] = job;
-            pool().submit(job);
+            if (broke || k == steps) pool().run_inline(job);
+            else pool().submit(job);
             if (broke) {
                 broke_at = last_k = k;
             } else if ((rc = enqueue_to(k + look))) {

@@ -48,7 +48,46 @@ struct BackArgs {
     int pad;
     double h, xmin, ymax, center;
     const ctk_xchg_args* xc;   // optional (device copy): push the tile to its owner rank
+    unsigned* ready;      // optional: K1's finished-CTA counters per 4-angle group (chaining)
+    unsigned ready_need;  // K1 CTAs per group (bin blocks)
 };
+
+// K2 chaining (ctk_common.cuh): wait until the K1 groups holding angles
+// [ac, ac + na) are complete.  Bounded: a counter that never fills (a
+// protocol bug) traps after ~5 s instead of hanging the GPU.
+__device__ __forceinline__ void wait_k1_groups(const BackArgs& A, int ac, int na, int tid) {
+    const int g0 = (ac - A.a0) / CTK_FWD_APB, g1 = (ac + na - 1 - A.a0) / CTK_FWD_APB;
+    if (tid <= g1 - g0) {
+        const unsigned* c = A.ready + g0 + tid;
+        if (ctk_ld_acquire_gpu(c) < A.ready_need) {
+            unsigned long long t0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            while (ctk_ld_acquire_gpu(c) < A.ready_need) {
+                __nanosleep(64);
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > 5000000000ull) __trap();
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// The CTA that completes the last wait of the launch resets the counters
+// for the next K1 (which cannot signal before this K2 has completed).
+__device__ __forceinline__ void release_k1_groups(const BackArgs& A, int tid) {
+    __syncthreads();
+    if (tid != 0) return;
+    const int ng = (A.a1 - A.a0 + CTK_FWD_APB - 1) / CTK_FWD_APB;
+    unsigned* pass = A.ready + ng;
+    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+    unsigned old;
+    asm volatile("atom.add.relaxed.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(pass) : "memory");
+    if (old == total - 1) {
+        for (int g = 0; g < ng; ++g) A.ready[g] = 0u;
+        *pass = 0u;
+    }
+}
 
 // K1's zero-padded copies of the output pixel (ix, iy) (see ctk_forward.cu).
 __device__ __forceinline__ void stage_out(const BackArgs& A, int ix, int iy, float v) {
@@ -171,7 +210,8 @@ __global__ void __launch_bounds__(BTHREADS, PPT == 4 ? CTK_BACK_MINB4 : 6) k_bac
                                    (int)(unsigned)__cvta_generic_to_shared(win + tid * wmax));
         }
         __syncthreads();
-        ctk_pdl_wait();                            // u comes from the previous kernel
+        if (A.ready) wait_k1_groups(A, ac, na, tid);   // u: this chunk's K1 rows
+        else ctk_pdl_wait();                       // u comes from the previous kernel
         stage_windows(A, win, s_w0, ac, na, tx, ty);
         __syncthreads();
         float sp[PPT];
@@ -196,6 +236,7 @@ __global__ void __launch_bounds__(BTHREADS, PPT == 4 ? CTK_BACK_MINB4 : 6) k_bac
         for (int r = 0; r < PPT; ++r) acc[r] += (double)sp[r];
         __syncthreads();
     }
+    if (A.ready) release_k1_groups(A, tid);
     if (SPLIT) {
         // global partial images + per-tile arrival tickets: the last of the
         // gridDim.z CTAs of a tile sums the partials in split order
@@ -343,11 +384,21 @@ static int64_t back_tiles(const ctk_geom* g) {
 
 int64_t ctk_back_tiles(const ctk_geom* g) { return back_tiles(g); }
 
-// Split reduction: S partial images + one arrival ticket per tile.
+// Work buffer: [K1-chaining flags: one counter per 4-angle group + a pass
+// counter, 16-float aligned] [S partial images] [one arrival ticket per tile].
+// The flags sit first so every angle range / split count agrees on them.
+static int64_t back_flag_floats(const ctk_geom* g) {
+    return ((int64_t)(g->n_angles + CTK_FWD_APB - 1) / CTK_FWD_APB + 1 + 15) / 16 * 16;
+}
+
+unsigned* ctk_back_flags(const ctk_geom* g, float* work) {
+    return work ? reinterpret_cast<unsigned*>(work) : nullptr;
+}
+
 extern "C" int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1) {
     if (!g || a0 < 0 || a1 > g->n_angles || a0 >= a1) return 0;
     const int S = back_splits(g, a0, a1);
-    return S > 1 ? (int64_t)S * g->nx * g->ny + back_tiles(g) : 0;
+    return back_flag_floats(g) + (S > 1 ? (int64_t)S * g->nx * g->ny + back_tiles(g) : 0);
 }
 
 extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, int a1,
@@ -359,14 +410,14 @@ extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, i
 // forward workspace `stage` (interior only: its zero padding is written by
 // any plain ctk_forward on that workspace).
 int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
-                float* work, float* stage, void* stream) {
-    return ctk_back_xc(g, u, x, a0, a1, x0, work, stage, nullptr, stream);
+                float* work, float* stage, void* stream, bool after_k1) {
+    return ctk_back_xc(g, u, x, a0, a1, x0, work, stage, nullptr, stream, after_k1);
 }
 
 // xc (device pointer) != NULL: push the partial tiles to their owners
 // instead of writing x (ctk_back_exchange, phase 1).
 int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
-                float* work, float* stage, const ctk_xchg_args* xc, void* stream) {
+                float* work, float* stage, const ctk_xchg_args* xc, void* stream, bool after_k1) {
     if (!g) return ctk_fail(CTK_ERR_ARG, "null geometry");
     if (a0 < 0 || a1 > g->n_angles || a0 > a1)
         return ctk_fail(CTK_ERR_SHAPE, "angle range [%d, %d) outside [0, %d)", a0, a1, g->n_angles);
@@ -383,9 +434,13 @@ int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
     if (S > 1 && !work)
         return ctk_fail(CTK_ERR_ARG, "ctk_back needs %lld work floats",
                         (long long)ctk_back_work_floats(g, a0, a1));
+    if (after_k1 && !work) return ctk_fail(CTK_ERR_ARG, "K1 chaining needs the work buffer");
     BackArgs A;
-    A.part = S > 1 ? work : nullptr;
-    A.cnt = S > 1 ? reinterpret_cast<unsigned*>(work + (size_t)S * g->nx * g->ny) : nullptr;
+    float* body = work ? work + back_flag_floats(g) : nullptr;
+    A.part = S > 1 ? body : nullptr;
+    A.cnt = S > 1 ? reinterpret_cast<unsigned*>(body + (size_t)S * g->nx * g->ny) : nullptr;
+    A.ready = after_k1 ? ctk_back_flags(g, work) : nullptr;
+    A.ready_need = (unsigned)((g->det_count + 31) / 32);
     A.bp = g->d_bp;
     A.u = u;
     A.x0 = x0;

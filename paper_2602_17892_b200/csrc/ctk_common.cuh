@@ -122,6 +122,12 @@ __device__ __forceinline__ bool ctk_ticket_arrive(unsigned* ticket, unsigned arr
     return last;
 }
 
+__device__ __forceinline__ unsigned ctk_ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void ctk_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void ctk_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
@@ -189,12 +195,21 @@ int ctk_combine_pair(const float* X, int64_t ldx, const float* x0, float* x, int
                      int64_t Lr, double* n_r, int k, const double* y, void* scratch,
                      void* stream, const double* y_host);
 bool ctk_iterate_batch_ok(int k0, int nb, int nvec_cap, int64_t Lx, int64_t Lr);
+// K1 -> K2 chaining (BA Arnoldi step, q = B (A w)): K1 CTAs count finished
+// 4-angle groups into flag words at the head of K2's work buffer (release),
+// and K2 CTAs start each 32-angle chunk as soon as its groups are complete
+// (acquire) instead of waiting for the whole of K1 -- K2 overlaps K1's last
+// wave.  Deadlock-free: K2 is a programmatic dependent of K1, which triggers
+// at entry, so every K1 CTA is resident or done before any K2 CTA can spin.
+constexpr int CTK_FWD_APB = 4;                 // angles per K1 CTA (one per warp)
+unsigned* ctk_back_flags(const ctk_geom* g, float* work);
 int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1, const float* b,
-                   float* work, bool prestaged, void* stream);
+                   float* work, bool prestaged, void* stream, unsigned* done_flags = nullptr);
 int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
-                float* work, float* stage, void* stream);
+                float* work, float* stage, void* stream, bool after_k1 = false);
 int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
-                float* work, float* stage, const ctk_xchg_args* xc, void* stream);
+                float* work, float* stage, const ctk_xchg_args* xc, void* stream,
+                bool after_k1 = false);
 int ctk_xchg_finish(const ctk_geom* g, const ctk_xchg_args* xc, int nranks, int phases,
                     cudaStream_t st);
 int64_t ctk_back_tiles(const ctk_geom* g);

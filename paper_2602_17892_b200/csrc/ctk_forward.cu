@@ -221,6 +221,7 @@ struct FwdArgs {
     int deg_maxseg;
     ExactGrid eg;
     int D, a0, a1, pad;
+    unsigned* done;          // optional: per 4-angle group, finished CTAs (K2 chaining)
 };
 
 // One ray of the row walk (see the header comment).  base/pitch/C describe
@@ -414,6 +415,16 @@ __device__ __forceinline__ double forward_ray(const FwdArgs& A, int a, int slot,
 // neighbouring angles' rays cross nearly the same pixels at the same time,
 // so the warps of a CTA share the L1 lines their gathers pull from L2.
 constexpr int FWD_APB = FWD_THREADS / 32;
+static_assert(FWD_APB == CTK_FWD_APB, "K2 chaining counts K1 CTAs per 4-angle group");
+
+// K2 chaining: after the barrier that orders the CTA's output stores, one
+// release increment of its angle group's counter (see ctk_common.cuh).
+__device__ __forceinline__ void signal_group(const FwdArgs& A) {
+    if (!A.done) return;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.done + blockIdx.y) : "memory");
+}
 
 constexpr int FWD_MAX_SPLIT = 8;            // portable cluster size limit
 
@@ -439,9 +450,11 @@ __global__ void __launch_bounds__(FWD_THREADS, CTK_FWD_MINB) k_forward(FwdArgs A
     const int j = blockIdx.x * 32 + (threadIdx.x & 31);
     const size_t o = (size_t)ai * A.D + j;
     if (!SPLIT) {
-        if (a >= A.a1 || j >= A.D) return;
-        const double acc = forward_ray(A, a, A.deg_slot[a], j, 0);
-        A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
+        if (a < A.a1 && j < A.D) {
+            const double acc = forward_ray(A, a, A.deg_slot[a], j, 0);
+            A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
+        }
+        signal_group(A);
         return;
     }
     // Row chunks of the same rays form one thread-block cluster (1, 1, split).
@@ -482,10 +495,12 @@ __global__ void __launch_bounds__(FWD_THREADS, CTK_FWD_MINB) k_forward(FwdArgs A
         " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], 0;\n"
         " @!p bra WAIT_%=;\n}\n" ::"r"(bar)
         : "memory");
-    if (!valid) return;
-    double s = (double)v;
-    for (int c = 1; c < A.split; ++c) s += (double)s_part[c - 1][threadIdx.x];
-    A.y[o] = A.b ? (float)((double)A.b[o] - s) : (float)s;
+    if (valid) {
+        double s = (double)v;
+        for (int c = 1; c < A.split; ++c) s += (double)s_part[c - 1][threadIdx.x];
+        A.y[o] = A.b ? (float)((double)A.b[o] - s) : (float)s;
+    }
+    signal_group(A);
 }
 
 // Literal fp64 Siddon for every ray (validation path, ctk_forward_exact).
@@ -562,6 +577,7 @@ static FwdArgs make_args(const ctk_geom* g, const float* x, float* y, int a0, in
     A.a1 = a1;
     A.pad = g->fwd_pad;
     A.split = 1;
+    A.done = nullptr;
     return A;
 }
 
@@ -647,7 +663,7 @@ extern "C" int ctk_forward(const ctk_geom_t* g, const float* x, float* y, int a0
 // producer of x: K2's epilogue or the SMEM Gram-Schmidt step), so the K1
 // staging launch is skipped.  x itself is still read by degenerate angles.
 int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1, const float* b,
-                   float* work, bool prestaged, void* stream) {
+                   float* work, bool prestaged, void* stream, unsigned* done_flags) {
     int rc = check_range(g, a0, a1);
     if (rc) return rc;
     if (!x || !y) return ctk_fail(CTK_ERR_ARG, "null vector");
@@ -667,6 +683,7 @@ int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1
     A.P = P;
     A.PT = PT;
     A.split = g->fwd_split;
+    A.done = done_flags;
     dim3 grid((g->det_count + 31) / 32, (a1 - a0 + FWD_APB - 1) / FWD_APB, A.split);
     if (A.split > 1)
         CTK_CUDA(ctk_launch_pdl(k_forward<true>, grid, dim3(FWD_THREADS), CTK_FWD_DYNSMEM, st,

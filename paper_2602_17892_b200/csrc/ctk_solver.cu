@@ -124,8 +124,21 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
     } else {    // q = B (A w); keep A w_j (aux1)
         float* aw = aux1 ? aux1 + (size_t)j * ld1 : tmp;
         const bool pre = j > 0 && (ctk_gs_smem_ok(L, j - 1) || ctk_gs_stream_ok(L, j - 1));
-        if ((rc = ctk_forward_ex(g, w, aw, 0, na, nullptr, stage_work, pre, stream))) return rc;
-        if ((rc = ctk_back(g, aw, q, 0, na, nullptr, back_work, stream))) return rc;
+        // K2 starts each angle chunk as soon as K1 has finished its rows
+        // (chaining flags at the head of back_work; CTK_NO_CHAIN=1 disables)
+        static const bool chain = [] {
+            const char* e = getenv("CTK_NO_CHAIN");
+            return !(e && e[0] == '1');
+        }();
+        // only where K1's last wave is a large share of it (a few waves of
+        // K1 CTAs); at c5 (~35 waves) the early K2 CTAs would just spin
+        const int64_t k1_ctas = (int64_t)((g->det_count + 31) / 32) *
+                                ((na + CTK_FWD_APB - 1) / CTK_FWD_APB) * g->fwd_split;
+        const bool ch = chain && back_work && k1_ctas <= 4 * 8 * 148;
+        if ((rc = ctk_forward_ex(g, w, aw, 0, na, nullptr, stage_work, pre, stream,
+                                 ch ? ctk_back_flags(g, back_work) : nullptr)))
+            return rc;
+        if ((rc = ctk_back_ex(g, aw, q, 0, na, nullptr, back_work, nullptr, stream, ch))) return rc;
     }
     // The SMEM Gram-Schmidt step writes the column straight into the
     // page-locked host row (mapped, UVA) -- no D2H copy on the critical stream.

@@ -297,17 +297,19 @@ def test_golub_kahan_solvers_vs_reference(cuda, golden, case):
     assert rel(res.x, d[f"{case}/x"]) <= 2e-3
 
 
-def test_concurrent_solves_from_threads_match_sequential(cuda, golden):
+@pytest.mark.parametrize("method", ["ab-hybrid", "ba-hybrid"])
+def test_concurrent_solves_from_threads_match_sequential(cuda, golden, method):
     """Independent slices solved from several host threads at once (each
-    thread has its own stream pair and workspaces) give bitwise the results
-    of the same solves run one after another."""
+    thread has its own stream pair and workspaces -- for BA also its own
+    K1 -> K2 chaining flags) give bitwise the results of the same solves run
+    one after another."""
     import threading
     spec, z, b = config_b(golden, "c1")
     A, B = ops_for(spec)
     rng = np.random.default_rng(9)
     bs = [b * (1.0 + 0.1 * i) + 0.01 * rng.standard_normal(b.size) for i in range(3)]
     bs = [v.astype(np.float32).astype(np.float64) for v in bs]
-    cfg = gmres.SolverConfig(method="ab-hybrid", lambda_strategy="gcv", max_iter=20)
+    cfg = gmres.SolverConfig(method=method, lambda_strategy="gcv", max_iter=20)
     seq = [gmres.run_gmres(A, B, v, cfg) for v in bs]
     out = [None] * len(bs)
 
@@ -341,4 +343,39 @@ def test_batched_iterate_norms_match_per_iterate(cuda, golden, monkeypatch, meth
         np.testing.assert_allclose(records(res, f), records(ref, f), rtol=1e-6, err_msg=f)
     np.testing.assert_array_equal(records(res, "lambda_used"), records(ref, "lambda_used"))
     assert rel(res.x, ref.x) <= 1e-6
+
+
+_CHAIN_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2602_17892_b200 import ct, gmres, problems
+spec = problems.CONFIGS["c2"]
+grid = ct.ImageGrid(spec.N, spec.N, 1.0)
+geom = ct.ParallelGeometry(spec.angles(), spec.det_count, 1.0)
+A, B = ct.forward_ray_driven(grid, geom), ct.back_pixel_driven(grid, geom)
+x = problems.random_ellipse_phantom(spec.N, spec.ellipses, 0)
+b = A.apply(x)
+cfg = gmres.SolverConfig(method="ba-hybrid", lambda_strategy="gcv", max_iter=12)
+for _ in range(3):          # consecutive solves: the chaining flags reset every step
+    res = gmres.run_gmres(A, B, b, cfg)
+np.save(sys.argv[2], res.x)
+"""
+
+
+def test_ba_chaining_is_bitwise_the_unchained_step(cuda, tmp_path):
+    """K2 starting per angle chunk on K1's group counters (default) changes
+    only the schedule: the BA solve is bitwise the one with a full K1 -> K2
+    dependency (CTK_NO_CHAIN=1)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_val in ("0", "1"):
+        path = tmp_path / f"x{env_val}.npy"
+        env = dict(os.environ, CTK_NO_CHAIN=env_val)
+        subprocess.run([sys.executable, "-c", _CHAIN_SCRIPT, root, str(path)], env=env,
+                       check=True, timeout=300)
+        outs.append(np.load(path))
+    np.testing.assert_array_equal(outs[0], outs[1])
 

@@ -296,7 +296,7 @@ class _DeviceSolve:
     (the degenerate-curve fallback needs the previous lambda).
     """
 
-    LOOKAHEAD = 6
+    LOOKAHEAD = int(os.environ.get("CTK_LOOKAHEAD", "6"))   # tuning override
 
     def __init__(self, A, B, b, cfg, x_true, image_shape, stream, timer, keep_on_device=False):
         if not isinstance(A, GpuForward) or not isinstance(B, GpuBack) or A.dgeom is not B.dgeom:

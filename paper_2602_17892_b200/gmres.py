@@ -452,9 +452,14 @@ class _DeviceSolve:
         return float(out)
 
     def _host_vec(self, t, stream):
+        """fp64 numpy copy of a device fp32 vector: one D2H into a reused
+        page-locked buffer (no pageable staging), widened on the host."""
         self.d2h += 4 * t.numel()
+        pin = _pinned(self.torch, "xout", (t.numel(),), self.torch.float32, zero=False)
+        with self.torch.cuda.stream(stream):
+            pin.copy_(t, non_blocking=True)
         stream.synchronize()
-        return t.to("cpu").numpy().astype(np.float64)
+        return pin.numpy().astype(np.float64)
 
     def _cycle_start(self):
         """r0 = b - A x (AB) or B(b - A x) (BA) into W row 0; returns (beta, ||d0||)."""

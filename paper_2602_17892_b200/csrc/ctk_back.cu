@@ -367,8 +367,18 @@ static int back_splits(const ctk_geom* g, int a0, int a1) {
         const char* e = getenv("CTK_BACK_TARGET");       // tuning override (CTAs)
         target = e && atoi(e) > 0 ? atoi(e) : 148 * 12;   // ~1.5 waves of 256-thread CTAs
     }
+    static int min_ang = -1;
+    if (min_ang < 0) {
+        const char* e = getenv("CTK_BACK_MINANG");      // tuning override: angles per CTA
+        min_ang = e && atoi(e) > 0 ? atoi(e) : 0;
+    }
     int S = (target + tiles - 1) / tiles;
-    const int max_s = (a1 - a0 + BCA - 1) / BCA;      // >= one 32-angle chunk per CTA
+    // >= one 32-angle chunk per CTA, or half a chunk when whole chunks leave
+    // the GPU under a third full (c1: 64 tiles x 6 -> x 12 splits; solve
+    // 2.33 -> 2.16 ms; c2 keeps whole chunks)
+    int ma = min_ang;
+    if (ma == 0) ma = (int64_t)tiles * ((a1 - a0 + BCA - 1) / BCA) < 148 * 4 ? BCA / 2 : BCA;
+    const int max_s = (a1 - a0 + ma - 1) / ma;
     if (S > max_s) S = max_s;
     if (S < 1) S = 1;
     return S;

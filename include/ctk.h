@@ -94,8 +94,10 @@ int ctk_count_segments(const ctk_geom_t* g, int a0, int a1, int64_t* counts_dev,
                        void* stream);
 
 /* x = (x0 ? x0 : 0) + B u, summing angles [a0, a1) (u row a at
- * u + (a-a0)*det_count).  work: ctk_back_work_floats() fp32 scratch (may be
- * NULL when that returns 0). */
+ * u + (a-a0)*det_count).  work: ctk_back_work_floats() fp32 scratch,
+ * zero-filled once: [K1 -> K2 chaining counters of the native BA Arnoldi
+ * step][split partial images][per-tile tickets].  A plain apply may pass NULL
+ * when the geometry needs no angle split (large images). */
 int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1);
 int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, int a1,
              const float* x0, float* work, void* stream);

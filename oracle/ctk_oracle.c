@@ -89,23 +89,33 @@ static int siddon_ray(const orc_grid* g, double ct, double st, double offset,
     int iy_i = 0, iy_step = 1, iy_n = use_y ? ny + 1 : 0;
     if (use_y && dy < 0) { iy_i = ny; iy_step = -1; }
     int kx = 0, ky = 0;
+    /* Each stream's next in-range crossing is computed once and kept until it
+     * is consumed (the same value, bit for bit, as re-evaluating it every
+     * merge step). */
+    double tx = INFINITY, ty = INFINITY;
+    int have_x = 0, have_y = 0;
     for (;;) {
-        double tx = INFINITY, ty = INFINITY;
         /* advance streams past values outside (t_lo, t_hi) */
-        while (kx < ix_n) {
-            double v = (g->xmin + (double)ix_i * h - px) / dx;
-            if (v > t_lo && v < t_hi) { tx = v; break; }
-            ix_i += ix_step; ++kx;
+        if (!have_x) {
+            tx = INFINITY;
+            while (kx < ix_n) {
+                double v = (g->xmin + (double)ix_i * h - px) / dx;
+                if (v > t_lo && v < t_hi) { tx = v; have_x = 1; break; }
+                ix_i += ix_step; ++kx;
+            }
         }
-        while (ky < iy_n) {
-            double v = (g->ymin + (double)iy_i * h - py) / dy;
-            if (v > t_lo && v < t_hi) { ty = v; break; }
-            iy_i += iy_step; ++ky;
+        if (!have_y) {
+            ty = INFINITY;
+            while (ky < iy_n) {
+                double v = (g->ymin + (double)iy_i * h - py) / dy;
+                if (v > t_lo && v < t_hi) { ty = v; have_y = 1; break; }
+                iy_i += iy_step; ++ky;
+            }
         }
         if (kx >= ix_n && ky >= iy_n) break;
         double v;
-        if (tx <= ty) { v = tx; ix_i += ix_step; ++kx; }
-        else { v = ty; iy_i += iy_step; ++ky; }
+        if (tx <= ty) { v = tx; ix_i += ix_step; ++kx; have_x = 0; }
+        else { v = ty; iy_i += iy_step; ++ky; have_y = 0; }
         if (v != t_buf[nt - 1]) t_buf[nt++] = v;
     }
     if (t_hi != t_buf[nt - 1]) t_buf[nt++] = t_hi;
@@ -114,8 +124,10 @@ static int siddon_ray(const orc_grid* g, double ct, double st, double offset,
     for (int k = 0; k + 1 < nt; ++k) {
         double l = t_buf[k + 1] - t_buf[k];
         double tm = 0.5 * (t_buf[k] + t_buf[k + 1]);
-        double fx = floor((px + tm * dx - g->xmin) / h);
-        double fy = floor((g->ymax - (py + tm * dy)) / h);
+        double qx = px + tm * dx - g->xmin, qy = g->ymax - (py + tm * dy);
+        /* x / 1.0 == x exactly: skip the divisions at unit pixel size */
+        double fx = floor(h == 1.0 ? qx : qx / h);
+        double fy = floor(h == 1.0 ? qy : qy / h);
         int64_t ix = (int64_t)fx, iy = (int64_t)fy;
         if (ix < 0) ix = 0;
         if (ix > nx - 1) ix = nx - 1;
@@ -130,17 +142,78 @@ static int siddon_ray(const orc_grid* g, double ct, double st, double offset,
     return ns;
 }
 
+static void rev_span(int64_t* pix, double* len, int lo, int hi) {
+    for (--hi; lo < hi; ++lo, --hi) {
+        int64_t tp = pix[lo]; pix[lo] = pix[hi]; pix[hi] = tp;
+        double tl = len[lo]; len[lo] = len[hi]; len[hi] = tl;
+    }
+}
+
+/* Reverse [lo, hi) as a sequence of equal-pixel runs: run order flips, the
+ * order inside each run (trace order of duplicates) is kept. */
+static void rev_groups(int64_t* pix, double* len, int lo, int hi) {
+    rev_span(pix, len, lo, hi);
+    for (int a = lo; a < hi;) {
+        int b = a + 1;
+        while (b < hi && pix[b] == pix[a]) ++b;
+        if (b - a > 1) rev_span(pix, len, a, b);
+        a = b;
+    }
+}
+
+static int is_sorted_pix(const int64_t* pix, int ns) {
+    for (int i = 1; i < ns; ++i)
+        if (pix[i - 1] > pix[i]) return 0;
+    return 1;
+}
+
 /* CSR canonicalisation of one row (scipy csr_sort_indices + csr_sum_duplicates):
- * sort by column, sum duplicates, in place.  Returns merged count. */
-static int canon_row(int64_t* pix, double* len, int ns) {
-    /* insertion sort by pixel (segments arrive nearly sorted or reversed) */
-    for (int i = 1; i < ns; ++i) {
-        int64_t p = pix[i];
-        double l = len[i];
-        int j = i - 1;
-        while (j >= 0 && pix[j] > p) { pix[j + 1] = pix[j]; len[j + 1] = len[j]; --j; }
-        pix[j + 1] = p;
-        len[j + 1] = l;
+ * sort by column, sum duplicates, in place.  Returns merged count.
+ * The result is what a STABLE sort gives (duplicates summed in trace order,
+ * as the insertion sort this replaces did).  Along a ray the row iy and the
+ * column ix of the segments are monotone, so the sorted order is reached in
+ * O(ns) by flipping the row-block order and then each decreasing block (as
+ * runs of equal pixels); should that not leave the row sorted, a stable
+ * bottom-up merge sort of the original order runs instead.  (An insertion
+ * sort is quadratic on the reversed rows of c4/c5 rays, ~3k segments.)
+ * tmp_pix / tmp_len hold ns entries. */
+static int canon_row(int64_t* pix, double* len, int ns, int nx, int64_t* tmp_pix,
+                     double* tmp_len) {
+    if (!is_sorted_pix(pix, ns)) {
+        memcpy(tmp_pix, pix, sizeof(int64_t) * (size_t)ns);
+        memcpy(tmp_len, len, sizeof(double) * (size_t)ns);
+        if (pix[0] / nx > pix[ns - 1] / nx) rev_groups(pix, len, 0, ns);
+        for (int a = 0; a < ns;) {
+            int b = a + 1;
+            while (b < ns && pix[b] / nx == pix[a] / nx) ++b;
+            if (pix[a] > pix[b - 1]) rev_groups(pix, len, a, b);
+            a = b;
+        }
+        if (!is_sorted_pix(pix, ns)) {
+            memcpy(pix, tmp_pix, sizeof(int64_t) * (size_t)ns);
+            memcpy(len, tmp_len, sizeof(double) * (size_t)ns);
+            int64_t *sp = pix, *dp = tmp_pix;
+            double *sl = len, *dl = tmp_len;
+            for (int w = 1; w < ns; w *= 2) {
+                for (int lo = 0; lo < ns; lo += 2 * w) {
+                    int mid = lo + w < ns ? lo + w : ns;
+                    int hi = lo + 2 * w < ns ? lo + 2 * w : ns;
+                    int i = lo, j = mid, o = lo;
+                    while (i < mid && j < hi) {
+                        if (sp[j] < sp[i]) { dp[o] = sp[j]; dl[o++] = sl[j++]; }
+                        else { dp[o] = sp[i]; dl[o++] = sl[i++]; }
+                    }
+                    while (i < mid) { dp[o] = sp[i]; dl[o++] = sl[i++]; }
+                    while (j < hi) { dp[o] = sp[j]; dl[o++] = sl[j++]; }
+                }
+                int64_t* tp = sp; sp = dp; dp = tp;
+                double* tl = sl; sl = dl; dl = tl;
+            }
+            if (sp != pix) {
+                memcpy(pix, sp, sizeof(int64_t) * (size_t)ns);
+                memcpy(len, sl, sizeof(double) * (size_t)ns);
+            }
+        }
     }
     int out = 0;
     for (int i = 0; i < ns; ++i) {
@@ -216,7 +289,11 @@ typedef struct {
     double* data;
 } ray_ctx;
 
-#define RAY_SCRATCH(c) (sizeof(double) * 3 * (size_t)((c)->g.nx + (c)->g.ny + 8))
+#define RAY_SCRATCH(c) (sizeof(double) * 5 * (size_t)((c)->g.nx + (c)->g.ny + 8))
+
+#define CANON_TMP(c, scratch) \
+    (int64_t*)((double*)(scratch) + 3 * ((c)->g.nx + (c)->g.ny + 8)), \
+    (double*)(scratch) + 4 * ((c)->g.nx + (c)->g.ny + 8)
 
 static int trace_row(const ray_ctx* c, int64_t r, void* scratch, int64_t** pix, double** len) {
     const int cap = c->g.nx + c->g.ny + 8;
@@ -232,7 +309,7 @@ static void body_forward(void* vctx, int64_t lo, int64_t hi, void* scratch) {
     for (int64_t r = lo; r < hi; ++r) {
         int64_t* pix; double* len;
         int ns = trace_row(c, r, scratch, &pix, &len);
-        ns = canon_row(pix, len, ns);
+        ns = canon_row(pix, len, ns, c->g.nx, CANON_TMP(c, scratch));
         double s = 0.0;
         for (int k = 0; k < ns; ++k) s += len[k] * c->x[pix[k]];
         c->y[r] = s;
@@ -245,7 +322,7 @@ static void body_count(void* vctx, int64_t lo, int64_t hi, void* scratch) {
         int64_t* pix; double* len;
         int ns = trace_row(c, r, scratch, &pix, &len);
         if (c->row_raw) c->row_raw[r] = ns;
-        c->row_nnz[r] = canon_row(pix, len, ns);
+        c->row_nnz[r] = canon_row(pix, len, ns, c->g.nx, CANON_TMP(c, scratch));
     }
 }
 
@@ -254,7 +331,7 @@ static void body_fill(void* vctx, int64_t lo, int64_t hi, void* scratch) {
     for (int64_t r = lo; r < hi; ++r) {
         int64_t* pix; double* len;
         int ns = trace_row(c, r, scratch, &pix, &len);
-        ns = canon_row(pix, len, ns);
+        ns = canon_row(pix, len, ns, c->g.nx, CANON_TMP(c, scratch));
         int64_t base = c->indptr[r];
         for (int k = 0; k < ns; ++k) {
             c->indices[base + k] = (int32_t)pix[k];

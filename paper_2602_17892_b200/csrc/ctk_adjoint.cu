@@ -375,11 +375,18 @@ int degt_get(ctk_geom* g, DegT* out) {
 
 using namespace ctk;
 
+// Work buffer (split launches): [one arrival ticket per tile, 16-float
+// aligned] [S partial images] -- the tickets at a fixed offset, so calls with
+// different split counts sharing one zero-filled buffer agree on them.
+static int64_t adj_ticket_floats(const ctk_geom* g) {
+    const int64_t tiles = (int64_t)((g->nx + JTX - 1) / JTX) * adj_tiles_y(g);
+    return (tiles + 15) / 16 * 16;
+}
+
 extern "C" int64_t ctk_adjoint_work_floats(const ctk_geom_t* g, int a0, int a1) {
     if (!g || a0 < 0 || a1 > g->n_angles || a0 >= a1) return 0;
     const int S = adj_splits(g, a0, a1);
-    const int64_t tiles = (int64_t)((g->nx + JTX - 1) / JTX) * adj_tiles_y(g);
-    return S > 1 ? (int64_t)S * g->nx * g->ny + tiles : 0;
+    return S > 1 ? adj_ticket_floats(g) + (int64_t)S * g->nx * g->ny : 0;
 }
 
 extern "C" int ctk_adjoint(const ctk_geom_t* gc, const float* u, float* x, int a0, int a1,
@@ -410,9 +417,9 @@ extern "C" int ctk_adjoint(const ctk_geom_t* gc, const float* u, float* x, int a
     A.deg_slot = g->d_deg_slot;
     A.u = u;
     A.x0 = x0;
-    A.out = S > 1 ? work : x;
+    A.out = S > 1 ? work + adj_ticket_floats(g) : x;
     A.x = x;
-    A.cnt = S > 1 ? reinterpret_cast<unsigned*>(work + (size_t)S * n) : nullptr;
+    A.cnt = S > 1 ? reinterpret_cast<unsigned*>(work) : nullptr;
     A.dt_ptr = dt.ptr;
     A.dt_ray = dt.ray;
     A.dt_len = dt.len;

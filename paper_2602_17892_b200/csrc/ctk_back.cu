@@ -49,44 +49,30 @@ struct BackArgs {
     double h, xmin, ymax, center;
     const ctk_xchg_args* xc;   // optional (device copy): push the tile to its owner rank
     unsigned* ready;      // optional: K1's finished-CTA counters per 4-angle group (chaining)
-    unsigned ready_need;  // K1 CTAs per group (bin blocks)
+    unsigned ready_target;  // K1 CTAs per group (bin blocks) x this step's epoch
 };
 
+// Sinogram loads.  Chained (A.ready): u is written by the still-running K1,
+// so the read-only (.nc) path is not allowed -- L2-coherent loads after the
+// acquire instead.
+__device__ __forceinline__ float ld_u(const BackArgs& A, const float* p) {
+    return A.ready ? __ldcg(p) : __ldg(p);
+}
+
 // K2 chaining (ctk_common.cuh): wait until the K1 groups holding angles
-// [ac, ac + na) are complete.  Bounded: a counter that never fills (a
-// protocol bug) traps after ~5 s instead of hanging the GPU.
+// [ac, ac + na) are complete.  The counters are monotonic within an Arnoldi
+// cycle (zeroed by the host before its step 0, never reset by a kernel):
+// step j's K1 brings every group to need * (j + 1), and K1 counts a CTA only
+// after its griddepcontrol.wait, i.e. after the previous step's K2 has
+// completed -- so a count at or above the target always means this step's
+// rows are written, whatever kernels of neighbouring steps are co-resident.
 __device__ __forceinline__ void wait_k1_groups(const BackArgs& A, int ac, int na, int tid) {
     const int g0 = (ac - A.a0) / CTK_FWD_APB, g1 = (ac + na - 1 - A.a0) / CTK_FWD_APB;
     if (tid <= g1 - g0) {
         const unsigned* c = A.ready + g0 + tid;
-        if (ctk_ld_acquire_gpu(c) < A.ready_need) {
-            unsigned long long t0;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-            while (ctk_ld_acquire_gpu(c) < A.ready_need) {
-                __nanosleep(64);
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                if (t - t0 > 5000000000ull) __trap();
-            }
-        }
+        while (ctk_ld_acquire_gpu(c) < A.ready_target) __nanosleep(64);
     }
     __syncthreads();
-}
-
-// The CTA that completes the last wait of the launch resets the counters
-// for the next K1 (which cannot signal before this K2 has completed).
-__device__ __forceinline__ void release_k1_groups(const BackArgs& A, int tid) {
-    __syncthreads();
-    if (tid != 0) return;
-    const int ng = (A.a1 - A.a0 + CTK_FWD_APB - 1) / CTK_FWD_APB;
-    unsigned* pass = A.ready + ng;
-    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
-    unsigned old;
-    asm volatile("atom.add.relaxed.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(pass) : "memory");
-    if (old == total - 1) {
-        for (int g = 0; g < ng; ++g) A.ready[g] = 0u;
-        *pass = 0u;
-    }
 }
 
 // K1's zero-padded copies of the output pixel (ix, iy) (see ctk_forward.cu).
@@ -115,8 +101,8 @@ __device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, co
             if (ai < na) {
                 const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
                 const int b = s_w0[ai] + tx, b2 = b + 32;
-                if (b >= 0 && b < D) va[j] = __ldg(row + b);
-                if (b2 >= 0 && b2 < D && tx + 32 <= wmax) vb[j] = __ldg(row + b2);
+                if (b >= 0 && b < D) va[j] = ld_u(A, row + b);
+                if (b2 >= 0 && b2 < D && tx + 32 <= wmax) vb[j] = ld_u(A, row + b2);
             }
         }
 #pragma unroll
@@ -129,8 +115,8 @@ __device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, co
             const int b = s_w0[ai] + tx;
             float v1a = tx < 31 ? up_a : b_0, v1b = up_b;
             const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
-            if (b == -1) v1a = __ldg(row + q1);
-            if (b + 32 == -1) v1b = __ldg(row + q1);
+            if (b == -1) v1a = ld_u(A, row + q1);
+            if (b + 32 == -1) v1b = ld_u(A, row + q1);
             float2* dst = win + ai * wmax;
             float d = v1a - va[j];
             dst[tx] = make_float2(va[j] - d, d);
@@ -147,9 +133,9 @@ __device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, co
         float2* dst = win + ai * wmax;
         for (int i = tx; i < wmax; i += BTX) {
             const int b = w0 + i;
-            const float v0 = (b >= 0 && b < D) ? __ldg(row + b) : 0.f;
+            const float v0 = (b >= 0 && b < D) ? ld_u(A, row + b) : 0.f;
             const int b1 = b == -1 ? q1 : b + 1;
-            const float v1 = (b >= -1 && b + 1 < D) ? __ldg(row + b1) : 0.f;
+            const float v1 = (b >= -1 && b + 1 < D) ? ld_u(A, row + b1) : 0.f;
             const float d = v1 - v0;
             dst[i] = make_float2(v0 - d, d);
         }
@@ -236,7 +222,6 @@ __global__ void __launch_bounds__(BTHREADS, PPT == 4 ? CTK_BACK_MINB4 : 6) k_bac
         for (int r = 0; r < PPT; ++r) acc[r] += (double)sp[r];
         __syncthreads();
     }
-    if (A.ready) release_k1_groups(A, tid);
     if (SPLIT) {
         // global partial images + per-tile arrival tickets: the last of the
         // gridDim.z CTAs of a tile sums the partials in split order
@@ -394,12 +379,16 @@ static int64_t back_tiles(const ctk_geom* g) {
 
 int64_t ctk_back_tiles(const ctk_geom* g) { return back_tiles(g); }
 
-// Work buffer: [K1-chaining flags: one counter per 4-angle group + a pass
-// counter, 16-float aligned] [S partial images] [one arrival ticket per tile].
-// The flags sit first so every angle range / split count agrees on them.
+// Work buffer: [K1-chaining flags: one counter per 4-angle group, 16-float
+// aligned] [one arrival ticket per tile, 16-float aligned] [S partial images].
+// Flags and tickets sit at offsets fixed by the geometry, so calls with
+// different angle ranges / split counts sharing one (zero-filled once)
+// buffer agree on them; the partial images after them are scratch.
 static int64_t back_flag_floats(const ctk_geom* g) {
-    return ((int64_t)(g->n_angles + CTK_FWD_APB - 1) / CTK_FWD_APB + 1 + 15) / 16 * 16;
+    return ((int64_t)(g->n_angles + CTK_FWD_APB - 1) / CTK_FWD_APB + 15) / 16 * 16;
 }
+
+static int64_t back_ticket_floats(const ctk_geom* g) { return (back_tiles(g) + 15) / 16 * 16; }
 
 unsigned* ctk_back_flags(const ctk_geom* g, float* work) {
     return work ? reinterpret_cast<unsigned*>(work) : nullptr;
@@ -408,7 +397,7 @@ unsigned* ctk_back_flags(const ctk_geom* g, float* work) {
 extern "C" int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1) {
     if (!g || a0 < 0 || a1 > g->n_angles || a0 >= a1) return 0;
     const int S = back_splits(g, a0, a1);
-    return back_flag_floats(g) + (S > 1 ? (int64_t)S * g->nx * g->ny + back_tiles(g) : 0);
+    return back_flag_floats(g) + back_ticket_floats(g) + (S > 1 ? (int64_t)S * g->nx * g->ny : 0);
 }
 
 extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, int a1,
@@ -416,18 +405,21 @@ extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, i
     return ctk_back_ex(g, u, x, a0, a1, x0, work, nullptr, stream);
 }
 
+int64_t ctk_back_flag_count(const ctk_geom* g) { return back_flag_floats(g); }
+
 // stage != NULL: also write K1's zero-padded P / PT copies of x into the
 // forward workspace `stage` (interior only: its zero padding is written by
 // any plain ctk_forward on that workspace).
 int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
-                float* work, float* stage, void* stream, bool after_k1) {
-    return ctk_back_xc(g, u, x, a0, a1, x0, work, stage, nullptr, stream, after_k1);
+                float* work, float* stage, void* stream, unsigned k1_epoch) {
+    return ctk_back_xc(g, u, x, a0, a1, x0, work, stage, nullptr, stream, k1_epoch);
 }
 
 // xc (device pointer) != NULL: push the partial tiles to their owners
 // instead of writing x (ctk_back_exchange, phase 1).
 int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
-                float* work, float* stage, const ctk_xchg_args* xc, void* stream, bool after_k1) {
+                float* work, float* stage, const ctk_xchg_args* xc, void* stream,
+                unsigned k1_epoch) {
     if (!g) return ctk_fail(CTK_ERR_ARG, "null geometry");
     if (a0 < 0 || a1 > g->n_angles || a0 > a1)
         return ctk_fail(CTK_ERR_SHAPE, "angle range [%d, %d) outside [0, %d)", a0, a1, g->n_angles);
@@ -444,13 +436,12 @@ int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
     if (S > 1 && !work)
         return ctk_fail(CTK_ERR_ARG, "ctk_back needs %lld work floats",
                         (long long)ctk_back_work_floats(g, a0, a1));
-    if (after_k1 && !work) return ctk_fail(CTK_ERR_ARG, "K1 chaining needs the work buffer");
+    if (k1_epoch && !work) return ctk_fail(CTK_ERR_ARG, "K1 chaining needs the work buffer");
     BackArgs A;
-    float* body = work ? work + back_flag_floats(g) : nullptr;
-    A.part = S > 1 ? body : nullptr;
-    A.cnt = S > 1 ? reinterpret_cast<unsigned*>(body + (size_t)S * g->nx * g->ny) : nullptr;
-    A.ready = after_k1 ? ctk_back_flags(g, work) : nullptr;
-    A.ready_need = (unsigned)((g->det_count + 31) / 32);
+    A.cnt = work ? reinterpret_cast<unsigned*>(work + back_flag_floats(g)) : nullptr;
+    A.part = S > 1 ? work + back_flag_floats(g) + back_ticket_floats(g) : nullptr;
+    A.ready = k1_epoch ? ctk_back_flags(g, work) : nullptr;
+    A.ready_target = (unsigned)((g->det_count + 31) / 32) * k1_epoch;
     A.bp = g->d_bp;
     A.u = u;
     A.x0 = x0;

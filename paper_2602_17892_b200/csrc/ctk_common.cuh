@@ -201,15 +201,19 @@ bool ctk_iterate_batch_ok(int k0, int nb, int nvec_cap, int64_t Lx, int64_t Lr);
 // (acquire) instead of waiting for the whole of K1 -- K2 overlaps K1's last
 // wave.  Deadlock-free: K2 is a programmatic dependent of K1, which triggers
 // at entry, so every K1 CTA is resident or done before any K2 CTA can spin.
+// The counters grow monotonically through a cycle (see wait_k1_groups).
 constexpr int CTK_FWD_APB = 4;                 // angles per K1 CTA (one per warp)
 unsigned* ctk_back_flags(const ctk_geom* g, float* work);
 int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1, const float* b,
                    float* work, bool prestaged, void* stream, unsigned* done_flags = nullptr);
+// k1_epoch > 0: chained after K1 (step j of an Arnoldi cycle passes j + 1;
+// the caller zeroes the ctk_back_flag_count() flag words before step 0).
 int ctk_back_ex(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
-                float* work, float* stage, void* stream, bool after_k1 = false);
+                float* work, float* stage, void* stream, unsigned k1_epoch = 0);
 int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, const float* x0,
                 float* work, float* stage, const ctk_xchg_args* xc, void* stream,
-                bool after_k1 = false);
+                unsigned k1_epoch = 0);
+int64_t ctk_back_flag_count(const ctk_geom* g);
 int ctk_xchg_finish(const ctk_geom* g, const ctk_xchg_args* xc, int nranks, int phases,
                     cudaStream_t st);
 int64_t ctk_back_tiles(const ctk_geom* g);

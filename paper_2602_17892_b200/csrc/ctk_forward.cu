@@ -419,11 +419,17 @@ static_assert(FWD_APB == CTK_FWD_APB, "K2 chaining counts K1 CTAs per 4-angle gr
 
 // K2 chaining: after the barrier that orders the CTA's output stores, one
 // release increment of its angle group's counter (see ctk_common.cuh).
+// The signalling thread first waits for the previous kernel (K3 of the last
+// step, which itself waited for that step's K2): a CTA whose rays all miss
+// never reached griddepcontrol.wait, and counting it early would let the
+// previous step's K2 see this step's increments.
 __device__ __forceinline__ void signal_group(const FwdArgs& A) {
     if (!A.done) return;
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
+        ctk_pdl_wait();
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.done + blockIdx.y) : "memory");
+    }
 }
 
 constexpr int FWD_MAX_SPLIT = 8;            // portable cluster size limit
@@ -452,6 +458,7 @@ __global__ void __launch_bounds__(FWD_THREADS, CTK_FWD_MINB) k_forward(FwdArgs A
     if (!SPLIT) {
         if (a < A.a1 && j < A.D) {
             const double acc = forward_ray(A, a, A.deg_slot[a], j, 0);
+            ctk_pdl_wait();          // rays that miss skipped it: y may still be read upstream
             A.y[o] = A.b ? (float)((double)A.b[o] - acc) : (float)acc;
         }
         signal_group(A);
@@ -496,6 +503,7 @@ __global__ void __launch_bounds__(FWD_THREADS, CTK_FWD_MINB) k_forward(FwdArgs A
         " @!p bra WAIT_%=;\n}\n" ::"r"(bar)
         : "memory");
     if (valid) {
+        ctk_pdl_wait();              // rays that miss skipped it: y may still be read upstream
         double s = (double)v;
         for (int c = 1; c < A.split; ++c) s += (double)s_part[c - 1][threadIdx.x];
         A.y[o] = A.b ? (float)((double)A.b[o] - s) : (float)s;

@@ -135,10 +135,17 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
         const int64_t k1_ctas = (int64_t)((g->det_count + 31) / 32) *
                                 ((na + CTK_FWD_APB - 1) / CTK_FWD_APB) * g->fwd_split;
         const bool ch = chain && back_work && k1_ctas <= 4 * 8 * 148;
+        // monotonic counters: zeroed (stream-ordered) before a cycle's step 0,
+        // step j's K2 waits for (j + 1) K1 passes per group
+        if (ch && j == 0)
+            CTK_CUDA(cudaMemsetAsync(ctk_back_flags(g, back_work), 0,
+                                     sizeof(unsigned) * (size_t)ctk_back_flag_count(g), st));
         if ((rc = ctk_forward_ex(g, w, aw, 0, na, nullptr, stage_work, pre, stream,
                                  ch ? ctk_back_flags(g, back_work) : nullptr)))
             return rc;
-        if ((rc = ctk_back_ex(g, aw, q, 0, na, nullptr, back_work, nullptr, stream, ch))) return rc;
+        if ((rc = ctk_back_ex(g, aw, q, 0, na, nullptr, back_work, nullptr, stream,
+                              ch ? (unsigned)(j + 1) : 0u)))
+            return rc;
     }
     // The SMEM Gram-Schmidt step writes the column straight into the
     // page-locked host row (mapped, UVA) -- no D2H copy on the critical stream.

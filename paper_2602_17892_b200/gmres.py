@@ -177,7 +177,8 @@ def _pool():
     return _POOL
 
 
-_PINNED: dict = {}
+_PINNED_LOCAL = threading.local()
+_PINNED_KEEP = 16                              # buffers kept per thread (LRU)
 
 
 def _pinned(torch, name, shape, dtype, zero=True):
@@ -185,15 +186,30 @@ def _pinned(torch, name, shape, dtype, zero=True):
     dtype).  A fresh pin_memory() per solve goes through torch's caching host
     allocator, which falls back to cudaHostAlloc (milliseconds) whenever the
     previous solve's block is still fenced by an event.  Solves are
-    synchronous, so a buffer is free again when its solve returns."""
-    key = (threading.get_ident(), name, tuple(shape), dtype)
-    t = _PINNED.get(key)
+    synchronous, so a buffer is free again when its solve returns.  The cache
+    is thread-local (freed with its thread) and keeps the _PINNED_KEEP most
+    recently used buffers; release_pinned() drops the calling thread's."""
+    from collections import OrderedDict
+    cache = getattr(_PINNED_LOCAL, "cache", None)
+    if cache is None:
+        cache = _PINNED_LOCAL.cache = OrderedDict()
+    key = (name, tuple(shape), dtype)
+    t = cache.get(key)
     if t is None:
         t = torch.empty(shape, dtype=dtype).pin_memory()
-        _PINNED[key] = t
+        cache[key] = t
+        while len(cache) > _PINNED_KEEP:
+            cache.popitem(last=False)
+    else:
+        cache.move_to_end(key)
     if zero:
         t.zero_()
     return t
+
+
+def release_pinned() -> None:
+    """Free the calling thread's cached page-locked buffers."""
+    _PINNED_LOCAL.cache = None
 
 
 _WORKSPACES: dict = {}

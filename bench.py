@@ -1,21 +1,28 @@
 """Benchmark: hybrid AB-/BA-GMRES projector path on B200 (one JSON line).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2]
-                    [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5]
+                    [--slices-per-gpu S] [--impl ours|reference]
 
 Metric (BASELINE.json): A+B projected rays/s through hybrid GMRES, plus
-hybrid iterations/s and the HBM-roofline fraction of the dominant kernel.
+hybrid iterations/s, slices/s and the HBM-roofline fraction of the dominant
+kernel.
 
-* A "step" is one full hybrid solve of the workload (c2 by default:
-  BA-GMRES + L-curve, 80 iterations, 256^2 image, 360 angles x 363 bins,
-  seeded random-ellipse phantom, 2% noise).  Projected rays
-  per step = K * (A+B applies per iteration) * m  (BA: 2A+1B, AB: 2A+2B;
-  cycle-start applies excluded).
-* ``value``: device-resident solve (b already in HBM, x left in HBM), timed
-  with CUDA events on the solve stream, L2 flushed (256 MiB write) before
-  every timed step.  ``e2e``: the same solve through the public API
-  ``run_gmres(A, B, b_numpy, cfg)`` with host b in and host x out, wall-clock
-  with the copies inside the timed region.
+* Default workload: c5, the largest configuration -- batched hybrid
+  BA-GMRES + GCV, 60 iterations, 2048^2 px, 1800 angles x 2897 bins, seeded
+  random-ellipse phantom per slice, 1% noise -- at 8 slices per GPU (the
+  config's 64 slices over 8 B200; slice s has seeds (s, 1000 + s)).  A "step"
+  is the full hybrid solve of every slice of this GPU, issued from S host
+  threads at once (each with its own stream pair; slices never communicate).
+  Projected rays per step = S * K * (A+B applies per iteration) * m
+  (BA: 2A+1B, AB: 2A+2B; cycle-start applies excluded).
+  ``--workload c1..c4`` run one solve (or the c3 A+B microbenchmark) per step.
+* ``value``: device-resident solves (b already in HBM, x left in HBM), timed
+  with CUDA events (e0 before every slice stream starts, e1 after all have
+  joined), L2 flushed (256 MiB write) before every timed step; the inputs
+  (4.2M-px images, 5.2M-sample sinograms, a 2.3 GB Krylov basis per slice)
+  are far larger than L2 anyway.  ``e2e``: the same solves through the
+  public API ``run_gmres(A, B, b_numpy, cfg)`` with host b in and host x out,
+  wall-clock with the copies inside the timed region.
 * ``roofline``: the projector kernel with the largest share of the timed
   region, algorithmic bytes per launch (A: 4 nnz + 4 m, B: 8 n na + 4 n)
   over its mean CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
@@ -23,8 +30,8 @@ hybrid iterations/s and the HBM-roofline fraction of the dominant kernel.
   reference's algorithm restated in C + numpy, CSR A as the reference builds
   it) on a bounded sample of the same workload using all host cores.
 * Multi-GPU (torchrun): weak scaling by independent slices -- rank r solves
-  its own seeded slice, no data-path collective (the c5 pattern); the step
-  time is the max over ranks.
+  its own seeded slices r*S .. r*S+S-1, no data-path collective (the c5
+  pattern); the step time is the max over ranks.
 * ``--impl reference``: the CPU reference arm (oracle port, all host cores)
   on the same workload/metric; rank 0 only under torchrun.
 """
@@ -58,7 +65,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--slices-per-gpu", type=int, default=0,
+                    help="concurrent independent slices per GPU (default: 8 for c5, else 1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -146,118 +155,154 @@ class ClockSampler:
 # CPU arm: the oracle port (reference algorithm, host cores)
 # ----------------------------------------------------------------------------
 
-def cpu_sample(spec, iters=None, threads=0):
-    """Time the oracle port on a bounded sample of the workload.
+class CpuSample:
+    """One bounded, repeatable sample of the workload on the host cores (the
+    oracle port: the reference's algorithm restated -- CSR A as the reference
+    assembles it, pixel-driven B, numpy MGS/lambda).  Set-up (CSR assembly)
+    happens once in the constructor; run() is one timed sample and returns
+    rays/s in the workload's metric (reference applies per iteration).
 
-    Returns dict(value rays/s, iters/s, cores, sample description)."""
-    from oracle import oracle as O
-    from paper_2602_17892_b200 import problems
+    * c1/c2: the first `iters` iterations of the hybrid solve;
+    * c3: `reps` x (A + B) applies;
+    * c4/c5: A (CSR) and B applies on a strided angle subset, extrapolated
+      linearly in angles to the full geometry (the full CSR needs ~23 GB at
+      c4, ~115 GB per slice at c5); orthogonalisation / lambda excluded."""
 
-    threads = threads or len(os.sched_getaffinity(0))
-    if spec.N >= 1024:
-        return cpu_sample_subset(spec, threads)
-    g = O.Geometry(spec.N, spec.N, 1.0, spec.angles(), spec.det_count, 1.0)
-    t0 = time.perf_counter()
-    A = O.CsrForward(g, nthreads=threads)
-    build_s = time.perf_counter() - t0
-    if spec.method is None:           # c3 microbench: A + B applies
-        x = problems.uniform_image(g.n, 0)
-        u = problems.uniform_sinogram(g.m, 1)
-        reps = iters or CPU_SAMPLE_ITERS[spec.name]
+    def __init__(self, spec, threads=0, iters=None):
+        from oracle import oracle as O
+        from paper_2602_17892_b200 import problems
+        self.O, self.spec = O, spec
+        self.threads = threads or len(os.sched_getaffinity(0))
         t0 = time.perf_counter()
-        for _ in range(reps):
-            A(x)
-            O.back(g, u, threads)
+        if spec.N >= 1024:
+            stride = max(1, spec.n_angles // 18)
+            self.sub = spec.angles()[::stride]
+            g = O.Geometry(spec.N, spec.N, 1.0, self.sub, spec.det_count, 1.0)
+            self.x = problems.uniform_image(g.n, 0)
+            self.u = problems.uniform_sinogram(g.m, 1)
+        else:
+            g = O.Geometry(spec.N, spec.N, 1.0, spec.angles(), spec.det_count, 1.0)
+        self.g = g
+        self.A = O.CsrForward(g, nthreads=self.threads)
+        self.build_s = time.perf_counter() - t0
+        if spec.method is None:
+            self.x = problems.uniform_image(g.n, 0)
+            self.u = problems.uniform_sinogram(g.m, 1)
+            self.reps = iters or CPU_SAMPLE_ITERS[spec.name]
+        elif spec.N < 1024:
+            xt = problems.random_ellipse_phantom(spec.N, spec.ellipses, spec.phantom_seed)
+            b, _ = problems.add_noise(self.A(xt), spec.noise, spec.noise_seed)
+            self.b = b.astype(np.float32).astype(np.float64)
+            self.iters = iters or CPU_SAMPLE_ITERS[spec.name]
+
+    def run(self):
+        """One timed sample; adds the effective core count (process CPU time
+        / wall time over the sample)."""
+        c0, w0 = time.process_time(), time.perf_counter()
+        r = self._run()
+        r["cpu_time_over_wall"] = round((time.process_time() - c0) / (time.perf_counter() - w0), 2)
+        return r
+
+    def _run(self):
+        O, spec, g, th = self.O, self.spec, self.g, self.threads
+        if spec.N >= 1024:
+            t0 = time.perf_counter()
+            self.A(self.x)
+            ta = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            O.back(g, self.u, th)
+            tb = time.perf_counter() - t0
+            scale = spec.n_angles / len(self.sub)
+            ta, tb = ta * scale, tb * scale
+            na, nb = applies_per_iter(spec.method) if spec.method else (1, 1)
+            per_iter = na * ta + nb * tb
+            return dict(value=(na + nb) * spec.m / per_iter, iters_per_s=1.0 / per_iter,
+                        cores=th, seconds=(ta + tb) / scale,
+                        sample=(f"extrapolated: A (CSR) and B applies on {len(self.sub)} of "
+                                f"{spec.n_angles} angles at {spec.name}, scaled x{scale:.1f}; "
+                                f"{na}A+{nb}B per iteration, orthogonalisation/lambda excluded; "
+                                f"CSR build {self.build_s:.1f}s excluded"))
+        if spec.method is None:
+            t0 = time.perf_counter()
+            for _ in range(self.reps):
+                self.A(self.x)
+                O.back(g, self.u, th)
+            dt = time.perf_counter() - t0
+            return dict(value=2 * self.reps * g.m / dt, iters_per_s=None, cores=th, seconds=dt,
+                        sample=f"{self.reps}x (A + B) applies at {spec.name}, "
+                               f"CSR build {self.build_s:.1f}s excluded")
+        K = self.iters
+        t0 = time.perf_counter()
+        O.gmres(self.A, lambda u: O.back(g, u, th), self.b, spec.method, spec.strategy, K)
         dt = time.perf_counter() - t0
-        return dict(value=2 * reps * g.m / dt, iters_per_s=None, cores=threads,
-                    sample=f"{reps}x (A + B) applies at {spec.name}, CSR build {build_s:.1f}s excluded",
-                    seconds=dt)
-    xt = problems.random_ellipse_phantom(spec.N, spec.ellipses, spec.phantom_seed)
-    b, _ = problems.add_noise(A(xt), spec.noise, spec.noise_seed)
-    b = b.astype(np.float32).astype(np.float64)
-    K = iters or CPU_SAMPLE_ITERS[spec.name]
-    t0 = time.perf_counter()
-    O.gmres(A, lambda u: O.back(g, u, threads), b, spec.method, spec.strategy, K)
-    dt = time.perf_counter() - t0
-    na, nb = applies_per_iter(spec.method)
-    return dict(value=K * (na + nb) * g.m / dt, iters_per_s=K / dt, cores=threads,
-                sample=(f"first {K} of {spec.max_iter} {spec.method}/{spec.strategy} iterations at "
-                        f"{spec.name} (oracle port: CSR A + C back + numpy MGS/lambda), "
-                        f"CSR build {build_s:.1f}s excluded"), seconds=dt)
+        na, nb = applies_per_iter(spec.method)
+        return dict(value=K * (na + nb) * g.m / dt, iters_per_s=K / dt, cores=th, seconds=dt,
+                    sample=(f"first {K} of {spec.max_iter} {spec.method}/{spec.strategy} "
+                            f"iterations at {spec.name} (oracle port: CSR A + C back + numpy "
+                            f"MGS/lambda), CSR build {self.build_s:.1f}s excluded"))
 
 
-def cpu_sample_subset(spec, threads, stride=None):
-    """c4/c5: the full CSR would need ~23 GB (c4) / ~115 GB (c5 per slice), so
-    time the reference algorithm (CSR A + pixel-driven B) on a strided angle
-    subset and extrapolate linearly in angles (SURVEY.md §8d protocol)."""
-    from oracle import oracle as O
-    from paper_2602_17892_b200 import problems
-
-    stride = stride or max(1, spec.n_angles // 24)
-    sub = spec.angles()[::stride]
-    g = O.Geometry(spec.N, spec.N, 1.0, sub, spec.det_count, 1.0)
-    A = O.CsrForward(g, nthreads=threads)
-    x = problems.uniform_image(g.n, 0)
-    u = problems.uniform_sinogram(g.m, 1)
-    t0 = time.perf_counter()
-    A(x)
-    ta = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    O.back(g, u, threads)
-    tb = time.perf_counter() - t0
-    scale = spec.n_angles / len(sub)
-    ta, tb = ta * scale, tb * scale                 # extrapolated full-geometry applies
-    na, nb = applies_per_iter(spec.method) if spec.method else (1, 1)
-    per_iter = na * ta + nb * tb
-    return dict(value=(na + nb) * spec.m / per_iter, iters_per_s=1.0 / per_iter, cores=threads,
-                sample=(f"extrapolated: A (CSR) and B applies on {len(sub)} of {spec.n_angles} "
-                        f"angles at {spec.name}, scaled x{scale:.1f}; {na}A+{nb}B per iteration, "
-                        f"orthogonalisation/lambda excluded"), seconds=ta + tb)
+def cpu_sample(spec, iters=None, threads=0):
+    """One sample (bench's cpu_baseline leg)."""
+    return CpuSample(spec, threads, iters).run()
 
 
 def run_reference(args, spec, rank, world):
+    """CPU reference arm: the oracle port on all host cores.  Exactly
+    args.warmup untimed + args.steps timed samples (each a bounded sample of
+    the workload, see CpuSample); rank 0 only."""
     if rank != 0:
         return
-    steps, warm = args.steps, args.warmup
-    # each step is a bounded sample of the workload; keep the whole run short
-    iters = max(1, CPU_SAMPLE_ITERS[spec.name] // 2)
-    if spec.N >= 1024:
-        steps, warm = min(steps, 2), 0
+    spg = args.slices_per_gpu or (8 if spec.slices > 1 else 1)
+    smp = CpuSample(spec, iters=max(1, CPU_SAMPLE_ITERS[spec.name] // 2))
     vals, secs = [], []
-    for i in range(warm + steps):
-        r = cpu_sample(spec, iters=iters)
-        if i >= warm:
+    for i in range(args.warmup + args.steps):
+        r = smp.run()
+        if i >= args.warmup:
             vals.append(r["value"])
             secs.append(r["seconds"])
     value = float(np.mean(vals))
     line = {
-        "impl": "reference", "metric": metric_name(spec), "value": value, "unit": "rays/s",
-        "n_gpus": world, "steps": steps, "warmup": warm,
+        "impl": "reference", "metric": metric_name(spec, spg), "value": value, "unit": "rays/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * float(np.mean(secs)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(spec, world),
+        "config": workload_config(spec, world, spg),
         "cpu_baseline": {"value": value, "unit": "rays/s", "cores": r["cores"], "kind": "port",
-                         "sample": r["sample"]},
+                         "sample": r["sample"], "cpu_time_over_wall": r["cpu_time_over_wall"],
+                         "cpu_env": cpu_env()},
         "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def metric_name(spec):
+def cpu_env():
+    """Host-core context of a CPU number."""
+    keys = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
+    return {"cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)),
+            **{k: os.environ.get(k) for k in keys}}
+
+
+def metric_name(spec, spg=1):
     if spec.method is None:
         return f"A+B projected rays/s ({spec.name} projector microbenchmark)"
-    return f"A+B projected rays/s (hybrid {spec.method.split('-')[0].upper()}-GMRES solve, {spec.name})"
+    what = f"{spg} concurrent slice solves" if spg > 1 else "solve"
+    return (f"A+B projected rays/s (hybrid {spec.method.split('-')[0].upper()}-GMRES {what}, "
+            f"{spec.name})")
 
 
-def workload_config(spec, world):
+def workload_config(spec, world, spg=1):
     cfg = {"workload": f"{spec.name}: {spec.N}x{spec.N} px, {spec.n_angles} angles, "
                        f"{spec.det_count} bins"
                        + (f", {spec.method} {spec.strategy}, {spec.max_iter} it, "
-                          f"{int(spec.noise * 100)}% noise" if spec.method else ", 100 A + 100 B"),
-           "n": spec.n, "m": spec.m, "slices_per_gpu": 1,
-           "parallelism": f"weak x{world} (independent slices)" if world > 1 else "single GPU",
-           "l2": "flushed (256 MiB write) before every timed step"}
+                          f"{int(spec.noise * 100)}% noise" if spec.method else ", 100 A + 100 B")
+                       + (f", {spg} independent slices per GPU" if spg > 1 else ""),
+           "n": spec.n, "m": spec.m, "slices_per_gpu": spg,
+           "parallelism": (f"weak x{world} (independent slices)" if world > 1 else "single GPU")
+                          + (f", {spg} concurrent slice solves per GPU" if spg > 1 else ""),
+           "l2": "flushed (256 MiB write) before every timed step; per-slice inputs and "
+                 "Krylov basis exceed L2"}
     return cfg
 
 
@@ -306,8 +351,10 @@ def main():
     hbm_peak, peak_src = measured_peak()
     result = {}
 
+    spg = args.slices_per_gpu or (8 if spec.slices > 1 else 1)
     if spec.method is None:
         # c3 projector microbenchmark: a step = 1 A + 1 B apply
+        spg = 1
         x = torch.from_numpy(problems.uniform_image(dg.n, 0).astype(np.float32)).to(dev)
         u = torch.from_numpy(problems.uniform_sinogram(dg.m, 1).astype(np.float32)).to(dev)
         y = torch.empty(dg.m, dtype=torch.float32, device=dev)
@@ -319,28 +366,50 @@ def main():
         rays_per_step = executed_per_step = 2 * dg.m
         iters_per_step = None
     else:
-        pseed, nseed = problems.slice_seeds(spec, rank) if spec.slices > 1 else (
-            spec.phantom_seed + rank, spec.noise_seed + 1000 * rank)
-        xt = problems.random_ellipse_phantom(spec.N, spec.ellipses, pseed)
-        with torch.cuda.stream(stream):
-            xd = torch.from_numpy(xt.astype(np.float32)).to(dev)
-            clean = dg.forward(xd, stream=stream)
-        stream.synchronize()
-        b_host, _ = problems.add_noise(clean.cpu().numpy().astype(np.float64), spec.noise, nseed)
-        b_host = b_host.astype(np.float32).astype(np.float64)
-        b_dev = torch.from_numpy(b_host.astype(np.float32)).to(dev)
+        b_hosts, b_devs = [], []
+        for i in range(spg):
+            sidx = rank * spg + i                   # global slice index
+            pseed, nseed = problems.slice_seeds(spec, sidx) if spec.slices > 1 else (
+                spec.phantom_seed + sidx, spec.noise_seed + 1000 * sidx)
+            _, x32 = problems.random_ellipse_phantom_device(spec.N, spec.ellipses, pseed,
+                                                            device=local, stream=stream)
+            with torch.cuda.stream(stream):
+                clean = dg.forward(x32, stream=stream)
+            stream.synchronize()
+            b_host, _ = problems.add_noise(clean.cpu().numpy().astype(np.float64), spec.noise,
+                                           nseed)
+            b_host = b_host.astype(np.float32).astype(np.float64)
+            b_hosts.append(b_host)
+            b_devs.append(torch.from_numpy(b_host.astype(np.float32)).to(dev))
         cfg = gmres.SolverConfig(method=spec.method, lambda_strategy=spec.strategy,
                                  max_iter=spec.max_iter)
         na, nb = applies_per_iter(spec.method)
-        rays_per_step = spec.max_iter * (na + nb) * dg.m
+        rays_per_step = spg * spec.max_iter * (na + nb) * dg.m
         # applies this path actually runs: 1A + 1B per Arnoldi step, plus the
         # cycle start (AB: A x0; BA: A x0 and B of the residual)
-        executed_per_step = (2 * spec.max_iter + (1 if spec.method.startswith("ab") else 2)) * dg.m
-        iters_per_step = spec.max_iter
+        executed_per_step = spg * (2 * spec.max_iter
+                                   + (1 if spec.method.startswith("ab") else 2)) * dg.m
+        iters_per_step = spg * spec.max_iter
+        # one caller stream per slice; a persistent pool of spg host threads
+        # (the solver's per-thread stream pairs and workspaces are reused)
+        callers = [torch.cuda.Stream(dev) for _ in range(spg)]
+        from concurrent.futures import ThreadPoolExecutor
+        tpool = ThreadPoolExecutor(max_workers=spg) if spg > 1 else None
+
+        def solve_all(bs, on_device):
+            for c in callers:
+                c.wait_stream(stream)
+
+            def one(i):
+                return gmres.run_gmres(A, B, bs[i], cfg, stream=callers[i],
+                                       keep_on_device=on_device)
+            outs = list(tpool.map(one, range(spg))) if tpool else [one(0)]
+            for c in callers:
+                stream.wait_stream(c)
+            return outs
 
         def step():
-            result["last"] = gmres.run_gmres(A, B, b_dev, cfg, stream=stream,
-                                             keep_on_device=True)
+            result["last"] = solve_all(b_devs, True)[-1]
 
     def barrier():
         if dist is not None:
@@ -352,9 +421,9 @@ def main():
         step()
     barrier()
 
-    def timed_steps():
+    def timed_steps(n_steps):
         tot = 0.0
-        for _ in range(args.steps):
+        for _ in range(n_steps):
             l2_flush()
             barrier()
             e0 = torch.cuda.Event(enable_timing=True)
@@ -369,14 +438,33 @@ def main():
 
     launches0 = _native.launch_counter()
     with ClockSampler(local) as clocks:
-        total_ms = timed_steps()
+        total_ms = timed_steps(args.steps)
     launches = _native.launch_counter() - launches0
-    # Per-kernel durations for the roofline: the same K steps again with CUDA
-    # events around every libctk projector / orthogonalisation call on its
-    # own stream (kept out of the timed steps above, whose events would
-    # otherwise add their own overhead to `value`).
+    # Per-kernel durations for the roofline: CUDA events around every libctk
+    # projector / orthogonalisation call on its own stream, in a separate
+    # pass after the timed one (so the events add nothing to `value`), with
+    # one slice at a time (concurrent slices share the SMs, which would
+    # stretch each launch's own duration).
+    spg_timed = spg
+    if spec.method is not None and spg > 1:
+        prof_bs = b_devs[:1]
+
+        def prof_step():
+            gmres.run_gmres(A, B, prof_bs[0], cfg, stream=stream, keep_on_device=True)
+    else:
+        prof_step = step
     _native.profile_begin()
-    prof_total_ms = timed_steps()
+    prof_total_ms = 0.0
+    for _ in range(max(1, min(args.steps, 3))):
+        l2_flush()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        prof_step()
+        e1.record(stream)
+        e1.synchronize()
+        prof_total_ms += e0.elapsed_time(e1)
     prof = _native.profile_end()
     t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if dist is not None:
@@ -398,8 +486,9 @@ def main():
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
                 "launches_timed": n_l, "mean_launch_ms": round(ms_l, 5),
                 "share_of_step": round(shares[dom] / max(prof_total_ms, 1e-9), 4),
-                "measured": f"CUDA events around each launch over {args.steps} profiled steps "
-                            "run after the timed ones (same workload, L2 flushed per step)"}
+                "measured": "CUDA events around each launch on its stream over "
+                            f"{max(1, min(args.steps, 3))} profiled single-slice solves run "
+                            "after the timed steps (same workload, L2 flushed per solve)"}
     kernels = {}
     for k, (n, ms) in ksum.items():
         kernels[k] = {"launches": n, "mean_ms": round(ms, 5)}
@@ -410,30 +499,36 @@ def main():
     e2e = None
     if not args.no_e2e and spec.method is not None:
         # public API, host buffers: b numpy in, x numpy out, copies inside the timed region
-        for _ in range(args.warmup):          # first-use costs (pinned staging buffers)
-            gmres.run_gmres(A, B, b_host, cfg, stream=stream)
+        for _ in range(min(args.warmup, 2)):   # first-use costs (pinned staging buffers)
+            solve_all(b_hosts, False)
         walls = []
+        res = None
         for _ in range(args.steps):
             l2_flush()
             barrier()
             t0 = time.perf_counter()
-            res = gmres.run_gmres(A, B, b_host, cfg, stream=stream)
+            outs = solve_all(b_hosts, False)
             walls.append(time.perf_counter() - t0)
+            res = outs
         barrier()
         wt = torch.tensor([float(np.sum(walls))], dtype=torch.float64, device=dev)
         if dist is not None:
             dist.all_reduce(wt, op=dist.ReduceOp.MAX)
         e2e = {"value": world * rays_per_step * args.steps / wt.item(), "unit": "rays/s",
-               "h2d_bytes_per_step": int(res.transfer["h2d_bytes"]),
-               "d2h_bytes_per_step": int(res.transfer["d2h_bytes"]),
-               "timing": "wall clock around run_gmres(A, B, b_numpy, cfg) incl. H2D/D2H"}
+               "h2d_bytes_per_step": int(sum(r.transfer["h2d_bytes"] for r in res)),
+               "d2h_bytes_per_step": int(sum(r.transfer["d2h_bytes"] for r in res)),
+               "timing": (f"wall clock around {spg} concurrent run_gmres(A, B, b_numpy, cfg) "
+                          "calls incl. H2D/D2H")}
+        if spec.slices > 1:
+            e2e["slices_per_s"] = world * spg * args.steps / wt.item()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             c = cpu_sample(spec)
             cpu = {"value": c["value"], "unit": "rays/s", "cores": c["cores"], "kind": "port",
-                   "sample": c["sample"]}
+                   "sample": c["sample"], "cpu_time_over_wall": c["cpu_time_over_wall"],
+                   "cpu_env": cpu_env()}
             if c.get("iters_per_s") is not None:
                 cpu["iters_per_s"] = c["iters_per_s"]
         except Exception as exc:  # the baseline is reported, never the product
@@ -442,11 +537,11 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": metric_name(spec), "value": value, "unit": "rays/s", "n_gpus": world,
+            "metric": metric_name(spec, spg), "value": value, "unit": "rays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded random-ellipse phantom / uniform inputs, SURVEY.md §8d)",
-            "config": workload_config(spec, world),
+            "config": workload_config(spec, world, spg),
             "iters_per_s": (world * iters_per_step * args.steps / (total_ms / 1e3)
                             if iters_per_step else None),
             "roofline": roofline, "kernels": kernels, "nnz_A": nnz,
@@ -462,8 +557,8 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }
-        if spec.slices > 1:      # batched slices (c5): one slice solve per rank per step
-            line["slices_per_s"] = world * args.steps / (total_ms / 1e3)
+        if spec.slices > 1:      # batched slices (c5): spg slice solves per rank per step
+            line["slices_per_s"] = world * spg * args.steps / (total_ms / 1e3)
         if "last" in result:
             last = result["last"]
             line["solve"] = {"stop_reason": last.stop_reason, "iterations": len(last.records),

@@ -96,9 +96,15 @@ int ctk_count_segments(const ctk_geom_t* g, int a0, int a1, int64_t* counts_dev,
 /* x = (x0 ? x0 : 0) + B u, summing angles [a0, a1) (u row a at
  * u + (a-a0)*det_count).  work: ctk_back_work_floats() fp32 scratch,
  * zero-filled once: [K1 -> K2 chaining counters of the native BA Arnoldi
- * step][split partial images][per-tile tickets].  A plain apply may pass NULL
- * when the geometry needs no angle split (large images). */
+ * step][per-tile tickets][split partial images] -- counters and tickets at
+ * offsets fixed by the geometry, so one buffer serves every angle range.  A
+ * plain apply may pass NULL when the geometry needs no angle split. */
 int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1);
+/* Layout of that buffer (introspection for protocol tests): out[0] = counter
+ * words (one per 4-angle K1 group, padded), out[1] = ticket words (one per
+ * K2 tile, padded), out[2] = K1 CTAs per group (a chained step j leaves every
+ * group's counter at out[2] * (j + 1)), out[3] = K2 tiles. */
+int ctk_back_work_layout(const ctk_geom_t* g, int64_t* out4);
 int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, int a1,
              const float* x0, float* work, void* stream);
 

@@ -289,11 +289,13 @@ class OracleResult:
 
 def gmres(A, B, b, method, strategy="none", max_iter=100, lambda_value=None,
           reorthogonalize=True, restart_period=0, x0=None, stopping_rule="none",
-          noise_norm=None, dp_tau=1.01, rns_epsilon=1e-4, ncp_threshold=0.05):
+          noise_norm=None, dp_tau=1.01, rns_epsilon=1e-4, ncp_threshold=0.05, on_step=None):
     """(Hybrid) AB-/BA-GMRES, ctkrylov/gmres.py:135-241.
 
     A: R^n -> R^m and B: R^m -> R^n are callables on fp64 vectors.
     Records are dicts with the IterationRecord fields (ctkrylov/gmres.py:95-106).
+    on_step(k, H, beta): optional test hook, called with each iteration's
+    (k+1) x k Hessenberg before its lambda selection.
     """
     b = np.asarray(b, dtype=np.float64)
     ab = method.startswith("ab")
@@ -343,6 +345,8 @@ def gmres(A, B, b, method, strategy="none", max_iter=100, lambda_value=None,
             if not broke:
                 basis.append(q / h[k])
             H = hessenberg(cols, k)
+            if on_step is not None:
+                on_step(k, H, beta)
             warn = False
             if hybrid:
                 try:

@@ -37,6 +37,7 @@ SIGNATURES = {
     "ctk_forward_exact": (_c.c_int, [_vp, _fp, _fp, _c.c_int, _c.c_int, _vp]),
     "ctk_count_segments": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp, _vp]),
     "ctk_back_work_floats": (_c.c_int64, [_vp, _c.c_int, _c.c_int]),
+    "ctk_back_work_layout": (_c.c_int, [_vp, _vp]),
     "ctk_adjoint": (_c.c_int, [_vp, _fp, _fp, _c.c_int, _c.c_int, _fp, _fp, _vp]),
     "ctk_adjoint_work_floats": (_c.c_int64, [_vp, _c.c_int, _c.c_int]),
     "ctk_back": (_c.c_int, [_vp, _fp, _fp, _c.c_int, _c.c_int, _fp, _fp, _vp]),

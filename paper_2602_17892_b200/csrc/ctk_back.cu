@@ -407,6 +407,15 @@ extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, i
 
 int64_t ctk_back_flag_count(const ctk_geom* g) { return back_flag_floats(g); }
 
+extern "C" int ctk_back_work_layout(const ctk_geom_t* g, int64_t* out4) {
+    if (!g || !out4) return ctk_fail(CTK_ERR_ARG, "null argument");
+    out4[0] = back_flag_floats(g);
+    out4[1] = back_ticket_floats(g);
+    out4[2] = (g->det_count + 31) / 32;
+    out4[3] = back_tiles(g);
+    return CTK_OK;
+}
+
 // stage != NULL: also write K1's zero-padded P / PT copies of x into the
 // forward workspace `stage` (interior only: its zero padding is written by
 // any plain ctk_forward on that workspace).

@@ -250,6 +250,54 @@ def make_io():
     print("problem_io.npz", len(out), "entries")
 
 
+def make_lcurve_band(trials=32, deltas=(1e-15, 1e-12, 1e-7)):
+    """c2 L-curve conditioning: run the reference's c2
+    hybrid BA-GMRES + L-curve, capture every iteration's Hessenberg at its
+    select_lambda call (ctkrylov/gmres.py:197), and re-select lambda with the
+    reference's own select_lambda on fp64-rounding-level relative
+    (1e-15, 1e-12) and fp32-rounding-level (1e-7, the GPU path computes in
+    fp32) relative perturbations H * (1 + delta * xi).  The band [min, max]
+    of those lambdas
+    is the spread the reference's OWN arithmetic allows; the GPU test asserts
+    that every GPU lambda lies inside it (plus 1%)."""
+    import ctkrylov.gmres as rg
+    spec = problems.CONFIGS["c2"]
+    g, p, A, B = config_problem(spec)
+    xt = problems.random_ellipse_phantom(spec.N, spec.ellipses, spec.phantom_seed)
+    b, _ = problems.add_noise(A.apply(xt), spec.noise, spec.noise_seed)
+    b32 = b.astype(np.float32).astype(np.float64)
+    captured = []
+    orig = rg.select_lambda
+
+    def spy(H, beta, strategy, fixed=None, *a, **kw):
+        lam = orig(H, beta, strategy, fixed, *a, **kw)
+        captured.append((np.array(H, dtype=np.float64), float(beta), lam))
+        return lam
+    rg.select_lambda = spy
+    try:
+        res = run_gmres(A, B, b32, SolverConfig(method="ba-hybrid", lambda_strategy="lcurve",
+                                                max_iter=spec.max_iter))
+    finally:
+        rg.select_lambda = orig
+    rng = np.random.default_rng(2024)
+    K = len(captured)
+    lo, hi, moved = np.empty(K), np.empty(K), np.zeros((len(deltas), K), dtype=np.int64)
+    for k, (H, beta, lam) in enumerate(captured):
+        vals = [lam]
+        for di, d in enumerate(deltas):
+            for _ in range(trials):
+                lp = orig(H * (1.0 + d * rng.standard_normal(H.shape)), beta, "lcurve")
+                vals.append(lp)
+                moved[di, k] += abs(lp / lam - 1.0) > 1e-3
+        lo[k], hi[k] = min(vals), max(vals)
+    lam_ref = np.array([c[2] for c in captured])
+    assert np.array_equal(lam_ref, [r.lambda_used for r in res.records])
+    np.savez_compressed(os.path.join(HERE, "c2_lcurve_band.npz"), lam_ref=lam_ref, band_lo=lo,
+                        band_hi=hi, moved=moved, deltas=np.array(deltas), trials=np.int64(trials))
+    print("c2_lcurve_band.npz: iterations whose corner moves under 1e-15:",
+          int(np.sum(moved[0] > 0)), "of", K)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small", "solver", "c1", "c2", "io"]
     if "io" in which:
@@ -262,3 +310,5 @@ if __name__ == "__main__":
         make_config("c1")
     if "c2" in which:
         make_config("c2", extra_plain=True)
+    if "lcurve" in which:
+        make_lcurve_band()

@@ -20,7 +20,8 @@ in for the reference here (VERDICT r01 "next round" item 1):
 
 Stored per config: the records (lambda, residual norms, ||x||) and x_final,
 quantised to int16 with a per-fixture scale (relative-L2 quantisation error
-stored and < 1e-5, i.e. under 1% of the 1e-3 bar).  b is NOT stored (c5:
+stored, < 1e-4, i.e. under 10% of the 1e-3 bar; the tests tighten their bar
+by it).  b is NOT stored (c5:
 21 MB of incompressible noise): the GPU test rebuilds it bit for bit with the
 same oracle forward of the same phantom and the same seeded noise draw.
 """
@@ -49,7 +50,7 @@ def quantise(x):
     scale = float(np.max(np.abs(x))) / 32767.0 or 1.0
     q = np.round(x / scale).astype(np.int16)
     err = np.linalg.norm(q * scale - x) / max(np.linalg.norm(x), 1e-300)
-    assert err < 1e-5, err
+    assert err < 1e-4, err          # <= 10% of the 1e-3 bar; the tests subtract it
     return q, scale, err
 
 
@@ -73,6 +74,7 @@ def make(name, iters, csr):
     res = O.gmres(A, lambda u: O.back(g, u), b, spec.method, spec.strategy, iters)
     print(f"{name}: {spec.method}/{spec.strategy} K={iters} {time.time() - t0:.1f}s "
           f"stop={res.stop_reason}", flush=True)
+    np.save(f"/tmp/{name}_x_oracle.npy", res.x)      # raw, in case the packing below fails
     q, scale, err = quantise(res.x)
     out = {"iters": np.int64(iters), "x_q": q, "x_scale": np.float64(scale),
            "x_quant_err": np.float64(err), "x_norm": np.float64(np.linalg.norm(res.x)),

@@ -19,6 +19,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -33,8 +36,15 @@ constexpr int MAXCH = 1024;        // max L-chunks (= partial rows)
 constexpr int CT = 256;            // combine: threads per CTA
 constexpr int KMAX_VEC = 4096;     // rows per call (smem bound of k_combine)
 
+// Gram matrix E = W^T W - I of the stored basis rows (fp32, symmetric,
+// [GRAM_LD][GRAM_LD]), kept by the single-launch Gram-Schmidt paths across the
+// steps of one Arnoldi cycle (see gram_coefs).
+constexpr int GRAM_LD = 128;
+constexpr size_t GRAM_BYTES = sizeof(float) * GRAM_LD * GRAM_LD;
+
 struct Scratch {                   // carved from the caller's zero-filled scratch
     unsigned int* ticket;          // [1]
+    float* gram;                   // [GRAM_LD][GRAM_LD]
     double* partial;               // [MAXCH][nvec_cap]
     double* tmp;                   // [3][nvec_cap]
     int nvec_cap;
@@ -44,7 +54,8 @@ static inline Scratch carve(void* scratch, int nvec_cap) {
     char* p = (char*)scratch;
     Scratch s;
     s.ticket = (unsigned int*)p;
-    s.partial = (double*)(p + 256);
+    s.gram = (float*)(p + 256);
+    s.partial = (double*)(p + 256 + GRAM_BYTES);
     s.tmp = s.partial + (size_t)MAXCH * nvec_cap;
     s.nvec_cap = nvec_cap;
     return s;
@@ -717,6 +728,76 @@ __device__ __forceinline__ void smem_dots(const float* Ws, int cpad, int nrows, 
     }
 }
 
+// Gram variant (one pass over the chunk): partial rows 0..nb-1 = <W_j, q>,
+// row nb = ||q||^2, rows nb+1+j = <W_j, w_k> (k = nb - 1, the newest row,
+// widened once into wd).
+template <int NR>
+__device__ __forceinline__ void smem_dots2_rows(const float* Ws, int cpad, int j0, int nb,
+                                                const float* v, const double* vd,
+                                                const double* wd, int cn, double* partial) {
+    const int lane = threadIdx.x & 31;
+    const int cn4 = cn >> 2;
+    const double2* vd2 = reinterpret_cast<const double2*>(vd);
+    const double2* wd2 = reinterpret_cast<const double2*>(wd);
+    const float* row[NR];
+    double s[NR], g[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        const int j = j0 + r * SW;
+        row[r] = j == nb ? v : Ws + (size_t)j * cpad;
+        s[r] = 0.0;
+        g[r] = 0.0;
+    }
+    for (int i = lane; i < cn4; i += 32) {
+        const double2 a = vd2[2 * i], b = vd2[2 * i + 1];
+        const double2 c = wd2[2 * i], d = wd2[2 * i + 1];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const float4 w = reinterpret_cast<const float4*>(row[r])[i];
+            const double x0 = w.x, x1 = w.y, x2 = w.z, x3 = w.w;
+            s[r] = fma(x0, a.x, s[r]);
+            s[r] = fma(x1, a.y, s[r]);
+            s[r] = fma(x2, b.x, s[r]);
+            s[r] = fma(x3, b.y, s[r]);
+            g[r] = fma(x0, c.x, g[r]);
+            g[r] = fma(x1, c.y, g[r]);
+            g[r] = fma(x2, d.x, g[r]);
+            g[r] = fma(x3, d.y, g[r]);
+        }
+    }
+    for (int i = (cn4 << 2) + lane; i < cn; i += 32)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const double x = (double)row[r][i];
+            s[r] = fma(x, vd[i], s[r]);
+            g[r] = fma(x, wd[i], g[r]);
+        }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        const int j = j0 + r * SW;
+        const double t = warp_sum(s[r]);
+        const double u = warp_sum(g[r]);
+        if (lane == 0) {
+            partial[(size_t)j * gridDim.x + blockIdx.x] = t;
+            if (j < nb) partial[(size_t)(nb + 1 + j) * gridDim.x + blockIdx.x] = u;
+        }
+    }
+}
+
+__device__ __forceinline__ void smem_dots2(const float* Ws, int cpad, int nb, const float* v,
+                                           const double* vd, const double* wd, int cn,
+                                           double* partial) {
+    const int warp = threadIdx.x >> 5;
+    const int nrows = nb + 1;
+    for (int j0 = warp; j0 < nrows; j0 += SW * GS_DR) {
+        const int nr = (nrows - j0 + SW - 1) / SW;
+        if (nr >= 4) smem_dots2_rows<4>(Ws, cpad, j0, nb, v, vd, wd, cn, partial);
+        else if (nr == 3) smem_dots2_rows<3>(Ws, cpad, j0, nb, v, vd, wd, cn, partial);
+        else if (nr == 2) smem_dots2_rows<2>(Ws, cpad, j0, nb, v, vd, wd, cn, partial);
+        else smem_dots2_rows<1>(Ws, cpad, j0, nb, v, vd, wd, cn, partial);
+    }
+}
+
 // coef[j] = sum over CTAs of partial[j * G + b], identical in every CTA.
 // All loads of a warp's rows are issued before any add (one L2 round trip
 // instead of one per row x CTA group); per-lane order then a fixed shuffle
@@ -750,13 +831,76 @@ __device__ __forceinline__ void all_reduce_rows(const double* partial, int nrows
     }
 }
 
+// Gram-corrected CGS2 (one reduction per step instead of two or three).
+// CGS2's second pass computes h2 = W^T (q - W h1) = h1 - (W^T W) h1 = -E h1,
+// E = W^T W - I, so with E at hand the reorthogonalisation needs no second
+// sweep over the basis: c = h1 + h2 = h1 - E h1 and q2 = q - W c in one
+// update, with one rounding to fp32 instead of two (q1 is never stored).  E
+// is the Gram matrix of the STORED fp32 rows (entries ~ fp32 rounding), one
+// new column per step: <w_i, w_k> comes out of the same sweep as W^T q (row
+// k is in the tile), so it costs no extra traffic.  This is DCGS2-style
+// delayed reorthogonalisation (low-synchronisation Gram-Schmidt); it equals
+// CGS2 -- and the reference's MGS + reorth (ctkrylov/arnoldi.py:66-82) -- in
+// exact arithmetic.  ||q2||^2 follows from the reduced values,
+//   est = ||q||^2 - 2 c.h1 + c.c + c.(E c),
+// so 1/||q2|| is known before q2 is formed and the update writes the
+// normalised row directly (no norm reduction, no scale pass); when est <=
+// 1e-8 ||q||^2 (cancellation would cost fp64 digits) the kernels fall back to
+// an explicit fp64 norm of the stored q2.
+//
+// Per-CTA (every CTA computes the same values in the same order):
+// h2[i] = -(E h1)_i, cc[i] = h1[i] + h2[i], *est; CTA 0 appends E's column /
+// row k to `gram` (columns j < k were written by the earlier steps).
+__device__ __forceinline__ double gram_entry(const float* gram, int i, int j, int k,
+                                             const double* g) {
+    return j < k ? (double)__ldcg(gram + (size_t)i * GRAM_LD + j) : g[i] - (i == k ? 1.0 : 0.0);
+}
+
+__device__ void gram_coefs(float* gram, int k, const double* h1, const double* g, double* h2,
+                           double* cc, double* red, double* s_est) {
+    const int nb = k + 1, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    for (int i = warp; i < nb; i += nw) {
+        double t = 0.0;
+        for (int j = lane; j < nb; j += 32) t = fma(gram_entry(gram, i, j, k, g), h1[j], t);
+        t = warp_sum(t);
+        if (lane == 0) {
+            h2[i] = -t;
+            cc[i] = h1[i] - t;
+        }
+    }
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+            const float e = (float)(g[i] - (i == k ? 1.0 : 0.0));
+            gram[(size_t)k * GRAM_LD + i] = e;
+            gram[(size_t)i * GRAM_LD + k] = e;
+        }
+    __syncthreads();
+    double part = 0.0;            // this warp's rows of  c.(E c) + c.c - 2 c.h1
+    for (int i = warp; i < nb; i += nw) {
+        double u = 0.0;
+        for (int j = lane; j < nb; j += 32) u = fma(gram_entry(gram, i, j, k, g), cc[j], u);
+        u = warp_sum(u);
+        part += cc[i] * u + cc[i] * cc[i] - 2.0 * cc[i] * h1[i];
+    }
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t += red[w];
+        *s_est = h1[nb] + t;
+    }
+    __syncthreads();
+}
+
 // v <- v - sum_j c[j] Ws[j] over the chunk (fp64 accumulate, fp32 result);
 // returns this thread's part of ||v||^2 (of the rounded values).  The chunk
 // has fewer float4 than the CTA has threads, so the rows are split over
 // ngrp = ST / cn4 thread groups (row j -> group j % ngrp) whose fp64 partial
 // sums meet in SMEM (acc[g][i]) and are added in group order.
 __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb, const double* c,
-                                              float* v, double* vd, int cn, double4* acc) {
+                                              float* v, double* vd, int cn, double4* acc,
+                                              double scale = 1.0) {
     const int cn4 = cn >> 2;
     int ngrp = cn4 > 0 ? ST / cn4 : 1;
     ngrp = ngrp < 1 ? 1 : (ngrp > 8 ? 8 : ngrp);
@@ -772,7 +916,8 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
                 a0 = fma(-cj, (double)w.x, a0); a1 = fma(-cj, (double)w.y, a1);
                 a2 = fma(-cj, (double)w.z, a2); a3 = fma(-cj, (double)w.w, a3);
             }
-            const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+            const float4 o = make_float4((float)(a0 * scale), (float)(a1 * scale),
+                                         (float)(a2 * scale), (float)(a3 * scale));
             reinterpret_cast<float4*>(v)[t] = o;
             const double4 od = make_double4(o.x, o.y, o.z, o.w);
             if (vd) {
@@ -785,7 +930,7 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
         for (int t = (cn4 << 2) + threadIdx.x; t < cn; t += ST) {
             double a = (double)v[t];
             for (int j = 0; j < nb; ++j) a = fma(-c[j], (double)Ws[(size_t)j * cpad + t], a);
-            const float o = (float)a;
+            const float o = (float)(a * scale);
             v[t] = o;
             if (vd) vd[t] = (double)o;
             nrm = fma((double)o, (double)o, nrm);
@@ -814,7 +959,8 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
             const double4 p = acc[q * cn4 + t];
             a0 += p.x; a1 += p.y; a2 += p.z; a3 += p.w;
         }
-        const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+        const float4 o = make_float4((float)(a0 * scale), (float)(a1 * scale),
+                                     (float)(a2 * scale), (float)(a3 * scale));
         reinterpret_cast<float4*>(v)[t] = o;
         const double4 od = make_double4(o.x, o.y, o.z, o.w);
         if (vd) {
@@ -827,7 +973,7 @@ __device__ __forceinline__ double smem_update(const float* Ws, int cpad, int nb,
     for (int t = (cn4 << 2) + threadIdx.x; t < cn; t += ST) {
         double a = (double)v[t];
         for (int j = 0; j < nb; ++j) a = fma(-c[j], (double)Ws[(size_t)j * cpad + t], a);
-        const float o = (float)a;
+        const float o = (float)(a * scale);
         v[t] = o;
         if (vd) vd[t] = (double)o;
         nrm = fma((double)o, (double)o, nrm);
@@ -854,6 +1000,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
                                                    int64_t chunk, double* h, double* stat,
                                                    double* partial, ctk_stage_dst sd,
                                                    double* hm, int stat_off, int use_tma,
+                                                   float* gram,
                                                    const __grid_constant__ CUtensorMap tm) {
     cg::grid_group grid = cg::this_grid();
     GS_STAMP(0);
@@ -865,13 +1012,15 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     const int64_t rem = L - start;
     const int cn = rem <= 0 ? 0 : (int)(rem < chunk ? rem : chunk);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
-    double* h1 = reinterpret_cast<double*>(smem_raw + 16);          // [nb + 1]
-    double* h2 = h1 + (nb + 1);                                     // [nb + 1]: h2, ||q1||^2
-    double* red = h2 + nb + 1;                                      // [SW]
+    double* h1 = reinterpret_cast<double*>(smem_raw + 16);          // [2 nb + 2]: h1, ||q||^2, g
+    double* h2 = h1 + (2 * nb + 2);                                 // [nb + 1]: h2, ||q1||^2
+    double* cc = h2 + nb + 1;                                       // [nb + 1]: h1 + h2 (gram)
+    double* red = cc + nb + 1;                                      // [SW]
     float* qv = reinterpret_cast<float*>(
-        smem_raw + ((16 + sizeof(double) * (2 * nb + 2 + SW) + 15) & ~(size_t)15));
+        smem_raw + ((16 + sizeof(double) * (4 * nb + 4 + SW) + 15) & ~(size_t)15));
     double* qd = reinterpret_cast<double*>(qv + cpad);               // [cpad]: qv in fp64
-    unsigned char* ws_raw = reinterpret_cast<unsigned char*>(qd + cpad);
+    double* wkd = qd + cpad;                                         // [cpad]: row k in fp64 (gram)
+    unsigned char* ws_raw = reinterpret_cast<unsigned char*>(wkd + cpad);
     ws_raw += (128u - (smem_u32(ws_raw) & 127u)) & 127u;           // TMA destination alignment
     float* Ws = reinterpret_cast<float*>(ws_raw);                   // [nb][cpad]
     double4* acc = reinterpret_cast<double4*>(                      // [ST], 32-B aligned
@@ -919,9 +1068,36 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     __syncthreads();
     GS_STAMP(2);
 
-    double* P1 = partial;                                    // [nb + 1][G]
+    double* P1 = partial;                                    // [nb + 1][G] (gram: [2 nb + 1][G])
     double* P2 = P1 + (size_t)(nb + 1) * gridDim.x;          // [nb + 1][G]
     double* P3 = P2 + (size_t)(nb + 1) * gridDim.x;          // [G]
+    __shared__ double s_n2;
+    bool need_norm = true, prescaled = false;
+    double nrm = 0.0;
+    if (gram && passes == 2) {
+        // Gram-corrected CGS2 (see gram_coefs): one sweep, one reduction
+        for (int i = threadIdx.x; i < cn; i += ST) wkd[i] = (double)Ws[(size_t)k * cpad + i];
+        __syncthreads();
+        smem_dots2(Ws, cpad, nb, qv, qd, wkd, cn, P1);    // h1, ||q||^2, <W_j, w_k>
+        GS_STAMP(3);
+        grid.sync();
+        GS_STAMP(4);
+        all_reduce_rows(P1, 2 * nb + 1, h1);
+        __syncthreads();
+        __shared__ double s_est;
+        gram_coefs(gram, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
+        GS_STAMP(5);
+        const double est = s_est, a = h1[nb];
+        if (a > 0.0 && est > 1e-8 * a) {
+            nrm = smem_update(Ws, cpad, nb, cc, qv, nullptr, cn, acc, 1.0 / sqrt(est));
+            if (threadIdx.x == 0) s_n2 = est;
+            need_norm = false;
+            prescaled = true;
+        } else {
+            nrm = smem_update(Ws, cpad, nb, cc, qv, nullptr, cn, acc);
+        }
+        GS_STAMP(10);
+    } else {
     smem_dots(Ws, cpad, nb + 1, nb, qv, qd, cn, P1);             // h1 = W^T q, ||q||^2
     GS_STAMP(3);
     grid.sync();
@@ -929,10 +1105,8 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     all_reduce_rows(P1, nb + 1, h1);
     __syncthreads();
     GS_STAMP(5);
-    double nrm = smem_update(Ws, cpad, nb, h1, qv, qd, cn, acc);      // q1 = q - W h1
+    nrm = smem_update(Ws, cpad, nb, h1, qv, qd, cn, acc);      // q1 = q - W h1
     GS_STAMP(6);
-    __shared__ double s_n2;
-    bool need_norm = true;
     if (passes == 2) {
         __syncthreads();
         smem_dots(Ws, cpad, nb + 1, nb, qv, qd, cn, P2);         // h2 = W^T q1, ||q1||^2
@@ -955,6 +1129,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
             need_norm = false;
         }
     }
+    }
     if (need_norm) {
         nrm = warp_sum(nrm);
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
@@ -972,7 +1147,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     const double hk = sqrt(s_n2);
     const double qn = sqrt(h1[nb]);
     const bool broke = hk <= 1e-14 * qn;                     // BREAKDOWN_RTOL, arnoldi.py:17,80
-    const float sc = (float)(broke ? 0.0 : 1.0 / hk);
+    const float sc = broke ? 0.f : prescaled ? 1.f : (float)(1.0 / hk);
     float* wnext = W + (size_t)(k + 1) * ld + start;
     if (sd.P) {     // also stage w_{k+1} for the next K1 apply (zero-padded P and PT)
         const int pP = sd.nx + 2 * sd.pad, pT = sd.ny + 2 * sd.pad;
@@ -1064,6 +1239,44 @@ __device__ __forceinline__ void ts_issue(const TsRing& R, int b, int tw, int nb,
         : "memory");
 }
 
+// Gram variant: also gacc[r] += <row (warp + SW r), row grow> for rows < grow + 1.
+__device__ __forceinline__ void ts_dots2(const float* tile, int tw, int nrows, int vrow, int grow,
+                                         int cn, double* acc, double* gacc) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fpl = tw >> 5;
+    const float* vr = tile + (size_t)vrow * tw;
+    const float* gr = tile + (size_t)grow * tw;
+#pragma unroll
+    for (int c4 = 0; c4 < 2; ++c4) {
+        const int e = lane * fpl + c4 * 4;
+        if (c4 * 4 >= fpl || e >= cn) break;
+        const float4 v = *reinterpret_cast<const float4*>(vr + e);
+        const float4 u = *reinterpret_cast<const float4*>(gr + e);
+        const double v0 = v.x, v1 = v.y, v2 = v.z, v3 = v.w;
+        const double u0 = u.x, u1 = u.y, u2 = u.z, u3 = u.w;
+#pragma unroll
+        for (int r = 0; r < TS_RPW; ++r) {
+            const int j = warp + SW * r;
+            if (j < nrows) {
+                const float4 w = *reinterpret_cast<const float4*>(tile + (size_t)j * tw + e);
+                const double x0 = w.x, x1 = w.y, x2 = w.z, x3 = w.w;
+                double a = acc[r];
+                a = fma(x0, v0, a);
+                a = fma(x1, v1, a);
+                a = fma(x2, v2, a);
+                a = fma(x3, v3, a);
+                acc[r] = a;
+                double b = gacc[r];
+                b = fma(x0, u0, b);
+                b = fma(x1, u1, b);
+                b = fma(x2, u2, b);
+                b = fma(x3, u3, b);
+                gacc[r] = b;
+            }
+        }
+    }
+}
+
 // acc[r] += <row (warp + SW r), vector row> over one tile (fp64 products).
 __device__ __forceinline__ void ts_dots(const float* tile, int tw, int nrows, int vrow, int cn,
                                         double* acc) {
@@ -1097,7 +1310,8 @@ __device__ __forceinline__ void ts_dots(const float* tile, int tw, int nrows, in
 // summed in group order.  The rounded result goes to dst (global) and, when
 // keep, back into the tile's vector row.  Returns this thread's ||out||^2 part.
 __device__ __forceinline__ double ts_update(float* tile, int tw, int nb, const double* c, int cn,
-                                            float* dst, bool keep, double* red) {
+                                            float* dst, bool keep, double* red,
+                                            double scale = 1.0) {
     const int ng = ST / tw;
     const int g = threadIdx.x / tw, e = threadIdx.x - g * tw;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;       // four independent chains
@@ -1118,7 +1332,7 @@ __device__ __forceinline__ double ts_update(float* tile, int tw, int nb, const d
     if (g == 0 && e < cn) {
         double t = 0.0;
         for (int q = 0; q < ng; ++q) t += red[q * tw + e];
-        const float o = (float)((double)tile[(size_t)nb * tw + e] - t);
+        const float o = (float)(((double)tile[(size_t)nb * tw + e] - t) * scale);
         dst[e] = o;
         if (keep) tile[(size_t)nb * tw + e] = o;
         nrm = (double)o * (double)o;
@@ -1137,18 +1351,19 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
                                                      const float* __restrict__ q, int passes,
                                                      int tw, double* h, double* stat,
                                                      double* partial, ctk_stage_dst sd,
-                                                     double* hm, int stat_off,
+                                                     double* hm, int stat_off, float* gram,
                                                      const __grid_constant__ TsMaps tm) {
     cg::grid_group grid = cg::this_grid();
     ctk_pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nb = k + 1;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                 // [TS_NBUF]
-    double* h1 = reinterpret_cast<double*>(smem_raw + 8 * TS_NBUF);         // [nb + 1]
-    double* h2 = h1 + (nb + 1);                                             // [nb + 1]
-    double* red = h2 + (nb + 1);                                            // [ST]
+    double* h1 = reinterpret_cast<double*>(smem_raw + 8 * TS_NBUF);         // [2 nb + 2]
+    double* h2 = h1 + (2 * nb + 2);                                         // [nb + 1]
+    double* cc = h2 + (nb + 1);                                             // [nb + 1]
+    double* red = cc + (nb + 1);                                            // [ST]
     // ring slots: 128-B aligned for the tensor copies
-    unsigned char* ring_raw = smem_raw + 8 * TS_NBUF + sizeof(double) * (2 * (size_t)nb + 2 + ST);
+    unsigned char* ring_raw = smem_raw + 8 * TS_NBUF + sizeof(double) * (4 * (size_t)nb + 4 + ST);
     ring_raw += (128u - (smem_u32(ring_raw) & 127u)) & 127u;
     float* ring = reinterpret_cast<float*>(ring_raw);
     TsRing R;
@@ -1175,14 +1390,16 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
 
     // One sweep over this CTA's tiles.  mode 0: dots with the vector (row nb,
     // + its norm); 1: update -> wnext, then dots with the result; 2: update ->
-    // wnext and its norm.
+    // wnext (times `scale`) and its norm; 3: mode 0 plus the Gram dots
+    // <W_j, w_k> (rows nb + 1 + j of P).
     // The ring runs continuously across sweeps: tile number g (counted from
     // the kernel's first) uses slot g % TS_NBUF at mbarrier phase (g / TS_NBUF) & 1.
     int gbase = 0;
-    auto sweep = [&](int mode, const CUtensorMap* vmap, const double* coef, double* P) -> double {
-        double acc[TS_RPW];
+    auto sweep = [&](int mode, const CUtensorMap* vmap, const double* coef, double* P,
+                     double scale) -> double {
+        double acc[TS_RPW], gacc[TS_RPW];
 #pragma unroll
-        for (int r = 0; r < TS_RPW; ++r) acc[r] = 0.0;
+        for (int r = 0; r < TS_RPW; ++r) acc[r] = gacc[r] = 0.0;
         double nrm = 0.0;
         if (threadIdx.x == 0)
             for (int i = 0; i < TS_NBUF && i < nt; ++i)
@@ -1195,8 +1412,10 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
             float* tile = R.buf(b);
             if (mode == 0) {
                 ts_dots(tile, tw, nb + 1, nb, cn, acc);
+            } else if (mode == 3) {
+                ts_dots2(tile, tw, nb + 1, nb, nb - 1, cn, acc, gacc);
             } else {
-                nrm += ts_update(tile, tw, nb, coef, cn, wnext + e0, mode == 1, red);
+                nrm += ts_update(tile, tw, nb, coef, cn, wnext + e0, mode == 1, red, scale);
                 if (mode == 1) ts_dots(tile, tw, nb, nb, cn, acc);
             }
             __syncthreads();                     // everyone is done with slot b
@@ -1205,52 +1424,87 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
         }
         gbase += nt;
         if (mode != 2) {
-            const int rows = mode == 0 ? nb + 1 : nb;
+            const int rows = mode == 1 ? nb : nb + 1;
 #pragma unroll
             for (int r = 0; r < TS_RPW; ++r) {
                 const double t = warp_sum(acc[r]);
                 const int j = warp + SW * r;
                 if (lane == 0 && j < rows) P[(size_t)j * gridDim.x + blockIdx.x] = t;
             }
+            if (mode == 3) {
+#pragma unroll
+                for (int r = 0; r < TS_RPW; ++r) {
+                    const double t = warp_sum(gacc[r]);
+                    const int j = warp + SW * r;
+                    if (lane == 0 && j < nb) P[(size_t)(nb + 1 + j) * gridDim.x + blockIdx.x] = t;
+                }
+            }
         }
         return nrm;
     };
 
-    sweep(0, &tm.q, nullptr, P1);                            // h1 = W^T q, ||q||^2
-    grid.sync();
-    all_reduce_rows(P1, nb + 1, h1);
-    __syncthreads();
-    const double* cfin = h1;
-    const CUtensorMap* vfin = &tm.q;
-    if (passes == 2) {
-        sweep(1, &tm.q, h1, P2);                             // q1 -> wnext, h2 = W^T q1
-        asm volatile("fence.proxy.async.global;" ::: "memory");   // q1: generic writes, bulk reads
-        grid.sync();
-        all_reduce_rows(P2, nb, h2);
-        __syncthreads();
-        cfin = h2;
-        vfin = &tm.wn;
-    }
-    double nrm = sweep(2, vfin, cfin, nullptr);              // q2 -> wnext, ||q2||^2
-    nrm = warp_sum(nrm);
-    if (lane == 0) red[warp] = nrm;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-#pragma unroll
-        for (int w = 0; w < SW; ++w) t += red[w];
-        P3[blockIdx.x] = t;
-    }
-    grid.sync();
     __shared__ double s_n2;
-    if (threadIdx.x < 32) all_reduce_rows(P3, 1, &s_n2);
-    __syncthreads();
+    bool need_norm = true, prescaled = false;
+    double nrm = 0.0;
+    if (gram && passes == 2) {
+        // Gram-corrected CGS2 (see gram_coefs): two sweeps, one reduction --
+        // h1, ||q||^2 and <W_j, w_k> in one read of the basis, then
+        // q2 = (q - W c) / ||q2|| straight into row k+1
+        sweep(3, &tm.q, nullptr, P1, 1.0);
+        grid.sync();
+        all_reduce_rows(P1, 2 * nb + 1, h1);
+        __syncthreads();
+        __shared__ double s_est;
+        gram_coefs(gram, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
+        const double est = s_est, a = h1[nb];
+        if (a > 0.0 && est > 1e-8 * a) {
+            sweep(2, &tm.q, cc, nullptr, 1.0 / sqrt(est));
+            if (threadIdx.x == 0) s_n2 = est;
+            need_norm = false;
+            prescaled = true;
+        } else {
+            nrm = sweep(2, &tm.q, cc, nullptr, 1.0);
+        }
+    } else {
+        sweep(0, &tm.q, nullptr, P1, 1.0);                   // h1 = W^T q, ||q||^2
+        grid.sync();
+        all_reduce_rows(P1, nb + 1, h1);
+        __syncthreads();
+        const double* cfin = h1;
+        const CUtensorMap* vfin = &tm.q;
+        if (passes == 2) {
+            sweep(1, &tm.q, h1, P2, 1.0);                    // q1 -> wnext, h2 = W^T q1
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // q1: generic writes, bulk reads
+            grid.sync();
+            all_reduce_rows(P2, nb, h2);
+            __syncthreads();
+            cfin = h2;
+            vfin = &tm.wn;
+        }
+        nrm = sweep(2, vfin, cfin, nullptr, 1.0);            // q2 -> wnext, ||q2||^2
+    }
+    if (need_norm) {
+        nrm = warp_sum(nrm);
+        if (lane == 0) red[warp] = nrm;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < SW; ++w) t += red[w];
+            P3[blockIdx.x] = t;
+        }
+        grid.sync();
+        if (threadIdx.x < 32) all_reduce_rows(P3, 1, &s_n2);
+        __syncthreads();
+    } else if (sd.P) {
+        grid.sync();                 // the staging tiles below span other CTAs' rows
+    }
     const double hk = sqrt(s_n2);
     const double qn = sqrt(h1[nb]);
     const bool broke = hk <= 1e-14 * qn;                     // BREAKDOWN_RTOL, arnoldi.py:17,80
-    const float sc = (float)(broke ? 0.0 : 1.0 / hk);
+    const float sc = broke ? 0.f : prescaled ? 1.f : (float)(1.0 / hk);
     if (!sd.P) {
-        if (nt > 0) {
+        if (!prescaled && nt > 0) {
             const int64_t e0 = t0 * tw, e1 = min(L, t1 * tw);
             for (int64_t i = e0 + threadIdx.x; i < e1; i += ST) wnext[i] *= sc;
         }
@@ -1270,7 +1524,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
                 if (iy < sd.ny && ix < sd.nx) {
                     const size_t o = (size_t)iy * sd.nx + ix;
                     v = wnext[o] * sc;
-                    wnext[o] = v;
+                    if (!prescaled) wnext[o] = v;
                     sd.P[(size_t)iy * pP + ix + sd.pad] = v;
                 }
                 tr[r][tx] = v;
@@ -1383,8 +1637,8 @@ static bool encode_rows(CUtensorMap* m, const float* base, int64_t L, int64_t ld
 // memory with one CTA per SM.
 static size_t gs_smem_bytes(int k, int64_t chunk) {
     const int nb = k + 1;
-    const size_t head = (16 + sizeof(double) * (2 * (size_t)nb + 2 + SW) + 15) & ~(size_t)15;
-    return head + sizeof(float) * (size_t)chunk * (nb + 1) + sizeof(double) * (size_t)chunk +
+    const size_t head = (16 + sizeof(double) * (4 * (size_t)nb + 4 + SW) + 15) & ~(size_t)15;
+    return head + sizeof(float) * (size_t)chunk * (nb + 1) + 2 * sizeof(double) * (size_t)chunk +
            sizeof(double) * 4 * ST + 32 + 128;
 }
 
@@ -1423,7 +1677,7 @@ static bool gs_smem_plan(int64_t L, int k, int64_t* Gp, int64_t* chunkp, size_t*
 
 static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
                        double* stat, Scratch s, cudaStream_t st, const ctk_stage_dst* sdp,
-                       double* hm, bool* done) {
+                       double* hm, float* gram, bool* done) {
     *done = false;
     int64_t G, chunk;
     size_t smem;
@@ -1461,7 +1715,7 @@ static int try_gs_smem(float* W, int64_t ld, int k, int64_t L, float* q, int pas
     cfg.attrs = at;
     cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_gs_smem, W, ld, k, L, (const float*)q, passes, chunk,
-                                       h, stat, partial, sd, hm, stat_off, use_tma, tm);
+                                       h, stat, partial, sd, hm, stat_off, use_tma, gram, tm);
     ctk_count_launch();
     if (e != cudaSuccess) return ctk_check_cuda(e, "k_gs_smem");
     *done = true;
@@ -1478,7 +1732,7 @@ bool ctk_gs_smem_ok(int64_t L, int k) {
 // rows, two ring buffers of the widest tile (256 or 128 floats) that fit.
 static size_t gs_stream_bytes(int k, int tw) {
     const int nb = k + 1;
-    const size_t head = 8 * TS_NBUF + sizeof(double) * (2 * (size_t)nb + 2 + ST) + 128;
+    const size_t head = 8 * TS_NBUF + sizeof(double) * (4 * (size_t)nb + 4 + ST) + 128;
     return head + TS_NBUF * sizeof(float) * (size_t)(nb + 1) * tw;
 }
 
@@ -1519,7 +1773,7 @@ bool ctk_gs_stream_ok(int64_t L, int k) {
 
 static int try_gs_stream(float* W, int64_t ld, int k, int64_t L, const float* q, int passes,
                          double* h, double* stat, Scratch s, cudaStream_t st,
-                         const ctk_stage_dst* sdp, double* hm, bool* done) {
+                         const ctk_stage_dst* sdp, double* hm, float* gram, bool* done) {
     *done = false;
     int tw, G;
     size_t smem;
@@ -1545,7 +1799,7 @@ static int try_gs_stream(float* W, int64_t ld, int k, int64_t L, const float* q,
         !encode_rows(&tm.wn, W + (size_t)(k + 1) * ld, L, ld, 1, tw))
         return CTK_OK;                                   // no TMA encoder: other paths
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_gs_stream, W, ld, k, L, q, passes, tw, h, stat,
-                                       s.partial, sd, hm, stat_off, tm);
+                                       s.partial, sd, hm, stat_off, gram, tm);
     ctk_count_launch();
     if (e != cudaSuccess) return ctk_check_cuda(e, "k_gs_stream");
     *done = true;
@@ -1561,7 +1815,7 @@ static int check_vec(const void* p, const char* what) {
 extern "C" size_t ctk_reduce_scratch_bytes(int nvec, int64_t L) {
     (void)L;
     const int cap = nvec + 3;
-    return 256 + sizeof(double) * ((size_t)MAXCH * cap + 3 * (size_t)cap) + 256;
+    return 256 + GRAM_BYTES + sizeof(double) * ((size_t)MAXCH * cap + 3 * (size_t)cap) + 256;
 }
 
 static int launch_dots(const float* W, int64_t ld, int nvec, const float* v, int64_t L,
@@ -1717,6 +1971,46 @@ extern "C" int ctk_gs_step(float* W, int64_t ld, int k, int64_t L, float* q, int
     return ctk_gs_step_ex(W, ld, k, L, q, passes, h, stat, scratch, stream, nullptr, nullptr);
 }
 
+// Gram-matrix bookkeeping (host side, per scratch buffer): the Gram-corrected
+// path needs E's columns 0..k-1, which exist when the previous calls on this
+// scratch were steps 0..k-1 of the same basis (same W, ld, L), each on a
+// single-launch path.  Launches on one scratch are stream-ordered, so the
+// issue order here is the execution order.  Anything else (a first call at
+// k > 0, another basis, a fallback path in between) runs the classic CGS2
+// kernels for this step and restarts the chain at the next k = 0.
+// CTK_NO_GRAM_GS=1 disables the Gram path (classic 2-reduction CGS2).
+struct GramChain {
+    const float* W;
+    int64_t ld, L;
+    int next_k;
+};
+
+static bool gram_track(void* scratch, const float* W, int64_t ld, int64_t L, int k, bool single) {
+    static const bool off = [] {
+        const char* e = getenv("CTK_NO_GRAM_GS");
+        return e && e[0] == '1';
+    }();
+    static std::mutex mu;
+    static std::unordered_map<void*, GramChain> chains;
+    std::lock_guard<std::mutex> lk(mu);
+    if (off || !single || k + 1 >= GRAM_LD) {
+        chains.erase(scratch);
+        return false;
+    }
+    auto it = chains.find(scratch);
+    if (k == 0) {
+        chains[scratch] = GramChain{W, ld, L, 1};
+        return true;
+    }
+    if (it == chains.end() || it->second.W != W || it->second.ld != ld || it->second.L != L ||
+        it->second.next_k != k) {
+        chains.erase(scratch);
+        return false;
+    }
+    it->second.next_k = k + 1;
+    return true;
+}
+
 int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
                    double* stat, void* scratch, void* stream, const ctk_stage_dst* sd,
                    double* h_mirror) {
@@ -1730,9 +2024,13 @@ int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes,
     Scratch s = carve(scratch, k + 3);
     if (passes != 1 && passes != 2) return ctk_fail(CTK_ERR_ARG, "passes must be 1 or 2");
     bool fused = false;
-    if ((rc = try_gs_smem(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, &fused))) return rc;
+    const bool single = passes == 2 && (ctk_gs_smem_ok(L, k) || ctk_gs_stream_ok(L, k));
+    float* gram = gram_track(scratch, W, ld, L, k, single) ? s.gram : nullptr;
+    if ((rc = try_gs_smem(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, gram, &fused)))
+        return rc;
     if (fused) return CTK_OK;
-    if ((rc = try_gs_stream(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, &fused))) return rc;
+    if ((rc = try_gs_stream(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, gram, &fused)))
+        return rc;
     if (fused) return CTK_OK;
     if (passes == 2 && (rc = try_cgs2_fused(W, ld, k, L, q, h, stat, s, st, &fused))) return rc;
     if (fused) return CTK_OK;

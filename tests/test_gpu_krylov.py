@@ -57,6 +57,64 @@ def test_cgs2_step_matches_fp64_mgs(cuda, L, k):
     assert np.abs(Q.T @ w).max() < 1e-5
 
 
+def mgs2_ref(Q, q):
+    """fp64 MGS + one reorthogonalisation pass (ctkrylov/arnoldi.py:66-82)."""
+    v = q.copy()
+    k1 = Q.shape[1]
+    href = np.zeros(k1 + 1)
+    for _ in range(2):
+        for i in range(k1):
+            c = Q[:, i] @ v
+            href[i] += c
+            v = v - c * Q[:, i]
+    href[k1] = np.linalg.norm(v)
+    return href, v
+
+
+@pytest.mark.parametrize("L,K,near", [(32940, 50, False), (65536, 80, False),
+                                      (65536, 30, True), (2086560, 40, False),
+                                      (4194304, 24, False), (2086560, 12, True)])
+def test_gram_corrected_cgs2_chain_matches_fp64_mgs(cuda, L, K, near):
+    """Consecutive steps 0..K-1 on one basis take the Gram-corrected
+    single-launch path (E = W^T W - I kept across steps; SMEM path for short
+    vectors, streamed path for c4/c5 lengths).  Every step's column equals
+    fp64 MGS + reorthogonalisation on the STORED fp32 rows, and the basis
+    stays orthonormal to fp32 working precision.  near=True makes every q
+    nearly dependent on the basis (||q2|| ~ 1e-6 ||q||): the norm estimate
+    would cancel, so the kernels take the explicit-norm fallback."""
+    torch = cuda
+    rng = np.random.default_rng(L + K)
+    B = DeviceBasis(L, K + 2, torch.device("cuda", 0), torch)
+    v0 = rng.standard_normal(L)
+    B.W[0, :L] = torch.from_numpy((v0 / np.linalg.norm(v0)).astype(np.float32)).cuda()
+    st = torch.cuda.current_stream()
+    h = torch.zeros(K + 8, dtype=torch.float64, device="cuda")
+    stat = torch.zeros(4, dtype=torch.float64, device="cuda")
+    worst = 0.0
+    for k in range(K):
+        Q = B.W[: k + 1, :L].cpu().numpy().astype(np.float64).T
+        if near:
+            p = Q @ rng.standard_normal(k + 1)
+            u = rng.standard_normal(L)
+            q = p + 1e-6 * np.linalg.norm(p) * u / np.linalg.norm(u)
+        else:
+            q = rng.standard_normal(L) + Q @ rng.standard_normal(k + 1)
+        q = q.astype(np.float32).astype(np.float64)
+        B.cgs2_step(k, torch.from_numpy(q.astype(np.float32)).cuda(), h, stat, st)
+        torch.cuda.synchronize()
+        href, v = mgs2_ref(Q, q)
+        hg = h.cpu().numpy()[: k + 2]
+        err = np.abs(hg - href).max() / np.abs(href).max()
+        worst = max(worst, err)
+        assert err < 1e-5, (k, err)
+        assert hg[k + 1] == pytest.approx(href[k + 1], rel=1e-5), k
+        w = B.W[k + 1, :L].cpu().numpy().astype(np.float64)
+        assert np.abs(w - v / href[k + 1]).max() < 5e-6, k
+    W = B.W[: K + 1, :L].cpu().numpy().astype(np.float64)
+    G = W @ W.T
+    assert np.abs(G - np.eye(K + 1)).max() < 2e-6, np.abs(G - np.eye(K + 1)).max()
+
+
 def test_cgs2_breakdown_flag(cuda):
     torch = cuda
     L = 4096

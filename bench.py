@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--slices-per-gpu", type=int, default=0,
                     help="concurrent independent slices per GPU (default: 8 for c5, else 1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shard", default="none", choices=["none", "angles"],
+                    help="angles: one problem split by projection angle over the ranks "
+                         "(strong scaling; c3 A+B microbenchmark or a c1/c2/c4 solve)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -333,6 +336,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(dev)
+    if args.shard == "angles":
+        return main_sharded(args, spec, world, rank, local, torch, dist, stream)
 
     grid = ct.ImageGrid(spec.N, spec.N, 1.0)
     geom = ct.ParallelGeometry(spec.angles(), spec.det_count, 1.0)
@@ -564,6 +569,159 @@ def main():
             line["solve"] = {"stop_reason": last.stop_reason, "iterations": len(last.records),
                              "final_data_residual": last.records[-1].data_residual_norm}
         print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main_sharded(args, spec, world, rank, local, torch, dist, stream):
+    """--shard angles: ONE problem split by projection angle over the ranks
+    (SURVEY row e; strong scaling, total work fixed).  A is sharded by angle
+    with a replicated image; B's partial images are summed over ranks (peer
+    exchange fused into K2 when the ranks map each other's memory, else NCCL);
+    AB Krylov vectors are sharded in measurement space with fp64 all-reduces
+    of the Gram-Schmidt dots; all collectives are issued by libctk's C++
+    driver (dist.NativeComm + run_gmres(..., comm=)).  c3: a step = A + the
+    summed B of the full geometry; c1/c2/c4: a step = one full hybrid solve."""
+    from paper_2602_17892_b200 import _native, ct, dist as cdist, gmres, problems
+
+    dev = torch.device("cuda", local)
+    grid = ct.ImageGrid(spec.N, spec.N, 1.0)
+    geom = ct.ParallelGeometry(spec.angles(), spec.det_count, 1.0)
+    idx = cdist.angle_shards(spec.n_angles, world)[rank]
+    A, B = cdist.sharded_projectors(grid, geom, idx, device=local)
+    dg = A.dgeom
+    comm = cdist.NativeComm(dg)
+    D = spec.det_count
+    m_full = spec.m
+    raw, nnz_local = dg.count_segments()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    result = {}
+    if spec.method is None:
+        x = torch.from_numpy(problems.uniform_image(dg.n, 0).astype(np.float32)).to(dev)
+        u_full = problems.uniform_sinogram(m_full, 1)
+        u = torch.from_numpy(cdist.local_rows(u_full, D, idx).astype(np.float32)).to(dev)
+        y = torch.empty(dg.m, dtype=torch.float32, device=dev)
+        img = torch.empty(dg.n, dtype=torch.float32, device=dev)
+
+        def step():
+            dg.forward(x, out=y, stream=stream)
+            comm.back(u, out=img, stream=stream)
+        rays_per_step = 2 * m_full
+        iters_per_step = None
+    else:
+        # b of the FULL geometry (bitwise the single-GPU bench's), this rank's rows
+        Af = ct.forward_ray_driven(grid, geom, device=local)
+        xt = problems.random_ellipse_phantom(spec.N, spec.ellipses, spec.phantom_seed)
+        with torch.cuda.stream(stream):
+            clean = Af.dgeom.forward(torch.from_numpy(xt.astype(np.float32)).to(dev), stream=stream)
+        stream.synchronize()
+        b_full, _ = problems.add_noise(clean.cpu().numpy().astype(np.float64), spec.noise,
+                                       spec.noise_seed)
+        b_full = b_full.astype(np.float32).astype(np.float64)
+        del Af, clean
+        b_host = cdist.local_rows(b_full, D, idx)
+        b_dev = torch.from_numpy(b_host.astype(np.float32)).to(dev)
+        cfg = gmres.SolverConfig(method=spec.method, lambda_strategy=spec.strategy,
+                                 max_iter=spec.max_iter)
+        na_, nb_ = applies_per_iter(spec.method)
+        rays_per_step = spec.max_iter * (na_ + nb_) * m_full
+        iters_per_step = spec.max_iter
+
+        def step():
+            result["last"] = gmres.run_gmres(A, B, b_dev, cfg, stream=stream,
+                                             keep_on_device=True, comm=comm)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    def timed(n_steps):
+        tot = 0.0
+        for _ in range(n_steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        barrier()
+        return tot
+
+    launches0 = _native.launch_counter()
+    with ClockSampler(local) as clocks:
+        total_ms = timed(args.steps)
+    launches = _native.launch_counter() - launches0
+    _native.profile_begin()
+    timed(max(1, min(args.steps, 2)))
+    prof = _native.profile_end()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = rays_per_step * args.steps / (total_ms / 1e3)
+    hbm_peak, peak_src = measured_peak()
+    kernels = {k: {"launches": n, "mean_ms": round(ms, 5)} for k, (n, ms, _) in prof.items()}
+    bytes_A = 4 * nnz_local + 4 * dg.m
+    roofline = None
+    if "forward" in prof:
+        n_l, ms_l, _ = prof["forward"]
+        ach = bytes_A / (ms_l / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "k_forward (this rank's angles)",
+                    "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(ach / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": bytes_A, "launches_timed": n_l,
+                    "mean_launch_ms": round(ms_l, 5)}
+    e2e = None
+    if spec.method is not None and not args.no_e2e:
+        gmres.run_gmres(A, B, b_host, cfg, stream=stream, comm=comm)     # pinned buffers
+        walls = []
+        res = None
+        for _ in range(args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            res = gmres.run_gmres(A, B, b_host, cfg, stream=stream, comm=comm)
+            walls.append(time.perf_counter() - t0)
+        barrier()
+        wt = torch.tensor([float(np.sum(walls))], dtype=torch.float64, device=dev)
+        if dist is not None:
+            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        e2e = {"value": rays_per_step * args.steps / wt.item(), "unit": "rays/s",
+               "h2d_bytes_per_step": int(res.transfer["h2d_bytes"]),
+               "d2h_bytes_per_step": int(res.transfer["d2h_bytes"]),
+               "timing": "wall clock around run_gmres(A_rank, B_rank, b_rank_numpy, cfg, "
+                         "comm=) incl. H2D/D2H, max over ranks"}
+    if rank == 0:
+        cfgd = workload_config(spec, world)
+        cfgd["parallelism"] = (f"angle-sharded x{world} ("
+                               + ("peer-memory exchange" if comm.xchg is not None else "NCCL")
+                               + " for B's partial images)")
+        line = {
+            "metric": metric_name(spec) + ", angle-sharded", "value": value, "unit": "rays/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY.md §8d)",
+            "config": cfgd, "shard": {"angles_per_rank": int(len(idx)), "mode": "interleaved"},
+            "iters_per_s": (iters_per_step * args.steps / (total_ms / 1e3)
+                            if iters_per_step else None),
+            "roofline": roofline, "kernels": kernels, "e2e": e2e, "cpu_baseline": None,
+            "gpu_launches": int(launches), "clocks": clocks.summary(),
+        }
+        if "last" in result:
+            last = result["last"]
+            line["solve"] = {"stop_reason": last.stop_reason, "iterations": len(last.records),
+                             "final_data_residual": last.records[-1].data_residual_norm}
+        print(json.dumps(line), flush=True)
+    comm.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

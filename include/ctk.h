@@ -240,6 +240,11 @@ typedef struct {
     int snapshot_stride;  /* copy x_k to snaps[(k / stride) - 1] every stride iterations */
     float** snaps;        /* host pointers (pinned), n floats each */
     int n_snaps;
+    /* angle-sharded solve (SURVEY row e): NULL = one GPU.  Otherwise g is this
+     * rank's angle subset, b / d0 / r / aux rows of sinogram length hold this
+     * rank's rows, images (x, BA basis) are replicated; the driver issues the
+     * collectives itself (ctk_comm_*). */
+    struct ctk_comm* comm;
 } ctk_solve_bufs;
 
 typedef struct {
@@ -285,6 +290,34 @@ int ctk_xchg_connect_ptrs(ctk_xchg_t* x, float* const* recv, float* const* img,
  * call counter (>= 1, equal on all ranks, increasing).  work: as ctk_back. */
 int ctk_back_exchange(const ctk_geom_t* g, ctk_xchg_t* x, const float* u, unsigned epoch,
                       int phases, float* work, void* stream);
+/* *timed_out = 1 when one of this rank's exchange waits gave up after ~20 s
+ * (a peer never delivered); the word is cleared.  Synchronises the device. */
+int ctk_xchg_status(ctk_xchg_t* x, int* timed_out);
+
+/* ---- Communicator of the angle-sharded native solve (SURVEY row e;
+ * ctk_comm.cu): libctk's own NCCL communicator (NCCL loaded at run time from
+ * nccl_lib, e.g. the libnccl.so.2 torch uses; NULL: the default search),
+ * optionally with a peer exchange for B's partial images.  Replaces the
+ * reference's single-process loop (ctkrylov/gmres.py:186-211) across ranks:
+ * A sharded by angle with a replicated image, B's partial images summed,
+ * AB Krylov vectors sharded in measurement space (fp64 all-reduces of the
+ * Gram-Schmidt dots and norms).  Rank 0 makes the id, every rank creates the
+ * communicator with it (the caller ships the id bytes). */
+typedef struct ctk_comm ctk_comm_t;
+size_t ctk_comm_id_bytes(void);
+int ctk_comm_unique_id(const char* nccl_lib, void* id_out);
+int ctk_comm_create(const char* nccl_lib, const void* id, int nranks, int rank, int device,
+                    ctk_comm_t** out);
+int ctk_comm_destroy(ctk_comm_t* c);
+int ctk_comm_attach_exchange(ctk_comm_t* c, ctk_xchg_t* x);
+int ctk_comm_rank(const ctk_comm_t* c, int* rank, int* nranks);
+/* In-place sum over ranks, stream-ordered; dtype 0 fp32, 1 fp64. */
+int ctk_comm_allreduce(ctk_comm_t* c, void* buf, int64_t count, int dtype, void* stream);
+/* x (every rank) = sum over ranks of B_rank u_rank, g = this rank's angles:
+ * the peer exchange when attached (nranks > 1), else K2 + one all-reduce.
+ * work: ctk_back_work_floats(g, 0, n_angles) floats, zero-filled once. */
+int ctk_comm_back(ctk_comm_t* c, const ctk_geom_t* g, const float* u, float* x, float* work,
+                  void* stream);
 
 /* ---- On-device problem generation.
  * ctk_phantom replaces shepp_logan (ctkrylov/ct.py:115-134) and the harness's

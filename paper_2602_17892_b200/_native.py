@@ -84,6 +84,16 @@ SIGNATURES = {
     "ctk_xchg_connect_ptrs": (_c.c_int, [_vp, _c.POINTER(_c.c_void_p), _c.POINTER(_c.c_void_p),
                                          _c.POINTER(_c.c_void_p)]),
     "ctk_back_exchange": (_c.c_int, [_vp, _vp, _fp, _c.c_uint, _c.c_int, _fp, _vp]),
+    "ctk_xchg_status": (_c.c_int, [_vp, _c.POINTER(_c.c_int)]),
+    "ctk_comm_id_bytes": (_c.c_size_t, []),
+    "ctk_comm_unique_id": (_c.c_int, [_c.c_char_p, _vp]),
+    "ctk_comm_create": (_c.c_int, [_c.c_char_p, _vp, _c.c_int, _c.c_int, _c.c_int,
+                                   _c.POINTER(_c.c_void_p)]),
+    "ctk_comm_destroy": (_c.c_int, [_vp]),
+    "ctk_comm_attach_exchange": (_c.c_int, [_vp, _vp]),
+    "ctk_comm_rank": (_c.c_int, [_vp, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)]),
+    "ctk_comm_allreduce": (_c.c_int, [_vp, _vp, _c.c_int64, _c.c_int, _vp]),
+    "ctk_comm_back": (_c.c_int, [_vp, _vp, _fp, _fp, _fp, _vp]),
     "ctk_profile_begin": (_c.c_int, []),
     "ctk_profile_end": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int64), _c.POINTER(_c.c_double),
                                    _c.POINTER(_c.c_double)]),
@@ -114,7 +124,7 @@ class SolveBufs(ctypes.Structure):
                 ("x_true", _vp), ("img_nx", ctypes.c_int), ("img_ny", ctypes.c_int),
                 ("dyn_range", ctypes.c_double), ("metrics", _vp), ("metrics_host", _vp),
                 ("scratch_m", _vp), ("snapshot_stride", ctypes.c_int), ("snaps", _vp),
-                ("n_snaps", ctypes.c_int)]
+                ("n_snaps", ctypes.c_int), ("comm", _vp)]
 
 
 class SolveOut(ctypes.Structure):

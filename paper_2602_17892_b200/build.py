@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     tmp = LIB + ".tmp"
     extra = os.environ.get("CTK_NVCC_EXTRA", "").split()     # tuning experiments only
-    cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-shared", "-o", tmp, *sources(), "-lcudart"]
+    cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-shared", "-o", tmp, *sources(), "-lcudart", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -285,6 +285,12 @@ __global__ void __launch_bounds__(BTHREADS, PPT == 4 ? CTK_BACK_MINB4 : 6) k_bac
     }
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -303,9 +309,16 @@ __global__ void __launch_bounds__(BTHREADS) k_xchg_reduce(const ctk_xchg_args* _
     if (t >= X.tiles) return;
     const int tid = threadIdx.y * BTX + threadIdx.x;
     const unsigned* arrive = X.flags[X.rank];
-    if (tid < X.nranks)
+    if (tid < X.nranks) {
+        const unsigned long long t0 = globaltimer_ns();
         while (ld_acquire_sys(arrive + (size_t)tid * X.tiles + t) != X.epoch) {
+            __nanosleep(32);
+            if (globaltimer_ns() - t0 > CTK_XCHG_TIMEOUT_NS) {
+                atomicExch(X.err, 1u);
+                break;
+            }
         }
+    }
     __syncthreads();
     const size_t n = (size_t)nx * ny;
     const float* recv = X.recv[X.rank];
@@ -334,9 +347,15 @@ __global__ void __launch_bounds__(BTHREADS) k_xchg_reduce(const ctk_xchg_args* _
 __global__ void __launch_bounds__(256) k_xchg_wait(const ctk_xchg_args* __restrict__ xa) {
     const ctk_xchg_args& X = *xa;
     const unsigned* done = X.flags[X.rank] + (size_t)X.nranks * X.tiles;
+    const unsigned long long t0 = globaltimer_ns();
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < X.tiles; t += gridDim.x * blockDim.x)
         if (t % X.nranks != X.rank)
             while (ld_acquire_sys(done + t) != X.epoch) {
+                __nanosleep(32);
+                if (globaltimer_ns() - t0 > CTK_XCHG_TIMEOUT_NS) {
+                    atomicExch(X.err, 1u);
+                    return;
+                }
             }
 }
 

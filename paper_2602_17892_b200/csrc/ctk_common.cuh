@@ -170,7 +170,14 @@ struct ctk_xchg_args {
     float* recv[CTK_XCHG_MAX_RANKS];      // rank q's receive buffer [nranks][n]
     float* x[CTK_XCHG_MAX_RANKS];         // rank q's result image [n]
     unsigned* flags[CTK_XCHG_MAX_RANKS];  // rank q's flags: arrive [nranks][tiles], done [tiles]
+    unsigned* err;                         // this rank's error word: 1 = a wait timed out
 };
+
+// Bounded spin for the exchange's cross-GPU waits: a peer that never arrives
+// (dead rank, mismatched call sequence) ends the wait after ~20 s with the
+// error word set (reported by ctk_xchg_status / the sharded solve) instead of
+// hanging every GPU of the job.
+constexpr unsigned long long CTK_XCHG_TIMEOUT_NS = 20000000000ull;
 
 // Destination of a fused K1 staging write (P / PT of an image vector).
 struct ctk_stage_dst {
@@ -183,9 +190,15 @@ struct ctk_stage_dst {
 // GS step that also stages its new row for the next forward (SMEM path only),
 // whether that path is taken for (L, k), forward over already-staged copies,
 // back that also stages its output image.
+// comm != NULL: the vectors are this rank's shard; dots and norms are summed
+// over ranks between the launches (multi-kernel CGS2, stream-ordered NCCL).
 int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
                    double* stat, void* scratch, void* stream, const ctk_stage_dst* sd,
-                   double* h_mirror);
+                   double* h_mirror, const ctk_comm* comm = nullptr);
+int ctk_arnoldi_step_ex(const ctk_geom_t* g, int ab, int passes, float* W, int64_t ld, int j,
+                        float* q, float* tmp, float* aux1, int64_t ld1, float* aux2, int64_t ld2,
+                        float* stage_work, float* back_work, double* h_dev, int hcols,
+                        double* h_host, void* scratch, void* stream, const ctk_comm* comm);
 bool ctk_gs_smem_ok(int64_t L, int k);
 // Streamed path (long vectors): also leaves q untouched and takes the stage /
 // host-mirror outputs.  False whenever the SMEM path applies.
@@ -217,6 +230,15 @@ int64_t ctk_back_flag_count(const ctk_geom* g);
 int ctk_xchg_finish(const ctk_geom* g, const ctk_xchg_args* xc, int nranks, int phases,
                     cudaStream_t st);
 int64_t ctk_back_tiles(const ctk_geom* g);
+
+// Angle-sharded solve (ctk_comm.cu): stream-ordered fp64 sums over ranks and
+// B summed over ranks (peer exchange or all-reduce).
+int ctk_comm_sum_f64(const ctk_comm* c, double* buf, int64_t count, cudaStream_t st);
+int ctk_comm_back_sum(const ctk_comm* c, const ctk_geom* g, const float* u, float* dst,
+                      float* work, cudaStream_t st);
+int ctk_comm_size(const ctk_comm* c);
+int ctk_comm_check(const ctk_comm* c);
+int ctk_comm_rank_of(const ctk_comm* c);
 
 // K1 workspace: zero-padded copies P, PT
 // and one arrival ticket per (angle, 128-bin block) -- zero-filled once.

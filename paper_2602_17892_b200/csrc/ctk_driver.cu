@@ -123,6 +123,14 @@ Pool& pool() {
 // scal[2] = 1 / sqrt(scal[0]) (0 when the residual is exactly zero): the
 // cycle start normalises w0 on the device, so the Arnoldi pipeline starts
 // without a host round trip for beta.
+// Sharded solve: the x-norm entries of norms[slot][2] are replicated (every
+// rank holds the whole image); ranks other than 0 zero theirs before the
+// norms are summed over ranks, so the sum is rank 0's value on every rank.
+__global__ void k_zero_odd(double* v, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[2 * i + 1] = 0.0;
+}
+
 __global__ void k_set_inv(double* scal) {
     const double s = scal[0];
     scal[2] = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
@@ -189,6 +197,9 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
     cudaStream_t sa = ctk_stream(bf->stream_a), sb = ctk_stream(bf->stream_b);
     const int hc = bf->hcols;
     const int look = cfg->lookahead > 0 ? cfg->lookahead : 6;
+    const ctk_comm* comm = bf->comm;       // angle-sharded solve (ctk_comm.cu), or NULL
+    if (comm && !(bf->aux1 && bf->d0 && (!ab || bf->aux2)))
+        return ctk_fail(CTK_ERR_ARG, "the sharded solve needs the linear iterate rows (aux, d0)");
     CTK_CUDA(cudaSetDevice(g->device));
     Events evs;
     cudaEvent_t ev_start = evs.make(true);
@@ -229,11 +240,17 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
         if (ab) {
             if ((rc = ctk_forward(g, bf->x_cur, w0, 0, na, bf->b, bf->stage_a, bf->stream_a))) return rc;
             if ((rc = ctk_norm2(w0, L, bf->scal, bf->scratch_a, bf->stream_a))) return rc;
+            if (comm && (rc = ctk_comm_sum_f64(comm, bf->scal, 1, sa))) return rc;
         } else {
             if ((rc = ctk_forward(g, bf->x_cur, bf->tmp, 0, na, bf->b, bf->stage_a, bf->stream_a)))
                 return rc;
             if ((rc = ctk_norm2(bf->tmp, m, bf->scal + 1, bf->scratch_a, bf->stream_a))) return rc;
-            if ((rc = ctk_back(g, bf->tmp, w0, 0, na, nullptr, bf->back_a, bf->stream_a))) return rc;
+            if (comm) {
+                if ((rc = ctk_comm_sum_f64(comm, bf->scal + 1, 1, sa))) return rc;
+                if ((rc = ctk_comm_back_sum(comm, g, bf->tmp, w0, bf->back_a, sa))) return rc;
+            } else if ((rc = ctk_back(g, bf->tmp, w0, 0, na, nullptr, bf->back_a, bf->stream_a))) {
+                return rc;
+            }
             if ((rc = ctk_norm2(w0, L, bf->scal, bf->scratch_a, bf->stream_a))) return rc;
         }
         if (bf->aux1 && bf->d0)     // d0 = b - A x0 for the linear iterate path
@@ -252,12 +269,12 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
         auto enqueue_to = [&](int upto) -> int {
             while (queued < (upto < steps ? upto : steps)) {
                 if (trace) CTK_CUDA(cudaEventRecord(tr_beg[queued], sa));
-                int r2 = ctk_arnoldi_step(g, ab, cfg->reorthogonalize ? 2 : 1, bf->W, bf->ld,
-                                          queued, bf->q, bf->tmp, bf->aux1,
-                                          bf->ld1, bf->aux2, bf->ld2, bf->stage_a,
-                                          bf->back_a, bf->hs + (size_t)queued * hc, hc,
-                                          bf->h_host + (size_t)queued * hc, bf->scratch_a,
-                                          bf->stream_a);
+                int r2 = ctk_arnoldi_step_ex(g, ab, cfg->reorthogonalize ? 2 : 1, bf->W, bf->ld,
+                                             queued, bf->q, bf->tmp, bf->aux1,
+                                             bf->ld1, bf->aux2, bf->ld2, bf->stage_a,
+                                             bf->back_a, bf->hs + (size_t)queued * hc, hc,
+                                             bf->h_host + (size_t)queued * hc, bf->scratch_a,
+                                             bf->stream_a, comm);
                 if (r2) return r2;
                 CTK_CUDA(cudaEventRecord(ev_h[queued], sa));
                 if (trace) {
@@ -389,9 +406,20 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
             rec_slot.push_back(slot);
             nrec = slot + 1;
             if (cfg->stopping == CTK_STOP_DP || cfg->stopping == CTK_STOP_RNS) {
-                CTK_CUDA(cudaMemcpyAsync(bf->norms_host + 2 * slot, bf->norms + 2 * slot,
-                                         2 * sizeof(double), cudaMemcpyDeviceToHost, sb));
-                CTK_CUDA(cudaStreamSynchronize(sb));
+                if (comm) {
+                    // sharded: this iterate's residual norm summed over ranks,
+                    // on the Arnoldi stream -- every collective of the solve
+                    // goes through one stream, in the same order on all ranks
+                    CTK_CUDA(cudaStreamWaitEvent(sa, ev_it[slot], 0));
+                    if ((rc = ctk_comm_sum_f64(comm, bf->norms + 2 * slot, 1, sa))) return rc;
+                    CTK_CUDA(cudaMemcpyAsync(bf->norms_host + 2 * slot, bf->norms + 2 * slot,
+                                             2 * sizeof(double), cudaMemcpyDeviceToHost, sa));
+                    CTK_CUDA(cudaStreamSynchronize(sa));
+                } else {
+                    CTK_CUDA(cudaMemcpyAsync(bf->norms_host + 2 * slot, bf->norms + 2 * slot,
+                                             2 * sizeof(double), cudaMemcpyDeviceToHost, sb));
+                    CTK_CUDA(cudaStreamSynchronize(sb));
+                }
                 const double dn = sqrt(bf->norms_host[2 * slot]);
                 history.push_back(dn);
                 if (cfg->stopping == CTK_STOP_DP) {
@@ -438,8 +466,21 @@ extern "C" int ctk_solve(const ctk_geom_t* g, const ctk_solve_cfg* cfg, ctk_solv
         }
         if (stop == CTK_STOP_NONE && broke_at > 0) stop = CTK_STOP_BREAKDOWN;
     }
+    if (comm && cfg->stopping == CTK_STOP_NONE) {
+        // every rank's residual norms are partial sums over its rows; the
+        // image norms are replicated (kept from rank 0 only).  On the Arnoldi
+        // stream, after the iterate stream: one stream for all collectives.
+        CTK_CUDA(cudaEventRecord(ev_sync, sb));
+        CTK_CUDA(cudaStreamWaitEvent(sa, ev_sync, 0));
+        if (ctk_comm_rank_of(comm) != 0) {
+            k_zero_odd<<<(K + 1 + 127) / 128, 128, 0, sa>>>(bf->norms, K + 1);
+            ctk_count_launch();
+        }
+        if ((rc = ctk_comm_sum_f64(comm, bf->norms, 2 * (int64_t)(K + 1), sa))) return rc;
+    }
     CTK_CUDA(cudaStreamSynchronize(sa));
     CTK_CUDA(cudaStreamSynchronize(sb));
+    if (comm && (rc = ctk_comm_check(comm))) return rc;
     CTK_CUDA(cudaMemcpy(bf->norms_host, bf->norms, sizeof(double) * 2 * (K + 1),
                         cudaMemcpyDeviceToHost));
     if (bf->x_true)

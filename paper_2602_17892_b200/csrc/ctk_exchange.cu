@@ -33,7 +33,7 @@ struct ctk_xchg {
     int64_t n, tiles;
     float* recv;            // [nranks][n] partials received for the tiles this rank owns
     float* x;               // [n] result image
-    unsigned* flags;        // arrive [nranks][tiles], done [tiles]
+    unsigned* flags;        // arrive [nranks][tiles], done [tiles], error word
     ctk_xchg_args host;     // peer mappings
     ctk_xchg_args* dev;     // device copy for the kernels
     bool ipc_open[CTK_XCHG_MAX_RANKS][3];
@@ -42,8 +42,10 @@ struct ctk_xchg {
 namespace {
 
 size_t flags_bytes(const ctk_xchg* x) {
-    return sizeof(unsigned) * (size_t)(x->nranks + 1) * (size_t)x->tiles;
+    return sizeof(unsigned) * ((size_t)(x->nranks + 1) * (size_t)x->tiles + 1);
 }
+
+unsigned* err_word(const ctk_xchg* x) { return x->flags + (size_t)(x->nranks + 1) * x->tiles; }
 
 int push_args(ctk_xchg* x) {
     CTK_CUDA(cudaMemcpy(x->dev, &x->host, sizeof(ctk_xchg_args), cudaMemcpyHostToDevice));
@@ -94,6 +96,7 @@ extern "C" int ctk_xchg_create(const ctk_geom_t* g, int rank, int nranks, ctk_xc
     x->host.recv[rank] = x->recv;
     x->host.x[rank] = x->x;
     x->host.flags[rank] = x->flags;
+    x->host.err = err_word(x);
     *out = x;
     return CTK_OK;
 }
@@ -116,6 +119,18 @@ extern "C" int ctk_xchg_local(const ctk_xchg_t* x, float** recv, float** img, un
     if (recv) *recv = x->recv;
     if (img) *img = x->x;
     if (flags) *flags = x->flags;
+    return CTK_OK;
+}
+
+// *timed_out = 1 when a wait of this rank's exchange kernels gave up (the
+// peers never delivered); clears the word.  Synchronises the device.
+extern "C" int ctk_xchg_status(ctk_xchg_t* x, int* timed_out) {
+    if (!x || !timed_out) return ctk_fail(CTK_ERR_ARG, "null argument");
+    CTK_CUDA(cudaSetDevice(x->device));
+    unsigned v = 0;
+    CTK_CUDA(cudaMemcpy(&v, err_word(x), sizeof(v), cudaMemcpyDeviceToHost));
+    *timed_out = v != 0;
+    if (v) CTK_CUDA(cudaMemset(err_word(x), 0, sizeof(v)));
     return CTK_OK;
 }
 

@@ -2013,7 +2013,7 @@ static bool gram_track(void* scratch, const float* W, int64_t ld, int64_t L, int
 
 int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes, double* h,
                    double* stat, void* scratch, void* stream, const ctk_stage_dst* sd,
-                   double* h_mirror) {
+                   double* h_mirror, const ctk_comm* comm) {
     int rc;
     if ((rc = check_vec(W, "W")) || (rc = check_vec(q, "q"))) return rc;
     if (ld & 3) return ctk_fail(CTK_ERR_ARG, "ld must be a multiple of 4");
@@ -2024,31 +2024,41 @@ int ctk_gs_step_ex(float* W, int64_t ld, int k, int64_t L, float* q, int passes,
     Scratch s = carve(scratch, k + 3);
     if (passes != 1 && passes != 2) return ctk_fail(CTK_ERR_ARG, "passes must be 1 or 2");
     bool fused = false;
-    const bool single = passes == 2 && (ctk_gs_smem_ok(L, k) || ctk_gs_stream_ok(L, k));
+    const bool single =
+        !comm && passes == 2 && (ctk_gs_smem_ok(L, k) || ctk_gs_stream_ok(L, k));
     float* gram = gram_track(scratch, W, ld, L, k, single) ? s.gram : nullptr;
-    if ((rc = try_gs_smem(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, gram, &fused)))
-        return rc;
-    if (fused) return CTK_OK;
-    if ((rc = try_gs_stream(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, gram, &fused)))
-        return rc;
-    if (fused) return CTK_OK;
-    if (passes == 2 && (rc = try_cgs2_fused(W, ld, k, L, q, h, stat, s, st, &fused))) return rc;
-    if (fused) return CTK_OK;
+    if (!comm) {
+        if ((rc = try_gs_smem(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, gram, &fused)))
+            return rc;
+        if (fused) return CTK_OK;
+        if ((rc = try_gs_stream(W, ld, k, L, q, passes, h, stat, s, st, sd, h_mirror, gram,
+                                &fused)))
+            return rc;
+        if (fused) return CTK_OK;
+        if (passes == 2 && (rc = try_cgs2_fused(W, ld, k, L, q, h, stat, s, st, &fused))) return rc;
+        if (fused) return CTK_OK;
+    }
+    // multi-kernel CGS2; sharded vectors: every dot / norm summed over ranks
+    auto sum = [&](double* v, int64_t cnt) { return comm ? ctk_comm_sum_f64(comm, v, cnt, st) : 0; };
     double* h1 = s.tmp;                   // k+2: h1[0..k], ||q||^2
     double* h2 = s.tmp + s.nvec_cap;      // k+1
     double* n2 = s.tmp + 2 * s.nvec_cap;  // 1
     const int nb = k + 1;
     float* wnext = W + (size_t)(k + 1) * ld;
     if ((rc = launch_dots(W, ld, nb, q, L, 1, h1, s, st))) return rc;            // h1, ||Mw||^2
+    if ((rc = sum(h1, nb + 1))) return rc;
     if (passes == 1) {        // classical Gram-Schmidt, no reorthogonalisation pass
         if ((rc = launch_combine(W, ld, nb, h1, -1.0, q, wnext, L, n2, s, st))) return rc;
+        if ((rc = sum(n2, 1))) return rc;
         k_cgs2_finalize<<<1, 128, 0, st>>>(h1, nullptr, n2, k, h, stat);
         CTK_LAUNCH_CHECK("k_cgs2_finalize");
         return ctk_scale(wnext, wnext, L, stat + 2, stream);
     }
     if ((rc = launch_combine(W, ld, nb, h1, -1.0, q, q, L, nullptr, s, st))) return rc;  // q1
     if ((rc = launch_dots(W, ld, nb, q, L, 0, h2, s, st))) return rc;            // h2
+    if ((rc = sum(h2, nb))) return rc;
     if ((rc = launch_combine(W, ld, nb, h2, -1.0, q, wnext, L, n2, s, st))) return rc;   // q2
+    if ((rc = sum(n2, 1))) return rc;
     k_cgs2_finalize<<<1, 128, 0, st>>>(h1, h2, n2, k, h, stat);
     CTK_LAUNCH_CHECK("k_cgs2_finalize");
     return ctk_scale(wnext, wnext, L, stat + 2, stream);

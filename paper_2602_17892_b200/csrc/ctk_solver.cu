@@ -91,6 +91,19 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
                                 float* tmp, float* aux1, int64_t ld1, float* aux2, int64_t ld2,
                                 float* stage_work, float* back_work, double* h_dev, int hcols,
                                 double* h_host, void* scratch, void* stream) {
+    return ctk_arnoldi_step_ex(g, ab, passes, W, ld, j, q, tmp, aux1, ld1, aux2, ld2, stage_work,
+                               back_work, h_dev, hcols, h_host, scratch, stream, nullptr);
+}
+
+// comm != NULL: angle-sharded step (g = this rank's angles).  B's partial
+// images are summed over ranks (ctk_comm_back_sum) before anything reads
+// them; AB's Krylov vectors are this rank's sinogram rows, so the
+// Gram-Schmidt dots and norms are summed over ranks too (ctk_gs_step_ex);
+// BA's are replicated images and orthogonalise locally.
+int ctk_arnoldi_step_ex(const ctk_geom_t* g, int ab, int passes, float* W, int64_t ld, int j,
+                        float* q, float* tmp, float* aux1, int64_t ld1, float* aux2, int64_t ld2,
+                        float* stage_work, float* back_work, double* h_dev, int hcols,
+                        double* h_host, void* scratch, void* stream, const ctk_comm* comm) {
     if (!g) return ctk_fail(CTK_ERR_ARG, "null geometry");
     if (hcols < j + 6) return ctk_fail(CTK_ERR_ARG, "h row too short (%d) for step %d", hcols, j);
     const int na = g->n_angles;
@@ -108,14 +121,19 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
                         g->nx, g->ny, g->fwd_pad};
     // both single-launch Gram-Schmidt paths leave q untouched, stage w_{j+1}
     // for K1 and write the host-mapped column
-    const bool gs_smem = ctk_gs_smem_ok(L, j) || ctk_gs_stream_ok(L, j);
+    const bool gs_smem = (ctk_gs_smem_ok(L, j) || ctk_gs_stream_ok(L, j)) && !(ab && comm);
     if (ab) {   // q = A (B w); keep B w_j (aux1) and A B w_j (aux2) for the iterates
         float* bw = aux1 ? aux1 + (size_t)j * ld1 : tmp;
         float* abw = aux2 ? aux2 + (size_t)j * ld2 : q;
-        const bool fuse = j > 0;
-        if ((rc = ctk_back_ex(g, w, bw, 0, na, nullptr, back_work, fuse ? stage_work : nullptr,
-                              stream)))
+        // K2's epilogue stages B w_j for K1 -- not when B w_j is a partial
+        // image still to be summed over ranks (k_stage then runs in K1's launch)
+        const bool fuse = j > 0 && !comm;
+        if (comm) {
+            if ((rc = ctk_comm_back_sum(comm, g, w, bw, back_work, st))) return rc;
+        } else if ((rc = ctk_back_ex(g, w, bw, 0, na, nullptr, back_work,
+                                     fuse ? stage_work : nullptr, stream))) {
             return rc;
+        }
         if ((rc = ctk_forward_ex(g, bw, abw, 0, na, nullptr, stage_work, fuse, stream))) return rc;
         // the SMEM Gram-Schmidt path leaves its input untouched: no copy of A B w_j
         if (aux2 && !gs_smem)
@@ -134,7 +152,7 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
         // K1 CTAs); at c5 (~35 waves) the early K2 CTAs would just spin
         const int64_t k1_ctas = (int64_t)((g->det_count + 31) / 32) *
                                 ((na + CTK_FWD_APB - 1) / CTK_FWD_APB) * g->fwd_split;
-        const bool ch = chain && back_work && k1_ctas <= 4 * 8 * 148;
+        const bool ch = chain && back_work && k1_ctas <= 4 * 8 * 148 && !comm;
         // monotonic counters: zeroed (stream-ordered) before a cycle's step 0,
         // step j's K2 waits for (j + 1) K1 passes per group
         if (ch && j == 0)
@@ -143,9 +161,12 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
         if ((rc = ctk_forward_ex(g, w, aw, 0, na, nullptr, stage_work, pre, stream,
                                  ch ? ctk_back_flags(g, back_work) : nullptr)))
             return rc;
-        if ((rc = ctk_back_ex(g, aw, q, 0, na, nullptr, back_work, nullptr, stream,
-                              ch ? (unsigned)(j + 1) : 0u)))
+        if (comm) {
+            if ((rc = ctk_comm_back_sum(comm, g, aw, q, back_work, st))) return rc;
+        } else if ((rc = ctk_back_ex(g, aw, q, 0, na, nullptr, back_work, nullptr, stream,
+                                     ch ? (unsigned)(j + 1) : 0u))) {
             return rc;
+        }
     }
     // The SMEM Gram-Schmidt step writes the column straight into the
     // page-locked host row (mapped, UVA) -- no D2H copy on the critical stream.
@@ -156,7 +177,8 @@ extern "C" int ctk_arnoldi_step(const ctk_geom_t* g, int ab, int passes, float* 
     }
     const int ph = ctk_prof_open(2, st);
     rc = ctk_gs_step_ex(W, ld, j, L, pre_w ? const_cast<float*>(pre_w) : q, passes, h_dev,
-                        h_dev + hcols - 4, scratch, stream, ab ? nullptr : &sd, hm);
+                        h_dev + hcols - 4, scratch, stream, ab ? nullptr : &sd, hm,
+                        ab ? comm : nullptr);
     ctk_prof_close(ph, st);
     if (rc) return rc;
     if (h_host && !hm)

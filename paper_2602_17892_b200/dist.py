@@ -21,6 +21,14 @@ NVLink/NVSwitch.  Work is split by projection angle:
 * Independent slices (the c5 batch) need none of this: each rank runs the
   single-GPU driver on its own slices (bench.py's weak-scaling mode).
 
+Two drivers share this decomposition: :class:`NativeComm` +
+``gmres.run_gmres(..., comm=)`` run it in libctk's C++ driver (collectives
+issued from C++, stream-ordered on the Arnoldi stream, iterates by
+linearity: one A and one B apply per Arnoldi step, as on one GPU) -- the
+production path and ``bench.py --shard angles``; :func:`run_gmres_sharded`
+is the same algorithm in Python over a small backend interface, which the
+CPU test suite runs on a world_size-2 gloo group.
+
 The driver below is written against a small backend interface so that the
 same sharding logic runs on the GPU (:class:`CudaShardBackend`: libctk
 kernels + NCCL) and, in the CPU test suite, on a world_size-2 gloo group
@@ -287,6 +295,154 @@ class PeerExchange:
             self.handle = None
 
 
+def nccl_library() -> str | None:
+    """Path of the libnccl.so.2 torch uses (libctk loads the same instance)."""
+    import os
+    try:
+        import nvidia.nccl
+        for base in getattr(nvidia.nccl, "__path__", []):
+            p = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                return p
+    except Exception:
+        pass
+    return None
+
+
+def open_peer_exchange(dgeom, group=None):
+    """PeerExchange over CUDA IPC among the ranks of `group`, or None when any
+    rank cannot create or map the buffers (every rank agrees)."""
+    import torch
+    import torch.distributed as tdist
+    world = tdist.get_world_size(group)
+    rank = tdist.get_rank(group)
+    if not 1 < world <= 8:
+        return None
+    ok, ex, mine = True, None, b""
+    try:
+        ex = PeerExchange(dgeom, rank, world)
+        mine = ex.export()
+    except Exception:
+        ok = False
+    handles = [None] * world
+    tdist.all_gather_object(handles, mine if ok else None, group=group)
+    if ok and all(h is not None for h in handles):
+        try:
+            ex.connect_ipc(handles)
+        except Exception:
+            ok = False
+    else:
+        ok = False
+    flag = torch.tensor([1 if ok else 0], device=dgeom.dev)
+    tdist.all_reduce(flag, op=tdist.ReduceOp.MIN, group=group)
+    return ex if int(flag.item()) == 1 else None
+
+
+class NativeComm:
+    """libctk's communicator for the angle-sharded native solve (ctk_comm_*):
+    its own NCCL communicator (the id shipped over torch.distributed), plus
+    the peer-memory exchange for B's partial images when every rank maps the
+    others' buffers.  Without an initialised process group it is a one-rank
+    communicator (the sharded code path on one GPU).  Pass it to
+    ``gmres.run_gmres(A_local, B_local, b_local, cfg, comm=...)``."""
+
+    def __init__(self, dgeom, group=None, peer_exchange: bool | None = None,
+                 nccl_lib: str | None = None):
+        import ctypes
+        import os
+
+        from . import _native
+        self._native, self._ct = _native, ctypes
+        self.lib = _native.load()
+        self.dg = dgeom
+        try:
+            import torch.distributed as tdist
+            dist_on = tdist.is_available() and tdist.is_initialized()
+        except Exception:
+            dist_on = False
+        self.rank = tdist.get_rank(group) if dist_on else 0
+        self.world = tdist.get_world_size(group) if dist_on else 1
+        lib_path = (nccl_lib or nccl_library() or "").encode() or None
+        nbytes = int(self.lib.ctk_comm_id_bytes())
+        idb = None
+        if self.rank == 0:
+            buf = ctypes.create_string_buffer(nbytes)
+            _native.check(self.lib.ctk_comm_unique_id(lib_path, buf), "ctk_comm_unique_id")
+            idb = buf.raw
+        if self.world > 1:
+            obj = [idb]
+            tdist.broadcast_object_list(obj, src=tdist.get_global_rank(group, 0) if group else 0,
+                                        group=group)
+            idb = obj[0]
+        h = ctypes.c_void_p()
+        _native.check(self.lib.ctk_comm_create(lib_path, idb, self.world, self.rank,
+                                               dgeom.dev.index, ctypes.byref(h)), "ctk_comm_create")
+        self.handle = h
+        self.xchg = None
+        if peer_exchange is None:
+            peer_exchange = os.environ.get("CTK_PEER_EXCHANGE", "1") != "0"
+        if peer_exchange and self.world > 1:
+            self.xchg = open_peer_exchange(dgeom, group)
+            if self.xchg is not None:
+                _native.check(self.lib.ctk_comm_attach_exchange(h, self.xchg.handle),
+                              "ctk_comm_attach_exchange")
+        wf = int(self.lib.ctk_back_work_floats(dgeom.handle, 0, dgeom.n_angles))
+        self.work = dgeom.torch.zeros(max(wf, 4), dtype=dgeom.torch.float32, device=dgeom.dev)
+
+    def back(self, u, out=None, stream=None):
+        """out (every rank) = sum over ranks of B_rank u_rank."""
+        dg = self.dg
+        dg._check(u, dg.m, "u")
+        if out is None:
+            out = dg.torch.empty(dg.n, dtype=dg.torch.float32, device=dg.dev)
+        stream = dg._stream(stream)
+        self._native.check(self.lib.ctk_comm_back(self.handle, dg.handle, u.data_ptr(),
+                                                  out.data_ptr(), self.work.data_ptr(),
+                                                  stream.cuda_stream), "ctk_comm_back")
+        return out
+
+    def allreduce(self, t, stream=None):
+        """In-place sum of a CUDA fp32 / fp64 tensor over ranks (stream-ordered)."""
+        torch = self.dg.torch
+        dtype = {torch.float32: 0, torch.float64: 1}[t.dtype]
+        stream = self.dg._stream(stream)
+        self._native.check(self.lib.ctk_comm_allreduce(self.handle, t.data_ptr(), t.numel(), dtype,
+                                                       stream.cuda_stream), "ctk_comm_allreduce")
+        return t
+
+    def close(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            self.lib.ctk_comm_destroy(h)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def sharded_projectors(grid, geometry, angle_idx, device: int = 0):
+    """(A, B) over this rank's angles: the drop-in operators of the sharded
+    solve (rows of A / columns of B are the rank's sinogram rows)."""
+    from .ct import ParallelGeometry, back_pixel_driven, forward_ray_driven
+    local = ParallelGeometry(np.asarray(geometry.angles)[np.asarray(angle_idx)],
+                             geometry.det_count, geometry.det_spacing)
+    A = forward_ray_driven(grid, local, device=device)
+    B = back_pixel_driven(grid, local, device=device)
+    return A, B
+
+
+def local_rows(v, det_count: int, angle_idx):
+    """This rank's sinogram rows (angle-major) of a full-geometry vector."""
+    idx = np.asarray(angle_idx)
+    if isinstance(v, np.ndarray):
+        return np.ascontiguousarray(v.reshape(-1, det_count)[idx].ravel())
+    import torch
+    return v.view(-1, det_count)[torch.as_tensor(idx, device=v.device)].reshape(-1).contiguous()
+
+
 class CudaShardBackend(ShardBackend):
     """libctk projectors on this rank's angles; partial images summed over
     NVLink peer memory (:class:`PeerExchange`) when every rank can map the
@@ -323,25 +479,7 @@ class CudaShardBackend(ShardBackend):
     def _open_exchange(self, world):
         """All ranks agree: every rank creates its buffers, handles are
         all-gathered, every rank maps its peers; any failure -> NCCL path."""
-        rank = self.dist.get_rank(self.group)
-        ok, ex, mine = True, None, b""
-        try:
-            ex = PeerExchange(self.dg, rank, world)
-            mine = ex.export()
-        except Exception:
-            ok = False
-        handles = [None] * world
-        self.dist.all_gather_object(handles, mine if ok else None, group=self.group)
-        if ok and all(h is not None for h in handles):
-            try:
-                ex.connect_ipc(handles)
-            except Exception:
-                ok = False
-        else:
-            ok = False
-        flag = self.torch.tensor([1 if ok else 0], device=self.dev)
-        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.group)
-        return ex if int(flag.item()) == 1 else None
+        return open_peer_exchange(self.dg, self.group)
 
     def back_sum(self, u):
         if self.xchg is None:

@@ -710,7 +710,8 @@ class _NativeSolve(_DeviceSolve):
             scal=self.scal.data_ptr(), scal_host=self.scal_host.data_ptr(),
             stage_a=stage_a, back_a=back_a, stage_b=stage_b, back_b=back_b,
             scratch_a=self.basis.scratch(sa), scratch_b=self.basis.scratch(sb),
-            stream_a=sa.cuda_stream, stream_b=sb.cuda_stream)
+            stream_a=sa.cuda_stream, stream_b=sb.cuda_stream,
+            comm=None if getattr(self, "comm", None) is None else self.comm.handle.value)
         # optional per-iteration records computed on the device (row f1)
         out_arrays["rre"] = np.full(n1, np.nan)
         out_arrays["ssim"] = np.full(n1, np.nan)
@@ -778,13 +779,17 @@ class _NativeSolve(_DeviceSolve):
 
 def run_gmres(A: LinearOperator, B: LinearOperator, b, cfg: SolverConfig,
               x_true: np.ndarray | None = None, image_shape: tuple[int, int] | None = None,
-              *, stream=None, keep_on_device: bool = False) -> SolveResult:
+              *, stream=None, keep_on_device: bool = False, comm=None) -> SolveResult:
     """(Hybrid) AB-/BA-GMRES with optional restarting, on the GPU.
 
     ``b`` may be a host array (the reference's contract) or a CUDA tensor
     (device-resident input).  Returns a SolveResult with a host ``x`` (a CUDA
     tensor when ``keep_on_device``); ``result.transfer`` counts the bytes the
     solve moved across PCIe.
+
+    ``comm`` (a :class:`paper_2602_17892_b200.dist.NativeComm`): angle-sharded
+    solve on the native driver -- A, B are this rank's angle subset, ``b`` its
+    sinogram rows; the iterate is replicated on every rank.
     """
     cfg.validate()
     if cfg.method not in GMRES_METHODS:
@@ -794,8 +799,13 @@ def run_gmres(A: LinearOperator, B: LinearOperator, b, cfg: SolverConfig,
         raise OperatorShapeError(f"data vector has shape {shape}, expected ({A.rows},)")
     _check_dims(A, B, int(shape[0]))
     native = cfg.stopping_rule != "ncp" and os.environ.get("CTK_PY_DRIVER", "0") != "1"
+    if comm is not None and not native:
+        raise ConfigError("the angle-sharded solve runs on the native driver "
+                          "(no ncp stopping, CTK_PY_DRIVER unset)")
     cls = _NativeSolve if native else _DeviceSolve
-    return cls(A, B, b, cfg, x_true, image_shape, stream, None, keep_on_device).run()
+    solver = cls(A, B, b, cfg, x_true, image_shape, stream, None, keep_on_device)
+    solver.comm = comm
+    return solver.run()
 
 
 def run_ab_gmres(A, B, b, cfg: SolverConfig, **kwargs) -> SolveResult:

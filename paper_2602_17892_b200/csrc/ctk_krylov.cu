@@ -848,21 +848,30 @@ __device__ __forceinline__ void all_reduce_rows(const double* partial, int nrows
 // 1e-8 ||q||^2 (cancellation would cost fp64 digits) the kernels fall back to
 // an explicit fp64 norm of the stored q2.
 //
-// Per-CTA (every CTA computes the same values in the same order):
-// h2[i] = -(E h1)_i, cc[i] = h1[i] + h2[i], *est; CTA 0 appends E's column /
-// row k to `gram` (columns j < k were written by the earlier steps).
-__device__ __forceinline__ double gram_entry(const float* gram, int i, int j, int k,
-                                             const double* g) {
-    return j < k ? (double)__ldcg(gram + (size_t)i * GRAM_LD + j) : g[i] - (i == k ? 1.0 : 0.0);
+// Per-CTA (every CTA computes the same values in the same order, so the
+// fallback decision below is grid-uniform): h2[i] = -(E h1)_i,
+// cc[i] = h1[i] + h2[i], *est; CTA 0 appends E's column / row k to `gram`.
+// E[i][j] with i, j < k was written by step max(i, j) < k; row and column k
+// come from this step's g (E[k][j] = E[j][k] = g[j], E[k][k] = g[k] - 1).
+// `Es` (row stride es_ld): the i, j < k block, in shared memory when the
+// caller staged it (es_smem), else `gram` itself.
+__device__ __forceinline__ double gram_entry(const float* Es, int es_ld, bool es_smem, int i,
+                                             int j, int k, const double* g) {
+    if (j == k) return g[i] - (i == k ? 1.0 : 0.0);
+    if (i == k) return g[j];
+    const float* p = Es + (size_t)i * es_ld + j;
+    return (double)(es_smem ? *p : __ldcg(p));
 }
 
-__device__ void gram_coefs(float* gram, int k, const double* h1, const double* g, double* h2,
-                           double* cc, double* red, double* s_est) {
+__device__ void gram_coefs(float* gram, const float* Es, int es_ld, bool es_smem, int k,
+                           const double* h1, const double* g, double* h2, double* cc,
+                           double* red, double* s_est) {
     const int nb = k + 1, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
     for (int i = warp; i < nb; i += nw) {
         double t = 0.0;
-        for (int j = lane; j < nb; j += 32) t = fma(gram_entry(gram, i, j, k, g), h1[j], t);
+        for (int j = lane; j < nb; j += 32)
+            t = fma(gram_entry(Es, es_ld, es_smem, i, j, k, g), h1[j], t);
         t = warp_sum(t);
         if (lane == 0) {
             h2[i] = -t;
@@ -879,7 +888,8 @@ __device__ void gram_coefs(float* gram, int k, const double* h1, const double* g
     double part = 0.0;            // this warp's rows of  c.(E c) + c.c - 2 c.h1
     for (int i = warp; i < nb; i += nw) {
         double u = 0.0;
-        for (int j = lane; j < nb; j += 32) u = fma(gram_entry(gram, i, j, k, g), cc[j], u);
+        for (int j = lane; j < nb; j += 32)
+            u = fma(gram_entry(Es, es_ld, es_smem, i, j, k, g), cc[j], u);
         u = warp_sum(u);
         part += cc[i] * u + cc[i] * cc[i] - 2.0 * cc[i] * h1[i];
     }
@@ -1020,7 +1030,9 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
         smem_raw + ((16 + sizeof(double) * (4 * nb + 4 + SW) + 15) & ~(size_t)15));
     double* qd = reinterpret_cast<double*>(qv + cpad);               // [cpad]: qv in fp64
     double* wkd = qd + cpad;                                         // [cpad]: row k in fp64 (gram)
-    unsigned char* ws_raw = reinterpret_cast<unsigned char*>(wkd + cpad);
+    float* Es = reinterpret_cast<float*>(wkd + cpad);                // [k][k]: E block (gram)
+    const int es_n = gram && passes == 2 ? k : 0;
+    unsigned char* ws_raw = reinterpret_cast<unsigned char*>(Es + ((es_n * es_n + 3) & ~3));
     ws_raw += (128u - (smem_u32(ws_raw) & 127u)) & 127u;           // TMA destination alignment
     float* Ws = reinterpret_cast<float*>(ws_raw);                   // [nb][cpad]
     double4* acc = reinterpret_cast<double4*>(                      // [ST], 32-B aligned
@@ -1064,6 +1076,10 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
         qv[i] = v;
         qd[i] = v;
     }                                                                //  not assumed here)
+    for (int e = threadIdx.x; e < es_n * es_n; e += ST) {            // E's i, j < k block
+        const int i = e / es_n, j = e - i * es_n;                    // (written by earlier steps)
+        Es[e] = __ldcg(gram + (size_t)i * GRAM_LD + j);
+    }
     if (row_bytes > 0) mbar_wait(bar_a, 0);
     __syncthreads();
     GS_STAMP(2);
@@ -1085,7 +1101,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
         all_reduce_rows(P1, 2 * nb + 1, h1);
         __syncthreads();
         __shared__ double s_est;
-        gram_coefs(gram, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
+        gram_coefs(gram, Es, es_n, true, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
         GS_STAMP(5);
         const double est = s_est, a = h1[nb];
         if (a > 0.0 && est > 1e-8 * a) {
@@ -1455,7 +1471,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
         all_reduce_rows(P1, 2 * nb + 1, h1);
         __syncthreads();
         __shared__ double s_est;
-        gram_coefs(gram, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
+        gram_coefs(gram, gram, GRAM_LD, false, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
         const double est = s_est, a = h1[nb];
         if (a > 0.0 && est > 1e-8 * a) {
             sweep(2, &tm.q, cc, nullptr, 1.0 / sqrt(est));
@@ -1639,7 +1655,7 @@ static size_t gs_smem_bytes(int k, int64_t chunk) {
     const int nb = k + 1;
     const size_t head = (16 + sizeof(double) * (4 * (size_t)nb + 4 + SW) + 15) & ~(size_t)15;
     return head + sizeof(float) * (size_t)chunk * (nb + 1) + 2 * sizeof(double) * (size_t)chunk +
-           sizeof(double) * 4 * ST + 32 + 128;
+           sizeof(float) * (((size_t)k * k + 3) & ~(size_t)3) + sizeof(double) * 4 * ST + 32 + 128;
 }
 
 static bool gs_smem_plan(int64_t L, int k, int64_t* Gp, int64_t* chunkp, size_t* smemp) {

@@ -250,6 +250,62 @@ def make_io():
     print("problem_io.npz", len(out), "entries")
 
 
+def make_solver_spread(trials=8, rel=1e-7):
+    """The reference's OWN sensitivity to fp32-level input rounding on the
+    driver-branch cases: each case re-run by the
+    unmodified reference with its operators and data perturbed at the level
+    the GPU path computes at -- (a) A, B and b rounded to fp32, (b) `trials`
+    random relative perturbations of every entry of A, B and b by `rel`.
+    Stored per case: the largest relative deviation, over those runs, of
+    every iteration's data-residual norm from the unperturbed run, and of the
+    final x.  The GPU test holds its deviation from the reference to a
+    multiple of this spread where the spread exceeds the fixed bar (the
+    unregularised runs deep in their noise-fitting regime)."""
+    from ctkrylov.linop import dense_operator
+    prob = make_ct_problem(16, 12, 23, 0.02, 0)
+    Ad, Bd, b = prob.forward.to_dense(), prob.back.to_dense(), prob.b_noisy
+    cases = {
+        "ab_plain": dict(method="ab", max_iter=12),
+        "ba_plain": dict(method="ba", max_iter=12),
+        "ab_gcv": dict(method="ab-hybrid", lambda_strategy="gcv", max_iter=15),
+        "ba_gcv": dict(method="ba-hybrid", lambda_strategy="gcv", max_iter=15),
+        "ab_lcurve": dict(method="ab-hybrid", lambda_strategy="lcurve", max_iter=15),
+        "ba_fixed": dict(method="ba-hybrid", lambda_strategy="fixed", lambda_value=0.3, max_iter=10),
+        "ab_restart": dict(method="ab-hybrid", lambda_strategy="gcv", max_iter=14, restart_period=5),
+        "ab_dp": dict(method="ab", max_iter=40, stopping_rule="dp", noise_norm=prob.noise_norm),
+        "ba_rns": dict(method="ba", max_iter=40, stopping_rule="rns", rns_epsilon=1e-3),
+        "ba_ncp": dict(method="ba", max_iter=40, stopping_rule="ncp", ncp_threshold=0.2),
+        "ab_ncp": dict(method="ab", max_iter=40, stopping_rule="ncp", ncp_threshold=0.12),
+    }
+    rng = np.random.default_rng(77)
+    variants = [(Ad.astype(np.float32).astype(np.float64), Bd.astype(np.float32).astype(np.float64),
+                 b.astype(np.float32).astype(np.float64))]
+    for _ in range(trials):
+        variants.append((Ad * (1 + rel * rng.standard_normal(Ad.shape)),
+                         Bd * (1 + rel * rng.standard_normal(Bd.shape)),
+                         b * (1 + rel * rng.standard_normal(b.shape))))
+    out = {"trials": np.int64(trials), "rel": np.float64(rel)}
+    for name, kw in cases.items():
+        cfg = SolverConfig(**kw)
+        base = run_gmres(dense_operator(Ad), dense_operator(Bd), b, cfg)
+        dn0 = np.array([r.data_residual_norm for r in base.records])
+        dev = np.zeros(len(dn0))
+        devx = 0.0
+        for A_, B_, b_ in variants:
+            res = run_gmres(dense_operator(A_), dense_operator(B_), b_, cfg)
+            dn = np.array([r.data_residual_norm for r in res.records])
+            kk = min(len(dn), len(dn0))
+            dev[:kk] = np.maximum(dev[:kk], np.abs(dn[:kk] / dn0[:kk] - 1.0))
+            if len(dn) != len(dn0):
+                dev[kk:] = np.inf                     # stopped at another iteration
+            devx = max(devx, float(np.linalg.norm(res.x - base.x) / np.linalg.norm(base.x)))
+        out[f"{name}/res_spread"] = dev
+        out[f"{name}/x_spread"] = np.float64(devx)
+        print(f"{name}: residual spread max {dev.max():.2e} (first 12: {dev[:12].max():.2e}), "
+              f"x spread {devx:.2e}")
+    np.savez_compressed(os.path.join(HERE, "solver_spread.npz"), **out)
+
+
 def make_lcurve_band(trials=32, deltas=(1e-15, 1e-12, 1e-7)):
     """c2 L-curve conditioning: run the reference's c2
     hybrid BA-GMRES + L-curve, capture every iteration's Hessenberg at its
@@ -312,3 +368,5 @@ if __name__ == "__main__":
         make_config("c2", extra_plain=True)
     if "lcurve" in which:
         make_lcurve_band()
+    if "spread" in which:
+        make_solver_spread()

@@ -146,15 +146,21 @@ def test_driver_branches_vs_reference(cuda, golden, case):
     n_ref = len(d[f"{case}/rec/k"])
     assert len(res.records) == n_ref
     got, ref = records(res, "data_residual_norm"), d[f"{case}/rec/data_residual_norm"]
-    np.testing.assert_allclose(got[:12], ref[:12], rtol=1e-3)
-    # Unregularised GMRES deep in its noise-fitting regime amplifies the fp32
-    # operator/basis rounding (the reference's own dense-vs-CSR operators
-    # already disagree there); the bar past iteration 12 is looser.
-    np.testing.assert_allclose(got[12:], ref[12:], rtol=5e-2)
+    # Per-iteration bar: 1e-3, or 3x the reference's OWN spread under
+    # fp32-level rounding of its operators and data where that is larger
+    # (tests/golden/solver_spread.npz, make_golden.py:make_solver_spread).
+    # Unregularised GMRES deep in its noise-fitting regime (ab_dp, ba_rns past
+    # ~iteration 15) amplifies input rounding by 1e5: the reference itself
+    # moves by up to 1.5e-2 / 4.4e-2 there -- measured, not assumed.
+    sp = golden("solver_spread")
+    spread = sp[f"{case}/res_spread"]
+    tol = np.maximum(1e-3, 3.0 * spread[: len(got)])
+    dev = np.abs(got / ref - 1.0)
+    assert np.all(dev <= tol), (np.nonzero(dev > tol)[0] + 1, dev.max())
     if "gcv" in case or "fixed" in case:
         lam, lam_ref = records(res, "lambda_used"), d[f"{case}/rec/lambda_used"]
         assert np.all(np.abs(lam / lam_ref - 1.0) <= 0.01)
-    assert rel(res.x, d[f"{case}/x"]) <= (2e-3 if len(got) <= 15 else 5e-2)
+    assert rel(res.x, d[f"{case}/x"]) <= max(2e-3, 3.0 * float(sp[f"{case}/x_spread"]))
 
 
 def test_device_resident_input_and_snapshots(cuda, golden):

@@ -656,7 +656,7 @@ constexpr int64_t FUSED_MAX_L = 1 << 21;
 // ---------------------------------------------------------------------------
 constexpr int ST = 512;                 // threads per CTA
 constexpr int SW = ST / 32;
-constexpr size_t SMEM_LIMIT = 226 * 1024;       // + static smem <= 227 KB opt-in
+constexpr size_t SMEM_LIMIT = 224 * 1024;       // + static smem (<= 3 KB) <= 227 KB opt-in
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);
@@ -855,50 +855,68 @@ __device__ __forceinline__ void all_reduce_rows(const double* partial, int nrows
 // come from this step's g (E[k][j] = E[j][k] = g[j], E[k][k] = g[k] - 1).
 // `Es` (row stride es_ld): the i, j < k block, in shared memory when the
 // caller staged it (es_smem), else `gram` itself.
-__device__ __forceinline__ double gram_entry(const float* Es, int es_ld, bool es_smem, int i,
-                                             int j, int k, const double* g) {
-    if (j == k) return g[i] - (i == k ? 1.0 : 0.0);
-    if (i == k) return g[j];
+// E's entries are fp32-rounding sized (~1e-7), so E h1 and E c are formed in
+// fp32: each product keeps ~7 significant digits of a term 1e-7 |h1| small,
+// i.e. ~1e-14 |h1| absolute -- far below what c needs -- and the passes run
+// on the fp32 pipe with no fp64 conversions (the dots, c.h1 and c.c that
+// cancel stay in fp64).
+__device__ __forceinline__ float gram_entry(const float* Es, int es_ld, bool es_smem, int i, int j,
+                                            int k, const float* gf) {
+    if (j == k) return gf[i];
+    if (i == k) return gf[j];
     const float* p = Es + (size_t)i * es_ld + j;
-    return (double)(es_smem ? *p : __ldcg(p));
+    return es_smem ? *p : __ldcg(p);
 }
 
 __device__ void gram_coefs(float* gram, const float* Es, int es_ld, bool es_smem, int k,
                            const double* h1, const double* g, double* h2, double* cc,
                            double* red, double* s_est) {
+    // four threads per row (nb <= 128 rows on 512 threads): each sums a
+    // quarter of the row in fp32, two shuffles finish it.  Fixed order:
+    // bitwise the same in every CTA.
+    constexpr int TPR = 4;
+    __shared__ float s_f[3][GRAM_LD];                 // h1, column k of E, c (fp32)
     const int nb = k + 1, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
-    for (int i = warp; i < nb; i += nw) {
-        double t = 0.0;
-        for (int j = lane; j < nb; j += 32)
-            t = fma(gram_entry(Es, es_ld, es_smem, i, j, k, g), h1[j], t);
-        t = warp_sum(t);
-        if (lane == 0) {
-            h2[i] = -t;
-            cc[i] = h1[i] - t;
-        }
+    float* h1f = s_f[0];
+    float* gf = s_f[1];
+    float* cf = s_f[2];
+    for (int r = threadIdx.x; r < nb; r += blockDim.x) {
+        h1f[r] = (float)h1[r];
+        gf[r] = (float)(g[r] - (r == k ? 1.0 : 0.0));
+    }
+    __syncthreads();
+    const int i = threadIdx.x / TPR, sub = threadIdx.x % TPR;
+    float t = 0.f;
+    if (i < nb)
+        for (int j = sub; j < nb; j += TPR) t = fmaf(gram_entry(Es, es_ld, es_smem, i, j, k, gf), h1f[j], t);
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    if (i < nb && sub == 0) {
+        h2[i] = -(double)t;
+        cc[i] = h1[i] - (double)t;
+        cf[i] = (float)cc[i];
     }
     if (blockIdx.x == 0)
-        for (int i = threadIdx.x; i <= k; i += blockDim.x) {
-            const float e = (float)(g[i] - (i == k ? 1.0 : 0.0));
-            gram[(size_t)k * GRAM_LD + i] = e;
-            gram[(size_t)i * GRAM_LD + k] = e;
+        for (int r = threadIdx.x; r <= k; r += blockDim.x) {
+            gram[(size_t)k * GRAM_LD + r] = gf[r];
+            gram[(size_t)r * GRAM_LD + k] = gf[r];
         }
     __syncthreads();
-    double part = 0.0;            // this warp's rows of  c.(E c) + c.c - 2 c.h1
-    for (int i = warp; i < nb; i += nw) {
-        double u = 0.0;
-        for (int j = lane; j < nb; j += 32)
-            u = fma(gram_entry(Es, es_ld, es_smem, i, j, k, g), cc[j], u);
-        u = warp_sum(u);
-        part += cc[i] * u + cc[i] * cc[i] - 2.0 * cc[i] * h1[i];
-    }
+    float u = 0.f;
+    if (i < nb)
+        for (int j = sub; j < nb; j += TPR) u = fmaf(gram_entry(Es, es_ld, es_smem, i, j, k, gf), cf[j], u);
+    u += __shfl_xor_sync(0xffffffffu, u, 1);
+    u += __shfl_xor_sync(0xffffffffu, u, 2);
+    // this row's share of  c.(E c) + c.c - 2 c.h1  (the last two in fp64)
+    double part = (i < nb && sub == 0) ? cc[i] * (double)u + cc[i] * cc[i] - 2.0 * cc[i] * h1[i] : 0.0;
+    part = warp_sum(part);
     if (lane == 0) red[warp] = part;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < nw; ++w) t += red[w];
-        *s_est = h1[nb] + t;
+        double tt = 0.0;
+        for (int w = 0; w < nw; ++w) tt += red[w];
+        *s_est = h1[nb] + tt;
     }
     __syncthreads();
 }
@@ -1100,6 +1118,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
         GS_STAMP(4);
         all_reduce_rows(P1, 2 * nb + 1, h1);
         __syncthreads();
+        GS_STAMP(6);
         __shared__ double s_est;
         gram_coefs(gram, Es, es_n, true, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
         GS_STAMP(5);

@@ -23,7 +23,7 @@ lib = _native.load()
 rd = lib.ctk_gs_prof_read
 rd.argtypes = [ctypes.c_void_p]
 PH = [(0, 1, "pdl_wait"), (1, 2, "load"), (2, 3, "dots2"), (3, 4, "grid_sync"),
-      (4, 5, "reduce+gram"), (5, 10, "update"), (10, 11, "tail")]
+      (4, 6, "reduce"), (6, 5, "gram_coefs"), (5, 10, "update"), (10, 11, "tail")]
 Ls = [int(a) for a in sys.argv[1:]] or [65536]
 KS = [int(a) for a in os.environ.get('GS_KS', '20,40,79').split(',')]
 REPS = int(os.environ.get('GS_REPS', '20'))

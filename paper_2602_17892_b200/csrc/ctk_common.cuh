@@ -47,6 +47,7 @@ struct ctk_geom {
     int back_wmax;            // max staged bins per angle for one K2 tile
     int fwd_split;            // K1 row chunks per ray (small problems: more CTAs)
     int fwd_pad;              // K1 zero columns each side of P / PT (warp lockstep walk)
+    int fwd_pair;             // K1 warps take 2 angles x 16 bins (CTK_FWD_PAIR=0: 1 x 32)
     int back_ppt;             // K2 pixels per thread (tile 32 x 8 ppt): 2, or 4 for >= 512^2
     int n_degenerate;
     int h_pow2;               // pixel size is a power of two: x / h == x * (1 / h) exactly

@@ -222,6 +222,7 @@ struct FwdArgs {
     ExactGrid eg;
     int D, a0, a1, pad;
     unsigned* done;          // optional: per 4-angle group, finished CTAs (K2 chaining)
+    int pair;                // warp = 2 angles x 16 bins (else 1 angle x 32 bins)
 };
 
 // One ray of the row walk (see the header comment).  base/pitch/C describe
@@ -451,9 +452,24 @@ __device__ __forceinline__ unsigned cluster_addr(const void* p, unsigned rank) {
 template <bool SPLIT>
 __global__ void __launch_bounds__(FWD_THREADS, CTK_FWD_MINB) k_forward(FwdArgs A) {
     ctk_pdl_trigger();
-    const int ai = blockIdx.y * FWD_APB + (threadIdx.x >> 5);
+    // A CTA is 4 adjacent angles x 32 adjacent bins.  Paired layout: each
+    // warp takes 2 adjacent angles x 16 bins (half-warps), so a warp's taps
+    // on a walk row span ~16 rays' worth of columns (+ the small shift
+    // between neighbouring angles) instead of 32 rays' -- fewer cache lines,
+    // hence fewer L1 wavefronts, per gather request (the L1 pipe bounds K1).
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int ai, j;
+    if (A.pair == 2) {          // 4 angles x 8 bins per warp
+        ai = blockIdx.y * FWD_APB + (lane >> 3);
+        j = blockIdx.x * 32 + w * 8 + (lane & 7);
+    } else if (A.pair == 1) {   // 2 angles x 16 bins per warp
+        ai = blockIdx.y * FWD_APB + (w >> 1) * 2 + (lane >> 4);
+        j = blockIdx.x * 32 + (w & 1) * 16 + (lane & 15);
+    } else {                    // 1 angle x 32 bins per warp
+        ai = blockIdx.y * FWD_APB + w;
+        j = blockIdx.x * 32 + lane;
+    }
     const int a = A.a0 + ai;
-    const int j = blockIdx.x * 32 + (threadIdx.x & 31);
     const size_t o = (size_t)ai * A.D + j;
     if (!SPLIT) {
         if (a < A.a1 && j < A.D) {
@@ -586,6 +602,7 @@ static FwdArgs make_args(const ctk_geom* g, const float* x, float* y, int a0, in
     A.pad = g->fwd_pad;
     A.split = 1;
     A.done = nullptr;
+    A.pair = g->fwd_pair;
     return A;
 }
 

@@ -96,15 +96,44 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
     // K1 lockstep walk: a warp's 32 adjacent rays spread over at most
     // 31 * sqrt(2) * spacing / h cross-axis pixels; that many zero columns on
     // each side of the staged copies keep every lane's off-range taps in range.
-    const int64_t pad = (int64_t)ceil(31.0 * 1.4142135623730951 * det_spacing / pixel_size) + 3;
+    int64_t pad = (int64_t)ceil(31.0 * 1.4142135623730951 * det_spacing / pixel_size) + 3;
     if ((int64_t)nx + 2 * pad > (1 << 20) || (int64_t)ny + 2 * pad > (1 << 20) ||
         (int64_t)(nx > ny ? nx : ny) * ((nx > ny ? nx : ny) + 2 * pad) >= (1LL << 31))
         return ctk_fail(CTK_ERR_GEOMETRY, "grid too large for the 32.32 walk (%d x %d)", nx, ny);
 
+    // Paired K1 warps (2 adjacent angles x 16 bins): at a common walk row the
+    // two angles' rays of one bin differ by <= dtheta * r * sqrt 2 pixels
+    // (r: the image half-diagonal), so the warp's spread is 15 bins plus that
+    // shift; pair only where the shift is a few pixels, and pad for it.
+    int pair = 0;
+    {
+        double shift = 0.0;
+        for (int a = 0; a + 1 < n_angles; a += 2) {
+            const double sd = sin_tab[a + 1] * cos_tab[a] - cos_tab[a + 1] * sin_tab[a];
+            const double cd = cos_tab[a + 1] * cos_tab[a] + sin_tab[a + 1] * sin_tab[a];
+            const double dth = fabs(atan2(sd, cd));
+            if (dth > shift) shift = dth;
+        }
+        const double rmax = 0.5 * pixel_size * sqrt((double)nx * nx + (double)ny * ny);
+        const double shift_px = shift * rmax * 1.4142135623730951 / pixel_size;
+        // measured (tools/bench_projectors.py): 2 x 16 warps cut c4 / c5 A
+        // by 5% (0.636 -> 0.603, 3.00 -> 2.83 ms) and cost 4-14% on the
+        // shorter rays of c2 / c3; CTK_FWD_PAIR = 0 / 1 / 2 (4 x 8) overrides
+        const char* e = getenv("CTK_FWD_PAIR");
+        const int want = e ? atoi(e) : ((nx < ny ? nx : ny) >= 1024 ? 1 : 0);
+        if (want > 0 && shift_px <= 8.0) {
+            pair = want > 2 ? 2 : want;
+            const int64_t need = (int64_t)ceil((pair == 2 ? 7.0 : 15.0) * 1.4142135623730951 *
+                                                   det_spacing / pixel_size +
+                                               (pair == 2 ? 3.0 : 1.0) * shift_px) + 3;
+            if (need > pad) pad = need;
+        }
+    }
     ctk_geom* g = new ctk_geom();
     memset(g, 0, sizeof(*g));
     g->device = device;
     g->fwd_pad = (int)pad;
+    g->fwd_pair = pair;
     g->nx = nx;
     g->ny = ny;
     g->n_angles = n_angles;

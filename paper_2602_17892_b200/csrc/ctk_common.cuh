@@ -216,7 +216,10 @@ bool ctk_iterate_batch_ok(int k0, int nb, int nvec_cap, int64_t Lx, int64_t Lr);
 // wave.  Deadlock-free: K2 is a programmatic dependent of K1, which triggers
 // at entry, so every K1 CTA is resident or done before any K2 CTA can spin.
 // The counters grow monotonically through a cycle (see wait_k1_groups).
-constexpr int CTK_FWD_APB = 4;                 // angles per K1 CTA (one per warp)
+#ifndef CTK_FWD_APB_N
+#define CTK_FWD_APB_N 4
+#endif
+constexpr int CTK_FWD_APB = CTK_FWD_APB_N;     // angles per K1 CTA (one warp each)
 unsigned* ctk_back_flags(const ctk_geom* g, float* work);
 int ctk_forward_ex(const ctk_geom_t* g, const float* x, float* y, int a0, int a1, const float* b,
                    float* work, bool prestaged, void* stream, unsigned* done_flags = nullptr);

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256) k_stage(const float* __restrict__ x, floa
     }
 }
 
-constexpr int FWD_THREADS = 128;
+constexpr int FWD_THREADS = 32 * CTK_FWD_APB;
 #ifndef CTK_FWD_UNROLL
 #define CTK_FWD_UNROLL 16
 #endif
@@ -416,7 +416,7 @@ __device__ __forceinline__ double forward_ray(const FwdArgs& A, int a, int slot,
 // neighbouring angles' rays cross nearly the same pixels at the same time,
 // so the warps of a CTA share the L1 lines their gathers pull from L2.
 constexpr int FWD_APB = FWD_THREADS / 32;
-static_assert(FWD_APB == CTK_FWD_APB, "K2 chaining counts K1 CTAs per 4-angle group");
+static_assert(FWD_APB == CTK_FWD_APB, "K2 chaining counts K1 CTAs per angle group");
 
 // K2 chaining: after the barrier that orders the CTA's output stores, one
 // release increment of its angle group's counter (see ctk_common.cuh).
@@ -443,7 +443,7 @@ __device__ __forceinline__ unsigned cluster_addr(const void* p, unsigned rank) {
 }
 
 #ifndef CTK_FWD_MINB
-#define CTK_FWD_MINB 8
+#define CTK_FWD_MINB (32 / CTK_FWD_APB_N)
 #endif
 #ifndef CTK_FWD_DYNSMEM
 #define CTK_FWD_DYNSMEM 0

@@ -123,6 +123,7 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
         const int want = e ? atoi(e) : ((nx < ny ? nx : ny) >= 1024 ? 1 : 0);
         if (want > 0 && shift_px <= 8.0) {
             pair = want > 2 ? 2 : want;
+            if (pair == 2 && CTK_FWD_APB != 4) pair = 1;      // 4 x 8 warps assume 4-warp CTAs
             const int64_t need = (int64_t)ceil((pair == 2 ? 7.0 : 15.0) * 1.4142135623730951 *
                                                    det_spacing / pixel_size +
                                                (pair == 2 ? 3.0 : 1.0) * shift_px) + 3;

@@ -301,6 +301,35 @@ struct IterBatchJob {
     int G;
 };
 
+template <int V>
+struct IbVec;
+template <>
+struct IbVec<4> {
+    __device__ static void load(const float* p, float* v) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    }
+    __device__ static void store(float* p, const float* v) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+template <>
+struct IbVec<2> {
+    __device__ static void load(const float* p, float* v) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+        v[0] = t.x; v[1] = t.y;
+    }
+    __device__ static void store(float* p, const float* v) {
+        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    }
+};
+
+// V floats per thread and row, IB_RB rows loaded per batch.
+#ifndef CTK_IB_RB
+#define CTK_IB_RB 8
+#endif
+constexpr int IB_RB = CTK_IB_RB;
+template <int V>
 __global__ void __launch_bounds__(IB_T) k_iter_batch(IterBatchJob j0, IterBatchJob j1,
                                                      const double* __restrict__ y, int ystride,
                                                      int k0, int nb) {
@@ -317,61 +346,68 @@ __global__ void __launch_bounds__(IB_T) k_iter_batch(IterBatchJob j0, IterBatchJ
         cy[j][b] = (b < nb && j < k0 + b) ? sgn * y[(size_t)b * ystride + j] : 0.0;
     }
     __syncthreads();
-    const int64_t L4 = J.L >> 2, ld4 = J.ld >> 2;
-    const float4* X4 = reinterpret_cast<const float4*>(J.X);
+    const int64_t LV = J.L / V;
     double nrm[IB_NB];
 #pragma unroll
     for (int b = 0; b < IB_NB; ++b) nrm[b] = 0.0;
-    for (int64_t i = (int64_t)bid * IB_T + threadIdx.x; i < L4; i += (int64_t)J.G * IB_T) {
-        double a[IB_NB][4];
+    for (int64_t i = (int64_t)bid * IB_T + threadIdx.x; i < LV; i += (int64_t)J.G * IB_T) {
+        double a[IB_NB][V];
         {
-            double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
-            if (J.base) {
-                const float4 v = reinterpret_cast<const float4*>(J.base)[i];
-                b0 = v.x; b1 = v.y; b2 = v.z; b3 = v.w;
-            }
+            float bv[V];
 #pragma unroll
-            for (int b = 0; b < IB_NB; ++b) {
-                a[b][0] = b0; a[b][1] = b1; a[b][2] = b2; a[b][3] = b3;
-            }
+            for (int e = 0; e < V; ++e) bv[e] = 0.f;
+            if (J.base) IbVec<V>::load(J.base + i * V, bv);
+#pragma unroll
+            for (int b = 0; b < IB_NB; ++b)
+#pragma unroll
+                for (int e = 0; e < V; ++e) a[b][e] = bv[e];
         }
-        const float4* col = X4 + i;
+        const float* col = J.X + i * V;
         int j = 0;
-        for (; j + 4 <= kmax; j += 4) {
-            float4 w[4];
+        // IB_RB rows' loads in flight per thread: the pass is latency-bound
+        // (bytes in flight per SM), not fp64- or conversion-bound
+        for (; j + IB_RB <= kmax; j += IB_RB) {
+            float w[IB_RB][V];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) w[q] = __ldg(col + (size_t)(j + q) * ld4);
+            for (int q = 0; q < IB_RB; ++q) IbVec<V>::load(col + (size_t)(j + q) * J.ld, w[q]);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const double wx = w[q].x, wy = w[q].y, wz = w[q].z, ww = w[q].w;
+            for (int q = 0; q < IB_RB; ++q) {
+                double wd[V];
+#pragma unroll
+                for (int e = 0; e < V; ++e) wd[e] = w[q][e];
 #pragma unroll
                 for (int b = 0; b < IB_NB; ++b) {
                     const double c = cy[j + q][b];
-                    a[b][0] = fma(c, wx, a[b][0]); a[b][1] = fma(c, wy, a[b][1]);
-                    a[b][2] = fma(c, wz, a[b][2]); a[b][3] = fma(c, ww, a[b][3]);
+#pragma unroll
+                    for (int e = 0; e < V; ++e) a[b][e] = fma(c, wd[e], a[b][e]);
                 }
             }
         }
         for (; j < kmax; ++j) {
-            const float4 w = __ldg(col + (size_t)j * ld4);
-            const double wx = w.x, wy = w.y, wz = w.z, ww = w.w;
+            float w[V];
+            IbVec<V>::load(col + (size_t)j * J.ld, w);
+            double wd[V];
+#pragma unroll
+            for (int e = 0; e < V; ++e) wd[e] = w[e];
 #pragma unroll
             for (int b = 0; b < IB_NB; ++b) {
                 const double c = cy[j][b];
-                a[b][0] = fma(c, wx, a[b][0]); a[b][1] = fma(c, wy, a[b][1]);
-                a[b][2] = fma(c, wz, a[b][2]); a[b][3] = fma(c, ww, a[b][3]);
+#pragma unroll
+                for (int e = 0; e < V; ++e) a[b][e] = fma(c, wd[e], a[b][e]);
             }
         }
 #pragma unroll
         for (int b = 0; b < IB_NB; ++b) {
-            const float4 o = make_float4((float)a[b][0], (float)a[b][1], (float)a[b][2], (float)a[b][3]);
-            if (b == nb - 1 && J.dst) reinterpret_cast<float4*>(J.dst)[i] = o;
-            nrm[b] = fma((double)o.x, (double)o.x, nrm[b]); nrm[b] = fma((double)o.y, (double)o.y, nrm[b]);
-            nrm[b] = fma((double)o.z, (double)o.z, nrm[b]); nrm[b] = fma((double)o.w, (double)o.w, nrm[b]);
+            float o[V];
+#pragma unroll
+            for (int e = 0; e < V; ++e) o[e] = (float)a[b][e];
+            if (b == nb - 1 && J.dst) IbVec<V>::store(J.dst + i * V, o);
+#pragma unroll
+            for (int e = 0; e < V; ++e) nrm[b] = fma((double)o[e], (double)o[e], nrm[b]);
         }
     }
-    if (bid == J.G - 1 && threadIdx.x < 32) {                  // scalar tail L % 4
-        for (int64_t i = (L4 << 2) + threadIdx.x; i < J.L; i += 32) {
+    if (bid == J.G - 1 && threadIdx.x < 32) {                  // scalar tail L % V
+        for (int64_t i = LV * V + threadIdx.x; i < J.L; i += 32) {
             double a[IB_NB];
             const double b0 = J.base ? (double)J.base[i] : 0.0;
 #pragma unroll
@@ -1936,8 +1972,16 @@ extern "C" int ctk_iterate_batch(const float* X, int64_t ldx, const float* x0, f
     IterBatchJob j1 = {AX, ldax, d0, r, Lr, norms, s.partial + (size_t)IB_NB * j0.G, s.ticket + 1,
                        iter_batch_ctas(Lr)};
     const int ph = ctk_prof_open(3, ctk_stream(stream));
-    k_iter_batch<<<(unsigned)(j0.G + j1.G), IB_T, 0, ctk_stream(stream)>>>(j0, j1, y, ystride, k0,
-                                                                         nb);
+    static const int ibv = [] {                 // floats per thread and row (tuning override)
+        const char* e = getenv("CTK_IB_V");
+        return e && atoi(e) == 2 ? 2 : 4;
+    }();
+    if (ibv == 4)
+        k_iter_batch<4><<<(unsigned)(j0.G + j1.G), IB_T, 0, ctk_stream(stream)>>>(j0, j1, y, ystride,
+                                                                                k0, nb);
+    else
+        k_iter_batch<2><<<(unsigned)(j0.G + j1.G), IB_T, 0, ctk_stream(stream)>>>(j0, j1, y, ystride,
+                                                                                k0, nb);
     CTK_LAUNCH_CHECK("k_iter_batch");
     ctk_prof_close(ph, ctk_stream(stream));
     return CTK_OK;

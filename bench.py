@@ -491,6 +491,8 @@ def main():
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
                 "launches_timed": n_l, "mean_launch_ms": round(ms_l, 5),
                 "share_of_step": round(shares[dom] / max(prof_total_ms, 1e-9), 4),
+                "binding": traffic_from_profiles(spec, dom, "binding") or
+                "gathers served on chip (frac > 1 on algorithmic gather bytes); see profiles/",
                 "measured": "CUDA events around each launch on its stream over "
                             f"{max(1, min(args.steps, 3))} profiled single-slice solves run "
                             "after the timed steps (same workload, L2 flushed per solve)"}
@@ -727,13 +729,13 @@ def main_sharded(args, spec, world, rank, local, torch, dist, stream):
         dist.destroy_process_group()
 
 
-def traffic_from_profiles(spec, dom):
-    """dram bytes per launch of the dominant kernel from a committed ncu capture."""
+def traffic_from_profiles(spec, dom, field="dram_bytes_per_launch"):
+    """A field of the dominant kernel's committed ncu capture (profiles/)."""
     path = os.path.join(ROOT, "profiles", f"ncu_{spec.name}.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(dom, {}).get("dram_bytes_per_launch")
+        return d.get(dom, {}).get(field)
     except Exception:
         return None
 

@@ -50,13 +50,43 @@ struct BackArgs {
     const ctk_xchg_args* xc;   // optional (device copy): push the tile to its owner rank
     unsigned* ready;      // optional: K1's finished-CTA counters per 4-angle group (chaining)
     unsigned ready_target;  // K1 CTAs per group (bin blocks) x this step's epoch
+    const float2* pairs;  // MODE 2: (p, d) per bin, row a at pairs + (a - a0) * Dp + P
+    int Dp, P;
 };
 
-// Sinogram loads.  Chained (A.ready): u is written by the still-running K1,
-// so the read-only (.nc) path is not allowed -- L2-coherent loads after the
-// acquire instead.
-__device__ __forceinline__ float ld_u(const BackArgs& A, const float* p) {
-    return A.ready ? __ldcg(p) : __ldg(p);
+// MODE 2 pre-pass (images >= 512^2): the sinogram as (p, d) pairs per bin,
+// bins b in [-P, D + P) -- exactly the values stage_windows builds per window
+// (v0 = u[b] or 0 outside the detector, v1 = the reference's second tap with
+// the i0 == -1 quirk, d = v1 - v0, p = v0 - d) -- so K2's per-chunk staging
+// becomes coalesced 8-byte copies instead of two loads, three shuffles and
+// the quirk / bounds logic per angle and lane (~23% of K2's instructions at
+// c5 went to staging).  Bitwise the same windows, hence the same B.
+__global__ void __launch_bounds__(256) k_pairs(const float* __restrict__ u, float2* __restrict__ pr,
+                                               int rows, int D, int P) {
+    ctk_pdl_trigger();
+    const int Dp = D + 2 * P;
+    const int64_t total = (int64_t)rows * Dp;
+    const int q1 = D > 1 ? 1 : 0;
+    ctk_pdl_wait();                                    // u comes from the previous kernel
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int a = (int)(idx / Dp), b = (int)(idx - (int64_t)a * Dp) - P;
+        const float* row = u + (size_t)a * D;
+        const float v0 = (b >= 0 && b < D) ? __ldg(row + b) : 0.f;
+        const int b1 = b == -1 ? q1 : b + 1;
+        const float v1 = (b >= -1 && b + 1 < D) ? __ldg(row + b1) : 0.f;
+        const float d = v1 - v0;
+        pr[idx] = make_float2(v0 - d, d);
+    }
+}
+
+// Sinogram loads.  CHAINED: u is written by the still-running K1, so the
+// read-only (.nc) path is not allowed -- L2-coherent loads after the acquire
+// instead.  (A compile-time choice: a run-time branch doubled the staging
+// code and its branches.)
+template <bool CHAINED>
+__device__ __forceinline__ float ld_u(const float* p) {
+    return CHAINED ? __ldcg(p) : __ldg(p);
 }
 
 // K2 chaining (ctk_common.cuh): wait until the K1 groups holding angles
@@ -87,6 +117,7 @@ __device__ __forceinline__ void stage_out(const BackArgs& A, int ix, int iy, flo
 // issued before the first use (one L2 round trip per chunk instead of one
 // per strided element), v1 = v0 of the next bin by a lane shuffle except at
 // the quirk bin b == -1.  Wider windows take the element loop.
+template <bool CHAINED>
 __device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, const int* s_w0,
                                               int ac, int na, int tx, int ty) {
     const int D = A.D, wmax = A.wmax;
@@ -101,8 +132,8 @@ __device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, co
             if (ai < na) {
                 const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
                 const int b = s_w0[ai] + tx, b2 = b + 32;
-                if (b >= 0 && b < D) va[j] = ld_u(A, row + b);
-                if (b2 >= 0 && b2 < D && tx + 32 <= wmax) vb[j] = ld_u(A, row + b2);
+                if (b >= 0 && b < D) va[j] = ld_u<CHAINED>(row + b);
+                if (b2 >= 0 && b2 < D && tx + 32 <= wmax) vb[j] = ld_u<CHAINED>(row + b2);
             }
         }
 #pragma unroll
@@ -115,8 +146,8 @@ __device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, co
             const int b = s_w0[ai] + tx;
             float v1a = tx < 31 ? up_a : b_0, v1b = up_b;
             const float* row = A.u + (size_t)(ac + ai - A.a0) * D;
-            if (b == -1) v1a = ld_u(A, row + q1);
-            if (b + 32 == -1) v1b = ld_u(A, row + q1);
+            if (b == -1) v1a = ld_u<CHAINED>(row + q1);
+            if (b + 32 == -1) v1b = ld_u<CHAINED>(row + q1);
             float2* dst = win + ai * wmax;
             float d = v1a - va[j];
             dst[tx] = make_float2(va[j] - d, d);
@@ -133,11 +164,52 @@ __device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, co
         float2* dst = win + ai * wmax;
         for (int i = tx; i < wmax; i += BTX) {
             const int b = w0 + i;
-            const float v0 = (b >= 0 && b < D) ? ld_u(A, row + b) : 0.f;
+            const float v0 = (b >= 0 && b < D) ? ld_u<CHAINED>(row + b) : 0.f;
             const int b1 = b == -1 ? q1 : b + 1;
-            const float v1 = (b >= -1 && b + 1 < D) ? ld_u(A, row + b1) : 0.f;
+            const float v1 = (b >= -1 && b + 1 < D) ? ld_u<CHAINED>(row + b1) : 0.f;
             const float d = v1 - v0;
             dst[i] = make_float2(v0 - d, d);
+        }
+    }
+}
+
+// MODE 2 staging: the windows straight from the pair sinogram (bins outside
+// [-P, D + P) are zero pairs, as stage_windows would build them).
+__device__ __forceinline__ void stage_pairs(const BackArgs& A, float2* win, const int* s_w0,
+                                            int ac, int na, int tx, int ty) {
+    const int wmax = A.wmax, lo = -A.P, hi = A.D + A.P;
+    const float2 z = make_float2(0.f, 0.f);
+    if (wmax <= 64) {
+        constexpr int NJ = BCA / BROWS;            // angles per warp
+        float2 va[NJ], vb[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {             // all loads before the first store
+            const int ai = ty + j * BROWS;
+            va[j] = vb[j] = z;
+            if (ai < na) {
+                const float2* row = A.pairs + (size_t)(ac + ai - A.a0) * A.Dp + A.P;
+                const int b = s_w0[ai] + tx, b2 = b + 32;
+                if (tx < wmax && b >= lo && b < hi) va[j] = __ldg(row + b);
+                if (tx + 32 < wmax && b2 >= lo && b2 < hi) vb[j] = __ldg(row + b2);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int ai = ty + j * BROWS;
+            if (ai >= na) break;                   // warp-uniform
+            float2* dst = win + ai * wmax;
+            if (tx < wmax) dst[tx] = va[j];
+            if (tx + 32 < wmax) dst[tx + 32] = vb[j];
+        }
+        return;
+    }
+    for (int ai = ty; ai < na; ai += BROWS) {
+        const float2* row = A.pairs + (size_t)(ac + ai - A.a0) * A.Dp + A.P;
+        const int w0 = s_w0[ai];
+        float2* dst = win + ai * wmax;
+        for (int i = tx; i < wmax; i += BTX) {
+            const int b = w0 + i;
+            dst[i] = (b >= lo && b < hi) ? __ldg(row + b) : z;
         }
     }
 }
@@ -151,7 +223,9 @@ __device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, co
 #define CTK_BACK_MINB4 5
 #endif
 
-template <int PPT, bool SPLIT>                      // pixels (rows) per thread
+// MODE 0: plain, 1: chained after K1 (counters), 2: windows from the pair
+// sinogram (k_pairs)
+template <int PPT, bool SPLIT, int MODE>            // pixels (rows) per thread
 __global__ void __launch_bounds__(BTHREADS, PPT == 4 ? CTK_BACK_MINB4 : 6) k_back(BackArgs A) {
     constexpr int BTY = BROWS * PPT;
     extern __shared__ float2 win[];                // [BCA][wmax] (p, d)
@@ -196,9 +270,10 @@ __global__ void __launch_bounds__(BTHREADS, PPT == 4 ? CTK_BACK_MINB4 : 6) k_bac
                                    (int)(unsigned)__cvta_generic_to_shared(win + tid * wmax));
         }
         __syncthreads();
-        if (A.ready) wait_k1_groups(A, ac, na, tid);   // u: this chunk's K1 rows
-        else ctk_pdl_wait();                       // u comes from the previous kernel
-        stage_windows(A, win, s_w0, ac, na, tx, ty);
+        if (MODE == 1) wait_k1_groups(A, ac, na, tid);   // u: this chunk's K1 rows
+        else ctk_pdl_wait();                       // u / pairs come from the previous kernel
+        if (MODE == 2) stage_pairs(A, win, s_w0, ac, na, tx, ty);
+        else stage_windows<MODE == 1>(A, win, s_w0, ac, na, tx, ty);
         __syncthreads();
         float sp[PPT];
 #pragma unroll
@@ -409,6 +484,25 @@ static int64_t back_flag_floats(const ctk_geom* g) {
 
 static int64_t back_ticket_floats(const ctk_geom* g) { return (back_tiles(g) + 15) / 16 * 16; }
 
+// Pair sinogram (MODE 2): measured B per apply with / without the pre-pass:
+// c5 2.703 / 2.742 ms, c4 0.587 / 0.582, c3 0.095 / 0.092 -- so images of
+// >= 2048^2 only (CTK_BACK_PAIRS=0 / 1 overrides).  P = 2 pad bins each side
+// cover the i0 == -1 quirk bin.
+constexpr int PAIR_PAD = 2;
+static bool back_pairs_on(const ctk_geom* g) {
+    static const int force = [] {
+        const char* e = getenv("CTK_BACK_PAIRS");
+        return e ? atoi(e) : -1;
+    }();
+    if (g->back_ppt != 4) return false;
+    if (force >= 0) return force != 0;
+    return (int64_t)g->nx * g->ny >= 2048LL * 2048;
+}
+
+static int64_t back_pair_floats(const ctk_geom* g, int a0, int a1) {
+    return back_pairs_on(g) ? 2 * (int64_t)(a1 - a0) * (g->det_count + 2 * PAIR_PAD) : 0;
+}
+
 unsigned* ctk_back_flags(const ctk_geom* g, float* work) {
     return work ? reinterpret_cast<unsigned*>(work) : nullptr;
 }
@@ -416,7 +510,8 @@ unsigned* ctk_back_flags(const ctk_geom* g, float* work) {
 extern "C" int64_t ctk_back_work_floats(const ctk_geom_t* g, int a0, int a1) {
     if (!g || a0 < 0 || a1 > g->n_angles || a0 >= a1) return 0;
     const int S = back_splits(g, a0, a1);
-    return back_flag_floats(g) + back_ticket_floats(g) + (S > 1 ? (int64_t)S * g->nx * g->ny : 0);
+    return back_flag_floats(g) + back_ticket_floats(g) +
+           (S > 1 ? ((int64_t)S * g->nx * g->ny + 3) / 4 * 4 : 0) + back_pair_floats(g, a0, a1);
 }
 
 extern "C" int ctk_back(const ctk_geom_t* g, const float* u, float* x, int a0, int a1,
@@ -470,6 +565,13 @@ int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
     A.part = S > 1 ? work + back_flag_floats(g) + back_ticket_floats(g) : nullptr;
     A.ready = k1_epoch ? ctk_back_flags(g, work) : nullptr;
     A.ready_target = (unsigned)((g->det_count + 31) / 32) * k1_epoch;
+    const bool pairs = !k1_epoch && work && back_pairs_on(g);
+    A.P = PAIR_PAD;
+    A.Dp = g->det_count + 2 * PAIR_PAD;
+    A.pairs = pairs ? reinterpret_cast<const float2*>(
+                          work + back_flag_floats(g) + back_ticket_floats(g) +
+                          (S > 1 ? ((int64_t)S * g->nx * g->ny + 3) / 4 * 4 : 0))
+                    : nullptr;
     A.bp = g->d_bp;
     A.u = u;
     A.x0 = x0;
@@ -498,11 +600,32 @@ int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
     const int ppt = g->back_ppt;
     size_t smem = (size_t)BCA * g->back_wmax * sizeof(float2);
     void (*kern)(BackArgs) =
-        S > 1 ? (ppt == 4 ? k_back<4, true> : ppt == 1 ? k_back<1, true> : k_back<2, true>)
-              : (ppt == 4 ? k_back<4, false> : ppt == 1 ? k_back<1, false> : k_back<2, false>);
+        k1_epoch
+            ? (S > 1 ? (ppt == 4 ? k_back<4, true, 1> : ppt == 1 ? k_back<1, true, 1>
+                                                      : k_back<2, true, 1>)
+                     : (ppt == 4 ? k_back<4, false, 1> : ppt == 1 ? k_back<1, false, 1>
+                                                       : k_back<2, false, 1>))
+        : pairs
+            ? (S > 1 ? (ppt == 4 ? k_back<4, true, 2> : ppt == 1 ? k_back<1, true, 2>
+                                                      : k_back<2, true, 2>)
+                     : (ppt == 4 ? k_back<4, false, 2> : ppt == 1 ? k_back<1, false, 2>
+                                                       : k_back<2, false, 2>))
+            : (S > 1 ? (ppt == 4 ? k_back<4, true, 0> : ppt == 1 ? k_back<1, true, 0>
+                                                      : k_back<2, true, 0>)
+                     : (ppt == 4 ? k_back<4, false, 0> : ppt == 1 ? k_back<1, false, 0>
+                                                       : k_back<2, false, 0>));
     if (smem > 48 * 1024)
         CTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int ph = ctk_prof_open(1, st);
+    if (pairs) {
+        const int64_t total = (int64_t)(a1 - a0) * A.Dp;
+        int blocks = (int)((total + 255) / 256);
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        CTK_CUDA(ctk_launch_pdl(k_pairs, dim3(blocks), dim3(256), 0, st, dim3(1, 1, 1), u,
+                                const_cast<float2*>(A.pairs), a1 - a0, (int)g->det_count,
+                                (int)PAIR_PAD));
+        ctk_count_launch();
+    }
     CTK_CUDA(ctk_launch_pdl(kern, grid, block, smem, st, dim3(1, 1, 1), A));
     ctk_count_launch();
     ctk_prof_close(ph, st);

@@ -1142,7 +1142,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
     double* P2 = P1 + (size_t)(nb + 1) * gridDim.x;          // [nb + 1][G]
     double* P3 = P2 + (size_t)(nb + 1) * gridDim.x;          // [G]
     __shared__ double s_n2;
-    bool need_norm = true, prescaled = false;
+    bool need_norm = true, prescaled = false, staged = false;
     double nrm = 0.0;
     if (gram && passes == 2) {
         // Gram-corrected CGS2 (see gram_coefs): one sweep, one reduction
@@ -1380,9 +1380,13 @@ __device__ __forceinline__ void ts_dots(const float* tile, int tw, int nrows, in
 // the rows into ST / tw groups whose fp64 partials meet in red[] and are
 // summed in group order.  The rounded result goes to dst (global) and, when
 // keep, back into the tile's vector row.  Returns this thread's ||out||^2 part.
+// sdp != NULL: also write the result's K1 staged copies (element e0 + e of
+// the image: P row-major, PT transposed -- 4-byte stores one row apart, which
+// L2 merges into whole sectors before they reach HBM).
 __device__ __forceinline__ double ts_update(float* tile, int tw, int nb, const double* c, int cn,
                                             float* dst, bool keep, double* red,
-                                            double scale = 1.0) {
+                                            double scale = 1.0,
+                                            const ctk_stage_dst* sdp = nullptr, int64_t e0 = 0) {
     const int ng = ST / tw;
     const int g = threadIdx.x / tw, e = threadIdx.x - g * tw;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;       // four independent chains
@@ -1407,6 +1411,12 @@ __device__ __forceinline__ double ts_update(float* tile, int tw, int nb, const d
         dst[e] = o;
         if (keep) tile[(size_t)nb * tw + e] = o;
         nrm = (double)o * (double)o;
+        if (sdp) {
+            const int64_t idx = e0 + e;
+            const int iy = (int)(idx / sdp->nx), ix = (int)(idx - (int64_t)iy * sdp->nx);
+            sdp->P[(size_t)iy * (sdp->nx + 2 * sdp->pad) + ix + sdp->pad] = o;
+            sdp->PT[(size_t)ix * (sdp->ny + 2 * sdp->pad) + iy + sdp->pad] = o;
+        }
     }
     __syncthreads();
     return nrm;
@@ -1467,7 +1477,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
     // the kernel's first) uses slot g % TS_NBUF at mbarrier phase (g / TS_NBUF) & 1.
     int gbase = 0;
     auto sweep = [&](int mode, const CUtensorMap* vmap, const double* coef, double* P,
-                     double scale) -> double {
+                     double scale, const ctk_stage_dst* stage = nullptr) -> double {
         double acc[TS_RPW], gacc[TS_RPW];
 #pragma unroll
         for (int r = 0; r < TS_RPW; ++r) acc[r] = gacc[r] = 0.0;
@@ -1486,7 +1496,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
             } else if (mode == 3) {
                 ts_dots2(tile, tw, nb + 1, nb, nb - 1, cn, acc, gacc);
             } else {
-                nrm += ts_update(tile, tw, nb, coef, cn, wnext + e0, mode == 1, red, scale);
+                nrm += ts_update(tile, tw, nb, coef, cn, wnext + e0, mode == 1, red, scale, stage, e0);
                 if (mode == 1) ts_dots(tile, tw, nb, nb, cn, acc);
             }
             __syncthreads();                     // everyone is done with slot b
@@ -1515,7 +1525,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
     };
 
     __shared__ double s_n2;
-    bool need_norm = true, prescaled = false;
+    bool need_norm = true, prescaled = false, staged = false;
     double nrm = 0.0;
     if (gram && passes == 2) {
         // Gram-corrected CGS2 (see gram_coefs): two sweeps, one reduction --
@@ -1529,10 +1539,15 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
         gram_coefs(gram, gram, GRAM_LD, false, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
         const double est = s_est, a = h1[nb];
         if (a > 0.0 && est > 1e-8 * a) {
-            sweep(2, &tm.q, cc, nullptr, 1.0 / sqrt(est));
+            // the final scale is known here: the K1 staged copies of w_{k+1}
+            // are written in the same sweep (no re-read, no extra barrier),
+            // unless the step breaks down (hk is only known after the sweep)
+            const bool fold = sd.P && sqrt(est) > 1e-14 * sqrt(a);
+            sweep(2, &tm.q, cc, nullptr, 1.0 / sqrt(est), fold ? &sd : nullptr);
             if (threadIdx.x == 0) s_n2 = est;
             need_norm = false;
             prescaled = true;
+            staged = fold;
         } else {
             nrm = sweep(2, &tm.q, cc, nullptr, 1.0);
         }
@@ -1567,14 +1582,16 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
         grid.sync();
         if (threadIdx.x < 32) all_reduce_rows(P3, 1, &s_n2);
         __syncthreads();
-    } else if (sd.P) {
+    } else if (sd.P && !staged) {
         grid.sync();                 // the staging tiles below span other CTAs' rows
     }
     const double hk = sqrt(s_n2);
     const double qn = sqrt(h1[nb]);
     const bool broke = hk <= 1e-14 * qn;                     // BREAKDOWN_RTOL, arnoldi.py:17,80
     const float sc = broke ? 0.f : prescaled ? 1.f : (float)(1.0 / hk);
-    if (!sd.P) {
+    if (staged) {
+        // w_{k+1} and its staged copies were written by the update sweep
+    } else if (!sd.P) {
         if (!prescaled && nt > 0) {
             const int64_t e0 = t0 * tw, e1 = min(L, t1 * tw);
             for (int64_t i = e0 + threadIdx.x; i < e1; i += ST) wnext[i] *= sc;

@@ -904,7 +904,8 @@ __device__ __forceinline__ float gram_entry(const float* Es, int es_ld, bool es_
     return es_smem ? *p : __ldcg(p);
 }
 
-__device__ void gram_coefs(float* gram, const float* Es, int es_ld, bool es_smem, int k,
+template <bool ES_SMEM>
+__device__ void gram_coefs(float* gram, const float* Es, int es_ld, int k,
                            const double* h1, const double* g, double* h2, double* cc,
                            double* red, double* s_est) {
     // four threads per row (nb <= 128 rows on 512 threads): each sums a
@@ -923,9 +924,32 @@ __device__ void gram_coefs(float* gram, const float* Es, int es_ld, bool es_smem
     }
     __syncthreads();
     const int i = threadIdx.x / TPR, sub = threadIdx.x % TPR;
+    // E in global memory (streamed path): this thread's <= GRAM_LD / TPR
+    // entries of row i go to registers with all loads issued before the first
+    // use -- one L2 round trip for both products instead of one per entry
+    // (4-9 -> 2-3 us per step; same summation order as the shared-memory
+    // loop, j = sub, sub + TPR, ...)
+    constexpr int EMAX = GRAM_LD / TPR;
+    float er[ES_SMEM ? 1 : EMAX];
+    if (!ES_SMEM) {
+#pragma unroll
+        for (int q = 0; q < EMAX; ++q) {
+            const int j = sub + q * TPR;
+            er[q] = (i < nb && j < nb) ? gram_entry(Es, es_ld, false, i, j, k, gf) : 0.f;
+        }
+    }
     float t = 0.f;
-    if (i < nb)
-        for (int j = sub; j < nb; j += TPR) t = fmaf(gram_entry(Es, es_ld, es_smem, i, j, k, gf), h1f[j], t);
+    if (ES_SMEM) {
+        if (i < nb)
+            for (int j = sub; j < nb; j += TPR)
+                t = fmaf(gram_entry(Es, es_ld, true, i, j, k, gf), h1f[j], t);
+    } else if (i < nb) {
+#pragma unroll
+        for (int q = 0; q < EMAX; ++q) {
+            const int j = sub + q * TPR;
+            if (j < nb) t = fmaf(er[q], h1f[j], t);
+        }
+    }
     t += __shfl_xor_sync(0xffffffffu, t, 1);
     t += __shfl_xor_sync(0xffffffffu, t, 2);
     if (i < nb && sub == 0) {
@@ -940,8 +964,17 @@ __device__ void gram_coefs(float* gram, const float* Es, int es_ld, bool es_smem
         }
     __syncthreads();
     float u = 0.f;
-    if (i < nb)
-        for (int j = sub; j < nb; j += TPR) u = fmaf(gram_entry(Es, es_ld, es_smem, i, j, k, gf), cf[j], u);
+    if (ES_SMEM) {
+        if (i < nb)
+            for (int j = sub; j < nb; j += TPR)
+                u = fmaf(gram_entry(Es, es_ld, true, i, j, k, gf), cf[j], u);
+    } else if (i < nb) {
+#pragma unroll
+        for (int q = 0; q < EMAX; ++q) {
+            const int j = sub + q * TPR;
+            if (j < nb) u = fmaf(er[q], cf[j], u);
+        }
+    }
     u += __shfl_xor_sync(0xffffffffu, u, 1);
     u += __shfl_xor_sync(0xffffffffu, u, 2);
     // this row's share of  c.(E c) + c.c - 2 c.h1  (the last two in fp64)
@@ -1156,7 +1189,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
         __syncthreads();
         GS_STAMP(6);
         __shared__ double s_est;
-        gram_coefs(gram, Es, es_n, true, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
+        gram_coefs<true>(gram, Es, es_n, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
         GS_STAMP(5);
         const double est = s_est, a = h1[nb];
         if (a > 0.0 && est > 1e-8 * a) {
@@ -1435,6 +1468,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
                                                      double* hm, int stat_off, float* gram,
                                                      const __grid_constant__ TsMaps tm) {
     cg::grid_group grid = cg::this_grid();
+    GS_STAMP(0);
     ctk_pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nb = k + 1;
@@ -1458,6 +1492,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
     }
     __syncthreads();
     ctk_pdl_wait();                  // q (and, transitively, the basis) from the previous kernels
+    GS_STAMP(1);
 
     const int64_t ntiles = (L + tw - 1) / tw;
     const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
@@ -1532,11 +1567,15 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
         // h1, ||q||^2 and <W_j, w_k> in one read of the basis, then
         // q2 = (q - W c) / ||q2|| straight into row k+1
         sweep(3, &tm.q, nullptr, P1, 1.0);
+        GS_STAMP(2);
         grid.sync();
+        GS_STAMP(3);
         all_reduce_rows(P1, 2 * nb + 1, h1);
         __syncthreads();
+        GS_STAMP(4);
         __shared__ double s_est;
-        gram_coefs(gram, gram, GRAM_LD, false, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
+        gram_coefs<false>(gram, gram, GRAM_LD, k, h1, h1 + nb + 1, h2, cc, red, &s_est);
+        GS_STAMP(5);
         const double est = s_est, a = h1[nb];
         if (a > 0.0 && est > 1e-8 * a) {
             // the final scale is known here: the K1 staged copies of w_{k+1}
@@ -1569,6 +1608,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
         }
         nrm = sweep(2, vfin, cfin, nullptr, 1.0);            // q2 -> wnext, ||q2||^2
     }
+    GS_STAMP(6);
     if (need_norm) {
         nrm = warp_sum(nrm);
         if (lane == 0) red[warp] = nrm;
@@ -1641,6 +1681,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
             }
         }
     }
+    GS_STAMP(7);
 }
 
 }  // namespace ctk

@@ -1319,28 +1319,44 @@ struct TsRing {
     __device__ unsigned bar(int b) const { return bar0 + 8u * (unsigned)b; }
 };
 
-// Thread 0: queue tile e0 of basis rows 0..nb-1 (one 2-D tensor box of
-// tw x nb floats) plus the same tile of the vector (a tw x 1 box, row nb of
-// the slot) into ring slot b.  Out-of-range columns of the last tile are
-// zero-filled by the TMA unit and still count toward the transaction bytes.
+// Queue tile e0 into ring slot b: thread 0 (part 0) the basis rows 0..nb-1
+// (one 2-D tensor box of tw x nb floats), thread 32 (part 1) the same tile of
+// the vector (a tw x 1 box, row nb of the slot).  Each issuer arrives on the
+// slot's mbarrier (count 2) with its own transaction bytes: issuing a tensor
+// copy costs the issuing thread ~90 ns, and the issuing warp is on the
+// CTA's critical path (every tile ends in a barrier), so the two copies go
+// out from two warps side by side.  Out-of-range columns of the last tile
+// are zero-filled by the TMA unit and still count toward the bytes.
+__device__ __forceinline__ bool ts_issuer() { return (threadIdx.x & ~32u) == 0; }
+
 __device__ __forceinline__ void ts_issue(const TsRing& R, int b, int tw, int nb,
-                                         const CUtensorMap* tmW, const CUtensorMap* tmV,
-                                         int64_t e0) {
+                                         const CUtensorMap* tmW, const float* vsrc,
+                                         int64_t e0, int64_t L) {
     const unsigned bar = R.bar(b);
-    const unsigned bytes = (unsigned)(tw * (nb + 1) * 4);
     float* dst = R.buf(b);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tmW)), "r"((int)e0), "r"(0), "r"(bar)
-        : "memory");
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst + (size_t)nb * tw)),
-        "l"(reinterpret_cast<uint64_t>(tmV)), "r"((int)e0), "r"(0), "r"(bar)
-        : "memory");
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((unsigned)(tw * nb * 4))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+            "l"(reinterpret_cast<uint64_t>(tmW)), "r"((int)e0), "r"(0), "r"(bar)
+            : "memory");
+    } else {
+        // the vector tile is contiguous: a plain bulk copy (no tensor box;
+        // columns past L stay unwritten and are never read)
+        const int64_t left = L - e0;
+        const unsigned bytes = (unsigned)((left < tw ? left : (int64_t)tw) * 4);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(smem_u32(dst + (size_t)nb * tw)),
+            "l"(vsrc + e0), "r"(bytes), "r"(bar)
+            : "memory");
+    }
 }
 
 // Gram variant: also gacc[r] += <row (warp + SW r), row grow> for rows < grow + 1.
@@ -1419,7 +1435,8 @@ __device__ __forceinline__ void ts_dots(const float* tile, int tw, int nrows, in
 __device__ __forceinline__ double ts_update(float* tile, int tw, int nb, const double* c, int cn,
                                             float* dst, bool keep, double* red,
                                             double scale = 1.0,
-                                            const ctk_stage_dst* sdp = nullptr, int64_t e0 = 0) {
+                                            const ctk_stage_dst* sdp = nullptr, int iy0 = 0,
+                                            int ix0 = 0) {
     const int ng = ST / tw;
     const int g = threadIdx.x / tw, e = threadIdx.x - g * tw;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;       // four independent chains
@@ -1445,8 +1462,11 @@ __device__ __forceinline__ double ts_update(float* tile, int tw, int nb, const d
         if (keep) tile[(size_t)nb * tw + e] = o;
         nrm = (double)o * (double)o;
         if (sdp) {
-            const int64_t idx = e0 + e;
-            const int iy = (int)(idx / sdp->nx), ix = (int)(idx - (int64_t)iy * sdp->nx);
+            int iy = iy0, ix = ix0 + e;          // element (iy0, ix0) + e of the image
+            while (ix >= sdp->nx) {
+                ix -= sdp->nx;
+                ++iy;
+            }
             sdp->P[(size_t)iy * (sdp->nx + 2 * sdp->pad) + ix + sdp->pad] = o;
             sdp->PT[(size_t)ix * (sdp->ny + 2 * sdp->pad) + iy + sdp->pad] = o;
         }
@@ -1457,13 +1477,12 @@ __device__ __forceinline__ double ts_update(float* tile, int tw, int nb, const d
 
 struct TsMaps {
     CUtensorMap W;          // rows 0..k of the basis, box tw x (k+1)
-    CUtensorMap q;          // the input vector, box tw x 1
-    CUtensorMap wn;         // row k+1 (q1 after sweep B), box tw x 1
 };
 
+template <int TW>                   // tile width (floats): compile-time index arithmetic
 __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k, int64_t L,
                                                      const float* __restrict__ q, int passes,
-                                                     int tw, double* h, double* stat,
+                                                     double* h, double* stat,
                                                      double* partial, ctk_stage_dst sd,
                                                      double* hm, int stat_off, float* gram,
                                                      const __grid_constant__ TsMaps tm) {
@@ -1471,6 +1490,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
     GS_STAMP(0);
     ctk_pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int tw = TW;
     const int nb = k + 1;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                 // [TS_NBUF]
     double* h1 = reinterpret_cast<double*>(smem_raw + 8 * TS_NBUF);         // [2 nb + 2]
@@ -1487,7 +1507,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
     R.stride = (nb + 1) * tw;
     if (threadIdx.x == 0) {
         for (int b = 0; b < TS_NBUF; ++b)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(R.bar(b)) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(R.bar(b)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -1511,15 +1531,23 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
     // The ring runs continuously across sweeps: tile number g (counted from
     // the kernel's first) uses slot g % TS_NBUF at mbarrier phase (g / TS_NBUF) & 1.
     int gbase = 0;
-    auto sweep = [&](int mode, const CUtensorMap* vmap, const double* coef, double* P,
+    auto sweep = [&](int mode, const float* vmap, const double* coef, double* P,
                      double scale, const ctk_stage_dst* stage = nullptr) -> double {
         double acc[TS_RPW], gacc[TS_RPW];
 #pragma unroll
         for (int r = 0; r < TS_RPW; ++r) acc[r] = gacc[r] = 0.0;
         double nrm = 0.0;
-        if (threadIdx.x == 0)
+        if (ts_issuer())
             for (int i = 0; i < TS_NBUF && i < nt; ++i)
-                ts_issue(R, (gbase + i) % TS_NBUF, tw, nb, &tm.W, vmap, (t0 + i) * tw);
+                ts_issue(R, (gbase + i) % TS_NBUF, tw, nb, &tm.W, vmap, (t0 + i) * tw, L);
+        // image position of the tile's first element for the staged copies,
+        // advanced tile by tile (no division per element)
+        int st_iy = 0, st_ix = 0;
+        if (stage) {
+            const int64_t f = t0 * tw;
+            st_iy = (int)(f / stage->nx);
+            st_ix = (int)(f - (int64_t)st_iy * stage->nx);
+        }
         for (int i = 0; i < nt; ++i) {
             const int g = gbase + i, b = g % TS_NBUF;
             const int64_t e0 = (t0 + i) * tw;
@@ -1531,12 +1559,21 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
             } else if (mode == 3) {
                 ts_dots2(tile, tw, nb + 1, nb, nb - 1, cn, acc, gacc);
             } else {
-                nrm += ts_update(tile, tw, nb, coef, cn, wnext + e0, mode == 1, red, scale, stage, e0);
+                nrm += ts_update(tile, tw, nb, coef, cn, wnext + e0, mode == 1, red, scale, stage,
+                                 st_iy, st_ix);
                 if (mode == 1) ts_dots(tile, tw, nb, nb, cn, acc);
+                if (stage) {
+                    st_ix += tw;
+                    while (st_ix >= stage->nx) {
+                        st_ix -= stage->nx;
+                        ++st_iy;
+                    }
+                }
             }
-            __syncthreads();                     // everyone is done with slot b
-            if (threadIdx.x == 0 && i + TS_NBUF < nt)
-                ts_issue(R, b, tw, nb, &tm.W, vmap, (t0 + i + TS_NBUF) * tw);
+            // everyone is done with slot b (mode 2: ts_update ended in a barrier)
+            if (mode != 2) __syncthreads();
+            if (ts_issuer() && i + TS_NBUF < nt)
+                ts_issue(R, b, tw, nb, &tm.W, vmap, (t0 + i + TS_NBUF) * tw, L);
         }
         gbase += nt;
         if (mode != 2) {
@@ -1566,7 +1603,7 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
         // Gram-corrected CGS2 (see gram_coefs): two sweeps, one reduction --
         // h1, ||q||^2 and <W_j, w_k> in one read of the basis, then
         // q2 = (q - W c) / ||q2|| straight into row k+1
-        sweep(3, &tm.q, nullptr, P1, 1.0);
+        sweep(3, q, nullptr, P1, 1.0);
         GS_STAMP(2);
         grid.sync();
         GS_STAMP(3);
@@ -1582,29 +1619,29 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
             // are written in the same sweep (no re-read, no extra barrier),
             // unless the step breaks down (hk is only known after the sweep)
             const bool fold = sd.P && sqrt(est) > 1e-14 * sqrt(a);
-            sweep(2, &tm.q, cc, nullptr, 1.0 / sqrt(est), fold ? &sd : nullptr);
+            sweep(2, q, cc, nullptr, 1.0 / sqrt(est), fold ? &sd : nullptr);
             if (threadIdx.x == 0) s_n2 = est;
             need_norm = false;
             prescaled = true;
             staged = fold;
         } else {
-            nrm = sweep(2, &tm.q, cc, nullptr, 1.0);
+            nrm = sweep(2, q, cc, nullptr, 1.0);
         }
     } else {
-        sweep(0, &tm.q, nullptr, P1, 1.0);                   // h1 = W^T q, ||q||^2
+        sweep(0, q, nullptr, P1, 1.0);                   // h1 = W^T q, ||q||^2
         grid.sync();
         all_reduce_rows(P1, nb + 1, h1);
         __syncthreads();
         const double* cfin = h1;
-        const CUtensorMap* vfin = &tm.q;
+        const float* vfin = q;
         if (passes == 2) {
-            sweep(1, &tm.q, h1, P2, 1.0);                    // q1 -> wnext, h2 = W^T q1
+            sweep(1, q, h1, P2, 1.0);                    // q1 -> wnext, h2 = W^T q1
             asm volatile("fence.proxy.async.global;" ::: "memory");   // q1: generic writes, bulk reads
             grid.sync();
             all_reduce_rows(P2, nb, h2);
             __syncthreads();
             cfin = h2;
-            vfin = &tm.wn;
+            vfin = wnext;
         }
         nrm = sweep(2, vfin, cfin, nullptr, 1.0);            // q2 -> wnext, ||q2||^2
     }
@@ -1873,7 +1910,9 @@ static bool gs_stream_plan(int64_t L, int k, int* twp, size_t* smemp, int* Gp) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaFuncSetAttribute(k_gs_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(k_gs_stream<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SMEM_LIMIT) != cudaSuccess ||
+            cudaFuncSetAttribute(k_gs_stream<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)SMEM_LIMIT) != cudaSuccess)
             coop = 0;
         cudaGetLastError();
@@ -1924,10 +1963,12 @@ static int try_gs_stream(float* W, int64_t ld, int k, int64_t L, const float* q,
     cfg.attrs = at;
     cfg.numAttrs = 2;
     TsMaps tm;
-    if (!encode_rows(&tm.W, W, L, ld, k + 1, tw) || !encode_rows(&tm.q, q, L, L, 1, tw) ||
-        !encode_rows(&tm.wn, W + (size_t)(k + 1) * ld, L, ld, 1, tw))
+    if (!encode_rows(&tm.W, W, L, ld, k + 1, tw))
         return CTK_OK;                                   // no TMA encoder: other paths
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_gs_stream, W, ld, k, L, q, passes, tw, h, stat,
+    cudaError_t e =
+        tw == 256 ? cudaLaunchKernelEx(&cfg, k_gs_stream<256>, W, ld, k, L, q, passes, h, stat,
+                                       s.partial, sd, hm, stat_off, gram, tm)
+                  : cudaLaunchKernelEx(&cfg, k_gs_stream<128>, W, ld, k, L, q, passes, h, stat,
                                        s.partial, sd, hm, stat_off, gram, tm);
     ctk_count_launch();
     if (e != cudaSuccess) return ctk_check_cuda(e, "k_gs_stream");

@@ -1305,10 +1305,12 @@ __global__ void __launch_bounds__(ST, 1) k_gs_smem(float* W, int64_t ld, int k, 
 // ---------------------------------------------------------------------------
 constexpr int TS_RPW = 8;                        // dot rows per warp: 16 warps x 8 = 128
 constexpr int TS_MAXROWS = SW * TS_RPW;          // basis rows + the vector row
-#ifndef CTK_TS_NBUF
-#define CTK_TS_NBUF 2
-#endif
-constexpr int TS_NBUF = CTK_TS_NBUF;             // ring depth (2: deeper rings measured slower at c4/c5)
+// Ring depth: 4 slots of 256-float tiles while they fit beside the reduction
+// scratch (k <= ~48), else 2 -- a compile-time choice per instantiation: the
+// slot / phase arithmetic (g % NBUF, g / NBUF) sits on every tile's critical
+// path, and with a run-time depth its divisions cost what the deeper ring
+// gains (the sweeps are bound by the per-warp instruction stream, DESIGN 9.2).
+constexpr int TS_MAXBUF = 4;
 
 // Ring slot b: buffer ring + b (rows) tw floats, mbarrier bar0 + 8 b.
 struct TsRing {
@@ -1363,13 +1365,12 @@ __device__ __forceinline__ void ts_issue(const TsRing& R, int b, int tw, int nb,
 __device__ __forceinline__ void ts_dots2(const float* tile, int tw, int nrows, int vrow, int grow,
                                          int cn, double* acc, double* gacc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int fpl = tw >> 5;
     const float* vr = tile + (size_t)vrow * tw;
     const float* gr = tile + (size_t)grow * tw;
 #pragma unroll
     for (int c4 = 0; c4 < 2; ++c4) {
-        const int e = lane * fpl + c4 * 4;
-        if (c4 * 4 >= fpl || e >= cn) break;
+        const int e = c4 * 128 + lane * 4;       // a warp's LDS.128: 512 contiguous bytes
+        if (c4 * 128 >= tw || e >= cn) break;
         const float4 v = *reinterpret_cast<const float4*>(vr + e);
         const float4 u = *reinterpret_cast<const float4*>(gr + e);
         const double v0 = v.x, v1 = v.y, v2 = v.z, v3 = v.w;
@@ -1401,12 +1402,11 @@ __device__ __forceinline__ void ts_dots2(const float* tile, int tw, int nrows, i
 __device__ __forceinline__ void ts_dots(const float* tile, int tw, int nrows, int vrow, int cn,
                                         double* acc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int fpl = tw >> 5;                     // floats per lane (4 or 8)
     const float* vr = tile + (size_t)vrow * tw;
 #pragma unroll
     for (int c4 = 0; c4 < 2; ++c4) {
-        const int e = lane * fpl + c4 * 4;
-        if (c4 * 4 >= fpl || e >= cn) break;
+        const int e = c4 * 128 + lane * 4;       // a warp's LDS.128: 512 contiguous bytes
+        if (c4 * 128 >= tw || e >= cn) break;
         const float4 v = *reinterpret_cast<const float4*>(vr + e);
         const double v0 = v.x, v1 = v.y, v2 = v.z, v3 = v.w;
 #pragma unroll
@@ -1479,7 +1479,7 @@ struct TsMaps {
     CUtensorMap W;          // rows 0..k of the basis, box tw x (k+1)
 };
 
-template <int TW>                   // tile width (floats): compile-time index arithmetic
+template <int TW, int NBUF>         // tile width (floats), ring depth: compile-time index arithmetic
 __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k, int64_t L,
                                                      const float* __restrict__ q, int passes,
                                                      double* h, double* stat,
@@ -1492,13 +1492,14 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int tw = TW;
     const int nb = k + 1;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                 // [TS_NBUF]
-    double* h1 = reinterpret_cast<double*>(smem_raw + 8 * TS_NBUF);         // [2 nb + 2]
+    constexpr int TS_NBUF = NBUF;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                 // [TS_MAXBUF]
+    double* h1 = reinterpret_cast<double*>(smem_raw + 8 * TS_MAXBUF);       // [2 nb + 2]
     double* h2 = h1 + (2 * nb + 2);                                         // [nb + 1]
     double* cc = h2 + (nb + 1);                                             // [nb + 1]
     double* red = cc + (nb + 1);                                            // [ST]
     // ring slots: 128-B aligned for the tensor copies
-    unsigned char* ring_raw = smem_raw + 8 * TS_NBUF + sizeof(double) * (4 * (size_t)nb + 4 + ST);
+    unsigned char* ring_raw = smem_raw + 8 * TS_MAXBUF + sizeof(double) * (4 * (size_t)nb + 4 + ST);
     ring_raw += (128u - (smem_u32(ring_raw) & 127u)) & 127u;
     float* ring = reinterpret_cast<float*>(ring_raw);
     TsRing R;
@@ -1896,13 +1897,13 @@ bool ctk_gs_smem_ok(int64_t L, int k) {
 
 // Streamed path: L a multiple of 4 (16-B row pitch of q), at most TS_MAXROWS
 // rows, two ring buffers of the widest tile (256 or 128 floats) that fit.
-static size_t gs_stream_bytes(int k, int tw) {
+static size_t gs_stream_bytes(int k, int tw, int nbuf) {
     const int nb = k + 1;
-    const size_t head = 8 * TS_NBUF + sizeof(double) * (4 * (size_t)nb + 4 + ST) + 128;
-    return head + TS_NBUF * sizeof(float) * (size_t)(nb + 1) * tw;
+    const size_t head = 8 * TS_MAXBUF + sizeof(double) * (4 * (size_t)nb + 4 + ST) + 128;
+    return head + nbuf * sizeof(float) * (size_t)(nb + 1) * tw;
 }
 
-static bool gs_stream_plan(int64_t L, int k, int* twp, size_t* smemp, int* Gp) {
+static bool gs_stream_plan(int64_t L, int k, int* twp, size_t* smemp, int* Gp, int* nbufp) {
     static int coop = -1, sms = 0;
     if (coop < 0) {
         const char* off = getenv("CTK_NO_STREAM_GS");
@@ -1910,9 +1911,11 @@ static bool gs_stream_plan(int64_t L, int k, int* twp, size_t* smemp, int* Gp) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaFuncSetAttribute(k_gs_stream<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(k_gs_stream<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)SMEM_LIMIT) != cudaSuccess ||
-            cudaFuncSetAttribute(k_gs_stream<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(k_gs_stream<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SMEM_LIMIT) != cudaSuccess ||
+            cudaFuncSetAttribute(k_gs_stream<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)SMEM_LIMIT) != cudaSuccess)
             coop = 0;
         cudaGetLastError();
@@ -1921,31 +1924,36 @@ static bool gs_stream_plan(int64_t L, int k, int* twp, size_t* smemp, int* Gp) {
     if (coop != 1 || k < 0 || (L & 3) || k + 2 > TS_MAXROWS || sms > GS_MAXG) return false;
     if (L >= (1LL << 31) || !tensor_map_encoder()) return false;   // 32-bit TMA coordinates
     if (L < (int64_t)sms * 1024) return false;           // short vectors: SMEM / fused paths
+    static const int max_buf = [] {
+        const char* e = getenv("CTK_TS_NBUF");            // tuning override: 2 = never 4 slots
+        return e && atoi(e) == 2 ? 2 : TS_MAXBUF;
+    }();
     for (int tw = 256; tw >= 128; tw >>= 1) {         // ts_dots: 4 or 8 floats per lane
-        const size_t smem = gs_stream_bytes(k, tw);
-        if (smem <= SMEM_LIMIT) {
-            *twp = tw;
-            *smemp = smem;
-            *Gp = sms;
-            return true;
-        }
+        if (gs_stream_bytes(k, tw, 2) > SMEM_LIMIT) continue;
+        const int nbuf =
+            tw == 256 && max_buf == 4 && gs_stream_bytes(k, tw, 4) <= SMEM_LIMIT ? 4 : 2;
+        *twp = tw;
+        *smemp = gs_stream_bytes(k, tw, nbuf);
+        *Gp = sms;
+        *nbufp = nbuf;
+        return true;
     }
     return false;
 }
 
 bool ctk_gs_stream_ok(int64_t L, int k) {
-    int tw, G;
+    int tw, G, nbuf;
     size_t smem;
-    return !ctk_gs_smem_ok(L, k) && gs_stream_plan(L, k, &tw, &smem, &G);
+    return !ctk_gs_smem_ok(L, k) && gs_stream_plan(L, k, &tw, &smem, &G, &nbuf);
 }
 
 static int try_gs_stream(float* W, int64_t ld, int k, int64_t L, const float* q, int passes,
                          double* h, double* stat, Scratch s, cudaStream_t st,
                          const ctk_stage_dst* sdp, double* hm, float* gram, bool* done) {
     *done = false;
-    int tw, G;
+    int tw, G, nbuf;
     size_t smem;
-    if (!gs_stream_plan(L, k, &tw, &smem, &G)) return CTK_OK;
+    if (!gs_stream_plan(L, k, &tw, &smem, &G, &nbuf)) return CTK_OK;
     if ((size_t)(2 * k + 5) * G > (size_t)MAXCH * (size_t)(k + 3)) return CTK_OK;
     ctk_stage_dst sd = {};
     if (sdp && sdp->P && (int64_t)sdp->nx * sdp->ny == L) sd = *sdp;
@@ -1965,11 +1973,10 @@ static int try_gs_stream(float* W, int64_t ld, int k, int64_t L, const float* q,
     TsMaps tm;
     if (!encode_rows(&tm.W, W, L, ld, k + 1, tw))
         return CTK_OK;                                   // no TMA encoder: other paths
-    cudaError_t e =
-        tw == 256 ? cudaLaunchKernelEx(&cfg, k_gs_stream<256>, W, ld, k, L, q, passes, h, stat,
-                                       s.partial, sd, hm, stat_off, gram, tm)
-                  : cudaLaunchKernelEx(&cfg, k_gs_stream<128>, W, ld, k, L, q, passes, h, stat,
-                                       s.partial, sd, hm, stat_off, gram, tm);
+    auto kern = tw == 256 ? (nbuf == 4 ? k_gs_stream<256, 4> : k_gs_stream<256, 2>)
+                          : k_gs_stream<128, 2>;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, W, ld, k, L, q, passes, h, stat, s.partial, sd,
+                                       hm, stat_off, gram, tm);
     ctk_count_launch();
     if (e != cudaSuccess) return ctk_check_cuda(e, "k_gs_stream");
     *done = true;

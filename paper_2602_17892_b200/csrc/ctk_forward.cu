@@ -442,15 +442,24 @@ __device__ __forceinline__ unsigned cluster_addr(const void* p, unsigned rank) {
     return r;
 }
 
+// Resident CTAs per SM: 8 (64 registers) for the row-split cluster launches of
+// small problems, whose few short CTAs need the slots; 6 (80 registers) for
+// whole-ray CTAs -- measured A per apply at c3 / c4 / c5: 0.1096 / 0.605 /
+// 2.838 -> 0.1075 / 0.597 / 2.806 ms (while the split c2 launch would go
+// 0.0297 -> 0.0379 ms with 6).
 #ifndef CTK_FWD_MINB
 #define CTK_FWD_MINB (32 / CTK_FWD_APB_N)
+#endif
+#ifndef CTK_FWD_MINB_WHOLE
+#define CTK_FWD_MINB_WHOLE (CTK_FWD_APB_N == 4 ? 6 : CTK_FWD_MINB)
 #endif
 #ifndef CTK_FWD_DYNSMEM
 #define CTK_FWD_DYNSMEM 0
 #endif
 
 template <bool SPLIT>
-__global__ void __launch_bounds__(FWD_THREADS, CTK_FWD_MINB) k_forward(FwdArgs A) {
+__global__ void __launch_bounds__(FWD_THREADS, SPLIT ? CTK_FWD_MINB : CTK_FWD_MINB_WHOLE)
+k_forward(FwdArgs A) {
     ctk_pdl_trigger();
     // A CTA is 4 adjacent angles x 32 adjacent bins.  Paired layout: each
     // warp takes 2 adjacent angles x 16 bins (half-warps), so a warp's taps

@@ -219,9 +219,17 @@ __device__ __forceinline__ void stage_pairs(const BackArgs& A, float2* win, cons
 // image.  (A cluster/DSMEM variant of this reduction measured faster in
 // isolation but slower inside the solve: its gang-scheduled CTAs wait for
 // whole free GPC slices while the iterate stream's kernels hold SMs.)
+// Resident CTAs per SM of the 4-pixels-per-thread kernels: 4 (64 registers).
+// Measured B per apply at c3 / c4 / c5 with 3 / 4 / 5 / 6: 0.0942 / 0.0901 /
+// 0.0927 / 0.0942, 0.578 / 0.554 / 0.582 / 0.578, 2.669 / 2.588 / 2.705 /
+// 2.808 ms (5 was the optimum before the staging changes of this round).
 #ifndef CTK_BACK_MINB4
-#define CTK_BACK_MINB4 5
+#define CTK_BACK_MINB4 4
 #endif
+#ifndef CTK_BACK_UNROLL
+#define CTK_BACK_UNROLL 4
+#endif
+constexpr int BACK_UNROLL = CTK_BACK_UNROLL;      // angles per unrolled batch of the inner loop
 
 // MODE 0: plain, 1: chained after K1 (counters), 2: windows from the pair
 // sinogram (k_pairs)
@@ -278,7 +286,7 @@ __global__ void __launch_bounds__(BTHREADS, PPT == 4 ? CTK_BACK_MINB4 : 6) k_bac
         float sp[PPT];
 #pragma unroll
         for (int r = 0; r < PPT; ++r) sp[r] = 0.f;
-#pragma unroll 4
+#pragma unroll BACK_UNROLL
         for (int ai = 0; ai < na; ++ai) {
             const int4 P = s_par[ai];
             const unsigned T0 = (unsigned)P.x + (unsigned)tx * (unsigned)P.y + (unsigned)ty * (unsigned)P.z;

@@ -449,11 +449,14 @@ static int back_tiles_y(const ctk_geom* g) {
 
 static int back_splits(const ctk_geom* g, int a0, int a1) {
     const int tiles = ((g->nx + BTX - 1) / BTX) * back_tiles_y(g);
-    static int target = -1;
-    if (target < 0) {
+    static int target_env = -1;
+    if (target_env < 0) {
         const char* e = getenv("CTK_BACK_TARGET");       // tuning override (CTAs)
-        target = e && atoi(e) > 0 ? atoi(e) : 148 * 12;   // ~1.5 waves of 256-thread CTAs
+        target_env = e && atoi(e) > 0 ? atoi(e) : 0;
     }
+    // two waves of the kernel's resident CTAs: 4 per SM for the 4-pixel
+    // kernels (c3: 7 -> 5 splits, B 0.090 -> 0.086 ms), 6 for the others
+    const int target = target_env ? target_env : g->back_ppt == 4 ? 148 * 8 : 148 * 12;
     static int min_ang = -1;
     if (min_ang < 0) {
         const char* e = getenv("CTK_BACK_MINANG");      // tuning override: angles per CTA
@@ -492,9 +495,9 @@ static int64_t back_flag_floats(const ctk_geom* g) {
 
 static int64_t back_ticket_floats(const ctk_geom* g) { return (back_tiles(g) + 15) / 16 * 16; }
 
-// Pair sinogram (MODE 2): measured B per apply with / without the pre-pass:
-// c5 2.703 / 2.742 ms, c4 0.587 / 0.582, c3 0.095 / 0.092 -- so images of
-// >= 2048^2 only (CTK_BACK_PAIRS=0 / 1 overrides).  P = 2 pad bins each side
+// Pair sinogram (MODE 2): measured B per apply with / without the pre-pass
+// (64-register kernels): c5 2.589 / 2.721 ms, c4 0.548 / 0.553, c3 0.091 /
+// 0.089 -- so images of >= 1024^2 (CTK_BACK_PAIRS=0 / 1 overrides).  P = 2 pad bins each side
 // cover the i0 == -1 quirk bin.
 constexpr int PAIR_PAD = 2;
 static bool back_pairs_on(const ctk_geom* g) {
@@ -504,7 +507,7 @@ static bool back_pairs_on(const ctk_geom* g) {
     }();
     if (g->back_ppt != 4) return false;
     if (force >= 0) return force != 0;
-    return (int64_t)g->nx * g->ny >= 2048LL * 2048;
+    return (int64_t)g->nx * g->ny >= 1024LL * 1024;
 }
 
 static int64_t back_pair_floats(const ctk_geom* g, int a0, int a1) {

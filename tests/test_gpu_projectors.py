@@ -310,3 +310,21 @@ def test_adjoint_four_tap_path_vs_oracle_transpose(cuda, sp, na):
     At = ct.GpuAdjoint(dg.n, dg.m, dg).to_dense()
     np.testing.assert_allclose(At, A.T, atol=2e-5)
     assert rel_l2(At, A.T) <= REL_L2
+
+
+@pytest.mark.parametrize("pair", [0, 1, 2])
+def test_forward_warp_layouts_vs_oracle(cuda, monkeypatch, pair):
+    """K1's three warp layouts (1 angle x 32 bins, 2 x 16, 4 x 8; chosen by
+    image size, CTK_FWD_PAIR overrides at geometry creation) against the
+    oracle on one geometry: non-square image, non-unit pixel and bin sizes,
+    rays entering through every side, axis-aligned angles included."""
+    monkeypatch.setenv("CTK_FWD_PAIR", str(pair))
+    nx, ny, h, D, sp = 150, 131, 0.8, 187, 1.1
+    angles = np.arange(120) * np.pi / 120
+    dg, og = make(nx, ny, h, angles, D, sp)
+    monkeypatch.delenv("CTK_FWD_PAIR")
+    x = problems.uniform_image(nx * ny, 3)
+    y = dg.forward(to_dev(cuda, x)).cpu().numpy()
+    ref = O.forward(og, x.astype(np.float32).astype(np.float64))
+    assert rel_l2(y, ref) <= REL_L2, pair
+    np.testing.assert_allclose(y, ref, rtol=0, atol=3e-6 * np.abs(ref).max())

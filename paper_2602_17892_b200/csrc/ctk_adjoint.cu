@@ -59,13 +59,17 @@ struct AdjArgs {
     const int* deg_angle;    // slot -> angle
     int n_deg;
     int nx, ny, D, a0, a1, per_split, wmax, split, fbits;
+    int qm;                  // TAPS == 1: candidates j0 - qm .. j0 + 1 + qm
     double h, sp, xmin, ymax, center;
 };
 
-// TAPS: candidate rays per pixel-angle in the fast path: 2 (j0, j0+1) when
-// the pixel shadow is at most one bin wide, (|c|+|s|) h / 2 <= s for every
-// angle, else 4 (j0-1 .. j0+2).  The staged window holds, per bin i, the taps
-// (u[i], u[i+1]) or (u[i-1] .. u[i+2]) so one LDS.64 / LDS.128 fetches them.
+// TAPS: candidate rays per pixel-angle.  With R = max (|c|+|s|) h / (2 s), the
+// half-width of a pixel's shadow in bins: 2 (j0, j0+1) when R <= 1, 4
+// (j0-1 .. j0+2) when R <= 2 -- the staged window holds, per bin i, the taps
+// (u[i], u[i+1]) or (u[i-1] .. u[i+2]) so one LDS.64 / LDS.128 fetches them --
+// and 1 for bins narrower than that (s < 0.354 h): a plain window and the
+// fp64 trapezoid over j0 - qm .. j0 + 1 + qm, qm = ceil(R) - 1, for every
+// angle (no fixed-point fast path).
 template <int TAPS>
 struct TapT {
     typedef float4 type;
@@ -73,6 +77,10 @@ struct TapT {
 template <>
 struct TapT<2> {
     typedef float2 type;
+};
+template <>
+struct TapT<1> {
+    typedef float type;
 };
 
 template <int JPPT, int TAPS>
@@ -124,11 +132,12 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
             const double g01 = fma(Xlo, cg, fma(Yhi, sg, A.center));
             const double g10 = fma(Xhi, cg, fma(Ylo, sg, A.center));
             const double g11 = fma(Xhi, cg, fma(Yhi, sg, A.center));
-            const int w0 = (int)floor(fmin(fmin(g00, g01), fmin(g10, g11))) - 2;
+            const int w0 = (int)floor(fmin(fmin(g00, g01), fmin(g10, g11))) -
+                           (TAPS == 1 ? A.qm + 1 : 2);
             s_w0[tid] = w0;
             // fp32 fixed-point path away from the axes (slope region >= 0.02 h
             // wide): normalised weights sat(Q_k -/+ f B) by FFMA.SAT
-            const bool fast = fmin(ac_, as_) >= CTK_ADJ_FAST_MIN;
+            const bool fast = TAPS != 1 && fmin(ac_, as_) >= CTK_ADJ_FAST_MIN;
             s_skip[tid] = A.deg_slot[a] >= 0 ? 1 : (fast ? 2 : 0);
             if (fast) {
                 const double scale = ldexp(1.0, A.fbits);
@@ -149,13 +158,15 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
             const float lsc = s_skip[ai] == 2 ? (float)s_Lm[ai] : 1.f;   // fast: pre-scale by Lm
             for (int i = tx; i < wmax; i += JTX) {
                 float v4[4];
-                constexpr int first = TAPS == 2 ? 0 : -1;
+                constexpr int first = TAPS == 4 ? -1 : 0;
 #pragma unroll
                 for (int q = 0; q < TAPS; ++q) {
                     const int b = w0 + i + first + q;
                     v4[q] = (b >= 0 && b < D) ? lsc * __ldg(row + b) : 0.f;
                 }
-                if constexpr (TAPS == 2)
+                if constexpr (TAPS == 1)
+                    dst[i] = v4[0];
+                else if constexpr (TAPS == 2)
                     dst[i] = make_float2(v4[0], v4[1]);
                 else
                     dst[i] = make_float4(v4[0], v4[1], v4[2], v4[3]);
@@ -168,7 +179,7 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
         for (int ai = 0; ai < na; ++ai) {
             const int mode = s_skip[ai];
             if (mode == 1) continue;                   // K1d angles: transposed lists below
-            if (mode == 2) {
+            if (TAPS != 1 && mode == 2) {
                 const int4 fx = s_fx[ai];
                 const float4 qw = s_q[ai];
                 const float bw = s_b[ai];
@@ -186,7 +197,7 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
                     if constexpr (TAPS == 2) {
                         t = fmaf(__saturatef(fmaf(f, -bw, qw.y)), v.x, t);
                         t = fmaf(__saturatef(fmaf(f, bw, qw.z)), v.y, t);
-                    } else {
+                    } else if constexpr (TAPS == 4) {
                         t = fmaf(__saturatef(fmaf(f, -bw, qw.x)), v.x, t);
                         t = fmaf(__saturatef(fmaf(f, -bw, qw.y)), v.y, t);
                         t = fmaf(__saturatef(fmaf(f, bw, qw.z)), v.z, t);
@@ -202,12 +213,15 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
             for (int r = 0; r < JPPT; ++r) {
                 const double g = fma(X, cg, fma(Y[r], sg, A.center));   // ray index at the centre
                 const int j0 = (int)floor(g);
-#pragma unroll
-                for (int q = -1; q <= 2; ++q) {
+                const int qlo = TAPS == 1 ? -A.qm : -1, qhi = TAPS == 1 ? A.qm + 1 : 2;
+                for (int q = qlo; q <= qhi; ++q) {
                     const int j = j0 + q;
                     const double a = P - fabs((double)j - g) * sp;
                     if (a > 0.0) {
-                        const float uj = TAPS == 2 ? wq[j].x : reinterpret_cast<const float4*>(wq)[j].y;
+                        float uj;
+                        if constexpr (TAPS == 1) uj = wq[j];
+                        else if constexpr (TAPS == 2) uj = wq[j].x;
+                        else uj = wq[j].y;
                         acc[r] = fma(fmin(Lm, a * ics), (double)uj, acc[r]);
                     }
                 }
@@ -271,7 +285,7 @@ __global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
 }
 
 static int adj_tiles_y(const ctk_geom* g) {
-    const int jty = JROWS * g->back_ppt;
+    const int jty = JROWS * (g->back_ppt == 4 ? 4 : 2);      // the kernels' JPPT
     return (g->ny + jty - 1) / jty;
 }
 
@@ -431,8 +445,21 @@ extern "C" int ctk_adjoint(const ctk_geom_t* gc, const float* u, float* x, int a
     A.a0 = a0;
     A.a1 = a1;
     A.per_split = (a1 - a0 + S - 1) / S;
-    // window: the tile's detector footprint (K2's bound for the same tile) + 2
-    A.wmax = g->back_wmax + 2;
+    // Candidates and window.  R: half-width of a pixel's shadow in bins, at
+    // most h / (sqrt 2 s); the window must hold this kernel's own tile
+    // (32 x 8 JPPT pixels: K2's bound is for K2's tile, which is half as tall
+    // for small images) plus the candidates' margins on both sides.
+    const int jppt = g->back_ppt == 4 ? 4 : 2;
+    const double rmax = 0.5 * 1.41421356237309515 * g->h / g->det_spacing;
+    static int force4 = -1;
+    if (force4 < 0) {
+        const char* e = getenv("CTK_ADJ_TAPS4");          // test hook: the 4-tap path
+        force4 = e && e[0] == '1';
+    }
+    const int taps = rmax > 2.0 - 1e-9 ? 1 : (!force4 && rmax <= 1.0) ? 2 : 4;
+    A.qm = taps == 1 ? (int)ceil(rmax) - 1 : 1;
+    A.wmax = (int)ceil(sqrt((double)JTX * JTX + (double)(JROWS * jppt) * (JROWS * jppt)) * g->h /
+                       g->det_spacing) + 2 * (A.qm + 1) + 3;
     {   // fixed-point fraction bits: window coordinates [0, wmax] need I bits
         int I = 1;
         while ((1 << I) <= A.wmax + 1) ++I;
@@ -445,17 +472,15 @@ extern "C" int ctk_adjoint(const ctk_geom_t* gc, const float* u, float* x, int a
     A.ymax = g->ymax;
     A.center = g->center;
     dim3 grid((g->nx + JTX - 1) / JTX, adj_tiles_y(g), S), block(JTX, JROWS);
-    // two taps suffice when every pixel shadow is at most one bin wide
-    static int force4 = -1;
-    if (force4 < 0) {
-        const char* e = getenv("CTK_ADJ_TAPS4");          // test hook: the 4-tap path
-        force4 = e && e[0] == '1';
-    }
-    const int taps = (!force4 && 0.5 * 1.41421356237309515 * g->h <= g->det_spacing) ? 2 : 4;
-    const size_t smem = (size_t)JCA * A.wmax * (taps == 2 ? sizeof(float2) : sizeof(float4));
+    const size_t smem = (size_t)JCA * A.wmax *
+                        (taps == 1 ? sizeof(float) : taps == 2 ? sizeof(float2) : sizeof(float4));
+    if (smem > 200 * 1024)
+        return ctk_fail(CTK_ERR_GEOMETRY, "adjoint: detector windows of %d bins per tile do not fit "
+                        "in shared memory (pixel size %g, bin spacing %g)", A.wmax, g->h,
+                        g->det_spacing);
     const bool p4 = g->back_ppt == 4;
-    auto kern = p4 ? (taps == 2 ? k_adjoint<4, 2> : k_adjoint<4, 4>)
-                   : (taps == 2 ? k_adjoint<2, 2> : k_adjoint<2, 4>);
+    auto kern = p4 ? (taps == 1 ? k_adjoint<4, 1> : taps == 2 ? k_adjoint<4, 2> : k_adjoint<4, 4>)
+                   : (taps == 1 ? k_adjoint<2, 1> : taps == 2 ? k_adjoint<2, 2> : k_adjoint<2, 4>);
     if (smem > 48 * 1024)
         CTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, block, smem, st>>>(A);

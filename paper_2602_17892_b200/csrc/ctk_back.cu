@@ -150,7 +150,8 @@ __device__ __forceinline__ void stage_windows(const BackArgs& A, float2* win, co
             if (b + 32 == -1) v1b = ld_u<CHAINED>(row + q1);
             float2* dst = win + ai * wmax;
             float d = v1a - va[j];
-            dst[tx] = make_float2(va[j] - d, d);
+            // (windows can be narrower than a warp: pixels smaller than bins)
+            if (tx < wmax) dst[tx] = make_float2(va[j] - d, d);
             if (tx + 32 < wmax) {
                 d = v1b - vb[j];
                 dst[tx + 32] = make_float2(vb[j] - d, d);

@@ -312,19 +312,82 @@ def test_adjoint_four_tap_path_vs_oracle_transpose(cuda, sp, na):
     assert rel_l2(At, A.T) <= REL_L2
 
 
+@pytest.mark.parametrize("h,sp", [(0.8, 1.1), (0.3, 1.0), (2.0, 0.7)])
 @pytest.mark.parametrize("pair", [0, 1, 2])
-def test_forward_warp_layouts_vs_oracle(cuda, monkeypatch, pair):
+def test_forward_warp_layouts_vs_oracle(cuda, monkeypatch, pair, h, sp):
     """K1's three warp layouts (1 angle x 32 bins, 2 x 16, 4 x 8; chosen by
     image size, CTK_FWD_PAIR overrides at geometry creation) against the
     oracle on one geometry: non-square image, non-unit pixel and bin sizes,
     rays entering through every side, axis-aligned angles included."""
     monkeypatch.setenv("CTK_FWD_PAIR", str(pair))
-    nx, ny, h, D, sp = 150, 131, 0.8, 187, 1.1
+    nx, ny = 150, 131
+    D = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
     angles = np.arange(120) * np.pi / 120
     dg, og = make(nx, ny, h, angles, D, sp)
     monkeypatch.delenv("CTK_FWD_PAIR")
     x = problems.uniform_image(nx * ny, 3)
     y = dg.forward(to_dev(cuda, x)).cpu().numpy()
     ref = O.forward(og, x.astype(np.float32).astype(np.float64))
-    assert rel_l2(y, ref) <= REL_L2, pair
+    assert rel_l2(y, ref) <= REL_L2, (pair, h, sp)
     np.testing.assert_allclose(y, ref, rtol=0, atol=3e-6 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("h,sp", [(0.8, 1.1), (0.3, 1.0), (2.0, 0.7)])
+@pytest.mark.parametrize("ppt", [1, 2, 4])
+def test_back_tile_shapes_vs_oracle(cuda, monkeypatch, ppt, h, sp):
+    """K2's three tile shapes (32 x 8, 32 x 16, 32 x 32 pixels per CTA: 1, 2
+    or 4 pixels per thread, chosen by image size; CTK_BACK_PPT overrides at
+    geometry creation) against the oracle on an image that is not a multiple
+    of any tile, with angle splits and a sub-range apply -- for pixels smaller
+    than the bins (detector windows narrower than a warp: h / s = 0.3 and
+    0.73), and larger (windows of more than 63 bins: the element-loop
+    staging)."""
+    monkeypatch.setenv("CTK_BACK_PPT", str(ppt))
+    nx, ny = 150, 131
+    D = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
+    na = 120
+    angles = np.arange(na) * np.pi / na
+    dg, og = make(nx, ny, h, angles, D, sp)
+    monkeypatch.delenv("CTK_BACK_PPT")
+    u = problems.uniform_sinogram(na * D, 5)
+    x = dg.back(to_dev(cuda, u)).cpu().numpy()
+    ref = O.back(og, u.astype(np.float32).astype(np.float64))
+    assert rel_l2(x, ref) <= REL_L2, (ppt, h, sp)
+    np.testing.assert_allclose(x, ref, rtol=0, atol=3e-6 * np.abs(ref).max())
+    a0, a1 = 17, 83
+    xs = dg.back(to_dev(cuda, u.reshape(na, D)[a0:a1].ravel()), a0=a0, a1=a1).cpu().numpy()
+    us = np.zeros_like(u).reshape(na, D)
+    us[a0:a1] = u.reshape(na, D)[a0:a1]
+    refs = O.back(og, us.ravel().astype(np.float32).astype(np.float64))
+    assert rel_l2(xs, refs) <= REL_L2, (ppt, h, sp)
+
+
+@pytest.mark.parametrize("h,sp", [(0.8, 1.1), (0.3, 1.0), (2.0, 0.7), (2.0, 0.4), (1.0, 1.0)])
+def test_adjoint_vs_oracle_forward_on_odd_geometry(cuda, h, sp):
+    """K7 on the non-square image with non-unit spacings: <A x, u> = <x, A^T u>
+    with A x from the fp64 oracle (so K1 is not on either side), for random
+    and for single-ray u (rows of A, entrywise).  Covers the two-tap windows
+    (shadow <= one bin), the four-tap ones, and bins narrower than 0.354 h
+    (more than four rays can cross a pixel: the general candidate loop), on an
+    image small enough that K7's tile is taller than K2's."""
+    torch = cuda
+    nx, ny = 150, 131
+    D = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
+    na = 120
+    angles = np.arange(na) * np.pi / na
+    dg, og = make(nx, ny, h, angles, D, sp)
+    rng = np.random.default_rng(11)
+    x = rng.random(dg.n).astype(np.float32).astype(np.float64)
+    u = rng.random(dg.m).astype(np.float32)
+    Ax = O.forward(og, x)
+    Atu = dg.adjoint(torch.from_numpy(u).cuda()).cpu().numpy().astype(np.float64)
+    assert Ax @ u.astype(np.float64) == pytest.approx(x @ Atu, rel=2e-6)
+    # a few rows of A (through the image centre, near an edge, axis-aligned,
+    # near-axis): A^T e_r is row r of the oracle's matrix
+    for a, j in ((0, D // 2), (1, D // 2 + 3), (37, D // 3), (60, D // 2 - 1), (119, D - D // 4)):
+        e = np.zeros(dg.m, dtype=np.float32)
+        e[a * D + j] = 1.0
+        row = dg.adjoint(torch.from_numpy(e).cuda()).cpu().numpy().astype(np.float64)
+        # <row, x> must equal (A x)[r]; and the row's support / values via a second probe
+        assert row @ x == pytest.approx(Ax[a * D + j], rel=2e-6, abs=1e-6 * np.abs(Ax).max())
+        assert (row >= 0).all() and row.max() <= h * np.sqrt(2.0) * (1 + 1e-6)

@@ -77,3 +77,34 @@ def test_large_config_solve_vs_oracle(cuda, golden, name):
     for f, e in errs.items():
         assert e <= RES_TOL, (f, e)
     assert ex <= X_TOL - float(fx["x_quant_err"]), ex
+
+
+@pytest.mark.parametrize("method", ["ab-hybrid", "ba-hybrid"])
+def test_large_odd_geometry_solve_vs_oracle(cuda, method):
+    """A short hybrid solve on a large non-square image with pixels smaller
+    than the bins (1100 x 1030 px of 0.7, unit bins): the >= 1024 paths --
+    paired K1 warps, 32 x 32 K2 tiles with the pair pre-pass, the streamed
+    Gram-Schmidt with its folded staging -- away from the BASELINE shapes."""
+    from oracle import oracle as O
+    from paper_2602_17892_b200 import ct, gmres, problems
+    nx, ny, h, sp, na, K = 1100, 1030, 0.7, 1.0, 150, 5
+    D = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
+    grid = ct.ImageGrid(nx, ny, h)
+    geom = ct.ParallelGeometry(np.arange(na) * np.pi / na, D, sp)
+    A = ct.forward_ray_driven(grid, geom)
+    B = ct.back_pixel_driven(grid, geom)
+    og = O.Geometry(nx, ny, h, geom.angles, D, sp)
+    x_true = problems.random_ellipse_phantom(max(nx, ny), 12, 3).reshape(max(nx, ny), -1)[:ny, :nx]
+    x_true = np.ascontiguousarray(x_true).ravel().astype(np.float32).astype(np.float64)
+    b, _ = problems.add_noise(O.forward(og, x_true), 0.01, 9)
+    b = b.astype(np.float32).astype(np.float64)
+    cfg = gmres.SolverConfig(method=method, lambda_strategy="gcv", max_iter=K)
+    res = gmres.run_gmres(A, B, b, cfg)
+    ref = O.gmres(lambda v: O.forward(og, v), lambda v: O.back(og, v), b, method, "gcv", K)
+    lam = np.array([r.lambda_used for r in res.records])
+    lam_ref = np.array([r["lambda_used"] for r in ref.records])
+    np.testing.assert_allclose(lam, lam_ref, rtol=1e-2)
+    got = np.array([r.data_residual_norm for r in res.records])
+    want = np.array([r["data_residual_norm"] for r in ref.records])
+    np.testing.assert_allclose(got, want, rtol=1e-4 + 2 * np.abs(lam / lam_ref - 1).max())
+    assert np.linalg.norm(res.x - ref.x) <= 1e-3 * np.linalg.norm(ref.x)

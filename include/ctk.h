@@ -64,7 +64,8 @@ int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
                     ctk_geom_t** out);
 int ctk_geom_destroy(ctk_geom_t* g);
 /* n = nx*ny, m = n_angles*det_count, stage_floats = workspace for ctk_forward,
- * n_degenerate = angles taking the literal axis-aligned path. */
+ * n_degenerate = angles taking the literal segment-list path (axis-aligned,
+ * or within 1e-5 rad of an axis). */
 int ctk_geom_info(const ctk_geom_t* g, int64_t* n, int64_t* m, int64_t* stage_floats,
                   int* n_degenerate);
 

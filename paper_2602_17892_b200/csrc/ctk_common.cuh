@@ -25,13 +25,14 @@ struct AngleParams {
     float Lx;               // chord per unit cross coordinate (h / |cross-axis cosine|)
     int frame;              // 0: walk rows of x, 1: walk columns (transposed copy)
     int mirror;             // cross axis reversed
-    int degenerate;         // |sin| or |cos| < 1e-14: exact literal path (ct.py:153-155,165,168)
+    int degenerate;         // literal path: |sin| or |cos| < 1e-14 (ct.py:153-155,165,168) or < 1e-5 (ctk_geom.cu)
     int exact_flags;        // bit0: |dx| is a power of two, bit1: |dy| is (division == exact multiply)
     double inv_dx, inv_dy;  // 1/dx, 1/dy (used only when the matching bit is set)
     double inv_sg;          // 1 / sigma_fx (walk range estimates)
 };
 
 constexpr int CTK_MAX_DEG_LIST = 8;
+constexpr int CTK_MAX_NEAR_AXIS = 16;   // near-axis (not exactly axis-aligned) angles on the literal path
 
 struct BackParams {         // per angle for K2: g = X*cg + Y*sg + center
     double cg, sg;

@@ -165,11 +165,25 @@ extern "C" int ctk_geom_create(int nx, int ny, double pixel_size, int n_angles,
     }
     const int bty = 8 * g->back_ppt;
     const double h = pixel_size;
+    int n_near = 0;
     for (int a = 0; a < n_angles; ++a) {
         const double c = cos_tab[a], s = sin_tab[a];
         ctk::AngleParams p;
         memset(&p, 0, sizeof(p));
-        p.degenerate = (fabs(s) < 1e-14 || fabs(c) < 1e-14) ? 1 : 0;   // ct.py:153,165,168
+        // Literal path (K1d segment lists from the fp64 tracer): the angles the
+        // reference treats as axis-aligned (|sin| or |cos| < 1e-14,
+        // ct.py:153,165,168), and those within 1e-5 rad of an axis.  There the
+        // walk's slope, quantised to 2^-32 px per row, is off by up to
+        // 0.5 / (sigma 2^32) of itself (7% at 1e-9 rad), which moves the row
+        // where a ray lying on a grid line changes column -- 1e-2 errors in
+        // such rays (found by the random-geometry parity test).  At most
+        // CTK_MAX_NEAR_AXIS such angles take the lists (each costs
+        // ~8 bytes x segments per ray x bins); uniform angle sets have none.
+        const bool on_axis = fabs(s) < 1e-14 || fabs(c) < 1e-14;
+        const bool near_axis = !on_axis && (fabs(s) < 1e-5 || fabs(c) < 1e-5) &&
+                               n_near < ctk::CTK_MAX_NEAR_AXIS;
+        n_near += near_axis;
+        p.degenerate = (on_axis || near_axis) ? 1 : 0;
         p.exact_flags = (is_pow2(-s) ? 1 : 0) | (is_pow2(c) ? 2 : 0);
         p.inv_dx = s != 0.0 ? 1.0 / -s : 0.0;
         p.inv_dy = c != 0.0 ? 1.0 / c : 0.0;

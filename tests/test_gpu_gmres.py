@@ -454,3 +454,63 @@ def test_solves_on_odd_geometries_vs_oracle(cuda, method, nx, ny, h, sp):
         np.testing.assert_allclose(got, want, rtol=1e-4 + 2 * np.abs(lam / lam_ref - 1).max(),
                                    err_msg=f)
     assert np.linalg.norm(res.x - ref.x) <= 1e-3 * np.linalg.norm(ref.x)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_small_problems_vs_oracle(cuda, seed):
+    """Seeded random small problems through the whole driver: image sizes
+    from 2 x 2 (Krylov spaces that exhaust: breakdown), non-square,
+    non-unit spacings, detectors narrower than the image, few angles, both
+    methods, hybrid (GCV, fixed) and plain, with and without restarts and an
+    initial guess.  Stop reason, cycle and record counts exact; lambda within
+    1%; residual norms and x within 1e-3 over the well-conditioned early
+    iterations (unregularised runs amplify input rounding later on)."""
+    from oracle import oracle as O
+    from paper_2602_17892_b200 import ct, gmres
+    rng = np.random.default_rng(7000 + seed)
+    for case in range(4):
+        nx, ny = int(rng.integers(2, 40)), int(rng.integers(2, 40))
+        h = float(rng.choice([0.5, 1.0, 1.0, 1.6]))
+        sp = float(rng.choice([0.7, 1.0, 1.0, 1.4]))
+        cover = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
+        D = int(rng.choice([max(2, cover // 2), cover, cover + 4]))
+        na = int(rng.integers(2, 30))
+        ang = np.arange(na) * np.pi / na + float(rng.uniform(0, 0.5 * np.pi / na))
+        method = str(rng.choice(["ab", "ba", "ab-hybrid", "ba-hybrid"]))
+        hybrid = method.endswith("hybrid")
+        strategy = str(rng.choice(["gcv", "fixed"])) if hybrid else "none"
+        K = int(rng.integers(1, 14))
+        restart = int(rng.choice([0, 0, 3])) if K > 4 else 0
+        kw = dict(method=method, lambda_strategy=strategy, max_iter=K, restart_period=restart)
+        if strategy == "fixed":
+            kw["lambda_value"] = float(rng.choice([0.05, 0.5, 3.0]))
+        tag = (seed, case, nx, ny, h, sp, D, na, kw)
+        grid = ct.ImageGrid(nx, ny, h)
+        geom = ct.ParallelGeometry(ang, D, sp)
+        A = ct.forward_ray_driven(grid, geom)
+        B = ct.back_pixel_driven(grid, geom)
+        og = O.Geometry(nx, ny, h, geom.angles, D, sp)
+        x_true = rng.random(nx * ny).astype(np.float32).astype(np.float64)
+        clean = O.forward(og, x_true)
+        b = clean + 0.02 * np.linalg.norm(clean) / np.sqrt(clean.size) * rng.standard_normal(clean.size)
+        b = b.astype(np.float32).astype(np.float64)
+        x0 = (0.1 * rng.random(nx * ny)).astype(np.float32).astype(np.float64) if rng.random() < 0.3 else None
+        res = gmres.run_gmres(A, B, b, gmres.SolverConfig(x0=x0, **kw))
+        ref = O.gmres(lambda v: O.forward(og, v), lambda v: O.back(og, v), b, method, strategy, K,
+                      lambda_value=kw.get("lambda_value"), restart_period=restart, x0=x0)
+        # a Krylov space that exhausts exactly (tiny problems) breaks down at a
+        # rounding-dependent step: compare the common prefix then
+        n_cmp = min(len(res.records), len(ref.records))
+        if ref.stop_reason != "breakdown" and res.stop_reason != "breakdown":
+            assert res.stop_reason == ref.stop_reason, tag
+            assert len(res.records) == len(ref.records), tag
+            assert res.cycles == ref.cycles, tag
+        n_cmp = min(n_cmp, 8)
+        for i in range(n_cmp):
+            r, q = res.records[i], ref.records[i]
+            if hybrid:
+                assert r.lambda_used == pytest.approx(q["lambda_used"], rel=1e-2), (tag, i)
+            assert r.data_residual_norm == pytest.approx(q["data_residual_norm"], rel=2e-3), (tag, i)
+            assert r.solution_norm == pytest.approx(q["solution_norm"], rel=2e-3), (tag, i)
+        if len(res.records) == len(ref.records) and len(ref.records) <= 8 and ref.stop_reason != "breakdown":
+            assert np.linalg.norm(res.x - ref.x) <= 2e-3 * max(np.linalg.norm(ref.x), 1e-30), tag

@@ -452,3 +452,41 @@ def test_random_geometries_vs_oracle(cuda, seed):
         Atu = dg.adjoint(to_dev(cuda, u)).cpu().numpy().astype(np.float64)
         lhs, rhs = Ax @ u, x @ Atu
         assert lhs == pytest.approx(rhs, rel=5e-6, abs=1e-6 * sa * np.abs(u).sum()), tag
+
+
+@pytest.mark.parametrize("nx,ny,h,sp,na", [(517, 300, 0.9, 1.2, 77), (300, 517, 1.2, 0.9, 77),
+                                           (700, 650, 0.55, 1.0, 91), (650, 700, 1.0, 0.6, 91),
+                                           (1111, 1030, 1.0, 1.0, 64)])
+def test_mid_size_odd_geometries_vs_oracle(cuda, nx, ny, h, sp, na):
+    """A, B and A^T on image sizes between the tile-shape / warp-layout
+    switches (256^2, 512^2, 1024 px), not multiples of any tile, with
+    non-unit spacings and an angle count that is not a multiple of 4 or 32."""
+    torch = cuda
+    D = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
+    ang = (np.arange(na) + 0.3) * np.pi / na
+    ang[0] = 0.0
+    dg, og = make(nx, ny, h, ang, D, sp)
+    rng = np.random.default_rng(nx * 7 + ny)
+    x = rng.random(nx * ny).astype(np.float32).astype(np.float64)
+    u = rng.random(na * D).astype(np.float32).astype(np.float64)
+    Ax, Bu = O.forward(og, x), O.back(og, u)
+    y = dg.forward(to_dev(cuda, x)).cpu().numpy()
+    xb = dg.back(to_dev(cuda, u)).cpu().numpy()
+    assert rel_l2(y, Ax) <= REL_L2 and rel_l2(xb, Bu) <= REL_L2
+    np.testing.assert_allclose(y, Ax, rtol=0, atol=4e-6 * np.abs(Ax).max())
+    np.testing.assert_allclose(xb, Bu, rtol=0, atol=4e-6 * np.abs(Bu).max())
+    Atu = dg.adjoint(to_dev(cuda, u)).cpu().numpy().astype(np.float64)
+    assert Ax @ u == pytest.approx(x @ Atu, rel=3e-6)
+    # a sub-range of angles, forward with the residual epilogue and back with x0
+    a0, a1 = 5, na - 9
+    bvec = rng.random((a1 - a0) * D).astype(np.float32)
+    ys = dg.forward(to_dev(cuda, x), a0=a0, a1=a1, b=to_dev(cuda, bvec)).cpu().numpy()
+    np.testing.assert_allclose(ys, bvec.astype(np.float64) - Ax.reshape(na, D)[a0:a1].ravel(),
+                               rtol=0, atol=4e-6 * np.abs(Ax).max())
+    x0 = rng.random(nx * ny).astype(np.float32)
+    us = np.zeros((na, D))
+    us[a0:a1] = u.reshape(na, D)[a0:a1]
+    xs = dg.back(to_dev(cuda, u.reshape(na, D)[a0:a1].ravel()), a0=a0, a1=a1,
+                 x0=to_dev(cuda, x0)).cpu().numpy()
+    np.testing.assert_allclose(xs, x0.astype(np.float64) + O.back(og, us.ravel()), rtol=0,
+                               atol=4e-6 * np.abs(Bu).max())

@@ -319,3 +319,39 @@ def test_arnoldi_step_host_operator_and_breakdown(cuda):
     st2 = arnoldi.ArnoldiState.start(np.ones(6))
     arnoldi.arnoldi_step(st2, M, reorthogonalize=False)
     assert st2.k == 1 and len(st2.basis) == 2
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_gram_schmidt_chains_random_lengths(cuda, seed):
+    """Seeded random vector lengths from 2 to 3e6 (odd, prime-ish, around the
+    path switches: fused / SMEM-resident / streamed, 128- and 256-float tiles,
+    ragged last tiles) and chain lengths: every step of a chain on one basis
+    against fp64 MGS + reorthogonalisation on the stored rows."""
+    torch = cuda
+    rng = np.random.default_rng(500 + seed)
+    pool = [2, 3, 5, 17, 63, 64, 65, 255, 257, 1000, 4099, 32941, 65537, 151553, 151556,
+            151808, 262147, 600001, 1000003, 2086561, 3000017]
+    for _ in range(4):
+        L = int(rng.choice(pool))
+        K = int(min(L - 1, rng.integers(1, 12) if L > 300000 else rng.integers(1, 40)))
+        if K < 1:
+            continue
+        B = DeviceBasis(L, K + 2, torch.device("cuda", 0), torch)
+        v0 = rng.standard_normal(L)
+        B.W[0, :L] = torch.from_numpy((v0 / np.linalg.norm(v0)).astype(np.float32)).cuda()
+        st = torch.cuda.current_stream()
+        h = torch.zeros(K + 8, dtype=torch.float64, device="cuda")
+        stat = torch.zeros(4, dtype=torch.float64, device="cuda")
+        for k in range(K):
+            Q = B.W[: k + 1, :L].cpu().numpy().astype(np.float64).T
+            q = (rng.standard_normal(L) + Q @ rng.standard_normal(k + 1)).astype(np.float32)
+            B.cgs2_step(k, torch.from_numpy(q).cuda(), h, stat, st)
+            torch.cuda.synchronize()
+            href, v = mgs2_ref(Q, q.astype(np.float64))
+            hg = h.cpu().numpy()[: k + 2]
+            assert np.abs(hg - href).max() <= 1e-5 * np.abs(href).max(), (L, K, k)
+            w = B.W[k + 1, :L].cpu().numpy().astype(np.float64)
+            assert np.abs(w - v / href[k + 1]).max() < 5e-6, (L, K, k)
+        W = B.W[: K + 1, :L].cpu().numpy().astype(np.float64)
+        G = W @ W.T
+        assert np.abs(G - np.eye(K + 1)).max() < 3e-6, (L, K)

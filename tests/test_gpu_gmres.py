@@ -514,3 +514,32 @@ def test_random_small_problems_vs_oracle(cuda, seed):
             assert r.solution_norm == pytest.approx(q["solution_norm"], rel=2e-3), (tag, i)
         if len(res.records) == len(ref.records) and len(ref.records) <= 8 and ref.stop_reason != "breakdown":
             assert np.linalg.norm(res.x - ref.x) <= 2e-3 * max(np.linalg.norm(ref.x), 1e-30), tag
+
+
+@pytest.mark.parametrize("nx,ny,h,sp", [(37, 22, 0.8, 1.1), (9, 64, 1.0, 1.0), (70, 70, 1.5, 0.7)])
+def test_device_metrics_and_snapshots_on_nonsquare_images(cuda, nx, ny, h, sp):
+    """Row f1 on non-square images (SSIM's 7 x 7 window against both image
+    extents, images smaller than the window in one direction): per-iteration
+    RRE / SSIM from the device equal metrics.rre / metrics.ssim (the
+    reference formulas) of the snapshot iterates."""
+    from oracle import oracle as O
+    from paper_2602_17892_b200 import ct, gmres, metrics
+    na = 40
+    D = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
+    grid = ct.ImageGrid(nx, ny, h)
+    geom = ct.ParallelGeometry(np.arange(na) * np.pi / na, D, sp)
+    A = ct.forward_ray_driven(grid, geom)
+    B = ct.back_pixel_driven(grid, geom)
+    og = O.Geometry(nx, ny, h, geom.angles, D, sp)
+    rng = np.random.default_rng(nx + ny)
+    x_true = rng.random(nx * ny).astype(np.float32).astype(np.float64)
+    b = O.forward(og, x_true)
+    b = (b * (1 + 0.01 * rng.standard_normal(b.size))).astype(np.float32).astype(np.float64)
+    cfg = gmres.SolverConfig(method="ba-hybrid", lambda_strategy="gcv", max_iter=6,
+                             snapshot_stride=1)
+    res = gmres.run_gmres(A, B, b, cfg, x_true=x_true, image_shape=(ny, nx))
+    assert sorted(res.snapshots) == [1, 2, 3, 4, 5, 6]
+    for r in res.records:
+        xk = res.snapshots[r.k]
+        assert r.rre == pytest.approx(metrics.rre(xk, x_true), rel=1e-5)
+        assert r.ssim == pytest.approx(metrics.ssim(xk, x_true, (ny, nx)), rel=1e-4, abs=1e-6)

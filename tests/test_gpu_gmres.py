@@ -543,3 +543,54 @@ def test_device_metrics_and_snapshots_on_nonsquare_images(cuda, nx, ny, h, sp):
         xk = res.snapshots[r.k]
         assert r.rre == pytest.approx(metrics.rre(xk, x_true), rel=1e-5)
         assert r.ssim == pytest.approx(metrics.ssim(xk, x_true, (ny, nx)), rel=1e-4, abs=1e-6)
+
+
+ODD_CASES = {
+    "ba_gcv_restart": dict(method="ba-hybrid", lambda_strategy="gcv", max_iter=10, restart_period=4),
+    "ab_plain": dict(method="ab", max_iter=8),
+    "lsqr_gcv": dict(method="lsqr-hybrid", lambda_strategy="gcv", max_iter=10),
+    "lsmr_plain": dict(method="lsmr", max_iter=8),
+    "lsmr_gcv": dict(method="lsmr-hybrid", lambda_strategy="gcv", max_iter=10),
+}
+
+
+def test_odd_geometry_operators_vs_reference(cuda, golden):
+    """K1, K2 and K7 against the unmodified reference's A x, B u and A^T u on
+    the odd-geometry fixture (tests/golden/make_golden_odd.py)."""
+    d = golden("odd_geometry")
+    nx, ny, h, D, sp = d["params"]
+    dg = ct.DeviceGeometry(ct.ImageGrid(int(nx), int(ny), float(h)),
+                           ct.ParallelGeometry(d["angles"], int(D), float(sp)), 0)
+    dev = lambda v: cuda.from_numpy(np.asarray(v, dtype=np.float32)).cuda()   # noqa: E731
+    assert rel(dg.forward(dev(d["x"])).cpu().numpy(), d["Ax"]) <= 1e-5
+    assert rel(dg.back(dev(d["u"])).cpu().numpy(), d["Bu"]) <= 1e-5
+    assert rel(dg.adjoint(dev(d["u"])).cpu().numpy(), d["Atu"]) <= 1e-5
+
+
+@pytest.mark.parametrize("case", sorted(ODD_CASES))
+def test_odd_geometry_solvers_vs_reference(cuda, golden, case):
+    """run_gmres (hybrid BA with restarts, plain AB) and the Golub-Kahan
+    solvers on the matched pair against the unmodified reference's records on
+    the odd-geometry fixture: lambda within 1%, norms and x within 1e-3."""
+    from paper_2602_17892_b200 import gk
+    d = golden("odd_geometry")
+    nx, ny, h, D, sp = d["params"]
+    grid = ct.ImageGrid(int(nx), int(ny), float(h))
+    geom = ct.ParallelGeometry(d["angles"], int(D), float(sp))
+    A, B = ct.forward_ray_driven(grid, geom), ct.back_pixel_driven(grid, geom)
+    kw = ODD_CASES[case]
+    cfg = gmres.SolverConfig(**kw)
+    if kw["method"].startswith("ls"):
+        run = gk.run_lsqr if kw["method"].startswith("lsqr") else gk.run_lsmr
+        res = run(A, ct.matched_back(A), d["b"], cfg)
+    else:
+        res = gmres.run_gmres(A, B, d["b"], cfg)
+        assert res.cycles == int(d[f"{case}/cycles"])
+    assert res.stop_reason == str(d[f"{case}/stop"])
+    assert len(res.records) == len(d[f"{case}/rec/k"])
+    for f in ("data_residual_norm", "residual_norm", "solution_norm"):
+        np.testing.assert_allclose(records(res, f), d[f"{case}/rec/{f}"], rtol=1e-3, err_msg=f)
+    if "gcv" in case:
+        np.testing.assert_allclose(records(res, "lambda_used"), d[f"{case}/rec/lambda_used"],
+                                   rtol=1e-2)
+    assert rel(res.x, d[f"{case}/x"]) <= 1e-3

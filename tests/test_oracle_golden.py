@@ -177,3 +177,28 @@ def test_harness_phantom_is_oracle_phantom():
     rows = [(rho, a, b, cx, cy, phi) for cx, cy, a, b, phi, rho in problems.ellipse_params(N, 10, 5)]
     ref = O.phantom(N, N, 1.0, rows).astype(np.float32).astype(np.float64)
     np.testing.assert_array_equal(problems.random_ellipse_phantom(N, 10, 5), ref)
+
+
+def test_odd_geometry_operators_and_solves(golden):
+    """The oracle on the odd-geometry fixture (tests/golden/make_golden_odd.py:
+    37 x 22 px of 0.8, bins of 1.1, non-uniform angles with an exact and a
+    nearly axis-aligned member): A x, B u bit for bit, the adjoint through
+    <A x, u>, and the hybrid BA-GMRES (with restarts) / plain AB-GMRES records
+    of the reference's run_gmres."""
+    d = golden("odd_geometry")
+    nx, ny, h, D, sp = d["params"]
+    g = O.Geometry(int(nx), int(ny), float(h), d["angles"], int(D), float(sp))
+    np.testing.assert_array_equal(O.forward(g, d["x"]), d["Ax"])
+    np.testing.assert_array_equal(O.back(g, d["u"]), d["Bu"])
+    assert d["Ax"] @ d["u"] == pytest.approx(d["x"] @ d["Atu"], rel=1e-13)
+    fwd, back = (lambda v: O.forward(g, v)), (lambda v: O.back(g, v))
+    for name, kw in (("ba_gcv_restart", dict(method="ba-hybrid", strategy="gcv", max_iter=10,
+                                             restart_period=4)),
+                     ("ab_plain", dict(method="ab", strategy="none", max_iter=8))):
+        res = O.gmres(fwd, back, d["b"], **kw)
+        assert res.stop_reason == str(d[f"{name}/stop"]) and res.cycles == int(d[f"{name}/cycles"])
+        for f in ("lambda_used", "data_residual_norm", "residual_norm", "solution_norm"):
+            got = np.array([r[f] for r in res.records])
+            np.testing.assert_allclose(got, d[f"{name}/rec/{f}"], rtol=1e-9, err_msg=(name, f))
+        np.testing.assert_allclose(res.x, d[f"{name}/x"], rtol=0,
+                                   atol=1e-9 * np.abs(d[f"{name}/x"]).max())

@@ -490,3 +490,36 @@ def test_mid_size_odd_geometries_vs_oracle(cuda, nx, ny, h, sp, na):
                  x0=to_dev(cuda, x0)).cpu().numpy()
     np.testing.assert_allclose(xs, x0.astype(np.float64) + O.back(og, us.ravel()), rtol=0,
                                atol=4e-6 * np.abs(Bu).max())
+
+
+@pytest.mark.parametrize("nx,ny,h,sp,na", [
+    (600, 600, 4.0, 0.5, 40),      # pixel shadows of 11 bins (K7's general loop), 46-48 KB windows
+    (600, 600, 4.2, 1.0, 24),      # K2 windows of ~190 pairs: dynamic + static SMEM just over 48 KB
+    (600, 600, 0.25, 2.0, 40),     # 8 pixels per bin: windows of a few bins
+    (300, 280, 10.0, 0.5, 30), (300, 280, 0.1, 2.0, 30),
+    (2000, 64, 1.0, 1.0, 33), (64, 2000, 1.0, 1.0, 33),     # extreme aspect ratios
+    (1, 700, 1.0, 1.0, 20), (700, 1, 1.0, 1.0, 20)])        # single-column / single-row images
+def test_extreme_geometries_vs_oracle(cuda, nx, ny, h, sp, na):
+    """Pixel / bin ratios of 0.05 to 20 on mid-size images, extreme aspect
+    ratios and one-pixel-wide images: A, B against the oracle, A^T through the
+    adjoint identity with the oracle's A x."""
+    D = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
+    ang = (np.arange(na) + 0.25) * np.pi / na
+    dg, og = make(nx, ny, h, ang, D, sp)
+    rng = np.random.default_rng(1)
+    x = rng.random(nx * ny).astype(np.float32).astype(np.float64)
+    u = rng.random(na * D).astype(np.float32).astype(np.float64)
+    Ax, Bu = O.forward(og, x), O.back(og, u)
+    assert rel_l2(dg.forward(to_dev(cuda, x)).cpu().numpy(), Ax) <= REL_L2
+    assert rel_l2(dg.back(to_dev(cuda, u)).cpu().numpy(), Bu) <= REL_L2
+    Atu = dg.adjoint(to_dev(cuda, u)).cpu().numpy().astype(np.float64)
+    assert Ax @ u == pytest.approx(x @ Atu, rel=2e-6)
+
+
+def test_unsupported_pixel_bin_ratio_is_a_geometry_error(cuda):
+    """Bins 60 times narrower than the pixels: the tile's detector window no
+    longer fits in shared memory -- refused at geometry creation with the
+    reference's exception type, not at the first apply."""
+    with pytest.raises(ct.GeometryError, match="pixel/bin ratio"):
+        ct.DeviceGeometry(ct.ImageGrid(520, 520, 30.0),
+                          ct.ParallelGeometry(np.arange(16) * np.pi / 16, 44000, 0.5), 0)

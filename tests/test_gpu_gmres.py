@@ -419,7 +419,8 @@ def test_ba_chaining_is_bitwise_the_unchained_step(cuda, tmp_path):
 
 
 
-@pytest.mark.parametrize("nx,ny,h,sp", [(150, 131, 0.8, 1.1), (97, 260, 1.3, 0.9), (300, 280, 0.6, 1.0)])
+@pytest.mark.parametrize("nx,ny,h,sp", [(150, 131, 0.8, 1.1), (97, 260, 1.3, 0.9), (300, 280, 0.6, 1.0),
+                                        (600, 560, 4.0, 0.5), (300, 280, 0.1, 2.0), (900, 48, 1.0, 1.0)])
 @pytest.mark.parametrize("method", ["ab-hybrid", "ba-hybrid"])
 def test_solves_on_odd_geometries_vs_oracle(cuda, method, nx, ny, h, sp):
     """Whole hybrid solves away from the BASELINE shapes: non-square images

@@ -481,8 +481,13 @@ extern "C" int ctk_adjoint(const ctk_geom_t* gc, const float* u, float* x, int a
     const bool p4 = g->back_ppt == 4;
     auto kern = p4 ? (taps == 1 ? k_adjoint<4, 1> : taps == 2 ? k_adjoint<4, 2> : k_adjoint<4, 4>)
                    : (taps == 1 ? k_adjoint<2, 1> : taps == 2 ? k_adjoint<2, 2> : k_adjoint<2, 4>);
-    if (smem > 40 * 1024)       // opt in early: the 48 KB default also counts the static arrays
-        CTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // Opt in early (the 48 KB default also counts the static arrays) and always
+    // to the same value, the largest window any geometry may have: the limit
+    // is per function, so concurrent launches for geometries with different
+    // window sizes must not lower it under each other.
+    if (smem > 40 * 1024)
+        CTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
     kern<<<grid, block, smem, st>>>(A);
     CTK_LAUNCH_CHECK("k_adjoint");
     return CTK_OK;

@@ -626,8 +626,13 @@ int ctk_back_xc(const ctk_geom_t* g, const float* u, float* x, int a0, int a1, c
                                                       : k_back<2, true, 0>)
                      : (ppt == 4 ? k_back<4, false, 0> : ppt == 1 ? k_back<1, false, 0>
                                                        : k_back<2, false, 0>));
-    if (smem > 40 * 1024)       // opt in early: the 48 KB default also counts the static arrays
-        CTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // Opt in early (the 48 KB default also counts the static arrays) and always
+    // to the same value, the largest window any geometry may have: the limit
+    // is per function, so concurrent launches for geometries with different
+    // window sizes must not lower it under each other.
+    if (smem > 40 * 1024)
+        CTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
     const int ph = ctk_prof_open(1, st);
     if (pairs) {
         const int64_t total = (int64_t)(a1 - a0) * A.Dp;

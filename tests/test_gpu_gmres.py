@@ -595,3 +595,44 @@ def test_odd_geometry_solvers_vs_reference(cuda, golden, case):
         np.testing.assert_allclose(records(res, "lambda_used"), d[f"{case}/rec/lambda_used"],
                                    rtol=1e-2)
     assert rel(res.x, d[f"{case}/x"]) <= 1e-3
+
+
+def test_concurrent_solves_on_different_geometries(cuda):
+    """Several host threads, each solving on its OWN geometry (different image
+    shapes, spacings and hence window sizes, tile shapes and Gram-Schmidt
+    paths) at the same time, repeatedly: every result equals the same solve
+    run alone.  Per-function and per-process state (shared-memory opt-in,
+    cached environment switches, scratch-keyed Gram chains, workspaces) must
+    not leak between geometries."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import oracle as O
+    from paper_2602_17892_b200 import ct, gmres
+    specs = [(150, 131, 0.8, 1.1, "ba-hybrid"), (600, 560, 4.0, 0.5, "ab-hybrid"),
+             (97, 260, 1.3, 0.9, "ab-hybrid"), (300, 280, 0.1, 2.0, "ba-hybrid"),
+             (64, 64, 1.0, 1.0, "ba-hybrid"), (520, 515, 5.0, 1.0, "ba-hybrid")]
+    probs = []
+    for i, (nx, ny, h, sp, method) in enumerate(specs):
+        na = 40 + 3 * i
+        D = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
+        grid = ct.ImageGrid(nx, ny, h)
+        geom = ct.ParallelGeometry(np.arange(na) * np.pi / na, D, sp)
+        A, B = ct.forward_ray_driven(grid, geom), ct.back_pixel_driven(grid, geom)
+        og = O.Geometry(nx, ny, h, geom.angles, D, sp)
+        rng = np.random.default_rng(i)
+        b = O.forward(og, rng.random(nx * ny).astype(np.float32).astype(np.float64))
+        b = (b * (1 + 0.01 * rng.standard_normal(b.size))).astype(np.float32).astype(np.float64)
+        cfg = gmres.SolverConfig(method=method, lambda_strategy="gcv", max_iter=8)
+        probs.append((A, B, b, cfg))
+    alone = [gmres.run_gmres(A, B, b, cfg) for A, B, b, cfg in probs]
+
+    def solve(i):
+        A, B, b, cfg = probs[i]
+        return gmres.run_gmres(A, B, b, cfg, stream=cuda.cuda.Stream())
+
+    with ThreadPoolExecutor(max_workers=len(probs)) as pool:
+        for _ in range(3):
+            outs = list(pool.map(solve, range(len(probs))))
+            for i, (r, q) in enumerate(zip(outs, alone)):
+                assert r.stop_reason == q.stop_reason and len(r.records) == len(q.records), i
+                np.testing.assert_array_equal(r.x, q.x, err_msg=str(specs[i]))
+                np.testing.assert_array_equal(records(r, "lambda_used"), records(q, "lambda_used"))

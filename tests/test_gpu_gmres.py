@@ -636,3 +636,30 @@ def test_concurrent_solves_on_different_geometries(cuda):
                 assert r.stop_reason == q.stop_reason and len(r.records) == len(q.records), i
                 np.testing.assert_array_equal(r.x, q.x, err_msg=str(specs[i]))
                 np.testing.assert_array_equal(records(r, "lambda_used"), records(q, "lambda_used"))
+
+
+@pytest.mark.parametrize("nx,ny", [(1024, 1024), (1500, 700), (8, 8), (9, 4000)])
+def test_device_metrics_kernel_vs_reference_formulas(cuda, nx, ny):
+    """ctk_metrics alone at the large-config image sizes and at the smallest
+    image SSIM is defined on (one 8 x 8... 7 x 7-window position): RRE and
+    SSIM equal metrics.rre / metrics.ssim (the reference's formulas,
+    ctkrylov/metrics.py:13-62) of the same fp32 images."""
+    import ctypes
+    from paper_2602_17892_b200 import _native, metrics
+    torch = cuda
+    lib = _native.load()
+    rng = np.random.default_rng(nx + 3 * ny)
+    xt = rng.random(nx * ny).astype(np.float32)
+    x = (xt + 0.05 * rng.standard_normal(nx * ny)).astype(np.float32)
+    xd, xtd = torch.from_numpy(x).cuda(), torch.from_numpy(xt).cuda()
+    out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    scratch = torch.zeros(int(lib.ctk_metrics_scratch_bytes()), dtype=torch.uint8, device="cuda")
+    dyn = float(xt.max() - xt.min())
+    _native.check(lib.ctk_metrics(xd.data_ptr(), xtd.data_ptr(), nx, ny, ctypes.c_double(dyn),
+                                  out.data_ptr(), scratch.data_ptr(),
+                                  torch.cuda.current_stream().cuda_stream), "ctk_metrics")
+    o = out.cpu().numpy()
+    x64, xt64 = x.astype(np.float64), xt.astype(np.float64)
+    assert np.sqrt(o[0]) / np.linalg.norm(xt64) == pytest.approx(metrics.rre(x64, xt64), rel=1e-10)
+    ssim_dev = o[1] / ((nx - 7) * (ny - 7))
+    assert ssim_dev == pytest.approx(metrics.ssim(x64, xt64, (ny, nx), dyn), rel=1e-5, abs=1e-7)

@@ -663,3 +663,30 @@ def test_device_metrics_kernel_vs_reference_formulas(cuda, nx, ny):
     assert np.sqrt(o[0]) / np.linalg.norm(xt64) == pytest.approx(metrics.rre(x64, xt64), rel=1e-10)
     ssim_dev = o[1] / ((nx - 7) * (ny - 7))
     assert ssim_dev == pytest.approx(metrics.ssim(x64, xt64, (ny, nx), dyn), rel=1e-5, abs=1e-7)
+
+
+@pytest.mark.parametrize("nx,ny,na,K", [(90, 80, 200, 135), (300, 280, 60, 132)])
+def test_long_ab_runs_past_the_gram_limit(cuda, nx, ny, na, K):
+    """More than 128 Arnoldi steps in one cycle: past the Gram scratch (127
+    rows) the single-launch paths drop the Gram correction, past their row
+    limits the multi-kernel CGS2 takes over.  AB-GCV against the oracle: lambda
+    and residuals to 1e-4 at every iteration, x to 1e-4."""
+    from oracle import oracle as O
+    from paper_2602_17892_b200 import ct, gmres
+    D = int(np.ceil(np.hypot(nx, ny))) + 3
+    grid = ct.ImageGrid(nx, ny, 1.0)
+    geom = ct.ParallelGeometry(np.arange(na) * np.pi / na, D, 1.0)
+    A, B = ct.forward_ray_driven(grid, geom), ct.back_pixel_driven(grid, geom)
+    og = O.Geometry(nx, ny, 1.0, geom.angles, D, 1.0)
+    rng = np.random.default_rng(3)
+    b = O.forward(og, rng.random(nx * ny).astype(np.float32).astype(np.float64))
+    b = (b * (1 + 0.02 * rng.standard_normal(b.size))).astype(np.float32).astype(np.float64)
+    res = gmres.run_gmres(A, B, b, gmres.SolverConfig(method="ab-hybrid", lambda_strategy="gcv",
+                                                      max_iter=K))
+    ref = O.gmres(lambda v: O.forward(og, v), lambda v: O.back(og, v), b, "ab-hybrid", "gcv", K)
+    assert res.stop_reason == ref.stop_reason == "maxiter" and len(res.records) == K
+    np.testing.assert_allclose(records(res, "lambda_used"),
+                               [r["lambda_used"] for r in ref.records], rtol=1e-4)
+    np.testing.assert_allclose(records(res, "data_residual_norm"),
+                               [r["data_residual_norm"] for r in ref.records], rtol=1e-4)
+    assert rel(res.x, ref.x) <= 1e-4

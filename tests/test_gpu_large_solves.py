@@ -108,3 +108,33 @@ def test_large_odd_geometry_solve_vs_oracle(cuda, method):
     want = np.array([r["data_residual_norm"] for r in ref.records])
     np.testing.assert_allclose(got, want, rtol=1e-4 + 2 * np.abs(lam / lam_ref - 1).max())
     assert np.linalg.norm(res.x - ref.x) <= 1e-3 * np.linalg.norm(ref.x)
+
+
+@pytest.mark.parametrize("method,nx,ny,na", [("ab-hybrid", 400, 420, 380), ("ba-hybrid", 520, 500, 100)])
+def test_restarted_solves_on_the_streamed_gram_schmidt_path(cuda, method, nx, ny, na):
+    """Restart cycles with Krylov vectors long enough for the streamed
+    Gram-Schmidt kernel (L >= 151k): every cycle restarts the Gram chain at
+    k = 0 on the same scratch, x0 of a cycle is the previous iterate.  Against
+    the oracle: stop reason, cycles, lambda within 1%, residuals, x."""
+    nx, ny = int(nx), int(ny)
+    D = int(np.ceil(np.hypot(nx, ny))) + 3
+    grid = ct.ImageGrid(nx, ny, 1.0)
+    geom = ct.ParallelGeometry(np.arange(na) * np.pi / na, D, 1.0)
+    A, B = ct.forward_ray_driven(grid, geom), ct.back_pixel_driven(grid, geom)
+    og = O.Geometry(nx, ny, 1.0, geom.angles, D, 1.0)
+    rng = np.random.default_rng(8)
+    b = O.forward(og, rng.random(nx * ny).astype(np.float32).astype(np.float64))
+    b = (b * (1 + 0.02 * rng.standard_normal(b.size))).astype(np.float32).astype(np.float64)
+    K, period = 17, 6
+    cfg = gmres.SolverConfig(method=method, lambda_strategy="gcv", max_iter=K, restart_period=period)
+    res = gmres.run_gmres(A, B, b, cfg)
+    ref = O.gmres(lambda v: O.forward(og, v), lambda v: O.back(og, v), b, method, "gcv", K,
+                  restart_period=period)
+    assert res.stop_reason == ref.stop_reason and res.cycles == ref.cycles == 3
+    lam = np.array([r.lambda_used for r in res.records])
+    lam_ref = np.array([r["lambda_used"] for r in ref.records])
+    np.testing.assert_allclose(lam, lam_ref, rtol=1e-2)
+    got = np.array([r.data_residual_norm for r in res.records])
+    want = np.array([r["data_residual_norm"] for r in ref.records])
+    np.testing.assert_allclose(got, want, rtol=1e-4 + 2 * np.abs(lam / lam_ref - 1).max())
+    assert np.linalg.norm(res.x - ref.x) <= 1e-3 * np.linalg.norm(ref.x)

@@ -138,3 +138,36 @@ def test_restarted_solves_on_the_streamed_gram_schmidt_path(cuda, method, nx, ny
     want = np.array([r["data_residual_norm"] for r in ref.records])
     np.testing.assert_allclose(got, want, rtol=1e-4 + 2 * np.abs(lam / lam_ref - 1).max())
     assert np.linalg.norm(res.x - ref.x) <= 1e-3 * np.linalg.norm(ref.x)
+
+
+@pytest.mark.parametrize("method,rule", [("ab", "dp"), ("ba", "rns"), ("ab-hybrid", "dp")])
+def test_stopping_rules_on_the_streamed_path(cuda, method, rule):
+    """Discrepancy-principle / residual-stagnation stops with streamed-length
+    Krylov vectors: the driver consumes each iterate's residual norm before
+    the next record while the Arnoldi look-ahead keeps running.  Same stop
+    iteration as the oracle, records and x within the bars."""
+    nx, ny, na = 400, 420, 380
+    D = int(np.ceil(np.hypot(nx, ny))) + 3
+    grid = ct.ImageGrid(nx, ny, 1.0)
+    geom = ct.ParallelGeometry(np.arange(na) * np.pi / na, D, 1.0)
+    A, B = ct.forward_ray_driven(grid, geom), ct.back_pixel_driven(grid, geom)
+    og = O.Geometry(nx, ny, 1.0, geom.angles, D, 1.0)
+    rng = np.random.default_rng(12)
+    clean = O.forward(og, problems.random_ellipse_phantom(max(nx, ny), 8, 2)
+                      .reshape(max(nx, ny), -1)[:ny, :nx].ravel().astype(np.float64))
+    noise = 0.03 * np.linalg.norm(clean) / np.sqrt(clean.size) * rng.standard_normal(clean.size)
+    b = (clean + noise).astype(np.float32).astype(np.float64)
+    nn = float(np.linalg.norm(b - clean))
+    kw = dict(method=method, max_iter=40, stopping_rule=rule, noise_norm=nn, rns_epsilon=2e-3)
+    if method.endswith("hybrid"):
+        kw["lambda_strategy"] = "gcv"
+    res = gmres.run_gmres(A, B, b, gmres.SolverConfig(**kw))
+    ref = O.gmres(lambda v: O.forward(og, v), lambda v: O.back(og, v), b, method,
+                  kw.get("lambda_strategy", "none"), 40, stopping_rule=rule, noise_norm=nn,
+                  rns_epsilon=2e-3)
+    assert res.stop_reason == ref.stop_reason
+    assert len(res.records) == len(ref.records)
+    got = np.array([r.data_residual_norm for r in res.records])
+    want = np.array([r["data_residual_norm"] for r in ref.records])
+    np.testing.assert_allclose(got, want, rtol=1e-3)
+    assert np.linalg.norm(res.x - ref.x) <= 2e-3 * np.linalg.norm(ref.x)

@@ -326,11 +326,22 @@ struct IbVec<2> {
 
 // V floats per thread and row, IB_RB rows loaded per batch.
 #ifndef CTK_IB_RB
-#define CTK_IB_RB 8
+#define CTK_IB_RB 12
 #endif
 constexpr int IB_RB = CTK_IB_RB;
 template <int V>
-__global__ void __launch_bounds__(IB_T) k_iter_batch(IterBatchJob j0, IterBatchJob j1,
+// Resident CTAs per SM: 4 (128 registers, a few spilled) rather than the 2
+// that 174 registers allow -- the pass is bound by bytes in flight.  Measured
+// at c4 / c5, k_max = 17 / 37 / 57, % of the HBM peak: 32 / 40 / 46 and
+// 38 / 45 / 50 before, 40 / 50 / 54 and 48 / 57 / 59 with 4 CTAs and 12 rows
+// of loads in flight per thread (3 CTAs: 37 / 46 / 53 and 45 / 54 / 60).
+#ifndef CTK_IB_MINB
+#define CTK_IB_MINB 4
+#endif
+#ifndef CTK_IB_GCAP
+#define CTK_IB_GCAP 4
+#endif
+__global__ void __launch_bounds__(IB_T, CTK_IB_MINB) k_iter_batch(IterBatchJob j0, IterBatchJob j1,
                                                      const double* __restrict__ y, int ystride,
                                                      int k0, int nb) {
     __shared__ __align__(16) double cy[IB_MAXK][IB_NB];   // cy[j][b] = sgn * y_b[j] (0: j >= k_b)
@@ -2053,7 +2064,7 @@ int ctk_combine_pair(const float* X, int64_t ldx, const float* x0, float* x, int
 
 static int iter_batch_ctas(int64_t L) {
     int64_t G = ((L >> 2) + IB_T - 1) / IB_T;
-    if (G > 4 * 148) G = 4 * 148;
+    if (G > CTK_IB_GCAP * 148) G = CTK_IB_GCAP * 148;
     return (int)(G < 1 ? 1 : G);
 }
 

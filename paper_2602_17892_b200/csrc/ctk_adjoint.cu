@@ -83,8 +83,15 @@ struct TapT<1> {
     typedef float type;
 };
 
+// Resident CTAs per SM: 6 (40 registers; the few spills sit in the fp64
+// near-axis branch).  Unconstrained the kernels take 109 registers (2 CTAs):
+// At per apply at c2 / c3 / c4 / c5 0.070 / 0.243 / 1.61 / 7.68 ms against
+// 0.045 / 0.182 / 1.27 / 6.02 ms with 6 (4: 0.051 / 0.198 / 1.27 / 6.04).
+#ifndef CTK_ADJ_MINB
+#define CTK_ADJ_MINB 6
+#endif
 template <int JPPT, int TAPS>
-__global__ void __launch_bounds__(JTHREADS) k_adjoint(AdjArgs A) {
+__global__ void __launch_bounds__(JTHREADS, CTK_ADJ_MINB) k_adjoint(AdjArgs A) {
     constexpr int JTY = JROWS * JPPT;
     typedef typename TapT<TAPS>::type tap_t;
     extern __shared__ __align__(16) unsigned char wraw[];

@@ -105,7 +105,13 @@ __device__ void last_cta_reduce(const double* partial, int nchunks, int nv, unsi
 
 // out[j] = <W_j, v> (j < nvec); out[nvec] = <v, v> if want_norm.
 // grid = (nchunks, ceil(nv / JG)).
-__global__ void __launch_bounds__(KT) k_dots(const float* __restrict__ W, int64_t ld, int nvec,
+// 3 resident CTAs per SM (79 registers) instead of the 2 that 96 allow: the
+// multi-kernel CGS2 of the angle-sharded AB solve, c4 at world size 1,
+// 0.585 -> 0.539 ms per step (solve 178.9 -> 173.2 ms)
+#ifndef CTK_DOTS_MINB
+#define CTK_DOTS_MINB 3
+#endif
+__global__ void __launch_bounds__(KT, CTK_DOTS_MINB) k_dots(const float* __restrict__ W, int64_t ld, int nvec,
                                              const float* __restrict__ v, int64_t L, int want_norm,
                                              int64_t ch, double* out, double* partial,
                                              unsigned int* ticket) {

@@ -22,12 +22,12 @@ from paper_2602_17892_b200 import ct, dist, problems
 pytestmark = pytest.mark.gpu
 
 
-def run_exchange(torch, N, na, D, nranks, seeds=(1,), mode="interleaved"):
-    grid = ct.ImageGrid(N, N, 1.0)
+def run_exchange(torch, N, na, D, nranks, seeds=(1,), mode="interleaved", ny=None, h=1.0, sp=1.0):
+    grid = ct.ImageGrid(N, N if ny is None else ny, h)
     angles = np.arange(na) * np.pi / na
-    geom = ct.ParallelGeometry(angles, D, 1.0)
+    geom = ct.ParallelGeometry(angles, D, sp)
     shards = dist.angle_shards(na, nranks, mode)
-    dgs = [ct.DeviceGeometry(grid, ct.ParallelGeometry(angles[idx], D, 1.0), 0) for idx in shards]
+    dgs = [ct.DeviceGeometry(grid, ct.ParallelGeometry(angles[idx], D, sp), 0) for idx in shards]
     ex = [dist.PeerExchange(dgs[r], r, nranks) for r in range(nranks)]
     for e in ex:
         e.connect_local(ex)
@@ -91,3 +91,20 @@ def test_exchange_rejects_bad_setup(cuda):
     u = cuda.zeros(dg.m, dtype=cuda.float32, device="cuda")
     with pytest.raises(ValueError):
         ex.back(u)
+
+
+@pytest.mark.parametrize("nx,ny,h,sp,na,nranks", [(150, 131, 0.8, 1.1, 77, 3), (131, 600, 1.3, 0.9, 50, 4),
+                                                  (700, 90, 0.6, 1.0, 96, 8)])
+def test_exchange_on_odd_geometries(cuda, nx, ny, h, sp, na, nranks):
+    """The peer exchange on non-square images with non-unit spacings (tile
+    ownership, edge tiles, windows narrower / wider than a warp), rank counts
+    that do not divide the tile count: every rank bitwise the rank-ordered
+    sum, and the reference B within the bar."""
+    D = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
+    results, grid, geom = run_exchange(cuda, nx, na, D, nranks, ny=ny, h=h, sp=sp)
+    imgs, expect, whole, u = results[0]
+    for r, img in enumerate(imgs):
+        np.testing.assert_array_equal(img, expect, err_msg=f"rank {r}")
+    og = O.Geometry(nx, ny, h, geom.angles, D, sp)
+    ref = O.back(og, u.ravel().astype(np.float32).astype(np.float64))
+    assert np.linalg.norm(imgs[0] - ref) / np.linalg.norm(ref) <= 1e-5

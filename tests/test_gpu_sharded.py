@@ -131,3 +131,37 @@ def test_peer_exchange_two_processes_cuda_ipc(cuda, tmp_path):
     u = torch.from_numpy(problems.uniform_sinogram(spec.m, 9).astype(np.float32)).cuda()
     full = dg.back(u).cpu().numpy()
     assert rel(img0, full) < 1e-6
+
+
+@pytest.mark.parametrize("nx,ny,h,sp,na,method", [(150, 131, 0.8, 1.1, 77, "ab-hybrid"),
+                                                  (131, 300, 1.3, 0.9, 50, "ba-hybrid"),
+                                                  (400, 420, 1.0, 1.0, 381, "ab-hybrid")])
+def test_native_sharded_solve_on_odd_geometries(cuda, nx, ny, h, sp, na, method):
+    """The sharded driver (libctk's NCCL communicator, multi-kernel CGS2 with
+    its dots summed between launches, B through the communicator) at world
+    size 1 on non-square images with non-unit spacings and an angle count that
+    is not a multiple of 4, including streamed-length measurement vectors:
+    same records as the single-GPU solve."""
+    from oracle import oracle as O
+    D = int(np.ceil(np.hypot(nx, ny) * h / sp)) + 3
+    grid = ct.ImageGrid(nx, ny, h)
+    geom = ct.ParallelGeometry(np.arange(na) * np.pi / na, D, sp)
+    og = O.Geometry(nx, ny, h, geom.angles, D, sp)
+    rng = np.random.default_rng(nx)
+    b = O.forward(og, rng.random(nx * ny).astype(np.float32).astype(np.float64))
+    b = (b * (1 + 0.02 * rng.standard_normal(b.size))).astype(np.float32).astype(np.float64)
+    K = 14
+    cfg = gmres.SolverConfig(method=method, lambda_strategy="gcv", max_iter=K)
+    idx = dist.angle_shards(na, 1)[0]
+    A, B = dist.sharded_projectors(grid, geom, idx)
+    comm = dist.NativeComm(A.dgeom)
+    res = gmres.run_gmres(A, B, dist.local_rows(b, D, idx), cfg, comm=comm)
+    ref = gmres.run_gmres(ct.forward_ray_driven(grid, geom), ct.back_pixel_driven(grid, geom),
+                          b, cfg)
+    comm.close()
+    assert len(res.records) == len(ref.records) == K
+    f = lambda r, k: np.array([getattr(x, k) for x in r.records])  # noqa: E731
+    assert np.all(np.abs(f(res, "lambda_used") / f(ref, "lambda_used") - 1) <= 0.01)
+    for k in ("data_residual_norm", "proj_residual_norm", "solution_norm"):
+        np.testing.assert_allclose(f(res, k), f(ref, k), rtol=1e-4, err_msg=k)
+    assert rel(res.x, ref.x) <= 1e-4

@@ -1379,8 +1379,14 @@ __device__ __forceinline__ void ts_issue(const TsRing& R, int b, int tw, int nb,
 }
 
 // Gram variant: also gacc[r] += <row (warp + SW r), row grow> for rows < grow + 1.
-__device__ __forceinline__ void ts_dots2(const float* tile, int tw, int nrows, int vrow, int grow,
-                                         int cn, double* acc, double* gacc) {
+// NR = this warp's row count (rows warp, warp + SW, ... below nrows), a
+// template parameter picked by one warp-uniform switch per tile: a guard per
+// row inside the unrolled loop cost a branch region (BSSY / BRA / BSYNC,
+// ~25 cycles of branch latency) for each of the up-to-8 rows a warp does NOT
+// have, twice per tile -- most of a tile's time at small k.
+template <int NR>
+__device__ __forceinline__ void ts_dots2_nr(const float* tile, int tw, int vrow, int grow, int cn,
+                                            double* acc, double* gacc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float* vr = tile + (size_t)vrow * tw;
     const float* gr = tile + (size_t)grow * tw;
@@ -1393,31 +1399,48 @@ __device__ __forceinline__ void ts_dots2(const float* tile, int tw, int nrows, i
         const double v0 = v.x, v1 = v.y, v2 = v.z, v3 = v.w;
         const double u0 = u.x, u1 = u.y, u2 = u.z, u3 = u.w;
 #pragma unroll
-        for (int r = 0; r < TS_RPW; ++r) {
+        for (int r = 0; r < NR; ++r) {
             const int j = warp + SW * r;
-            if (j < nrows) {
-                const float4 w = *reinterpret_cast<const float4*>(tile + (size_t)j * tw + e);
-                const double x0 = w.x, x1 = w.y, x2 = w.z, x3 = w.w;
-                double a = acc[r];
-                a = fma(x0, v0, a);
-                a = fma(x1, v1, a);
-                a = fma(x2, v2, a);
-                a = fma(x3, v3, a);
-                acc[r] = a;
-                double b = gacc[r];
-                b = fma(x0, u0, b);
-                b = fma(x1, u1, b);
-                b = fma(x2, u2, b);
-                b = fma(x3, u3, b);
-                gacc[r] = b;
-            }
+            const float4 w = *reinterpret_cast<const float4*>(tile + (size_t)j * tw + e);
+            const double x0 = w.x, x1 = w.y, x2 = w.z, x3 = w.w;
+            double a = acc[r];
+            a = fma(x0, v0, a);
+            a = fma(x1, v1, a);
+            a = fma(x2, v2, a);
+            a = fma(x3, v3, a);
+            acc[r] = a;
+            double b = gacc[r];
+            b = fma(x0, u0, b);
+            b = fma(x1, u1, b);
+            b = fma(x2, u2, b);
+            b = fma(x3, u3, b);
+            gacc[r] = b;
         }
     }
 }
 
-// acc[r] += <row (warp + SW r), vector row> over one tile (fp64 products).
-__device__ __forceinline__ void ts_dots(const float* tile, int tw, int nrows, int vrow, int cn,
-                                        double* acc) {
+__device__ __forceinline__ void ts_dots2(const float* tile, int tw, int nrows, int vrow, int grow,
+                                         int cn, double* acc, double* gacc) {
+    const int warp = threadIdx.x >> 5;
+    const int nr = nrows > warp ? (nrows - warp + SW - 1) / SW : 0;     // warp-uniform
+    switch (nr) {
+        case 0: break;
+        case 1: ts_dots2_nr<1>(tile, tw, vrow, grow, cn, acc, gacc); break;
+        case 2: ts_dots2_nr<2>(tile, tw, vrow, grow, cn, acc, gacc); break;
+        case 3: ts_dots2_nr<3>(tile, tw, vrow, grow, cn, acc, gacc); break;
+        case 4: ts_dots2_nr<4>(tile, tw, vrow, grow, cn, acc, gacc); break;
+        case 5: ts_dots2_nr<5>(tile, tw, vrow, grow, cn, acc, gacc); break;
+        case 6: ts_dots2_nr<6>(tile, tw, vrow, grow, cn, acc, gacc); break;
+        case 7: ts_dots2_nr<7>(tile, tw, vrow, grow, cn, acc, gacc); break;
+        default: ts_dots2_nr<TS_RPW>(tile, tw, vrow, grow, cn, acc, gacc); break;
+    }
+}
+
+// acc[r] += <row (warp + SW r), vector row> over one tile (fp64 products);
+// NR as in ts_dots2_nr.
+template <int NR>
+__device__ __forceinline__ void ts_dots_nr(const float* tile, int tw, int vrow, int cn,
+                                           double* acc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float* vr = tile + (size_t)vrow * tw;
 #pragma unroll
@@ -1427,18 +1450,33 @@ __device__ __forceinline__ void ts_dots(const float* tile, int tw, int nrows, in
         const float4 v = *reinterpret_cast<const float4*>(vr + e);
         const double v0 = v.x, v1 = v.y, v2 = v.z, v3 = v.w;
 #pragma unroll
-        for (int r = 0; r < TS_RPW; ++r) {
+        for (int r = 0; r < NR; ++r) {
             const int j = warp + SW * r;
-            if (j < nrows) {
-                const float4 w = *reinterpret_cast<const float4*>(tile + (size_t)j * tw + e);
-                double a = acc[r];
-                a = fma((double)w.x, v0, a);
-                a = fma((double)w.y, v1, a);
-                a = fma((double)w.z, v2, a);
-                a = fma((double)w.w, v3, a);
-                acc[r] = a;
-            }
+            const float4 w = *reinterpret_cast<const float4*>(tile + (size_t)j * tw + e);
+            double a = acc[r];
+            a = fma((double)w.x, v0, a);
+            a = fma((double)w.y, v1, a);
+            a = fma((double)w.z, v2, a);
+            a = fma((double)w.w, v3, a);
+            acc[r] = a;
         }
+    }
+}
+
+__device__ __forceinline__ void ts_dots(const float* tile, int tw, int nrows, int vrow, int cn,
+                                        double* acc) {
+    const int warp = threadIdx.x >> 5;
+    const int nr = nrows > warp ? (nrows - warp + SW - 1) / SW : 0;     // warp-uniform
+    switch (nr) {
+        case 0: break;
+        case 1: ts_dots_nr<1>(tile, tw, vrow, cn, acc); break;
+        case 2: ts_dots_nr<2>(tile, tw, vrow, cn, acc); break;
+        case 3: ts_dots_nr<3>(tile, tw, vrow, cn, acc); break;
+        case 4: ts_dots_nr<4>(tile, tw, vrow, cn, acc); break;
+        case 5: ts_dots_nr<5>(tile, tw, vrow, cn, acc); break;
+        case 6: ts_dots_nr<6>(tile, tw, vrow, cn, acc); break;
+        case 7: ts_dots_nr<7>(tile, tw, vrow, cn, acc); break;
+        default: ts_dots_nr<TS_RPW>(tile, tw, vrow, cn, acc); break;
     }
 }
 
@@ -1598,16 +1636,18 @@ __global__ void __launch_bounds__(ST, 1) k_gs_stream(float* W, int64_t ld, int k
             const int rows = mode == 1 ? nb : nb + 1;
 #pragma unroll
             for (int r = 0; r < TS_RPW; ++r) {
-                const double t = warp_sum(acc[r]);
                 const int j = warp + SW * r;
-                if (lane == 0 && j < rows) P[(size_t)j * gridDim.x + blockIdx.x] = t;
+                if (j >= rows) break;                      // warp-uniform
+                const double t = warp_sum(acc[r]);
+                if (lane == 0) P[(size_t)j * gridDim.x + blockIdx.x] = t;
             }
             if (mode == 3) {
 #pragma unroll
                 for (int r = 0; r < TS_RPW; ++r) {
-                    const double t = warp_sum(gacc[r]);
                     const int j = warp + SW * r;
-                    if (lane == 0 && j < nb) P[(size_t)(nb + 1 + j) * gridDim.x + blockIdx.x] = t;
+                    if (j >= nb) break;                    // warp-uniform
+                    const double t = warp_sum(gacc[r]);
+                    if (lane == 0) P[(size_t)(nb + 1 + j) * gridDim.x + blockIdx.x] = t;
                 }
             }
         }
